@@ -1,0 +1,184 @@
+/* ozmm_b200 -- B200-native (sm_100a) ozIMMU_H emulated DGEMM: the C ABI.
+ *
+ * This is the drop-in boundary for the reference's hot path, the ozIMMU_H
+ * preset of the Ozaki-scheme GEMM in /root/reference/proj:
+ *
+ *   MatrixF64   ozaki_gemm   (alpha, A, B, beta, C, cfg)   include/ozmm/scheme.hpp:92-95
+ *   OzakiResult ozaki_gemm_ex(alpha, A, B, beta, C, cfg)   include/ozmm/scheme.hpp:96-98
+ *   OzakiResult ozaki_mm     (A, B, cfg)                   include/ozmm/scheme.hpp:89-90
+ *   cfg = config_for(Method::ozIMMU_H, k)                  src/scheme.cpp:137-159
+ *
+ * Everything here is plain C: pointers, sizes, status codes.  No exception,
+ * no C++ or torch type crosses it.  The C++ adapter with the reference's own
+ * signature (ozmm::gpu::ozaki_gemm_ex over any row-major matrix type) is the
+ * header-only paper_2409_13313_b200/cpp/ozmm_gpu.hpp; the Python mirror is
+ * paper_2409_13313_b200/ozmm.py.  INTEGRATION.md shows the bindings.
+ *
+ * Conventions (matching the reference):
+ *   - ROW-MAJOR storage, like the reference's Eigen RowMajor DenseMatrix
+ *     (include/ozmm/types.hpp:13-16).  op(A) is m x n, op(B) is n x p, C is
+ *     m x p; n is the INNER dimension (the paper's naming).
+ *     ld* is the row stride in elements.  transa = 'T' means A is stored
+ *     n x m and op(A) = A^T (same for transb).  Column-major BLAS callers
+ *     swap operands: C^T = op(B)^T op(A)^T (bit-identical: transpose symmetry,
+ *     SURVEY.md Appendix A.5).
+ *   - Result: C <- fl(fl(alpha * D) + fl(beta * C)) elementwise
+ *     (src/scheme.cpp:286-287).  As in the reference, fl(beta*C) is ALWAYS
+ *     formed, also for beta == 0 (so C must hold finite values; a NaN/inf in
+ *     C propagates even when beta == 0, exactly like the reference).
+ *   - The reference returns a NEW matrix and never modifies C; here C is
+ *     overwritten in place (BLAS style).  The adapters restore the copy-out.
+ *   - Device pointers, stream-ordered on the handle's stream.  The _host
+ *     variant takes host pointers and is synchronous.
+ *   - Inputs must be finite.  Rows/columns whose max magnitude is >= 2^921
+ *     make the reference throw std::overflow_error (src/split.cpp:124-125):
+ *     here OZMM_ERR_RANGE.  Row scales below 2^-1000 set the underflow flag
+ *     (SplitMatrix::underflow_flagged, split.hpp:40).
+ */
+#ifndef OZMM_B200_H
+#define OZMM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OZMM_B200_VERSION 1
+
+/* Status codes.  The reference's exception types map as:
+ *   std::invalid_argument (shapes, k, n range; scheme.cpp:230-231, :278,
+ *                          split.cpp:34-36, :212-214)   -> OZMM_ERR_ARG
+ *   ConfigError (scheme.hpp:20-22, scheme.cpp:162)      -> OZMM_ERR_CONFIG
+ *   std::overflow_error (row max >= 2^921, split.cpp:124-125) -> OZMM_ERR_RANGE
+ *   OverflowError (INT32 chunk overflow, int_gemm.hpp:15-26; unreachable with
+ *                  the derived r, reachable only via force_r) -> not detected
+ *                  on the GPU: the tensor core wraps like OverflowMode::Wrapping. */
+typedef enum {
+  OZMM_OK = 0,
+  OZMM_ERR_ARG = 1,
+  OZMM_ERR_CONFIG = 2,
+  OZMM_ERR_RANGE = 3,
+  OZMM_ERR_CUDA = 5,
+  OZMM_ERR_NCCL = 6,
+  OZMM_ERR_UNSUPPORTED = 7,
+  OZMM_ERR_INTERNAL = 9
+} ozmm_status_t;
+
+typedef struct ozmm_handle_s* ozmm_handle_t;
+
+/* Runtime-tallied operation counts; same fields as OpCounts (scheme.hpp:45-50). */
+typedef struct {
+  int64_t int8_gemms;   /* slice products issued: k(k+1)/2 */
+  int64_t fp64_flushes; /* FP64 folds per element: w */
+  int64_t r;            /* max products per INT32 chunk (compute_r) */
+  int64_t w;            /* closed-form flush count (flush_count_w) */
+} ozmm_counts_t;
+
+/* Phase timings in seconds (CUDA events on the handle's stream); same fields
+ * as PhaseTimings (scheme.hpp:52-58).  The INT8 GEMMs, the FP64 accumulation
+ * and the alpha/beta epilogue are ONE fused kernel here: its time is reported
+ * in int_gemm, and accum_fp64 = copy = 0. */
+typedef struct {
+  double split_a;
+  double split_b;
+  double int_gemm;
+  double accum_fp64;
+  double copy;
+} ozmm_timings_t;
+
+/* Options of ozmm_dgemm_ex; zero-initialise for the defaults.  force_beta /
+ * force_r mirror the test-only SchemeConfig overrides (scheme.hpp:29-30). */
+typedef struct {
+  int force_beta;          /* 0: derive beta from n (compute_beta) */
+  int64_t force_r;         /* 0: derive r from (n, beta) (compute_r) */
+  int timings;             /* nonzero: fill ozmm_timings_t (adds event records) */
+  int sync_check;          /* nonzero: synchronise after slicing and return
+                              OZMM_ERR_RANGE before the GEMM, like the reference's
+                              throw; otherwise the range flag is deferred to
+                              ozmm_sync_status() */
+  int32_t* chunk_dump;     /* nullable device buffer [w][m][p]: the INT32 chunk
+                              sums in flush order (debug / parity) */
+  int tile_n;              /* 0 = auto; else 32, 64 or 128 output columns per CTA */
+} ozmm_options_t;
+
+/* ---- handle ------------------------------------------------------------- */
+int ozmm_create(ozmm_handle_t* handle, int device);
+int ozmm_destroy(ozmm_handle_t handle);
+/* stream: a cudaStream_t (NULL = legacy default stream). */
+int ozmm_set_stream(ozmm_handle_t handle, void* stream);
+/* Message of the last failing call on this handle (or thread, when handle is NULL). */
+const char* ozmm_last_error(ozmm_handle_t handle);
+const char* ozmm_status_string(int status);
+/* Waits for the handle's stream; returns OZMM_ERR_RANGE if any split since the
+ * last query saw a line max >= 2^921, and sets *underflow (nullable) when a
+ * line scale fell below 2^-1000.  Clears both flags. */
+int ozmm_sync_status(ozmm_handle_t handle, int* underflow);
+/* Bytes of device workspace the handle currently owns (grown lazily). */
+size_t ozmm_workspace_bytes(ozmm_handle_t handle);
+
+/* ---- closed forms (host only, no device work) ---------------------------- */
+int ozmm_compute_beta(int64_t n, int* beta);              /* split.cpp:211-216 */
+int ozmm_compute_r(int64_t n, int beta, int64_t* r);      /* int_gemm.cpp:253-258 */
+/* counts for (k, r): int8_gemms = k(k+1)/2, w = flush_count_w (scheme.cpp:105-115,
+ * :176-184); accumulation = 1 (Groupwise) for ozIMMU_H. */
+int ozmm_op_counts(int k, int64_t r, ozmm_counts_t* counts);
+
+/* ---- the emulated DGEMM --------------------------------------------------- */
+int ozmm_dgemm(ozmm_handle_t h, char transa, char transb, int64_t m, int64_t n, int64_t p,
+               double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+               double beta, double* C, int64_t ldc, int k);
+
+int ozmm_dgemm_ex(ozmm_handle_t h, char transa, char transb, int64_t m, int64_t n, int64_t p,
+                  double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+                  double beta, double* C, int64_t ldc, int k, const ozmm_options_t* opt,
+                  ozmm_counts_t* counts, ozmm_timings_t* timings);
+
+/* Host-pointer variant (what the reference API takes): copies A, B, C to the
+ * device, runs ozmm_dgemm_ex, copies C back.  Synchronous.  Range errors are
+ * returned directly (sync_check is implied). */
+int ozmm_dgemm_host(ozmm_handle_t h, char transa, char transb, int64_t m, int64_t n, int64_t p,
+                    double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+                    double beta, double* C, int64_t ldc, int k, const ozmm_options_t* opt,
+                    ozmm_counts_t* counts, ozmm_timings_t* timings);
+
+/* ---- the two halves, for sharded (multi-GPU) callers and parity tests ---- */
+/* Row stride of a slice plane for inner dimension n: round_up(n, 16). */
+int64_t ozmm_slice_ld(int64_t n);
+
+/* K1: RN constant-shift split of `lines` lines of length n (split.cpp:151-198).
+ *   side 'L': lines are the rows of op(X) where op(X) is lines x n
+ *             (trans 'N': X stored lines x n; 'T': X stored n x lines).
+ *   side 'R': lines are the columns of op(X) where op(X) is n x lines
+ *             (trans 'N': X stored n x lines; 'T': X stored lines x n).
+ * slices: device [k][lines][lds] int8 (lds = ozmm_slice_ld(n) unless larger);
+ * shift: device [lines] doubles (const_shift).  beta: 0 = compute_beta(n). */
+int ozmm_split(ozmm_handle_t h, char side, char trans, int64_t lines, int64_t n,
+               const double* X, int64_t ldx, int k, int beta, int8_t* slices, int64_t lds,
+               double* shift);
+
+/* K2+K3 over already-split operands: C <- alpha * D + beta * C with D the
+ * group-wise ozIMMU_H accumulation of A slices [k][m][lds_a] / mu [m] and
+ * B slices [k][p][lds_b] / nu [p] (B stored transposed: row j = column j of
+ * op(B)).  n is the inner dimension the slices were cut for; beta_bits the
+ * slice width used; r = 0 derives compute_r(n, beta_bits). */
+int ozmm_gemm_slices(ozmm_handle_t h, int64_t m, int64_t n, int64_t p, int k, int beta_bits,
+                     int64_t r, const int8_t* As, int64_t lds_a, const double* mu,
+                     const int8_t* Bs, int64_t lds_b, const double* nu, double alpha,
+                     double beta, double* C, int64_t ldc, const ozmm_options_t* opt);
+
+/* ---- input generator (host, OpenMP) --------------------------------------- */
+/* The reference's phi test matrices (src/generate.cpp:11-29,
+ * include/ozmm/generate.hpp:11-21): entry (i, j) of the GLOBAL rows x cols
+ * matrix is (U - 0.5) * exp(phi * N) drawn from counter index (i*cols + j)*3.
+ * Writes the block [row0, row0+nrows) x [col0, col0+ncols) into out (row
+ * stride ldo), so any shard of a matrix can be generated independently. */
+int ozmm_gen_phi_block(int64_t rows, int64_t cols, double phi, uint64_t seed, int64_t row0,
+                       int64_t nrows, int64_t col0, int64_t ncols, double* out, int64_t ldo);
+uint64_t ozmm_counter_hash(uint64_t seed, uint64_t ctr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OZMM_B200_H */

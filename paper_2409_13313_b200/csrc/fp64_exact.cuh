@@ -1,0 +1,77 @@
+// Bit-exact FP64 helpers shared by the slicer and the GEMM epilogue.
+//
+// Every rounded FP64 operation on the ozIMMU_H path is written with an
+// explicit _rn intrinsic so nvcc can neither contract a*b+c into an FMA nor
+// reorder: this is the GPU form of the reference's -ffp-contract=off rule
+// (proj/src/CMakeLists.txt:18-20).
+#pragma once
+
+#include <cstdint>
+
+namespace ozb {
+
+// 2^e as a double, exactly as std::ldexp(1.0, e) rounds it: normal for
+// e >= -1022, subnormal down to 2^-1074, 0 below (2^-1075 is a tie that rounds
+// to even = 0), +inf above 1023.
+__host__ __device__ __forceinline__ double pow2(int e) {
+  uint64_t bits;
+  if (e >= -1022) {
+    if (e > 1023) bits = 0x7FF0000000000000ull;
+    else bits = static_cast<uint64_t>(e + 1023) << 52;
+  } else if (e >= -1074) {
+    bits = 1ull << (e + 1074);
+  } else {
+    bits = 0;
+  }
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double(static_cast<long long>(bits));
+#else
+  double d;
+  __builtin_memcpy(&d, &bits, 8);
+  return d;
+#endif
+}
+
+// ufp_exponent (proj/include/ozmm/ufp.hpp:35-41): e with 2^e <= |c| < 2^(e+1),
+// subnormals via the position of the top set bit.  c must be finite, nonzero.
+__device__ __forceinline__ int ufp_exponent(double c) {
+  const uint64_t b = static_cast<uint64_t>(__double_as_longlong(c)) & 0x7FFFFFFFFFFFFFFFull;
+  const int biased = static_cast<int>(b >> 52);
+  if (biased > 0) return biased - 1023;
+  return (63 - __clzll(static_cast<long long>(b))) - 1074;
+}
+
+// static_cast<std::int8_t>(double) exactly as g++ compiles it on x86-64
+// (cvttsd2si to int32 -- 0x80000000 for NaN/inf/out of range -- then the low
+// byte).  In range it is truncation toward zero.  Used by extract_row
+// (proj/src/split.cpp:114).
+__device__ __forceinline__ int8_t x86_cast_i8(double q) {
+  int32_t v;
+  if (!(q > -2147483649.0 && q < 2147483648.0)) v = INT32_MIN;
+  else v = __double2int_rz(q);
+  return static_cast<int8_t>(static_cast<uint8_t>(static_cast<uint32_t>(v)));
+}
+
+// x / 2^e for x an exact multiple of 2^e (the quotient is an integer), i.e.
+// the correctly rounded division of extract_row, without a division.
+__device__ __forceinline__ double div_pow2(double x, int e) {
+  if (e >= -1023) return __dmul_rn(x, pow2(-e));
+  return __dmul_rn(__dmul_rn(x, pow2(1000)), pow2(-e - 1000));
+}
+
+// Per-line splitting parameters of rn_const_shift_rows / rn_unit
+// (proj/src/split.cpp:121-130, :158-166) for line max `rm`:
+//   pe0 = ufp_exponent(rm); bump if rm >= (2 - 2^-beta) * 2^pe0;
+//   PE = pe0 + bump; const_shift = 2^PE; unit_s = 2^(PE + 1 - beta*s).
+// Returns PE, or INT32_MIN for a zero line.  *range set when pe0 > 920,
+// *under when pe0 < -1000.
+__device__ __forceinline__ int line_pe(double rm, int beta, bool* under, bool* range) {
+  if (rm == 0.0) return INT32_MIN;
+  const int pe0 = ufp_exponent(rm);
+  if (pe0 < -1000) *under = true;
+  if (pe0 > 920) *range = true;
+  const double threshold = __dmul_rn(2.0 - pow2(-beta), pow2(pe0));  // == ldexp(2-2^-b, pe0)
+  return pe0 + (rm >= threshold ? 1 : 0);
+}
+
+}  // namespace ozb

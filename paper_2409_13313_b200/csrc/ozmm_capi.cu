@@ -1,0 +1,571 @@
+// Host side of the C ABI (include/ozmm_b200.h): handle + workspace, the
+// ozIMMU_H orchestration (split op(A) rows, split op(B) columns, fused GEMM),
+// TMA descriptor encoding and the launch configuration.
+//
+// Mirrors ozaki_gemm_ex / ozaki_mm (proj/src/scheme.cpp:228-291) for the
+// ozIMMU_H preset (config_for, :153-156): RoundNearestConstShift splits of A
+// (Left) and B (Right) with beta = compute_beta(n), then group-wise
+// accumulation with r = compute_r(n, beta), then the alpha/beta epilogue.
+// There is no CPU fallback: every numeric step runs in the kernels below.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/ozmm_b200.h"
+#include "ozimmu_gemm.cuh"
+#include "schedule.hpp"
+#include "slicer.cuh"
+
+namespace {
+
+thread_local std::string g_thread_err;
+
+struct Handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  // workspace (grown lazily, owned)
+  int8_t* slices_a = nullptr;
+  size_t slices_a_bytes = 0;
+  int8_t* slices_b = nullptr;
+  size_t slices_b_bytes = 0;
+  double* mu = nullptr;
+  size_t mu_n = 0;
+  double* nu = nullptr;
+  size_t nu_n = 0;
+  unsigned long long* colmax = nullptr;
+  size_t colmax_n = 0;
+  int* flags = nullptr;  // [0] underflow, [1] range
+  double* dev_c_scratch = nullptr;
+  cudaEvent_t ev[5] = {};
+  bool gemm_attr_set[3] = {false, false, false};
+  int num_sms = 148;
+  size_t smem_optin = 232448;
+};
+
+int set_err(Handle* h, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (h) h->err = buf;
+  g_thread_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(h, call)                                                               \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return set_err(h, OZMM_ERR_CUDA, "%s failed: %s (%s:%d)", #call,                  \
+                     cudaGetErrorString(e_), __FILE__, __LINE__);                       \
+  } while (0)
+
+template <class T>
+int ensure(Handle* h, T** ptr, size_t* have, size_t want) {
+  if (*have >= want && *ptr) return OZMM_OK;
+  if (*ptr) {
+    cudaFree(*ptr);
+    *ptr = nullptr;
+    *have = 0;
+  }
+  CUDA_TRY(h, cudaMalloc(reinterpret_cast<void**>(ptr), std::max<size_t>(want, 256) * sizeof(T)));
+  *have = std::max<size_t>(want, 256);
+  return OZMM_OK;
+}
+
+// ---- TMA descriptor encoding through the driver entry point (no -lcuda) ----
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// 3-D int8 map over slice planes [k][lines][lds]: box = 32 B of K x rows x 1 slice,
+// 32-byte swizzle (matches the UMMA descriptors built in the kernel).
+int make_slice_map(Handle* h, CUtensorMap* map, const int8_t* base, int64_t lds, int64_t lines,
+                   int k, uint32_t box_rows) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return set_err(h, OZMM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(lds), static_cast<cuuint64_t>(lines),
+                              static_cast<cuuint64_t>(k)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(lds),
+                                 static_cast<cuuint64_t>(lds * lines)};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(ozb::kBK), box_rows, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(h, OZMM_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", r);
+  return OZMM_OK;
+}
+
+bool is_trans(char t) { return t == 'T' || t == 't' || t == 'C' || t == 'c'; }
+bool valid_trans(char t) { return is_trans(t) || t == 'N' || t == 'n'; }
+
+// ---- K1 launch ----------------------------------------------------------------
+// Lines of op(X): row mode when the line is contiguous in memory.
+int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const double* X, int64_t ldx,
+                 int k, int beta, int8_t* S, int64_t lds, double* shift) {
+  const int64_t plane = lines * lds;
+  if (row_mode) {
+    const bool vec = (reinterpret_cast<uintptr_t>(X) % 16 == 0) && (ldx % 2 == 0);
+    const dim3 grid(static_cast<unsigned>((lines + 7) / 8));
+    if (vec)
+      ozb::slice_rows_kernel<true><<<grid, 256, 0, h->stream>>>(X, ldx, lines, n, lds, k, beta, S,
+                                                                plane, shift, h->flags);
+    else
+      ozb::slice_rows_kernel<false><<<grid, 256, 0, h->stream>>>(X, ldx, lines, n, lds, k, beta,
+                                                                 S, plane, shift, h->flags);
+  } else {
+    if (int rc = ensure(h, &h->colmax, &h->colmax_n, static_cast<size_t>(lines))) return rc;
+    CUDA_TRY(h, cudaMemsetAsync(h->colmax, 0, sizeof(unsigned long long) * lines, h->stream));
+    const int64_t rows_per_block = 512;
+    const dim3 g1(static_cast<unsigned>((lines + 31) / 32),
+                  static_cast<unsigned>((n + rows_per_block - 1) / rows_per_block));
+    ozb::colmax_kernel<<<g1, 256, 0, h->stream>>>(X, ldx, n, lines, rows_per_block, h->colmax);
+    const dim3 g2(static_cast<unsigned>((lines + 31) / 32), static_cast<unsigned>((lds + 127) / 128));
+    ozb::slice_cols_kernel<<<g2, 256, 0, h->stream>>>(X, ldx, n, lines, lds, k, beta, h->colmax,
+                                                       S, plane, shift, h->flags);
+  }
+  CUDA_TRY(h, cudaGetLastError());
+  return OZMM_OK;
+}
+
+// ---- K2+K3 launch -------------------------------------------------------------
+constexpr size_t kSmemReserve = 2048;  // barriers, tmem slot, alignment slack (+ nu cache)
+
+template <int kBN>
+int launch_gemm_bn(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_bits, int64_t r,
+                   const int8_t* As, int64_t lds_a, const double* mu, const int8_t* Bs,
+                   int64_t lds_b, const double* nu, double alpha, double beta, const double* Cin,
+                   double* Cout, int64_t ldc, int32_t* dump) {
+  using Cfg = ozb::GemmCfg<kBN>;
+  const size_t budget = h->smem_optin - kSmemReserve - kBN * sizeof(double);
+  const int64_t max_stage = static_cast<int64_t>(budget / 3);
+  auto slot_bytes = [](int a, int b) {
+    return static_cast<int64_t>(a) * Cfg::kATile + static_cast<int64_t>(b) * Cfg::kBTile;
+  };
+  const ozb::Schedule S = ozb::make_schedule(k, r, Cfg::kNAcc, max_stage, slot_bytes);
+  if (S.batches.size() > static_cast<size_t>(ozb::kMaxBatches) ||
+      S.passes.size() > static_cast<size_t>(ozb::kMaxPasses) ||
+      S.products.size() > static_cast<size_t>(ozb::kMaxProducts) ||
+      S.chunks.size() > static_cast<size_t>(ozb::kMaxChunks))
+    return set_err(h, OZMM_ERR_UNSUPPORTED, "schedule too large (k=%d, r=%lld)", k,
+                   static_cast<long long>(r));
+  const size_t stage_bytes = slot_bytes(S.a_slots, S.b_slots);
+  const int stages = static_cast<int>(std::min<size_t>(8, budget / stage_bytes));
+  if (stages < 2)
+    return set_err(h, OZMM_ERR_UNSUPPORTED, "pipeline stage (%zu B) exceeds smem budget",
+                   stage_bytes);
+
+  ozb::GemmParams P;  // ~3 KB, passed by value as __grid_constant__
+  std::memset(&P, 0, sizeof P);
+  P.m = static_cast<int>(m);
+  P.p = static_cast<int>(p);
+  P.n_kb = static_cast<int>((std::max(lds_a, lds_b) + ozb::kBK - 1) / ozb::kBK);
+  P.tiles_m = static_cast<int>((m + ozb::kBM - 1) / ozb::kBM);
+  P.tiles_n = static_cast<int>((p + kBN - 1) / kBN);
+  P.group_m = 16;
+  P.nbatch = static_cast<int>(S.batches.size());
+  P.npass = static_cast<int>(S.passes.size());
+  P.beta = beta_bits;
+  P.stages = stages;
+  P.a_slots = S.a_slots;
+  P.b_slots = S.b_slots;
+  P.n_chunks = static_cast<int>(S.chunks.size());
+  P.alpha = alpha;
+  P.beta_c = beta;
+  P.mu = mu;
+  P.nu = nu;
+  P.c_in = Cin;
+  P.c_out = Cout;
+  P.ldc = ldc;
+  P.dump = dump;
+  for (size_t b = 0; b < S.batches.size(); ++b) {
+    P.b_c0[b] = static_cast<uint8_t>(S.batches[b].c0);
+    P.b_nc[b] = static_cast<uint8_t>(S.batches[b].nc);
+    P.b_pass0[b] = static_cast<uint8_t>(S.batches[b].pass0);
+    P.b_pass1[b] = static_cast<uint8_t>(S.batches[b].pass1);
+  }
+  for (size_t q = 0; q < S.passes.size(); ++q) {
+    P.p_alo[q] = static_cast<uint8_t>(S.passes[q].alo);
+    P.p_ahi[q] = static_cast<uint8_t>(S.passes[q].ahi);
+    P.p_blo[q] = static_cast<uint8_t>(S.passes[q].blo);
+    P.p_bhi[q] = static_cast<uint8_t>(S.passes[q].bhi);
+    P.p_p0[q] = static_cast<uint16_t>(S.passes[q].p0);
+    P.p_p1[q] = static_cast<uint16_t>(S.passes[q].p1);
+  }
+  for (size_t i = 0; i < S.products.size(); ++i) {
+    P.pr_ci[i] = static_cast<uint8_t>(S.products[i].ci | (S.products[i].first ? 0x80 : 0));
+    P.pr_s[i] = static_cast<uint8_t>(S.products[i].s);
+    P.pr_t[i] = static_cast<uint8_t>(S.products[i].t);
+  }
+  for (size_t c = 0; c < S.chunks.size(); ++c) P.c_g[c] = static_cast<uint8_t>(S.chunks[c].g);
+
+  CUtensorMap map_a, map_b;
+  if (int rc = make_slice_map(h, &map_a, As, lds_a, m, k, ozb::kBM)) return rc;
+  if (int rc = make_slice_map(h, &map_b, Bs, lds_b, p, k, kBN)) return rc;
+
+  const size_t smem = stages * stage_bytes + kSmemReserve + kBN * sizeof(double);
+  const int bn_idx = kBN == 32 ? 0 : (kBN == 64 ? 1 : 2);
+  if (!h->gemm_attr_set[bn_idx]) {
+    CUDA_TRY(h, cudaFuncSetAttribute(ozb::ozimmu_gemm_kernel<kBN>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(h->smem_optin)));
+    h->gemm_attr_set[bn_idx] = true;
+  }
+  const dim3 grid(static_cast<unsigned>(P.tiles_m * P.tiles_n));
+  ozb::ozimmu_gemm_kernel<kBN><<<grid, ozb::kGemmThreads, smem, h->stream>>>(map_a, map_b, P);
+  CUDA_TRY(h, cudaGetLastError());
+  return OZMM_OK;
+}
+
+int launch_gemm(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_bits, int64_t r,
+                const int8_t* As, int64_t lds_a, const double* mu, const int8_t* Bs, int64_t lds_b,
+                const double* nu, double alpha, double beta, const double* Cin, double* Cout,
+                int64_t ldc, const ozmm_options_t* opt) {
+  int32_t* dump = opt ? opt->chunk_dump : nullptr;
+  const int tile_n = opt && opt->tile_n ? opt->tile_n : 64;
+  switch (tile_n) {
+    case 32:
+      return launch_gemm_bn<32>(h, m, n, p, k, beta_bits, r, As, lds_a, mu, Bs, lds_b, nu, alpha,
+                                beta, Cin, Cout, ldc, dump);
+    case 64:
+      return launch_gemm_bn<64>(h, m, n, p, k, beta_bits, r, As, lds_a, mu, Bs, lds_b, nu, alpha,
+                                beta, Cin, Cout, ldc, dump);
+    case 128:
+      return launch_gemm_bn<128>(h, m, n, p, k, beta_bits, r, As, lds_a, mu, Bs, lds_b, nu,
+                                 alpha, beta, Cin, Cout, ldc, dump);
+    default:
+      return set_err(h, OZMM_ERR_ARG, "tile_n must be 32, 64 or 128 (got %d)", tile_n);
+  }
+}
+
+int check_range_sync(Handle* h) {
+  int f[2] = {0, 0};
+  CUDA_TRY(h, cudaMemcpyAsync(f, h->flags, sizeof f, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  if (f[1]) {
+    CUDA_TRY(h, cudaMemsetAsync(h->flags + 1, 0, sizeof(int), h->stream));
+    return set_err(h, OZMM_ERR_RANGE, "split: row magnitude too large for shift extraction");
+  }
+  return OZMM_OK;
+}
+
+}  // namespace
+
+// =============================================================================
+extern "C" {
+
+int ozmm_create(ozmm_handle_t* out, int device) {
+  if (!out) return set_err(nullptr, OZMM_ERR_ARG, "null handle pointer");
+  Handle* h = new Handle();
+  h->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    delete h;
+    return set_err(nullptr, OZMM_ERR_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
+  }
+  int major = 0, minor = 0, sms = 0, optin = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (major != 10 || minor != 0) {
+    delete h;
+    return set_err(nullptr, OZMM_ERR_UNSUPPORTED,
+                   "device %d is sm_%d%d; this library is built for sm_100a (B200) only", device,
+                   major, minor);
+  }
+  h->num_sms = sms;
+  h->smem_optin = static_cast<size_t>(optin);
+  if (cudaMalloc(&h->flags, 2 * sizeof(int)) != cudaSuccess ||
+      cudaMemset(h->flags, 0, 2 * sizeof(int)) != cudaSuccess) {
+    delete h;
+    return set_err(nullptr, OZMM_ERR_CUDA, "flag allocation failed");
+  }
+  for (auto& ev : h->ev) cudaEventCreate(&ev);
+  *out = reinterpret_cast<ozmm_handle_t>(h);
+  return OZMM_OK;
+}
+
+int ozmm_destroy(ozmm_handle_t handle) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return OZMM_OK;
+  cudaSetDevice(h->device);
+  cudaFree(h->slices_a);
+  cudaFree(h->slices_b);
+  cudaFree(h->mu);
+  cudaFree(h->nu);
+  cudaFree(h->colmax);
+  cudaFree(h->flags);
+  cudaFree(h->dev_c_scratch);
+  for (auto& ev : h->ev) cudaEventDestroy(ev);
+  delete h;
+  return OZMM_OK;
+}
+
+int ozmm_set_stream(ozmm_handle_t handle, void* stream) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return set_err(nullptr, OZMM_ERR_ARG, "null handle");
+  h->stream = static_cast<cudaStream_t>(stream);
+  return OZMM_OK;
+}
+
+const char* ozmm_last_error(ozmm_handle_t handle) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  return h ? h->err.c_str() : g_thread_err.c_str();
+}
+
+const char* ozmm_status_string(int s) {
+  switch (s) {
+    case OZMM_OK: return "ok";
+    case OZMM_ERR_ARG: return "invalid argument";
+    case OZMM_ERR_CONFIG: return "configuration error";
+    case OZMM_ERR_RANGE: return "row magnitude too large for shift extraction";
+    case OZMM_ERR_CUDA: return "CUDA error";
+    case OZMM_ERR_NCCL: return "NCCL error";
+    case OZMM_ERR_UNSUPPORTED: return "unsupported";
+    default: return "internal error";
+  }
+}
+
+int ozmm_sync_status(ozmm_handle_t handle, int* underflow) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return set_err(nullptr, OZMM_ERR_ARG, "null handle");
+  int f[2] = {0, 0};
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  CUDA_TRY(h, cudaMemcpy(f, h->flags, sizeof f, cudaMemcpyDeviceToHost));
+  CUDA_TRY(h, cudaMemset(h->flags, 0, sizeof f));
+  if (underflow) *underflow = f[0];
+  if (f[1]) return set_err(h, OZMM_ERR_RANGE, "split: row magnitude too large for shift extraction");
+  return OZMM_OK;
+}
+
+size_t ozmm_workspace_bytes(ozmm_handle_t handle) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return 0;
+  return h->slices_a_bytes + h->slices_b_bytes + 8 * (h->mu_n + h->nu_n + h->colmax_n);
+}
+
+int ozmm_compute_beta(int64_t n, int* beta) {
+  if (!beta) return set_err(nullptr, OZMM_ERR_ARG, "null output");
+  if (n < 1) return set_err(nullptr, OZMM_ERR_ARG, "compute_beta: n must be >= 1");
+  if (n > (int64_t(1) << 29)) return set_err(nullptr, OZMM_ERR_ARG, "compute_beta: n > 2^29 unsupported");
+  *beta = ozb::compute_beta_host(n);
+  return OZMM_OK;
+}
+
+int ozmm_compute_r(int64_t n, int beta, int64_t* r) {
+  if (!r) return set_err(nullptr, OZMM_ERR_ARG, "null output");
+  if (n < 1 || beta < 1) return set_err(nullptr, OZMM_ERR_ARG, "compute_r: bad arguments");
+  *r = ozb::compute_r_host(n, beta);
+  return OZMM_OK;
+}
+
+int ozmm_op_counts(int k, int64_t r, ozmm_counts_t* c) {
+  if (!c) return set_err(nullptr, OZMM_ERR_ARG, "null output");
+  if (k < 1 || r < 1) return set_err(nullptr, OZMM_ERR_CONFIG, "op_counts: bad arguments");
+  c->int8_gemms = static_cast<int64_t>(k) * (k + 1) / 2;
+  c->r = r;
+  c->w = ozb::flush_count_w_host(k, r);
+  c->fp64_flushes = c->w;
+  return OZMM_OK;
+}
+
+int64_t ozmm_slice_ld(int64_t n) { return (n + 15) / 16 * 16; }
+
+int ozmm_split(ozmm_handle_t handle, char side, char trans, int64_t lines, int64_t n,
+               const double* X, int64_t ldx, int k, int beta, int8_t* slices, int64_t lds,
+               double* shift) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return set_err(nullptr, OZMM_ERR_ARG, "null handle");
+  if (side != 'L' && side != 'R') return set_err(h, OZMM_ERR_ARG, "side must be 'L' or 'R'");
+  if (!valid_trans(trans)) return set_err(h, OZMM_ERR_ARG, "trans must be 'N' or 'T'");
+  if (lines < 1 || n < 1) return set_err(h, OZMM_ERR_ARG, "split: empty matrix");
+  if (k < 1 || k > ozb::kMaxK) return set_err(h, OZMM_ERR_ARG, "split: k must be in 1..%d", ozb::kMaxK);
+  if (lds < ozmm_slice_ld(n) || lds % 16) return set_err(h, OZMM_ERR_ARG, "split: lds too small or not a multiple of 16");
+  if (beta == 0) {
+    beta = ozb::compute_beta_host(n);
+    if (beta < 0) return set_err(h, OZMM_ERR_ARG, "compute_beta: n out of range");
+  } else if (beta < 1 || beta > 7) {
+    return set_err(h, OZMM_ERR_ARG, "split: forced beta outside 1..7");
+  }
+  // Left/'N' and Right/'T' have contiguous lines; the others are strided.
+  const bool row_mode = (side == 'L') != is_trans(trans);
+  const int64_t need_ld = row_mode ? n : lines;
+  if (ldx < need_ld) return set_err(h, OZMM_ERR_ARG, "split: leading dimension too small");
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  return launch_split(h, row_mode, lines, n, X, ldx, k, beta, slices, lds, shift);
+}
+
+int ozmm_gemm_slices(ozmm_handle_t handle, int64_t m, int64_t n, int64_t p, int k, int beta_bits,
+                     int64_t r, const int8_t* As, int64_t lds_a, const double* mu, const int8_t* Bs,
+                     int64_t lds_b, const double* nu, double alpha, double beta, double* C,
+                     int64_t ldc, const ozmm_options_t* opt) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return set_err(nullptr, OZMM_ERR_ARG, "null handle");
+  if (m < 1 || n < 1 || p < 1) return set_err(h, OZMM_ERR_ARG, "empty shape");
+  if (m > INT32_MAX || p > INT32_MAX) return set_err(h, OZMM_ERR_ARG, "m, p must fit int32");
+  if (k < 1 || k > ozb::kMaxK) return set_err(h, OZMM_ERR_CONFIG, "k must be in 1..%d", ozb::kMaxK);
+  if (beta_bits < 1 || beta_bits > 7) return set_err(h, OZMM_ERR_ARG, "beta_bits outside 1..7");
+  if (ldc < p) return set_err(h, OZMM_ERR_ARG, "ldc < p");
+  if (lds_a % 16 || lds_b % 16 || lds_a < n || lds_b < n)
+    return set_err(h, OZMM_ERR_ARG, "slice strides must be multiples of 16 and >= n");
+  if (r == 0) r = ozb::compute_r_host(n, beta_bits);
+  if (r < 1) return set_err(h, OZMM_ERR_CONFIG, "force_r must be >= 1");
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  return launch_gemm(h, m, n, p, k, beta_bits, r, As, lds_a, mu, Bs, lds_b, nu, alpha, beta, C, C,
+                     ldc, opt);
+}
+
+int ozmm_dgemm_ex(ozmm_handle_t handle, char transa, char transb, int64_t m, int64_t n, int64_t p,
+                  double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+                  double beta, double* C, int64_t ldc, int k, const ozmm_options_t* opt,
+                  ozmm_counts_t* counts, ozmm_timings_t* timings) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return set_err(nullptr, OZMM_ERR_ARG, "null handle");
+  if (!valid_trans(transa) || !valid_trans(transb))
+    return set_err(h, OZMM_ERR_ARG, "trans must be 'N' or 'T'");
+  // validate_config (scheme.cpp:161-174) then the split argument checks (split.cpp:33-37)
+  if (k < 1) return set_err(h, OZMM_ERR_CONFIG, "k must be >= 1");
+  if (k > ozb::kMaxK) return set_err(h, OZMM_ERR_UNSUPPORTED, "k > %d not supported on the GPU path", ozb::kMaxK);
+  if (m < 1 || n < 1 || p < 1) return set_err(h, OZMM_ERR_ARG, "split: empty matrix");
+  if (m > INT32_MAX || p > INT32_MAX) return set_err(h, OZMM_ERR_ARG, "m, p must fit int32");
+  const int fb = opt ? opt->force_beta : 0;
+  int beta_bits;
+  if (fb) {
+    if (fb < 1 || fb > 7) return set_err(h, OZMM_ERR_ARG, "split: forced beta outside 1..7");
+    beta_bits = fb;
+  } else {
+    beta_bits = ozb::compute_beta_host(n);
+    if (beta_bits < 0) return set_err(h, OZMM_ERR_ARG, "compute_beta: n > 2^29 unsupported");
+  }
+  const int64_t fr = opt ? opt->force_r : 0;
+  if (fr < 0) return set_err(h, OZMM_ERR_CONFIG, "force_r must be >= 1");
+  const int64_t r = fr ? fr : ozb::compute_r_host(n, beta_bits);
+  const int64_t lda_need = is_trans(transa) ? m : n, ldb_need = is_trans(transb) ? n : p;
+  if (lda < lda_need || ldb < ldb_need || ldc < p)
+    return set_err(h, OZMM_ERR_ARG, "leading dimension too small");
+
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  const int64_t lds = ozmm_slice_ld(n);
+  if (int rc = ensure(h, &h->slices_a, &h->slices_a_bytes, static_cast<size_t>(k) * m * lds)) return rc;
+  if (int rc = ensure(h, &h->slices_b, &h->slices_b_bytes, static_cast<size_t>(k) * p * lds)) return rc;
+  if (int rc = ensure(h, &h->mu, &h->mu_n, static_cast<size_t>(m))) return rc;
+  if (int rc = ensure(h, &h->nu, &h->nu_n, static_cast<size_t>(p))) return rc;
+
+  const bool want_t = (opt && opt->timings) || timings;
+  if (want_t) CUDA_TRY(h, cudaEventRecord(h->ev[0], h->stream));
+  // split A (Left, rows of op(A)) -- split.cpp:233 via scheme.cpp:248
+  if (int rc = launch_split(h, !is_trans(transa), m, n, A, lda, k, beta_bits, h->slices_a, lds, h->mu)) return rc;
+  if (want_t) CUDA_TRY(h, cudaEventRecord(h->ev[1], h->stream));
+  // split B (Right, columns of op(B)) -- scheme.cpp:251
+  if (int rc = launch_split(h, is_trans(transb), p, n, B, ldb, k, beta_bits, h->slices_b, lds, h->nu)) return rc;
+  if (want_t) CUDA_TRY(h, cudaEventRecord(h->ev[2], h->stream));
+  if (opt && opt->sync_check)
+    if (int rc = check_range_sync(h)) return rc;
+  // fused group-wise accumulation + epilogue -- scheme.cpp:261-263, :286-287
+  if (int rc = launch_gemm(h, m, n, p, k, beta_bits, r, h->slices_a, lds, h->mu, h->slices_b, lds,
+                           h->nu, alpha, beta, C, C, ldc, opt))
+    return rc;
+  if (want_t) CUDA_TRY(h, cudaEventRecord(h->ev[3], h->stream));
+  if (counts) {
+    counts->int8_gemms = static_cast<int64_t>(k) * (k + 1) / 2;
+    counts->r = r;
+    counts->w = ozb::flush_count_w_host(k, r);
+    counts->fp64_flushes = static_cast<int64_t>(ozb::make_chunks(k, r).size());
+  }
+  if (timings) {
+    CUDA_TRY(h, cudaEventSynchronize(h->ev[3]));
+    float t01, t12, t23;
+    cudaEventElapsedTime(&t01, h->ev[0], h->ev[1]);
+    cudaEventElapsedTime(&t12, h->ev[1], h->ev[2]);
+    cudaEventElapsedTime(&t23, h->ev[2], h->ev[3]);
+    timings->split_a = t01 * 1e-3;
+    timings->split_b = t12 * 1e-3;
+    timings->int_gemm = t23 * 1e-3;
+    timings->accum_fp64 = 0.0;
+    timings->copy = 0.0;
+  }
+  return OZMM_OK;
+}
+
+int ozmm_dgemm(ozmm_handle_t h, char transa, char transb, int64_t m, int64_t n, int64_t p,
+               double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+               double beta, double* C, int64_t ldc, int k) {
+  return ozmm_dgemm_ex(h, transa, transb, m, n, p, alpha, A, lda, B, ldb, beta, C, ldc, k, nullptr,
+                       nullptr, nullptr);
+}
+
+int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, int64_t n,
+                    int64_t p, double alpha, const double* A, int64_t lda, const double* B,
+                    int64_t ldb, double beta, double* C, int64_t ldc, int k,
+                    const ozmm_options_t* opt, ozmm_counts_t* counts, ozmm_timings_t* timings) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return set_err(nullptr, OZMM_ERR_ARG, "null handle");
+  if (m < 1 || n < 1 || p < 1) return set_err(h, OZMM_ERR_ARG, "split: empty matrix");
+  const int64_t arows = is_trans(transa) ? n : m, brows = is_trans(transb) ? p : n;
+  const int64_t acols = is_trans(transa) ? m : n, bcols = is_trans(transb) ? n : p;
+  if (lda < acols || ldb < bcols || ldc < p) return set_err(h, OZMM_ERR_ARG, "leading dimension too small");
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  double *dA = nullptr, *dB = nullptr, *dC = nullptr;
+  auto cleanup = [&] {
+    cudaFree(dA);
+    cudaFree(dB);
+    cudaFree(dC);
+  };
+  if (cudaMalloc(&dA, sizeof(double) * arows * acols) != cudaSuccess ||
+      cudaMalloc(&dB, sizeof(double) * brows * bcols) != cudaSuccess ||
+      cudaMalloc(&dC, sizeof(double) * m * p) != cudaSuccess) {
+    cleanup();
+    return set_err(h, OZMM_ERR_CUDA, "device allocation for host operands failed");
+  }
+  int rc = OZMM_OK;
+  cudaError_t e = cudaMemcpy2DAsync(dA, sizeof(double) * acols, A, sizeof(double) * lda,
+                                    sizeof(double) * acols, arows, cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(dB, sizeof(double) * bcols, B, sizeof(double) * ldb, sizeof(double) * bcols,
+                          brows, cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(dC, sizeof(double) * p, C, sizeof(double) * ldc, sizeof(double) * p, m,
+                          cudaMemcpyHostToDevice, h->stream);
+  if (e != cudaSuccess) rc = set_err(h, OZMM_ERR_CUDA, "H2D copy failed: %s", cudaGetErrorString(e));
+  ozmm_options_t o = opt ? *opt : ozmm_options_t{};
+  o.sync_check = 1;
+  if (rc == OZMM_OK)
+    rc = ozmm_dgemm_ex(handle, transa, transb, m, n, p, alpha, dA, acols, dB, bcols, beta, dC, p, k,
+                       &o, counts, timings);
+  if (rc == OZMM_OK) {
+    e = cudaMemcpy2DAsync(C, sizeof(double) * ldc, dC, sizeof(double) * p, sizeof(double) * p, m,
+                          cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) rc = set_err(h, OZMM_ERR_CUDA, "D2H copy failed: %s", cudaGetErrorString(e));
+  }
+  cleanup();
+  return rc;
+}
+
+}  // extern "C"

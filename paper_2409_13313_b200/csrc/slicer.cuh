@@ -1,0 +1,176 @@
+// K1 -- the slicing kernels (ozIMMU_H round-to-nearest, constant shift).
+//
+// Restates rn_const_shift_rows (proj/src/split.cpp:151-173) with rn_unit
+// (:121-130) and extract_row (:109-117) on the GPU, bit-exactly:
+//   per line (row of op(A) / column of op(B)):  rm = max |x|,
+//     pe0 = ufp_exponent(rm), bump = rm >= (2-2^-beta) 2^pe0, PE = pe0+bump,
+//     shift = 2^PE, unit_s = 2^(PE+1-beta*s);
+//   per element, s = 1..k:  sigma = 0.75*2^53*unit_s,
+//     x = (w + sigma) - sigma, slice_s = int8(x / unit_s), w -= x.
+//
+// Output layout (the GEMM's K-major operand layout): slices[s][line][0..lds),
+// one int8 plane of `lines x lds` bytes per slice, where lds = round_up(n, 16)
+// so every line starts 16-byte aligned for TMA; bytes [n, lds) are written as
+// zeros.  The shift vector is written as doubles (const_shift, split.hpp:37).
+//
+// Two access patterns, both one coalesced read of the FP64 input plus one
+// 16-byte-vector write per slice:
+//   * slice_rows_kernel: lines are contiguous rows (A, or B when transb='T').
+//     One warp per line: pass 1 max-reduces the row with warp shuffles,
+//     pass 2 re-reads it (L2/L1 hit) and emits 16 elements per lane per step.
+//   * colmax_kernel + slice_cols_kernel: lines are strided columns (B, or A
+//     when transa='T').  Pass 1 reduces column maxima (warp-coalesced rows,
+//     smem tree + atomicMax on the IEEE bit pattern, which orders like the
+//     value for |x|).  Pass 2 reads 32-column x 128-row tiles coalesced and
+//     writes each column's 16-byte slice runs: the transposed K-major planes.
+#pragma once
+
+#include <cstdint>
+
+#include "fp64_exact.cuh"
+
+namespace ozb {
+
+constexpr double kSigmaScale = 6755399441055744.0;  // 0.75 * 2^53 (split.cpp:16)
+
+// flags[0] |= underflow (pe < -1000), flags[1] |= range (pe > 920).
+__device__ __forceinline__ void report_flags(int* flags, bool under, bool range) {
+  if (under) atomicOr(flags + 0, 1);
+  if (range) atomicOr(flags + 1, 1);
+}
+
+// Slice 16 consecutive elements of one line (w[] is updated in place) and
+// store the k 16-byte runs.  PE == INT32_MIN marks a zero line.
+__device__ __forceinline__ void emit16(double (&w)[16], int PE, int beta, int k,
+                                       int8_t* dst, int64_t plane) {
+  for (int s = 1; s <= k; ++s) {
+    uint32_t packed[4] = {0u, 0u, 0u, 0u};
+    if (PE != INT32_MIN) {
+      const int ue = PE + 1 - beta * s;
+      const double unit = pow2(ue);
+      if (unit != 0.0) {
+        const double sigma = __dmul_rn(kSigmaScale, unit);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const double x = __dadd_rn(__dadd_rn(w[e], sigma), -sigma);
+          const int8_t q = x86_cast_i8(div_pow2(x, ue));
+          w[e] = __dadd_rn(w[e], -x);
+          packed[e >> 2] |= static_cast<uint32_t>(static_cast<uint8_t>(q)) << (8 * (e & 3));
+        }
+      } else {
+        // unit underflowed to 0: the reference computes x = w, int8(w/0) = 0
+        // (cvttsd2si of +-inf/NaN), w -= x -> 0.
+#pragma unroll
+        for (int e = 0; e < 16; ++e) w[e] = __dadd_rn(w[e], -w[e]);
+      }
+    }
+    *reinterpret_cast<uint4*>(dst + static_cast<int64_t>(s - 1) * plane) =
+        make_uint4(packed[0], packed[1], packed[2], packed[3]);
+  }
+}
+
+// One warp per row.  X: rows x len (row stride ld doubles).
+template <bool kVec>
+__global__ void __launch_bounds__(256) slice_rows_kernel(const double* __restrict__ X, int64_t ld,
+                                                         int64_t rows, int64_t len, int64_t lds,
+                                                         int k, int beta,
+                                                         int8_t* __restrict__ S, int64_t plane,
+                                                         double* __restrict__ shift,
+                                                         int* __restrict__ flags) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+  if (row >= rows) return;
+  const double* x = X + row * ld;
+
+  // pass 1: row max of |x|
+  double rm = 0.0;
+  if (kVec) {
+    const int64_t len2 = len & ~int64_t(1);
+    for (int64_t j = 2 * lane; j < len2; j += 64) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(x + j));
+      rm = fmax(rm, fmax(fabs(v.x), fabs(v.y)));
+    }
+    if ((len & 1) && lane == 0) rm = fmax(rm, fabs(x[len - 1]));
+  } else {
+    for (int64_t j = lane; j < len; j += 32) rm = fmax(rm, fabs(x[j]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) rm = fmax(rm, __shfl_xor_sync(0xffffffffu, rm, o));
+
+  bool under = false, range = false;
+  const int PE = line_pe(rm, beta, &under, &range);
+  if (lane == 0) {
+    shift[row] = PE == INT32_MIN ? 0.0 : pow2(PE);
+    report_flags(flags, under, range);
+  }
+
+  // pass 2: 16 consecutive elements per lane per step
+  int8_t* out = S + row * lds;
+  for (int64_t base = 16 * lane; base < lds; base += 512) {
+    double w[16];
+    if (kVec && base + 16 <= len) {
+#pragma unroll
+      for (int e = 0; e < 16; e += 2) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(x + base + e));
+        w[e] = v.x;
+        w[e + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) w[e] = base + e < len ? x[base + e] : 0.0;
+    }
+    emit16(w, PE, beta, k, out + base, plane);
+  }
+}
+
+// Column maxima of |X| for X: len x cols (row stride ld).  colmax holds the
+// IEEE bit pattern of the max (must be zeroed first).  Block 32 x 8 threads.
+__global__ void __launch_bounds__(256) colmax_kernel(const double* __restrict__ X, int64_t ld,
+                                                     int64_t len, int64_t cols, int64_t rows_per_block,
+                                                     unsigned long long* __restrict__ colmax) {
+  __shared__ double red[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t col = static_cast<int64_t>(blockIdx.x) * 32 + tx;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_block;
+  const int64_t r1 = min(len, r0 + rows_per_block);
+  double m = 0.0;
+  if (col < cols)
+    for (int64_t r = r0 + ty; r < r1; r += 8) m = fmax(m, fabs(__ldg(X + r * ld + col)));
+  red[ty][tx] = m;
+  __syncthreads();
+  if (ty == 0) {
+#pragma unroll
+    for (int q = 1; q < 8; ++q) m = fmax(m, red[q][tx]);
+    if (col < cols && m != 0.0)
+      atomicMax(colmax + col, static_cast<unsigned long long>(__double_as_longlong(m)));
+  }
+}
+
+// Slices of the columns of X (len x cols, row stride ld) written as the rows
+// of the transposed planes S[s][col][0..lds).  Block 32 x 8: thread (tx, ty)
+// owns column c0+tx and the 16 rows n0 + 16*ty .. +16 of a 128-row tile.
+__global__ void __launch_bounds__(256) slice_cols_kernel(const double* __restrict__ X, int64_t ld,
+                                                         int64_t len, int64_t cols, int64_t lds,
+                                                         int k, int beta,
+                                                         const unsigned long long* __restrict__ colmax,
+                                                         int8_t* __restrict__ S, int64_t plane,
+                                                         double* __restrict__ shift,
+                                                         int* __restrict__ flags) {
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t col = static_cast<int64_t>(blockIdx.x) * 32 + tx;
+  const int64_t base = static_cast<int64_t>(blockIdx.y) * 128 + 16 * ty;
+  if (col >= cols || base >= lds) return;
+  const double rm = __longlong_as_double(static_cast<long long>(colmax[col]));
+  bool under = false, range = false;
+  const int PE = line_pe(rm, beta, &under, &range);
+  if (blockIdx.y == 0 && ty == 0) {
+    shift[col] = PE == INT32_MIN ? 0.0 : pow2(PE);
+    report_flags(flags, under, range);
+  }
+  double w[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) w[e] = base + e < len ? __ldg(X + (base + e) * ld + col) : 0.0;
+  emit16(w, PE, beta, k, S + col * lds + base, plane);
+}
+
+}  // namespace ozb
