@@ -1,0 +1,427 @@
+#!/usr/bin/env python
+"""Benchmark: ozIMMU_H emulated DGEMM on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[2], the metric's "n=16384"): C3 = m=n=p=16384,
+k=8 (the reference default, scheme.hpp:25), phi=0.5, alpha=1, beta=0, inputs
+from the reference's phi generator (generate.cpp:11-29) on the host.  At N>1
+the C matrix is 2-D block-sharded (paper_2409_13313_b200/grid2d.py) with NCCL
+all-gathers of slice panels; total work is fixed (strong scaling).
+
+One "step" = one full emulated DGEMM: split A, split B, fused group-wise INT8
+GEMM + FP64 epilogue (+ the slice all-gathers at N>1).
+
+JSON line keys (one line, rank 0):
+  value / ms_per_step -- device-timed, inputs resident in HBM (CUDA events,
+      barrier + synchronize on both sides, max over ranks);
+  e2e -- same metric through the reference-facing host C-ABI call
+      (ozmm_dgemm_host): pinned host A, B, C copied in and C copied out
+      inside the timed region every step;
+  roofline -- the dominant kernel (the fused tcgen05 GEMM): INT8 ops per
+      launch / its CUDA-event duration vs the INT8 peak;
+  cpu_baseline -- the unmodified reference (oracle/_ref) on the host cores,
+      on a bounded sub-block sample of the same problem;
+  cublas_dgemm -- native FP64 DGEMM (torch.matmul -> cuBLAS) on the same
+      device buffers, for context (not on our path).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "emulated DGEMM TFLOPS (2mnp/t) at n=16384 vs cuBLAS DGEMM; max rel err vs phi"
+UNIT = "TFLOPS"
+SPEC_INT8_TOPS = 4500.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--m", type=int, default=16384)
+    ap.add_argument("--n", type=int, default=16384)
+    ap.add_argument("--p", type=int, default=16384)
+    ap.add_argument("--k", type=int, default=8)
+    ap.add_argument("--phi", type=float, default=0.5)
+    ap.add_argument("--tile-n", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cublas", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=1024,
+                    help="rows of A / columns of B in the CPU-baseline sub-block")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d, "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+            "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons, n = [], None, set(), 0
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            n += 1
+            for name, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": 0}
+        load = [s for s in sm if s > 0.3 * (smax or 2000)] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": n}
+
+
+# ------------------------------------------------------------------ reference arm
+def cpu_reference(m_s, n, p_s, k, phi, steps, warmup, threads=None):
+    """The reference CPU implementation (oracle/_ref, else the C port) on a
+    bounded sub-block: rows 0..m_s of A, columns 0..p_s of B of the n=16384
+    problem (sub-block locality: identical per-entry work and results)."""
+    from oracle import oracle as orc  # checker/baseline only (bench cpu leg)
+    lib = orc.best()
+    if threads:
+        lib.set_threads(threads)
+    from paper_2409_13313_b200 import ozmm
+    A = ozmm.gen_phi_block(m_s, n, phi, ozmm.counter_hash(0, 1))
+    B = ozmm.gen_phi_block(n, p_s, phi, ozmm.counter_hash(0, 2))
+    C = np.zeros((m_s, p_s))
+    times = []
+    for it in range(warmup + steps):
+        t0 = time.perf_counter()
+        lib.gemm(1.0, A, B, 0.0, C, k=k)
+        dt = time.perf_counter() - t0
+        if it >= warmup:
+            times.append(dt)
+    t = sum(times) / len(times)
+    return {
+        "value": 2.0 * m_s * n * p_s / t / 1e12,
+        "unit": UNIT,
+        "cores": lib.thread_count(),
+        "kind": lib.kind,
+        "sample": f"ozaki_gemm_ex(ozIMMU_H, k={k}) on the {m_s}x{n} x {n}x{p_s} sub-block "
+                  f"(rows/cols of the m=n=p={n} problem, phi={phi}); {len(times)} timed call(s), "
+                  f"{t:.2f} s each",
+        "seconds_per_call": t,
+    }
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    k = args.k
+    ms = args.cpu_sample
+    # bounded: a few seconds per step on the box's host cores
+    steps, warm = max(1, min(args.steps, 3)), min(args.warmup, 1)
+    cb = cpu_reference(ms, args.n, ms, k, args.phi, steps, warm)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
+        "n_gpus": world, "steps": steps, "warmup": warm,
+        "ms_per_step": cb["seconds_per_call"] * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64 (int8 slices, int32 accum)",
+        "data": "synthetic (reference phi generator)",
+        "config": {"workload": f"C3 m=n=p={args.n}, k={k}, phi={args.phi}, alpha=1, beta=0; "
+                               f"CPU sample = {ms}x{args.n}x{ms} sub-block",
+                   "m": args.m, "n": args.n, "p": args.p, "k": k},
+        "cpu_baseline": {kk: cb[kk] for kk in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference_arm(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2409_13313_b200 import ozmm
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    m, n, p, k, phi = args.m, args.n, args.p, args.k, args.phi
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    seed_a, seed_b, seed_c = (ozmm.counter_hash(0, i) for i in (1, 2, 3))
+    cfg = ozmm.config_for(ozmm.Method.ozIMMU_H, k)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    t_gen = time.perf_counter()
+    if world == 1:
+        hA = torch.from_numpy(ozmm.gen_phi_block(m, n, phi, seed_a)).pin_memory()
+        hB = torch.from_numpy(ozmm.gen_phi_block(n, p, phi, seed_b)).pin_memory()
+        hC = torch.zeros((m, p), dtype=torch.float64).pin_memory()
+        A, B, C = hA.to(dev), hB.to(dev), hC.to(dev)
+        h = ozmm.Handle(local)
+        h.set_stream(stream.cuda_stream)
+        gemm_ms = []
+
+        def step(timed=False):
+            res = ozmm.ozaki_gemm_ex(1.0, A, B, 0.0, C, cfg, handle=h, out=C, timings=timed,
+                                     tile_n=args.tile_n)
+            if timed:
+                gemm_ms.append(res.timings.int_gemm * 1e3)
+            return res
+        launches_per_step = 4  # slice_rows(A), colmax(B), slice_cols(B), fused GEMM
+    else:
+        from paper_2409_13313_b200.grid2d import Backend, Grid2DGemm
+        be = Backend(local)
+        G = Grid2DGemm(m, n, p, k, backend=be)
+        L = G.L
+        hA = torch.from_numpy(ozmm.gen_phi_block(m, n, phi, seed_a, L.a_row0, L.ms, 0, n)).pin_memory()
+        hB = torch.from_numpy(ozmm.gen_phi_block(n, p, phi, seed_b, 0, n, L.b_col0, L.ps)).pin_memory()
+        hC = torch.zeros((L.mr, L.pcols), dtype=torch.float64).pin_memory()
+        A, B, C = hA.to(dev), hB.to(dev), hC.to(dev)
+        gemm_ms = []
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+        def step(timed=False):
+            G.step(A, B, C, 1.0, 0.0)
+
+        launches_per_step = 4
+    t_gen = time.perf_counter() - t_gen
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(timed=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    t_step = max_over_ranks(e0.elapsed_time(e1) / args.steps)  # ms
+    flops = 2.0 * m * n * p
+    value = flops / (t_step * 1e-3) / 1e12
+
+    # dominant kernel time (the fused GEMM) for the roofline
+    if world > 1:
+        torch.cuda.synchronize()
+        for _ in range(2):
+            G.backend.split(A, k, "L", False, G.beta_bits, G.a_loc, G.mu_loc)
+        ev0.record(stream)
+        reps = max(2, min(args.steps, 3))
+        for _ in range(reps):
+            G.backend.gemm(L.mr, L.n, L.pcols, k, G.beta_bits, G.a_pan, G.mu_pan, G.b_pan,
+                           G.nu_pan, 1.0, 0.0, C)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        gemm_ms = [ev0.elapsed_time(ev1) / reps]
+        gm, gp = L.mr, L.pcols
+    else:
+        gm, gp = m, p
+    t_gemm = sum(gemm_ms) / len(gemm_ms)
+    int8_ops = k * (k + 1) / 2 * 2.0 * gm * n * gp
+    pk, pk_src = peaks()
+    int8_peak = 2.0 * pk["bf16_tflops"]
+    achieved = int8_ops / (t_gemm * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "gemm_dram_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tj = json.load(f)
+        if (tj.get("m"), tj.get("n"), tj.get("p"), tj.get("k")) == (gm, n, gp, k):
+            traffic = tj.get("dram_bytes_per_launch")
+
+    # ---- e2e through the host-pointer C ABI (reference calling convention)
+    e2e = None
+    if not args.no_e2e:
+        es = max(1, args.e2e_steps)
+        if world == 1:
+            hout = torch.empty_like(hC).pin_memory()
+            npA, npB, npC, npO = hA.numpy(), hB.numpy(), hC.numpy(), hout.numpy()
+            opt = ozmm.Options()
+            cnt, tim = ozmm.Counts(), ozmm.Timings()
+            import ctypes
+            h.set_stream(None)
+
+            def e2e_call():
+                np.copyto(npO, npC)  # host C -> result buffer (reference returns a new matrix)
+                h.check(ozmm.lib.ozmm_dgemm_host(
+                    h.h, b"N", b"N", m, n, p, 1.0, npA.ctypes.data, n, npB.ctypes.data, p, 0.0,
+                    npO.ctypes.data, p, k, ctypes.byref(opt), ctypes.byref(cnt), None))
+            e2e_call()
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(es):
+                e2e_call()
+            t_e2e = (time.perf_counter() - t0) / es
+            h.set_stream(stream.cuda_stream)
+            h2d = 8 * (m * n + n * p + m * p)
+            d2h = 8 * m * p
+        else:
+            def e2e_call():
+                A.copy_(hA, non_blocking=True)
+                B.copy_(hB, non_blocking=True)
+                C.copy_(hC, non_blocking=True)
+                G.step(A, B, C, 1.0, 0.0)
+                hC.copy_(C, non_blocking=True)
+                torch.cuda.synchronize()
+            e2e_call()
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(es):
+                e2e_call()
+            t_e2e = (time.perf_counter() - t0) / es
+            h2d = 8 * (L.ms * n + n * L.ps + L.mr * L.pcols) * world
+            d2h = 8 * m * p
+        t_e2e = max_over_ranks(t_e2e)
+        e2e = {"value": flops / t_e2e / 1e12, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e * 1e3,
+               "api": "ozmm_dgemm_host (host pointers, pinned)" if world == 1 else
+                      "per-rank pinned H2D of the shard + Grid2DGemm.step + D2H of the C block"}
+
+    # ---- context: native cuBLAS DGEMM on the same device buffers
+    cublas = None
+    if rank == 0 and world == 1 and not args.no_cublas:
+        out = torch.empty_like(C)
+        for _ in range(2):
+            torch.matmul(A, B, out=out)
+        torch.cuda.synchronize()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        for _ in range(3):
+            torch.matmul(A, B, out=out)
+        c1.record(stream)
+        torch.cuda.synchronize()
+        t_cb = c0.elapsed_time(c1) / 3
+        cublas = {"tflops": flops / (t_cb * 1e-3) / 1e12, "ms": t_cb}
+        # INT8 tensor-core context: cuBLASLt s8xs8->s32 GEMM
+        try:
+            a8 = torch.randint(-64, 64, (8192, 8192), dtype=torch.int8, device=dev)
+            b8 = torch.randint(-64, 64, (8192, 8192), dtype=torch.int8, device=dev).t()
+            for _ in range(2):
+                torch._int_mm(a8, b8)
+            torch.cuda.synchronize()
+            c0.record(stream)
+            for _ in range(5):
+                torch._int_mm(a8, b8)
+            c1.record(stream)
+            torch.cuda.synchronize()
+            cublas["int8_cublaslt_tops_8192"] = 2 * 8192 ** 3 / (c0.elapsed_time(c1) / 5e3) / 1e12
+        except Exception as ex:  # context only
+            cublas["int8_cublaslt_error"] = str(ex)[:120]
+        del out
+
+    # ---- CPU baseline (rank 0, N=1): the reference on the host cores
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cb = cpu_reference(args.cpu_sample, n, args.cpu_sample, k, phi, 1, 0)
+            cpu = {kk: cb[kk] for kk in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as ex:
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {ex}"[:200]}
+
+    if rank == 0:
+        pr, pc = (1, 1) if world == 1 else (G.L.pr, G.L.pc)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64 (int8 slices x int8 -> int32 tensor cores, exact f64 epilogue)",
+            "data": "synthetic: reference phi generator (generate.cpp), host-generated",
+            "config": {"workload": f"C3: m=n=p={n} emulated DGEMM, ozIMMU_H k={k} (paper default), "
+                                   f"phi={phi}, alpha=1, beta=0" if (m, n, p) == (16384,) * 3 else
+                                   f"m={m} n={n} p={p} ozIMMU_H k={k} phi={phi}",
+                       "m": m, "n": n, "p": p, "k": k, "phi": phi,
+                       "parallelism": f"grid{pr}x{pc}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (3 x 8*16384^2 B = 6.4 GB vs 126 MB)",
+                       "tile_n": args.tile_n or 64},
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": int8_peak,
+                         "unit": "TFLOP/s", "frac": achieved / int8_peak, "traffic": traffic,
+                         "kernel": "ozimmu_gemm_kernel (tcgen05 kind::i8 + fused FP64 epilogue)",
+                         "algorithmic_ops_per_launch": int8_ops,
+                         "kernel_ms": t_gemm,
+                         "peak_source": f"2 x bf16_tflops ({pk_src}, MEASURED_PEAKS.json): dense "
+                                        "INT8 = 2 x dense BF16 on B200",
+                         "frac_of_spec_4500": achieved / SPEC_INT8_TOPS},
+            "cpu_baseline": cpu,
+            "cublas_dgemm": cublas,
+            "clocks": clk,
+            "host_input_gen_s": t_gen,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

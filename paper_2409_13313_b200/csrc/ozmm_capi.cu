@@ -42,7 +42,13 @@ struct Handle {
   unsigned long long* colmax = nullptr;
   size_t colmax_n = 0;
   int* flags = nullptr;  // [0] underflow, [1] range
-  double* dev_c_scratch = nullptr;
+  // device staging for the host-pointer entry (grown lazily, reused)
+  double* host_a = nullptr;
+  size_t host_a_n = 0;
+  double* host_b = nullptr;
+  size_t host_b_n = 0;
+  double* host_c = nullptr;
+  size_t host_c_n = 0;
   cudaEvent_t ev[5] = {};
   bool gemm_attr_set[3] = {false, false, false};
   int num_sms = 148;
@@ -321,7 +327,9 @@ int ozmm_destroy(ozmm_handle_t handle) {
   cudaFree(h->nu);
   cudaFree(h->colmax);
   cudaFree(h->flags);
-  cudaFree(h->dev_c_scratch);
+  cudaFree(h->host_a);
+  cudaFree(h->host_b);
+  cudaFree(h->host_c);
   for (auto& ev : h->ev) cudaEventDestroy(ev);
   delete h;
   return OZMM_OK;
@@ -367,7 +375,8 @@ int ozmm_sync_status(ozmm_handle_t handle, int* underflow) {
 size_t ozmm_workspace_bytes(ozmm_handle_t handle) {
   Handle* h = reinterpret_cast<Handle*>(handle);
   if (!h) return 0;
-  return h->slices_a_bytes + h->slices_b_bytes + 8 * (h->mu_n + h->nu_n + h->colmax_n);
+  return h->slices_a_bytes + h->slices_b_bytes +
+         8 * (h->mu_n + h->nu_n + h->colmax_n + h->host_a_n + h->host_b_n + h->host_c_n);
 }
 
 int ozmm_compute_beta(int64_t n, int* beta) {
@@ -531,18 +540,10 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   const int64_t acols = is_trans(transa) ? m : n, bcols = is_trans(transb) ? n : p;
   if (lda < acols || ldb < bcols || ldc < p) return set_err(h, OZMM_ERR_ARG, "leading dimension too small");
   CUDA_TRY(h, cudaSetDevice(h->device));
-  double *dA = nullptr, *dB = nullptr, *dC = nullptr;
-  auto cleanup = [&] {
-    cudaFree(dA);
-    cudaFree(dB);
-    cudaFree(dC);
-  };
-  if (cudaMalloc(&dA, sizeof(double) * arows * acols) != cudaSuccess ||
-      cudaMalloc(&dB, sizeof(double) * brows * bcols) != cudaSuccess ||
-      cudaMalloc(&dC, sizeof(double) * m * p) != cudaSuccess) {
-    cleanup();
-    return set_err(h, OZMM_ERR_CUDA, "device allocation for host operands failed");
-  }
+  if (int rc = ensure(h, &h->host_a, &h->host_a_n, static_cast<size_t>(arows) * acols)) return rc;
+  if (int rc = ensure(h, &h->host_b, &h->host_b_n, static_cast<size_t>(brows) * bcols)) return rc;
+  if (int rc = ensure(h, &h->host_c, &h->host_c_n, static_cast<size_t>(m) * p)) return rc;
+  double *dA = h->host_a, *dB = h->host_b, *dC = h->host_c;
   int rc = OZMM_OK;
   cudaError_t e = cudaMemcpy2DAsync(dA, sizeof(double) * acols, A, sizeof(double) * lda,
                                     sizeof(double) * acols, arows, cudaMemcpyHostToDevice, h->stream);
@@ -564,7 +565,6 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) rc = set_err(h, OZMM_ERR_CUDA, "D2H copy failed: %s", cudaGetErrorString(e));
   }
-  cleanup();
   return rc;
 }
 

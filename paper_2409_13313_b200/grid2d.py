@@ -1,0 +1,195 @@
+"""2-D block partition of the ozIMMU_H emulated DGEMM across ranks.
+
+One process per GPU (``torch.distributed``, backend "nccl" on GPUs).  The
+ranks form a Pr x Pc grid; rank (gr, gc) owns the C block (gr, gc) of size
+(m/Pr) x (p/Pc).  The reference is single-process: this
+partition is new, and it is bit-identical to the 1-GPU result because every
+entry of D depends only on its row of op(A) (+ mu_i), its column of op(B)
+(+ nu_j) and n -- the slicer is line-local (proj/src/split.cpp:157-171) and
+the group-wise accumulation is entry-local (proj/src/scheme.cpp:81-101).
+
+Per step each rank:
+  1. slices m/(Pr*Pc) FULL rows of op(A) from its row panel and p/(Pr*Pc)
+     FULL columns of op(B) from its column panel (K1; row maxima are local),
+  2. all-gathers the INT8 slice planes + shift vectors: A planes inside its
+     row communicator (the Pc ranks sharing gr), B planes inside its column
+     communicator (the Pr ranks sharing gc).  No reductions: NCCL only
+     broadcasts slice panels, as the north star asks,
+  3. runs the fused K2+K3 kernel on its C block.
+
+The compute backend is injectable (``Backend``): the default calls the CUDA
+library; tests/test_grid2d_gloo.py drives the same orchestration under gloo
+on CPU with a test-only backend to check the gather/partition logic.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+
+def grid_shape(world: int) -> tuple[int, int]:
+    """Pr x Pc with Pr <= Pc as square as possible: 1x1, 2x1, 2x2, 2x4 ..."""
+    if world == 2:
+        return 2, 1
+    pr = int(math.isqrt(world))
+    while world % pr:
+        pr -= 1
+    return pr, world // pr
+
+
+@dataclass
+class Layout:
+    m: int
+    n: int
+    p: int
+    pr: int
+    pc: int
+    gr: int
+    gc: int
+
+    @property
+    def mr(self):  # rows of the C block / A row panel
+        return self.m // self.pr
+
+    @property
+    def pcols(self):  # cols of the C block / B column panel
+        return self.p // self.pc
+
+    @property
+    def ms(self):  # A rows this rank slices
+        return self.mr // self.pc
+
+    @property
+    def ps(self):  # B cols this rank slices
+        return self.pcols // self.pr
+
+    @property
+    def a_row0(self):  # first global row of op(A) this rank slices
+        return self.gr * self.mr + self.gc * self.ms
+
+    @property
+    def b_col0(self):  # first global column of op(B) this rank slices
+        return self.gc * self.pcols + self.gr * self.ps
+
+    @property
+    def c_row0(self):
+        return self.gr * self.mr
+
+    @property
+    def c_col0(self):
+        return self.gc * self.pcols
+
+
+def make_layout(m: int, n: int, p: int, world: int, rank: int) -> Layout:
+    pr, pc = grid_shape(world)
+    if m % (pr * pc) or p % (pr * pc):
+        raise ValueError(f"m={m}, p={p} must be divisible by Pr*Pc={pr * pc}")
+    return Layout(m, n, p, pr, pc, rank // pc, rank % pc)
+
+
+class Backend:
+    """CUDA backend: K1 / K2+K3 through the C ABI (no CPU fallback)."""
+
+    def __init__(self, device: int):
+        from . import ozmm
+        self.oz = ozmm
+        self.device = torch.device("cuda", device)
+        self.handle = ozmm.Handle(device)
+
+    def empty(self, shape, dtype):
+        return torch.empty(shape, dtype=dtype, device=self.device)
+
+    def split(self, x, k: int, side: str, trans: bool, beta: int, out_slices, out_shift):
+        oz = self.oz
+        rows, cols = x.shape
+        if side == "L":
+            lines, n = (cols, rows) if trans else (rows, cols)
+        else:
+            n, lines = (cols, rows) if trans else (rows, cols)
+        self.handle.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
+        self.handle.check(oz.lib.ozmm_split(
+            self.handle.h, side.encode(), b"T" if trans else b"N", lines, n, x.data_ptr(),
+            x.stride(0), k, beta, out_slices.data_ptr(), out_slices.shape[-1],
+            out_shift.data_ptr()))
+
+    def gemm(self, m, n, p, k, beta_bits, a_slices, mu, b_slices, nu, alpha, beta, c):
+        oz = self.oz
+        self.handle.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
+        opt = oz.Options()
+        self.handle.check(oz.lib.ozmm_gemm_slices(
+            self.handle.h, m, n, p, k, beta_bits, 0, a_slices.data_ptr(), a_slices.shape[-1],
+            mu.data_ptr(), b_slices.data_ptr(), b_slices.shape[-1], nu.data_ptr(), alpha, beta,
+            c.data_ptr(), c.stride(0), ctypes.byref(opt)))
+
+
+class Grid2DGemm:
+    """Sharded emulated DGEMM over a Pr x Pc rank grid.
+
+    Buffers are allocated once; ``step(a_rows, b_cols, c_block)`` runs one
+    emulated GEMM on this rank's shard:
+      a_rows: op(A) rows [a_row0, a_row0 + ms) -- (ms x n), or its transpose
+              (n x ms) when transa;
+      b_cols: op(B) columns [b_col0, b_col0 + ps) -- (n x ps), or (ps x n) when
+              transb;
+      c_block: C block (mr x pcols), overwritten with alpha*D + beta*C.
+    """
+
+    def __init__(self, m, n, p, k, *, world=None, rank=None, backend=None, transa=False,
+                 transb=False, group_factory=None):
+        self.world = world if world is not None else dist.get_world_size()
+        self.rank = rank if rank is not None else dist.get_rank()
+        self.L = make_layout(m, n, p, self.world, self.rank)
+        self.k = k
+        self.transa, self.transb = transa, transb
+        from .ozmm import compute_beta, slice_ld  # closed forms (host)
+        self.beta_bits = compute_beta(n)
+        self.lds = slice_ld(n)
+        self.backend = backend
+        L = self.L
+        # every rank must create every group, in the same order
+        make = group_factory or (lambda ranks: dist.new_group(ranks))
+        self.row_group = self.col_group = None
+        for gr in range(L.pr):
+            ranks = [gr * L.pc + gc for gc in range(L.pc)]
+            g = make(ranks)
+            if gr == L.gr:
+                self.row_group = g
+        for gc in range(L.pc):
+            ranks = [gr * L.pc + gc for gr in range(L.pr)]
+            g = make(ranks)
+            if gc == L.gc:
+                self.col_group = g
+        be = backend
+        self.a_loc = be.empty((k, L.ms, self.lds), torch.int8)
+        self.mu_loc = be.empty((L.ms,), torch.float64)
+        self.b_loc = be.empty((k, L.ps, self.lds), torch.int8)
+        self.nu_loc = be.empty((L.ps,), torch.float64)
+        self.a_pan = be.empty((k, L.mr, self.lds), torch.int8)
+        self.mu_pan = be.empty((L.mr,), torch.float64)
+        self.b_pan = be.empty((k, L.pcols, self.lds), torch.int8)
+        self.nu_pan = be.empty((L.pcols,), torch.float64)
+
+    def _gather(self, out, inp, group, nranks):
+        if nranks == 1:
+            out.copy_(inp)
+        else:
+            dist.all_gather_into_tensor(out, inp, group=group)
+
+    def step(self, a_rows, b_cols, c_block, alpha=1.0, beta=0.0):
+        L, k = self.L, self.k
+        be = self.backend
+        be.split(a_rows, k, "L", self.transa, self.beta_bits, self.a_loc, self.mu_loc)
+        be.split(b_cols, k, "R", self.transb, self.beta_bits, self.b_loc, self.nu_loc)
+        # slice planes in order s = 1..k: group g of the GEMM needs slices <= g-1
+        for s in range(k):
+            self._gather(self.a_pan[s], self.a_loc[s], self.row_group, L.pc)
+            self._gather(self.b_pan[s], self.b_loc[s], self.col_group, L.pr)
+        self._gather(self.mu_pan, self.mu_loc, self.row_group, L.pc)
+        self._gather(self.nu_pan, self.nu_loc, self.col_group, L.pr)
+        be.gemm(L.mr, L.n, L.pcols, k, self.beta_bits, self.a_pan, self.mu_pan, self.b_pan,
+                self.nu_pan, alpha, beta, c_block)
+        return c_block
