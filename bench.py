@@ -288,7 +288,10 @@ def main():
     t_gemm = sum(gemm_ms) / len(gemm_ms)
     int8_ops = k * (k + 1) / 2 * 2.0 * gm * n * gp
     pk, pk_src = peaks()
-    int8_peak = 2.0 * pk["bf16_tflops"]
+    # The GEMM runs back to back inside a ~1 s timed loop at the 1 kW power cap:
+    # the sustained bf16 figure is the matching denominator (dense INT8 = 2x BF16).
+    int8_peak = 2.0 * pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    int8_peak_burst = 2.0 * pk["bf16_tflops"]
     achieved = int8_ops / (t_gemm * 1e-3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "gemm_dram_traffic.json")
@@ -410,8 +413,10 @@ def main():
                          "kernel": "ozimmu_gemm_kernel (tcgen05 kind::i8 + fused FP64 epilogue)",
                          "algorithmic_ops_per_launch": int8_ops,
                          "kernel_ms": t_gemm,
-                         "peak_source": f"2 x bf16_tflops ({pk_src}, MEASURED_PEAKS.json): dense "
-                                        "INT8 = 2 x dense BF16 on B200",
+                         "peak_source": f"2 x bf16_tflops_sustained ({pk_src}, MEASURED_PEAKS.json):"
+                                        " dense INT8 = 2 x dense BF16 on B200; kernel timed inside"
+                                        " a long power-capped loop",
+                         "frac_of_burst": achieved / int8_peak_burst,
                          "frac_of_spec_4500": achieved / SPEC_INT8_TOPS},
             "cpu_baseline": cpu,
             "cublas_dgemm": cublas,

@@ -100,7 +100,10 @@ typedef struct {
                               ozmm_sync_status() */
   int32_t* chunk_dump;     /* nullable device buffer [w][m][p]: the INT32 chunk
                               sums in flush order (debug / parity) */
-  int tile_n;              /* 0 = auto; else 32, 64 or 128 output columns per CTA */
+  int tile_n;              /* 0 = auto; 32/64/128: single-CTA kernel with that many
+                              output columns per CTA (forces cta_pair = 1) */
+  int cta_pair;            /* 0 = auto (CTA-pair kernel, M = 256 x N = 128 per 2-CTA
+                              cluster), 1 = single-CTA kernel, 2 = CTA-pair kernel */
 } ozmm_options_t;
 
 /* ---- handle ------------------------------------------------------------- */

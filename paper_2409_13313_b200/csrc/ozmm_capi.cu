@@ -19,6 +19,7 @@
 
 #include "../../include/ozmm_b200.h"
 #include "ozimmu_gemm.cuh"
+#include "ozimmu_gemm_pair.cuh"
 #include "schedule.hpp"
 #include "slicer.cuh"
 
@@ -51,6 +52,7 @@ struct Handle {
   size_t host_c_n = 0;
   cudaEvent_t ev[5] = {};
   bool gemm_attr_set[3] = {false, false, false};
+  bool pair_attr_set = false;
   int num_sms = 148;
   size_t smem_optin = 232448;
 };
@@ -162,37 +164,17 @@ int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const doubl
 // ---- K2+K3 launch -------------------------------------------------------------
 constexpr size_t kSmemReserve = 2048;  // barriers, tmem slot, alignment slack (+ nu cache)
 
-template <int kBN>
-int launch_gemm_bn(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_bits, int64_t r,
-                   const int8_t* As, int64_t lds_a, const double* mu, const int8_t* Bs,
-                   int64_t lds_b, const double* nu, double alpha, double beta, const double* Cin,
-                   double* Cout, int64_t ldc, int32_t* dump) {
-  using Cfg = ozb::GemmCfg<kBN>;
-  const size_t budget = h->smem_optin - kSmemReserve - kBN * sizeof(double);
-  const int64_t max_stage = static_cast<int64_t>(budget / 3);
-  auto slot_bytes = [](int a, int b) {
-    return static_cast<int64_t>(a) * Cfg::kATile + static_cast<int64_t>(b) * Cfg::kBTile;
-  };
-  const ozb::Schedule S = ozb::make_schedule(k, r, Cfg::kNAcc, max_stage, slot_bytes);
-  if (S.batches.size() > static_cast<size_t>(ozb::kMaxBatches) ||
-      S.passes.size() > static_cast<size_t>(ozb::kMaxPasses) ||
-      S.products.size() > static_cast<size_t>(ozb::kMaxProducts) ||
-      S.chunks.size() > static_cast<size_t>(ozb::kMaxChunks))
-    return set_err(h, OZMM_ERR_UNSUPPORTED, "schedule too large (k=%d, r=%lld)", k,
-                   static_cast<long long>(r));
-  const size_t stage_bytes = slot_bytes(S.a_slots, S.b_slots);
-  const int stages = static_cast<int>(std::min<size_t>(8, budget / stage_bytes));
-  if (stages < 2)
-    return set_err(h, OZMM_ERR_UNSUPPORTED, "pipeline stage (%zu B) exceeds smem budget",
-                   stage_bytes);
-
-  ozb::GemmParams P;  // ~3 KB, passed by value as __grid_constant__
+// Fills the kernel parameter block from the host schedule.
+void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t p, int64_t lds_a,
+                 int64_t lds_b, int tiles_m, int tiles_n, int beta_bits, int stages, double alpha,
+                 double beta, const double* mu, const double* nu, const double* Cin, double* Cout,
+                 int64_t ldc, int32_t* dump) {
   std::memset(&P, 0, sizeof P);
   P.m = static_cast<int>(m);
   P.p = static_cast<int>(p);
   P.n_kb = static_cast<int>((std::max(lds_a, lds_b) + ozb::kBK - 1) / ozb::kBK);
-  P.tiles_m = static_cast<int>((m + ozb::kBM - 1) / ozb::kBM);
-  P.tiles_n = static_cast<int>((p + kBN - 1) / kBN);
+  P.tiles_m = tiles_m;
+  P.tiles_n = tiles_n;
   P.group_m = 16;
   P.nbatch = static_cast<int>(S.batches.size());
   P.npass = static_cast<int>(S.passes.size());
@@ -229,11 +211,44 @@ int launch_gemm_bn(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_b
     P.pr_t[i] = static_cast<uint8_t>(S.products[i].t);
   }
   for (size_t c = 0; c < S.chunks.size(); ++c) P.c_g[c] = static_cast<uint8_t>(S.chunks[c].g);
+}
 
+bool schedule_fits(const ozb::Schedule& S) {
+  return S.batches.size() <= static_cast<size_t>(ozb::kMaxBatches) &&
+         S.passes.size() <= static_cast<size_t>(ozb::kMaxPasses) &&
+         S.products.size() <= static_cast<size_t>(ozb::kMaxProducts) &&
+         S.chunks.size() <= static_cast<size_t>(ozb::kMaxChunks);
+}
+
+// Single-CTA kernel: 128 x kBN tile per CTA.
+template <int kBN>
+int launch_gemm_bn(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_bits, int64_t r,
+                   const int8_t* As, int64_t lds_a, const double* mu, const int8_t* Bs,
+                   int64_t lds_b, const double* nu, double alpha, double beta, const double* Cin,
+                   double* Cout, int64_t ldc, int32_t* dump) {
+  using Cfg = ozb::GemmCfg<kBN>;
+  const size_t budget = h->smem_optin - kSmemReserve - kBN * sizeof(double);
+  const int64_t max_stage = static_cast<int64_t>(budget / 3);
+  auto slot_bytes = [](int a, int b) {
+    return static_cast<int64_t>(a) * Cfg::kATile + static_cast<int64_t>(b) * Cfg::kBTile;
+  };
+  const ozb::Schedule S = ozb::make_schedule(k, r, Cfg::kNAcc, max_stage, slot_bytes);
+  if (!schedule_fits(S))
+    return set_err(h, OZMM_ERR_UNSUPPORTED, "schedule too large (k=%d, r=%lld)", k,
+                   static_cast<long long>(r));
+  const size_t stage_bytes = slot_bytes(S.a_slots, S.b_slots);
+  const int stages = static_cast<int>(std::min<size_t>(8, budget / stage_bytes));
+  if (stages < 2)
+    return set_err(h, OZMM_ERR_UNSUPPORTED, "pipeline stage (%zu B) exceeds smem budget",
+                   stage_bytes);
+  ozb::GemmParams P;  // ~3 KB, passed by value as __grid_constant__
+  const int tiles_m = static_cast<int>((m + ozb::kBM - 1) / ozb::kBM);
+  const int tiles_n = static_cast<int>((p + kBN - 1) / kBN);
+  fill_params(P, S, m, p, lds_a, lds_b, tiles_m, tiles_n, beta_bits, stages, alpha, beta, mu, nu,
+              Cin, Cout, ldc, dump);
   CUtensorMap map_a, map_b;
   if (int rc = make_slice_map(h, &map_a, As, lds_a, m, k, ozb::kBM)) return rc;
   if (int rc = make_slice_map(h, &map_b, Bs, lds_b, p, k, kBN)) return rc;
-
   const size_t smem = stages * stage_bytes + kSmemReserve + kBN * sizeof(double);
   const int bn_idx = kBN == 32 ? 0 : (kBN == 64 ? 1 : 2);
   if (!h->gemm_attr_set[bn_idx]) {
@@ -242,8 +257,50 @@ int launch_gemm_bn(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_b
                                      static_cast<int>(h->smem_optin)));
     h->gemm_attr_set[bn_idx] = true;
   }
-  const dim3 grid(static_cast<unsigned>(P.tiles_m * P.tiles_n));
+  const dim3 grid(static_cast<unsigned>(tiles_m * tiles_n));
   ozb::ozimmu_gemm_kernel<kBN><<<grid, ozb::kGemmThreads, smem, h->stream>>>(map_a, map_b, P);
+  CUDA_TRY(h, cudaGetLastError());
+  return OZMM_OK;
+}
+
+// CTA-pair kernel: 256 x kBN tile per 2-CTA cluster (cta_group::2).
+template <int kBN>
+int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_bits, int64_t r,
+                     const int8_t* As, int64_t lds_a, const double* mu, const int8_t* Bs,
+                     int64_t lds_b, const double* nu, double alpha, double beta,
+                     const double* Cin, double* Cout, int64_t ldc, int32_t* dump) {
+  using Cfg = ozb::PairCfg<kBN>;
+  const size_t budget = h->smem_optin - kSmemReserve - kBN * sizeof(double);
+  const int64_t max_stage = static_cast<int64_t>(budget / 3);
+  auto slot_bytes = [](int a, int b) {
+    return static_cast<int64_t>(a) * Cfg::kATile + static_cast<int64_t>(b) * Cfg::kBTile;
+  };
+  const ozb::Schedule S = ozb::make_schedule(k, r, Cfg::kNAcc, max_stage, slot_bytes);
+  if (!schedule_fits(S))
+    return set_err(h, OZMM_ERR_UNSUPPORTED, "schedule too large (k=%d, r=%lld)", k,
+                   static_cast<long long>(r));
+  const size_t stage_bytes = slot_bytes(S.a_slots, S.b_slots);
+  const int stages = static_cast<int>(std::min<size_t>(8, budget / stage_bytes));
+  if (stages < 2)
+    return set_err(h, OZMM_ERR_UNSUPPORTED, "pipeline stage (%zu B) exceeds smem budget",
+                   stage_bytes);
+  ozb::GemmParams P;
+  const int tiles_m = static_cast<int>((m + 2 * ozb::kBM - 1) / (2 * ozb::kBM));
+  const int tiles_n = static_cast<int>((p + kBN - 1) / kBN);
+  fill_params(P, S, m, p, lds_a, lds_b, tiles_m, tiles_n, beta_bits, stages, alpha, beta, mu, nu,
+              Cin, Cout, ldc, dump);
+  CUtensorMap map_a, map_b;
+  if (int rc = make_slice_map(h, &map_a, As, lds_a, m, k, ozb::kBM)) return rc;
+  if (int rc = make_slice_map(h, &map_b, Bs, lds_b, p, k, Cfg::kBHalf)) return rc;
+  const size_t smem = stages * stage_bytes + kSmemReserve + kBN * sizeof(double);
+  if (!h->pair_attr_set) {
+    CUDA_TRY(h, cudaFuncSetAttribute(ozb::ozimmu_gemm_pair_kernel<kBN>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(h->smem_optin)));
+    h->pair_attr_set = true;
+  }
+  const dim3 grid(static_cast<unsigned>(2 * tiles_m * tiles_n));
+  ozb::ozimmu_gemm_pair_kernel<kBN><<<grid, ozb::kPairThreads, smem, h->stream>>>(map_a, map_b, P);
   CUDA_TRY(h, cudaGetLastError());
   return OZMM_OK;
 }
@@ -253,8 +310,12 @@ int launch_gemm(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_bits
                 const double* nu, double alpha, double beta, const double* Cin, double* Cout,
                 int64_t ldc, const ozmm_options_t* opt) {
   int32_t* dump = opt ? opt->chunk_dump : nullptr;
-  const int tile_n = opt && opt->tile_n ? opt->tile_n : 64;
-  switch (tile_n) {
+  const int tile_n = opt ? opt->tile_n : 0;
+  const int pair = opt ? opt->cta_pair : 0;
+  if (pair == 2 || (pair == 0 && tile_n == 0))
+    return launch_gemm_pair<128>(h, m, n, p, k, beta_bits, r, As, lds_a, mu, Bs, lds_b, nu, alpha,
+                                 beta, Cin, Cout, ldc, dump);
+  switch (tile_n ? tile_n : 64) {
     case 32:
       return launch_gemm_bn<32>(h, m, n, p, k, beta_bits, r, As, lds_a, mu, Bs, lds_b, nu, alpha,
                                 beta, Cin, Cout, ldc, dump);

@@ -67,7 +67,8 @@ class Timings(C.Structure):
 
 class Options(C.Structure):
     _fields_ = [("force_beta", C.c_int), ("force_r", C.c_int64), ("timings", C.c_int),
-                ("sync_check", C.c_int), ("chunk_dump", C.c_void_p), ("tile_n", C.c_int)]
+                ("sync_check", C.c_int), ("chunk_dump", C.c_void_p), ("tile_n", C.c_int),
+                ("cta_pair", C.c_int)]
 
 
 _SIG = {
@@ -291,7 +292,7 @@ def _is_cuda_tensor(x) -> bool:
 
 
 def _options(cfg: SchemeConfig | None, timings: bool = False, dump=None, tile_n: int = 0,
-             sync_check: bool = False) -> Options:
+             sync_check: bool = False, cta_pair: int = 0) -> Options:
     o = Options()
     if cfg is not None:
         o.force_beta = cfg.force_beta
@@ -300,6 +301,7 @@ def _options(cfg: SchemeConfig | None, timings: bool = False, dump=None, tile_n:
     o.sync_check = int(sync_check)
     o.chunk_dump = dump.data_ptr() if dump is not None else None
     o.tile_n = tile_n
+    o.cta_pair = cta_pair
     return o
 
 
