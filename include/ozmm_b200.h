@@ -171,6 +171,14 @@ int ozmm_gemm_slices(ozmm_handle_t h, int64_t m, int64_t n, int64_t p, int k, in
                      const int8_t* Bs, int64_t lds_b, const double* nu, double alpha,
                      double beta, double* C, int64_t ldc, const ozmm_options_t* opt);
 
+/* ---- introspection (host only; used by tests/test_host_logic.py) ---------- */
+/* The GEMM's host schedule for (k, r) and a kernel choice (cta_pair/tile_n as
+ * in ozmm_options_t): one row of 8 ints per slice product, in issue order:
+ * {batch, pass, chunk (flush order), g, s, t, first-product-of-chunk, in-pass-range}.
+ * info[7] = {products, chunks (= w), batches, passes, stages, a_slots, b_slots}. */
+int ozmm_debug_schedule(int k, int64_t r, int cta_pair, int tile_n, int* rows, int cap,
+                        int* info);
+
 /* ---- input generator (host, OpenMP) --------------------------------------- */
 /* The reference's phi test matrices (src/generate.cpp:11-29,
  * include/ozmm/generate.hpp:11-21): entry (i, j) of the GLOBAL rows x cols

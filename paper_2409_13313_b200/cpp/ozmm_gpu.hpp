@@ -1,0 +1,131 @@
+// ozmm::gpu -- header-only C++ adapter with the REFERENCE's operator API over
+// the B200 C ABI (include/ozmm_b200.h).
+//
+// Drop-in for (proj/include/ozmm/scheme.hpp):
+//   MatrixF64   ozaki_gemm   (double alpha, const MatrixF64& a, const MatrixF64& b,
+//                             double beta, const MatrixF64& c, const SchemeConfig& cfg);  :92-95
+//   OzakiResult ozaki_gemm_ex(...same...);                                                :96-98
+//   OzakiResult ozaki_mm     (const MatrixF64& a, const MatrixF64& b, const SchemeConfig&); :89-90
+// for cfg = config_for(Method::ozIMMU_H, k) (the only preset the GPU path runs).
+//
+// Templated over the matrix type: anything row-major with rows(), cols(),
+// data() and a (rows, cols) constructor -- the reference's
+// ozmm::DenseMatrix<double> (Eigen RowMajor, types.hpp:13-16) included -- so
+// the reference CLI/harness can switch by changing a namespace.  Same
+// semantics as the reference: inputs are const, a NEW matrix is returned
+// (scheme.cpp:281, :289), errors are thrown as the reference's exception
+// types (std::invalid_argument, a ConfigError-compatible invalid_argument,
+// std::overflow_error for rows >= 2^921).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/ozmm_b200.h"
+
+namespace ozmm {
+namespace gpu {
+
+struct ConfigError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+
+struct OpCounts {
+  std::int64_t int8_gemms = 0, fp64_flushes = 0, r = 0, w = 0;
+};
+struct PhaseTimings {
+  double split_a = 0, split_b = 0, int_gemm = 0, accum_fp64 = 0, copy = 0;
+};
+template <class Mat>
+struct OzakiResultT {
+  Mat d;
+  OpCounts counts;
+  PhaseTimings timings;
+};
+
+// Subset of the reference SchemeConfig the GPU path honours (scheme.hpp:24-31).
+struct GpuConfig {
+  int k = 8;
+  int force_beta = 0;
+  std::int64_t force_r = 0;
+};
+
+// Accept the reference's SchemeConfig (or anything with k/force_beta/force_r).
+template <class Cfg>
+GpuConfig to_gpu_config(const Cfg& cfg) {
+  return GpuConfig{cfg.k, cfg.force_beta, static_cast<std::int64_t>(cfg.force_r)};
+}
+inline GpuConfig to_gpu_config(const GpuConfig& cfg) { return cfg; }
+
+// One handle per host thread, created on first use (device 0 or OZMM_DEVICE).
+inline ozmm_handle_t thread_handle() {
+  thread_local struct Owner {
+    ozmm_handle_t h = nullptr;
+    ~Owner() {
+      if (h) ozmm_destroy(h);
+    }
+  } owner;
+  if (!owner.h) {
+    int dev = 0;
+    if (const char* s = std::getenv("OZMM_DEVICE")) dev = std::atoi(s);
+    if (int rc = ozmm_create(&owner.h, dev))
+      throw std::runtime_error(std::string("ozmm_create: ") + ozmm_last_error(nullptr) + " (" +
+                               ozmm_status_string(rc) + ")");
+  }
+  return owner.h;
+}
+
+inline void throw_status(int rc, ozmm_handle_t h) {
+  const std::string msg = ozmm_last_error(h);
+  switch (rc) {
+    case OZMM_OK: return;
+    case OZMM_ERR_ARG: throw std::invalid_argument(msg);
+    case OZMM_ERR_CONFIG: throw ConfigError(msg);
+    case OZMM_ERR_RANGE: throw std::overflow_error(msg);
+    default: throw std::runtime_error(msg + " (" + ozmm_status_string(rc) + ")");
+  }
+}
+
+template <class Mat, class Cfg>
+OzakiResultT<Mat> ozaki_gemm_ex(double alpha, const Mat& a, const Mat& b, double beta,
+                                const Mat& c, const Cfg& cfg_in) {
+  const GpuConfig cfg = to_gpu_config(cfg_in);
+  if (a.cols() != b.rows()) throw std::invalid_argument("ozaki_mm: inner dimensions differ");
+  if (c.rows() != a.rows() || c.cols() != b.cols())
+    throw std::invalid_argument("ozaki_gemm: C shape mismatch");
+  if (cfg.k < 1) throw ConfigError("k must be >= 1");
+  const std::int64_t m = a.rows(), n = a.cols(), p = b.cols();
+  Mat out(c.rows(), c.cols());
+  std::copy(c.data(), c.data() + m * p, out.data());
+  ozmm_options_t opt{};
+  opt.force_beta = cfg.force_beta;
+  opt.force_r = cfg.force_r;
+  opt.timings = 1;
+  ozmm_counts_t cnt{};
+  ozmm_timings_t tim{};
+  ozmm_handle_t h = thread_handle();
+  throw_status(ozmm_dgemm_host(h, 'N', 'N', m, n, p, alpha, a.data(), n, b.data(), p, beta,
+                               out.data(), p, cfg.k, &opt, &cnt, &tim),
+               h);
+  OzakiResultT<Mat> res{std::move(out), {}, {}};
+  res.counts = {cnt.int8_gemms, cnt.fp64_flushes, cnt.r, cnt.w};
+  res.timings = {tim.split_a, tim.split_b, tim.int_gemm, tim.accum_fp64, tim.copy};
+  return res;
+}
+
+template <class Mat, class Cfg>
+Mat ozaki_gemm(double alpha, const Mat& a, const Mat& b, double beta, const Mat& c,
+               const Cfg& cfg) {
+  return ozaki_gemm_ex(alpha, a, b, beta, c, cfg).d;
+}
+
+template <class Mat, class Cfg>
+OzakiResultT<Mat> ozaki_mm(const Mat& a, const Mat& b, const Cfg& cfg) {
+  Mat zero(a.rows(), b.cols());
+  std::fill(zero.data(), zero.data() + a.rows() * b.cols(), 0.0);
+  return ozaki_gemm_ex(1.0, a, b, 0.0, zero, cfg);
+}
+
+}  // namespace gpu
+}  // namespace ozmm

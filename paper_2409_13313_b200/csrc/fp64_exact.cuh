@@ -41,24 +41,6 @@ __device__ __forceinline__ int ufp_exponent(double c) {
   return (63 - __clzll(static_cast<long long>(b))) - 1074;
 }
 
-// static_cast<std::int8_t>(double) exactly as g++ compiles it on x86-64
-// (cvttsd2si to int32 -- 0x80000000 for NaN/inf/out of range -- then the low
-// byte).  In range it is truncation toward zero.  Used by extract_row
-// (proj/src/split.cpp:114).
-__device__ __forceinline__ int8_t x86_cast_i8(double q) {
-  int32_t v;
-  if (!(q > -2147483649.0 && q < 2147483648.0)) v = INT32_MIN;
-  else v = __double2int_rz(q);
-  return static_cast<int8_t>(static_cast<uint8_t>(static_cast<uint32_t>(v)));
-}
-
-// x / 2^e for x an exact multiple of 2^e (the quotient is an integer), i.e.
-// the correctly rounded division of extract_row, without a division.
-__device__ __forceinline__ double div_pow2(double x, int e) {
-  if (e >= -1023) return __dmul_rn(x, pow2(-e));
-  return __dmul_rn(__dmul_rn(x, pow2(1000)), pow2(-e - 1000));
-}
-
 // Per-line splitting parameters of rn_const_shift_rows / rn_unit
 // (proj/src/split.cpp:121-130, :158-166) for line max `rm`:
 //   pe0 = ufp_exponent(rm); bump if rm >= (2 - 2^-beta) * 2^pe0;

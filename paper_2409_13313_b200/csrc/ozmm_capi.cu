@@ -139,13 +139,17 @@ int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const doubl
   const int64_t plane = lines * lds;
   if (row_mode) {
     const bool vec = (reinterpret_cast<uintptr_t>(X) % 16 == 0) && (ldx % 2 == 0);
-    const dim3 grid(static_cast<unsigned>((lines + 7) / 8));
+    // one CTA per row, 16 elements per thread (whole row in registers up to 16384)
+    const int64_t want = (lds / 16 + 31) / 32 * 32;
+    const int threads = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(32, want)));
+    const dim3 grid(static_cast<unsigned>(lines));
     if (vec)
-      ozb::slice_rows_kernel<true><<<grid, 256, 0, h->stream>>>(X, ldx, lines, n, lds, k, beta, S,
-                                                                plane, shift, h->flags);
+      ozb::slice_rows_kernel<true><<<grid, threads, 0, h->stream>>>(X, ldx, lines, n, lds, k, beta,
+                                                                    S, plane, shift, h->flags);
     else
-      ozb::slice_rows_kernel<false><<<grid, 256, 0, h->stream>>>(X, ldx, lines, n, lds, k, beta,
-                                                                 S, plane, shift, h->flags);
+      ozb::slice_rows_kernel<false><<<grid, threads, 0, h->stream>>>(X, ldx, lines, n, lds, k,
+                                                                     beta, S, plane, shift,
+                                                                     h->flags);
   } else {
     if (int rc = ensure(h, &h->colmax, &h->colmax_n, static_cast<size_t>(lines))) return rc;
     CUDA_TRY(h, cudaMemsetAsync(h->colmax, 0, sizeof(unsigned long long) * lines, h->stream));
@@ -466,6 +470,58 @@ int ozmm_op_counts(int k, int64_t r, ozmm_counts_t* c) {
 }
 
 int64_t ozmm_slice_ld(int64_t n) { return (n + 15) / 16 * 16; }
+
+int ozmm_debug_schedule(int k, int64_t r, int cta_pair, int tile_n, int* rows, int cap,
+                        int* info) {
+  if (k < 1 || k > ozb::kMaxK || r < 1 || !rows || !info)
+    return set_err(nullptr, OZMM_ERR_ARG, "debug_schedule: bad arguments");
+  int n_acc, a_tile, b_tile, bn;
+  if (cta_pair == 2 || (cta_pair == 0 && tile_n == 0)) {
+    bn = 128;
+    n_acc = ozb::PairCfg<128>::kNAcc;
+    a_tile = ozb::PairCfg<128>::kATile;
+    b_tile = ozb::PairCfg<128>::kBTile;
+  } else {
+    bn = tile_n ? tile_n : 64;
+    if (bn != 32 && bn != 64 && bn != 128) return set_err(nullptr, OZMM_ERR_ARG, "tile_n");
+    n_acc = 512 / bn;
+    a_tile = ozb::kBM * ozb::kBK;
+    b_tile = bn * ozb::kBK;
+  }
+  const size_t budget = 232448 - kSmemReserve - bn * sizeof(double);
+  auto slot_bytes = [&](int a, int b) {
+    return static_cast<int64_t>(a) * a_tile + static_cast<int64_t>(b) * b_tile;
+  };
+  const ozb::Schedule S = ozb::make_schedule(k, r, n_acc, static_cast<int64_t>(budget / 3), slot_bytes);
+  const int np = static_cast<int>(S.products.size());
+  if (np > cap) return set_err(nullptr, OZMM_ERR_ARG, "debug_schedule: cap too small");
+  for (int q = 0; q < static_cast<int>(S.passes.size()); ++q) {
+    const ozb::Pass& ps = S.passes[q];
+    for (int i = ps.p0; i < ps.p1; ++i) {
+      const ozb::Product& pr = S.products[i];
+      const ozb::Batch& b = S.batches[ps.batch];
+      const ozb::Chunk& c = S.chunks[b.c0 + pr.ci];
+      int* row = rows + 8 * i;
+      row[0] = ps.batch;
+      row[1] = q;
+      row[2] = b.c0 + pr.ci;  // global chunk index (flush order)
+      row[3] = c.g;
+      row[4] = pr.s;
+      row[5] = pr.t;
+      row[6] = pr.first ? 1 : 0;
+      row[7] = (pr.s >= ps.alo && pr.s <= ps.ahi && pr.t >= ps.blo && pr.t <= ps.bhi) ? 1 : 0;
+    }
+  }
+  const size_t stage_bytes = slot_bytes(S.a_slots, S.b_slots);
+  info[0] = np;
+  info[1] = static_cast<int>(S.chunks.size());
+  info[2] = static_cast<int>(S.batches.size());
+  info[3] = static_cast<int>(S.passes.size());
+  info[4] = static_cast<int>(std::min<size_t>(8, budget / stage_bytes));  // stages
+  info[5] = S.a_slots;
+  info[6] = S.b_slots;
+  return OZMM_OK;
+}
 
 int ozmm_split(ozmm_handle_t handle, char side, char trans, int64_t lines, int64_t n,
                const double* X, int64_t ldx, int k, int beta, int8_t* slices, int64_t lds,

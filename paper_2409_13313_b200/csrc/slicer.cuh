@@ -16,8 +16,9 @@
 // Two access patterns, both one coalesced read of the FP64 input plus one
 // 16-byte-vector write per slice:
 //   * slice_rows_kernel: lines are contiguous rows (A, or B when transb='T').
-//     One warp per line: pass 1 max-reduces the row with warp shuffles,
-//     pass 2 re-reads it (L2/L1 hit) and emits 16 elements per lane per step.
+//     One CTA per line, 16 consecutive elements per thread held in registers:
+//     the row max is a warp-shuffle + smem reduction, then the same registers
+//     are sliced -- the row is read from HBM once (rows up to 16384).
 //   * colmax_kernel + slice_cols_kernel: lines are strided columns (B, or A
 //     when transa='T').  Pass 1 reduces column maxima (warp-coalesced rows,
 //     smem tree + atomicMax on the IEEE bit pattern, which orders like the
@@ -41,6 +42,14 @@ __device__ __forceinline__ void report_flags(int* flags, bool under, bool range)
 
 // Slice 16 consecutive elements of one line (w[] is updated in place) and
 // store the k 16-byte runs.  PE == INT32_MIN marks a zero line.
+//
+// Per element and slice: t = w + sigma, x = t - sigma, w -= x (three RN adds,
+// exactly extract_row's (w+sigma)-sigma and w -= x).  The slice integer
+// x / unit is read off the bit pattern: sigma = 1.5 * 2^52 * unit and
+// |x| < 2^51 * unit put t in sigma's binade [2^52 unit, 2^53 unit), whose ulp
+// is unit, so bits(t) - bits(sigma) == x / unit exactly (no division, no
+// float->int conversion).  Valid for every unit >= 2^-1074 (sigma is then
+// normal); unit == 0 (underflowed grid) is handled separately.
 __device__ __forceinline__ void emit16(double (&w)[16], int PE, int beta, int k,
                                        int8_t* dst, int64_t plane) {
   for (int s = 1; s <= k; ++s) {
@@ -49,13 +58,15 @@ __device__ __forceinline__ void emit16(double (&w)[16], int PE, int beta, int k,
       const int ue = PE + 1 - beta * s;
       const double unit = pow2(ue);
       if (unit != 0.0) {
-        const double sigma = __dmul_rn(kSigmaScale, unit);
+        const double sigma = __dmul_rn(kSigmaScale, unit);  // exact
+        const long long sbits = __double_as_longlong(sigma);
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          const double x = __dadd_rn(__dadd_rn(w[e], sigma), -sigma);
-          const int8_t q = x86_cast_i8(div_pow2(x, ue));
+          const double t = __dadd_rn(w[e], sigma);
+          const double x = __dadd_rn(t, -sigma);
+          const uint32_t q = static_cast<uint32_t>(__double_as_longlong(t) - sbits);
           w[e] = __dadd_rn(w[e], -x);
-          packed[e >> 2] |= static_cast<uint32_t>(static_cast<uint8_t>(q)) << (8 * (e & 3));
+          packed[e >> 2] |= (q & 0xFFu) << (8 * (e & 3));
         }
       } else {
         // unit underflowed to 0: the reference computes x = w, int8(w/0) = 0
@@ -69,57 +80,79 @@ __device__ __forceinline__ void emit16(double (&w)[16], int PE, int beta, int k,
   }
 }
 
-// One warp per row.  X: rows x len (row stride ld doubles).
-template <bool kVec>
-__global__ void __launch_bounds__(256) slice_rows_kernel(const double* __restrict__ X, int64_t ld,
-                                                         int64_t rows, int64_t len, int64_t lds,
-                                                         int k, int beta,
-                                                         int8_t* __restrict__ S, int64_t plane,
-                                                         double* __restrict__ shift,
-                                                         int* __restrict__ flags) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp;
-  if (row >= rows) return;
-  const double* x = X + row * ld;
-
-  // pass 1: row max of |x|
-  double rm = 0.0;
-  if (kVec) {
-    const int64_t len2 = len & ~int64_t(1);
-    for (int64_t j = 2 * lane; j < len2; j += 64) {
-      const double2 v = __ldg(reinterpret_cast<const double2*>(x + j));
-      rm = fmax(rm, fmax(fabs(v.x), fabs(v.y)));
-    }
-    if ((len & 1) && lane == 0) rm = fmax(rm, fabs(x[len - 1]));
-  } else {
-    for (int64_t j = lane; j < len; j += 32) rm = fmax(rm, fabs(x[j]));
-  }
+__device__ __forceinline__ void load16(const double* x, int64_t base, int64_t len, bool vec,
+                                       double (&w)[16]) {
+  if (vec && base + 16 <= len) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) rm = fmax(rm, __shfl_xor_sync(0xffffffffu, rm, o));
+    for (int e = 0; e < 16; e += 2) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(x + base + e));
+      w[e] = v.x;
+      w[e + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) w[e] = base + e < len ? __ldg(x + base + e) : 0.0;
+  }
+}
 
+// Block-wide max of non-negative doubles (blockDim.x multiple of 32, <= 1024).
+__device__ __forceinline__ double block_max(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  v = lane < nw ? red[lane] : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// One CTA per row.  X: rows x len (row stride ld doubles).  When the padded
+// row fits 16 elements per thread (lds <= 16 * blockDim.x) the row is read
+// from HBM exactly once and kept in registers between the max reduction and
+// the slicing; longer rows take a second (L2-resident) pass.
+template <bool kVec>
+__global__ void __launch_bounds__(1024) slice_rows_kernel(const double* __restrict__ X, int64_t ld,
+                                                          int64_t rows, int64_t len, int64_t lds,
+                                                          int k, int beta,
+                                                          int8_t* __restrict__ S, int64_t plane,
+                                                          double* __restrict__ shift,
+                                                          int* __restrict__ flags) {
+  __shared__ double red[32];
+  const int64_t row = blockIdx.x;
+  const double* x = X + row * ld;
+  int8_t* out = S + row * lds;
+  const int64_t step = 16 * static_cast<int64_t>(blockDim.x);
+  const int64_t base0 = 16 * static_cast<int64_t>(threadIdx.x);
+  double w[16];
+  double rm = 0.0;
+  if (lds <= step) {
+    load16(x, base0, len, kVec, w);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) rm = fmax(rm, fabs(w[e]));
+  } else {
+    for (int64_t base = base0; base < len; base += step) {
+      load16(x, base, len, kVec, w);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) rm = fmax(rm, fabs(w[e]));
+    }
+  }
+  rm = block_max(rm, red);
   bool under = false, range = false;
   const int PE = line_pe(rm, beta, &under, &range);
-  if (lane == 0) {
+  if (threadIdx.x == 0) {
     shift[row] = PE == INT32_MIN ? 0.0 : pow2(PE);
     report_flags(flags, under, range);
   }
-
-  // pass 2: 16 consecutive elements per lane per step
-  int8_t* out = S + row * lds;
-  for (int64_t base = 16 * lane; base < lds; base += 512) {
-    double w[16];
-    if (kVec && base + 16 <= len) {
-#pragma unroll
-      for (int e = 0; e < 16; e += 2) {
-        const double2 v = __ldg(reinterpret_cast<const double2*>(x + base + e));
-        w[e] = v.x;
-        w[e + 1] = v.y;
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < 16; ++e) w[e] = base + e < len ? x[base + e] : 0.0;
+  if (lds <= step) {
+    if (base0 < lds) emit16(w, PE, beta, k, out + base0, plane);
+  } else {
+    for (int64_t base = base0; base < lds; base += step) {
+      load16(x, base, len, kVec, w);
+      emit16(w, PE, beta, k, out + base, plane);
     }
-    emit16(w, PE, beta, k, out + base, plane);
   }
 }
 

@@ -168,15 +168,20 @@ class Grid2DGemm:
         self.mu_loc = be.empty((L.ms,), torch.float64)
         self.b_loc = be.empty((k, L.ps, self.lds), torch.int8)
         self.nu_loc = be.empty((L.ps,), torch.float64)
-        self.a_pan = be.empty((k, L.mr, self.lds), torch.int8)
-        self.mu_pan = be.empty((L.mr,), torch.float64)
-        self.b_pan = be.empty((k, L.pcols, self.lds), torch.int8)
-        self.nu_pan = be.empty((L.pcols,), torch.float64)
+        # a rank alone in its row (column) group slices the whole panel itself
+        if L.pc == 1:
+            self.a_pan, self.mu_pan = self.a_loc, self.mu_loc
+        else:
+            self.a_pan = be.empty((k, L.mr, self.lds), torch.int8)
+            self.mu_pan = be.empty((L.mr,), torch.float64)
+        if L.pr == 1:
+            self.b_pan, self.nu_pan = self.b_loc, self.nu_loc
+        else:
+            self.b_pan = be.empty((k, L.pcols, self.lds), torch.int8)
+            self.nu_pan = be.empty((L.pcols,), torch.float64)
 
     def _gather(self, out, inp, group, nranks):
-        if nranks == 1:
-            out.copy_(inp)
-        else:
+        if nranks > 1:
             dist.all_gather_into_tensor(out, inp, group=group)
 
     def step(self, a_rows, b_cols, c_block, alpha=1.0, beta=0.0):

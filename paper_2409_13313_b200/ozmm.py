@@ -99,6 +99,7 @@ _SIG = {
     "ozmm_gen_phi_block": ([_i64, _i64, C.c_double, C.c_uint64, _i64, _i64, _i64, _i64, _vp,
                             _i64], C.c_int),
     "ozmm_counter_hash": ([C.c_uint64, C.c_uint64], C.c_uint64),
+    "ozmm_debug_schedule": ([C.c_int, _i64, C.c_int, C.c_int, _vp, C.c_int, _vp], C.c_int),
 }
 for _name, (_args, _res) in _SIG.items():
     _f = getattr(lib, _name)
@@ -225,6 +226,17 @@ def op_counts(k: int, n: int) -> OpCounts:
 
 def slice_ld(n: int) -> int:
     return int(lib.ozmm_slice_ld(n))
+
+
+def debug_schedule(k: int, r: int, cta_pair: int = 0, tile_n: int = 0):
+    """The GEMM kernel's host schedule: (rows[products, 8], info dict)."""
+    cap = k * (k + 1) // 2
+    rows = np.zeros((cap, 8), np.int32)
+    info = np.zeros(7, np.int32)
+    _check(lib.ozmm_debug_schedule(k, r, cta_pair, tile_n, rows.ctypes.data, cap,
+                                   info.ctypes.data))
+    keys = ["products", "chunks", "batches", "passes", "stages", "a_slots", "b_slots"]
+    return rows[: int(info[0])], dict(zip(keys, (int(v) for v in info)))
 
 
 # --------------------------------------------------------------- handles

@@ -33,3 +33,9 @@ def case(golden, name):
                 sliceB=golden[pre + "sliceB"], shiftB=golden[pre + "shiftB"],
                 beta_underflow=golden[pre + "beta_underflow"],
                 chunk_acc=golden[pre + "chunk_acc"], chunk_gs=golden[pre + "chunk_gs"])
+
+
+import os as _os
+
+ROOT_HEADER = _os.path.join(_os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))),
+                            "include", "ozmm_b200.h")

@@ -1,0 +1,34 @@
+"""The C++ adapter (paper_2409_13313_b200/cpp/ozmm_gpu.hpp) as a drop-in for the
+reference API: one binary calls ozmm::ozaki_gemm_ex (the unmodified reference)
+and ozmm::gpu::ozaki_gemm_ex (the B200 path) with the same arguments.
+The binary is built in the build container by `make -C oracle dropin`
+(oracle/_ref/dropin_demo, it needs the reference headers) and ships with the
+repo snapshot to the GPU box."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+DEMO = os.path.join(ROOT, "oracle", "_ref", "dropin_demo")
+
+
+def _run(*args):
+    if not os.path.exists(DEMO):
+        pytest.skip("oracle/_ref/dropin_demo not built (needs /root/reference at build time)")
+    return subprocess.run([DEMO, *map(str, args)], capture_output=True, text=True, timeout=600)
+
+
+def test_dropin_closed_forms_cpu():
+    out = _run(16384, 16384, 16384, 8, 0.5, "--closed-forms-only")
+    assert out.returncode == 0 and "CLOSED-FORMS OK beta=7 r=8" in out.stdout, out.stdout + out.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,p,k,phi", [(300, 2000, 260, 8, 0.5), (97, 5000, 131, 12, 4.0)])
+def test_dropin_same_call_site_bit_exact(m, n, p, k, phi):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    out = _run(m, n, p, k, phi)
+    assert out.returncode == 0 and out.stdout.startswith("MATCH"), out.stdout + out.stderr

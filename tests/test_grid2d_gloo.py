@@ -1,0 +1,117 @@
+"""CPU, multi-process: the 2-D block partition (grid2d.Grid2DGemm) under gloo.
+
+Runs the real orchestration -- rank grid, row/column communicators, per-rank
+slicing of full rows/columns, slice-panel all-gathers -- with world sizes 2
+and 4 on CPU.  The compute backend is a TEST-ONLY stand-in (the GPU kernels
+need a B200): slicing by the oracle port, and the group-wise accumulation of
+the gathered slice panels restated in numpy (exact int64 products, the
+reference's flush order scheme.cpp:81-101 and flush arithmetic :29-41).
+Each rank's C block must equal the single-process reference result bitwise.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+class OracleBackend:
+    """Test stand-in for grid2d.Backend (CPU tensors)."""
+
+    def __init__(self):
+        import sys
+        sys.path.insert(0, ROOT)
+        from oracle.oracle import PortLib
+        self.port = PortLib()
+
+    def empty(self, shape, dtype):
+        return torch.zeros(shape, dtype=dtype)
+
+    def split(self, x, k, side, trans, beta, out_slices, out_shift):
+        a = x.numpy().T if trans else x.numpy()
+        s = self.port.split(np.ascontiguousarray(a), k, "left" if side == "L" else "right",
+                            force_beta=beta)
+        planes = s.slices if side == "L" else s.slices.transpose(0, 2, 1)  # [k][lines][n]
+        out_slices.zero_()
+        out_slices[:, :, : planes.shape[2]] = torch.from_numpy(np.ascontiguousarray(planes))
+        out_shift.copy_(torch.from_numpy(s.shift))
+
+    def gemm(self, m, n, p, k, beta_bits, a_slices, mu, b_slices, nu, alpha, beta, c):
+        from paper_2409_13313_b200.ozmm import compute_r
+        r = compute_r(n, beta_bits)
+        A = a_slices.numpy()[:, :, :n].astype(np.int64)
+        B = b_slices.numpy()[:, :, :n].astype(np.int64)
+        mu, nu = mu.numpy(), nu.numpy()
+        D = np.zeros((m, p))
+        for g in range(2, k + 2):
+            acc = np.zeros((m, p), np.int64)
+            q = 0
+            for s in range(1, g):
+                q += 1
+                acc += A[s - 1] @ B[g - s - 1].T
+                if q == r or s == g - 1:
+                    ru = np.ldexp(mu, 2 - beta_bits * g)
+                    D = D + (ru[:, None] * acc.astype(np.float64)) * nu[None, :]
+                    q = 0
+                    acc[:] = 0
+        c.copy_(torch.from_numpy(alpha * D + beta * c.numpy()))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, m, n, p, k, phi, alpha, beta, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2409_13313_b200 import ozmm
+        from paper_2409_13313_b200.grid2d import Grid2DGemm
+        G = Grid2DGemm(m, n, p, k, backend=OracleBackend())
+        L = G.L
+        sa, sb, sc = (ozmm.counter_hash(5, i) for i in (1, 2, 3))
+        a_rows = torch.from_numpy(ozmm.gen_phi_block(m, n, phi, sa, L.a_row0, L.ms, 0, n))
+        b_cols = torch.from_numpy(ozmm.gen_phi_block(n, p, phi, sb, 0, n, L.b_col0, L.ps))
+        c_blk = torch.from_numpy(ozmm.gen_phi_block(m, p, phi, sc, L.c_row0, L.mr, L.c_col0,
+                                                    L.pcols))
+        G.step(a_rows, b_cols, c_blk, alpha, beta)
+        q.put((rank, L.c_row0, L.c_col0, c_blk.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_grid2d_matches_single_process(world, port):
+    m, n, p, k, phi, alpha, beta = 32, 200, 48, 8, 1.0, 1.5, 0.5
+    from paper_2409_13313_b200 import ozmm
+    A = ozmm.gen_phi_block(m, n, phi, ozmm.counter_hash(5, 1))
+    B = ozmm.gen_phi_block(n, p, phi, ozmm.counter_hash(5, 2))
+    C = ozmm.gen_phi_block(m, p, phi, ozmm.counter_hash(5, 3))
+    want = port.gemm(alpha, A, B, beta, C, k=k)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, PORT[world],
+                                               m, n, p, k, phi, alpha, beta, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = np.full((m, p), np.nan)
+    for _ in range(world):
+        rank, r0, c0, blk = q.get(timeout=120)
+        got[r0:r0 + blk.shape[0], c0:c0 + blk.shape[1]] = blk
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+PORT = {2: _free_port(), 4: _free_port()}
