@@ -43,6 +43,7 @@ constexpr int kMaxChunks = 256;    // >= k(k+1)/2 for k <= kMaxK
 constexpr int kMaxProducts = 256;  // k(k+1)/2 for k <= kMaxK
 constexpr int kMaxBatches = 128;
 constexpr int kMaxPasses = 192;
+constexpr int kMaxAGroups = 256;
 constexpr int kGemmThreads = 320;
 constexpr int kEpiWarps = 8;
 
@@ -56,6 +57,7 @@ struct GemmParams {
   int stages;          // smem pipeline depth
   int a_slots, b_slots;  // slice tiles per stage (max over passes)
   int n_chunks;
+  int hint_a, hint_b;  // L2 policies of the A / B slice loads (0 normal, 1 evict_first, 2 evict_last)
   double alpha, beta_c;
   const double* mu;    // [m] row shifts of op(A)
   const double* nu;    // [p] column shifts of op(B)
@@ -72,6 +74,11 @@ struct GemmParams {
   uint8_t pr_ci[kMaxProducts], pr_s[kMaxProducts], pr_t[kMaxProducts];
   // per chunk in flush order: group g
   uint8_t c_g[kMaxChunks];
+  // CTA-pair kernel: per pass the A-slice groups [p_g0, p_g1); per group the
+  // A slice and its product range (products are sorted by A slice in a pass)
+  uint16_t p_g0[kMaxPasses], p_g1[kMaxPasses];
+  uint8_t ag_s[kMaxAGroups];
+  uint16_t ag_p0[kMaxAGroups], ag_p1[kMaxAGroups];
 };
 
 template <int kBN>

@@ -1,21 +1,29 @@
-// K2+K3, CTA-pair variant: the same fused ozIMMU_H GEMM as ozimmu_gemm.cuh,
-// computed by a 2-CTA cluster with tcgen05 cta_group::2 (UMMA M = 256).
+// K2+K3, CTA-pair variant: the fused ozIMMU_H GEMM computed by a 2-CTA
+// cluster with tcgen05 cta_group::2 (UMMA M = 256, N = kBN).
 //
-// Why: with M = 128 x N = 64 per CTA the tensor core's shared-memory operand
-// fetch (A 128x32 B + B 64x32 B per 32-cycle MMA) saturates before the INT8
-// datapath (ncu: sm__pipe_tc_cycles_active 83 % at 45 % tensor utilisation,
-// profiles/r1/gemm_v1_bn64_*).  In a CTA pair each SM still owns 128 rows of
-// the output, but the B operand is split N/2 + N/2 across the two SMs and a
-// 256 x kBN x 32 MMA takes kBN/2 cycles: per SM 4 KB + kBN*16 B of operand
-// reads per kBN/2 cycles (96 B/cycle at kBN = 128 instead of 192).
+// Why a pair: with M = 128 x N = 64 per CTA the tensor core's shared-memory
+// operand fetch (A 128x32 B + B 64x32 B per 32-cycle MMA) saturates before the
+// INT8 datapath (ncu: sm__pipe_tc_cycles_active 83 % at 45 % tensor
+// utilisation, profiles/r1/gemm_v1_bn64_*).  In a CTA pair each SM owns 128
+// rows of the output but the B operand is split N/2 + N/2 across the two SMs:
+// per SM 4 KB + kBN*16 B of operand reads per kBN/2-cycle MMA.
+//
+// Pipeline (per CTA; K advances in 128-byte blocks, 128-byte swizzle):
+//   * B buffers (2): for the current K block every B slice of the pass
+//     (kBN/2 rows x 128 B each), resident while all of the block's MMAs run;
+//   * A ring (kARing stages): one A slice tile (128 rows x 128 B) per stage,
+//     streamed in pass order; when A_s lands the MMA thread issues every
+//     product of the pass that uses A_s (4 MMAs of K = 32 each) into its
+//     chunk accumulator.
+// One TMA box per 128-byte row keeps the TMA request count 4x below a
+// 32-byte-row design (ncu: l1tex2xbar request cycles were 87 % busy there).
 //
 // Roles per CTA (384 threads): warp 0 = TMA producer (both CTAs load their own
-// A rows and their half of the B rows; the bytes are counted on the LEADER's
-// full barrier), warp 1 = TMEM allocator (both) + MMA issuer (leader only),
+// A rows and their half of the B rows; bytes are counted on the LEADER's
+// barriers), warp 1 = TMEM allocator (both) + MMA issuer (leader only),
 // warps 4..11 = epilogue (each CTA drains its own TMEM: its 128 rows x kBN
 // columns, 64 columns per warp).  Commits multicast to both CTAs' barriers;
-// the epilogues of both CTAs release the accumulators on the leader's
-// tmem_empty barrier.
+// both CTAs' epilogues release the accumulators on the leader's tmem_empty.
 #pragma once
 
 #include "ozimmu_gemm.cuh"
@@ -24,13 +32,17 @@ namespace ozb {
 
 constexpr int kPairThreads = 384;
 constexpr int kPairEpiWarps = 8;  // per CTA
+constexpr int kKB = 128;          // bytes of K per block (= one 128B swizzle row)
+constexpr int kBBufs = 2;
 
 template <int kBN>
 struct PairCfg {
   static constexpr int kNAcc = 512 / kBN;
   static constexpr int kBHalf = kBN / 2;                  // B rows loaded per CTA
-  static constexpr uint32_t kATile = kBM * kBK;           // 4 KB
-  static constexpr uint32_t kBTile = kBHalf * kBK;        // bytes per CTA per B slice
+  static constexpr uint32_t kATile = kBM * kKB;           // 16 KB
+  static constexpr uint32_t kBTile = kBHalf * kKB;        // bytes per CTA per B slice
+  static constexpr int kMaxBSlots = 8;                    // B slices resident per K block
+  static constexpr uint32_t kBBuf = kMaxBSlots * kBTile;  // one B buffer
   static constexpr uint32_t kIdesc = ptx::idesc_i8(2 * kBM, kBN);
 };
 
@@ -43,11 +55,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t a_bytes = P.a_slots * Cfg::kATile;
-  const uint32_t stage_bytes = a_bytes + P.b_slots * Cfg::kBTile;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + P.stages * stage_bytes);
-  uint64_t* empty = full + P.stages;
-  uint64_t* tmem_full = empty + P.stages;
+  const int n_a = P.stages;  // A ring depth
+  uint8_t* bbuf = smem;
+  uint8_t* aring = smem + kBBufs * Cfg::kBBuf;
+  uint64_t* b_full = reinterpret_cast<uint64_t*>(aring + n_a * Cfg::kATile);
+  uint64_t* b_empty = b_full + kBBufs;
+  uint64_t* a_full = b_empty + kBBufs;
+  uint64_t* a_empty = a_full + n_a;
+  uint64_t* tmem_full = a_empty + n_a;
   uint64_t* tmem_empty = tmem_full + 1;
   uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tmem_empty + 1);
   double* nu_s = reinterpret_cast<double*>(tmem_base_smem + 4);
@@ -65,13 +80,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   const int tm = first_m + (bid % per_group) % gm;  // pair row-block (256 rows)
   const int tn = (bid % per_group) / gm;
   const int row_base = tm * 2 * kBM + static_cast<int>(rank) * kBM;
+  const int n_kb = P.n_kb;  // 128-byte K blocks
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&map_a);
     ptx::tma_prefetch_desc(&map_b);
-    for (int s = 0; s < P.stages; ++s) {
-      ptx::mbar_init(full + s, 1);
-      ptx::mbar_init(empty + s, 1);
+    for (int s = 0; s < kBBufs; ++s) {
+      ptx::mbar_init(b_full + s, 1);
+      ptx::mbar_init(b_empty + s, 1);
+    }
+    for (int s = 0; s < n_a; ++s) {
+      ptx::mbar_init(a_full + s, 1);
+      ptx::mbar_init(a_empty + s, 1);
     }
     ptx::mbar_init(tmem_full, 1);
     ptx::mbar_init(tmem_empty, 2 * kPairEpiWarps);
@@ -90,26 +110,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
     if (ptx::elect_one()) {
-      int stage = 0;
-      uint32_t phase = 0;
+      int bi = 0, ai = 0;
+      uint32_t bph = 0, aph = 0;
+      const int b_row = tn * kBN + static_cast<int>(rank) * Cfg::kBHalf;
+      const uint64_t pol_a = ptx::l2_policy(P.hint_a), pol_b = ptx::l2_policy(P.hint_b);
       for (int q = 0; q < P.npass; ++q) {
-        const int alo = P.p_alo[q], ahi = P.p_ahi[q], blo = P.p_blo[q], bhi = P.p_bhi[q];
-        const uint32_t tx =
-            2u * ((ahi - alo + 1) * Cfg::kATile + (bhi - blo + 1) * Cfg::kBTile);
-        for (int kb = 0; kb < P.n_kb; ++kb) {
-          ptx::mbar_wait(empty + stage, phase ^ 1);
-          uint8_t* st = smem + stage * stage_bytes;
-          const uint32_t fb = ptx::mapa_shared(full + stage, 0);
-          if (leader) ptx::mbar_arrive_expect_tx(full + stage, tx);
-          for (int s = alo; s <= ahi; ++s)
-            ptx::tma_load_3d_pair(st + (s - alo) * Cfg::kATile, &map_a, fb, kb * kBK, row_base,
-                                  s - 1);
-          for (int t = blo; t <= bhi; ++t)
-            ptx::tma_load_3d_pair(st + a_bytes + (t - blo) * Cfg::kBTile, &map_b, fb, kb * kBK,
-                                  tn * kBN + static_cast<int>(rank) * Cfg::kBHalf, t - 1);
-          if (++stage == P.stages) {
-            stage = 0;
-            phase ^= 1;
+        const int blo = P.p_blo[q], bhi = P.p_bhi[q], g0 = P.p_g0[q], g1 = P.p_g1[q];
+        const uint32_t btx = 2u * (bhi - blo + 1) * Cfg::kBTile;
+        for (int kb = 0; kb < n_kb; ++kb) {
+          ptx::mbar_wait(b_empty + bi, bph ^ 1);
+          {
+            const uint32_t fb = ptx::mapa_shared(b_full + bi, 0);
+            if (leader) ptx::mbar_arrive_expect_tx(b_full + bi, btx);
+            uint8_t* dst = bbuf + bi * Cfg::kBBuf;
+            for (int t = blo; t <= bhi; ++t)
+              ptx::tma_load_3d_pair_hint(dst + (t - blo) * Cfg::kBTile, &map_b, fb, kb * kKB,
+                                         b_row, t - 1, pol_b);
+          }
+          if (++bi == kBBufs) {
+            bi = 0;
+            bph ^= 1;
+          }
+          for (int g = g0; g < g1; ++g) {
+            ptx::mbar_wait(a_empty + ai, aph ^ 1);
+            const uint32_t fa = ptx::mapa_shared(a_full + ai, 0);
+            if (leader) ptx::mbar_arrive_expect_tx(a_full + ai, 2u * Cfg::kATile);
+            ptx::tma_load_3d_pair_hint(aring + ai * Cfg::kATile, &map_a, fa, kb * kKB, row_base,
+                                       P.ag_s[g] - 1, pol_a);
+            if (++ai == n_a) {
+              ai = 0;
+              aph ^= 1;
+            }
           }
         }
       }
@@ -117,34 +148,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------- MMA issuer (leader CTA)
     if (leader) {
-      int stage = 0;
-      uint32_t phase = 0;
+      int bi = 0, ai = 0;
+      uint32_t bph = 0, aph = 0;
       for (int b = 0; b < P.nbatch; ++b) {
         ptx::mbar_wait(tmem_empty, (b & 1) ^ 1);
         ptx::tc_fence_after();
         for (int q = P.b_pass0[b]; q < P.b_pass1[b]; ++q) {
-          const int alo = P.p_alo[q], blo = P.p_blo[q], p0 = P.p_p0[q], p1 = P.p_p1[q];
-          for (int kb = 0; kb < P.n_kb; ++kb) {
-            ptx::mbar_wait(full + stage, phase);
+          const int blo = P.p_blo[q], g0 = P.p_g0[q], g1 = P.p_g1[q];
+          for (int kb = 0; kb < n_kb; ++kb) {
+            ptx::mbar_wait(b_full + bi, bph);
             ptx::tc_fence_after();
-            if (ptx::elect_one()) {
-              const uint32_t sa = ptx::smem_u32(smem + stage * stage_bytes);
-              const uint32_t sb = sa + a_bytes;
-              for (int pr = p0; pr < p1; ++pr) {
-                const uint32_t ci = P.pr_ci[pr];
-                const uint64_t adesc =
-                    ptx::smem_desc(sa + (P.pr_s[pr] - alo) * Cfg::kATile, 256, 6);
-                const uint64_t bdesc =
-                    ptx::smem_desc(sb + (P.pr_t[pr] - blo) * Cfg::kBTile, 256, 6);
-                const uint32_t acc = (kb > 0 || !(ci & 0x80u)) ? 1u : 0u;
-                ptx::mma_i8_pair(tmem_base + (ci & 0x7Fu) * kBN, adesc, bdesc, Cfg::kIdesc, acc);
+            const uint32_t sb = ptx::smem_u32(bbuf + bi * Cfg::kBBuf);
+            for (int g = g0; g < g1; ++g) {
+              ptx::mbar_wait(a_full + ai, aph);
+              ptx::tc_fence_after();
+              if (ptx::elect_one()) {
+                const uint64_t adesc = ptx::smem_desc(ptx::smem_u32(aring + ai * Cfg::kATile), 1024, 2);
+                for (int pr = P.ag_p0[g]; pr < P.ag_p1[g]; ++pr) {
+                  const uint32_t ci = P.pr_ci[pr];
+                  const uint64_t bdesc =
+                      ptx::smem_desc(sb + (P.pr_t[pr] - blo) * Cfg::kBTile, 1024, 2);
+                  const uint32_t d = tmem_base + (ci & 0x7Fu) * kBN;
+                  const bool first = kb == 0 && (ci & 0x80u);
+#pragma unroll
+                  for (int j = 0; j < kKB / kBK; ++j)  // K = 32 per MMA: +32 B = +2 in desc.lo
+                    ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, Cfg::kIdesc,
+                                     (first && j == 0) ? 0u : 1u);
+                }
+                ptx::mma_commit_pair(a_empty + ai, 0x3);  // A stage free in both CTAs
               }
-              ptx::mma_commit_pair(empty + stage, 0x3);  // free this stage in both CTAs
+              __syncwarp();
+              if (++ai == n_a) {
+                ai = 0;
+                aph ^= 1;
+              }
             }
+            if (ptx::elect_one()) ptx::mma_commit_pair(b_empty + bi, 0x3);
             __syncwarp();
-            if (++stage == P.stages) {
-              stage = 0;
-              phase ^= 1;
+            if (++bi == kBBufs) {
+              bi = 0;
+              bph ^= 1;
             }
           }
         }
@@ -155,7 +198,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   } else if (warp >= 4) {
     // --------------------------------------------------------- epilogue
     const int quarter = warp & 3;          // TMEM lane quarter
-    const int cslice = (warp - 4) >> 2;    // 0/1: which 64-column half
+    const int cslice = (warp - 4) >> 2;    // 0/1: which column half
     constexpr int kCols = kBN / 2;         // columns per epilogue warp
     constexpr int kLd = 16;
     const int row = row_base + quarter * 32 + lane;

@@ -117,18 +117,19 @@ EncodeFn encode_fn() {
 // 3-D int8 map over slice planes [k][lines][lds]: box = 32 B of K x rows x 1 slice,
 // 32-byte swizzle (matches the UMMA descriptors built in the kernel).
 int make_slice_map(Handle* h, CUtensorMap* map, const int8_t* base, int64_t lds, int64_t lines,
-                   int64_t plane, int k, uint32_t box_rows) {
+                   int64_t plane, int k, uint32_t box_rows, uint32_t box_k = ozb::kBK,
+                   CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_32B) {
   EncodeFn fn = encode_fn();
   if (!fn) return set_err(h, OZMM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(lds), static_cast<cuuint64_t>(lines),
                               static_cast<cuuint64_t>(k)};
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>(lds),
                                  static_cast<cuuint64_t>(plane)};
-  const cuuint32_t box[3] = {static_cast<cuuint32_t>(ozb::kBK), box_rows, 1};
+  const cuuint32_t box[3] = {box_k, box_rows, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims,
-                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_err(h, OZMM_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", r);
   return OZMM_OK;
@@ -183,8 +184,12 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
   P.n_kb = static_cast<int>((std::max(lds_a, lds_b) + ozb::kBK - 1) / ozb::kBK);
   P.tiles_m = tiles_m;
   P.tiles_n = tiles_n;
-  P.group_m = 4;  // tile-row group of the raster (measured: 4 minimises DRAM re-reads)
+  P.group_m = 2;  // tile-row group of the raster (measured sweep, tools/l2_sweep.sh)
   if (const char* g = std::getenv("OZMM_GROUP_M")) P.group_m = std::max(1, std::atoi(g));
+  P.hint_a = 2;  // A panels are reused by every column tile of the group: keep them in L2
+  P.hint_b = 0;
+  if (const char* g = std::getenv("OZMM_HINT_A")) P.hint_a = std::atoi(g);
+  if (const char* g = std::getenv("OZMM_HINT_B")) P.hint_b = std::atoi(g);
   P.nbatch = static_cast<int>(S.batches.size());
   P.npass = static_cast<int>(S.passes.size());
   P.beta = beta_bits;
@@ -220,13 +225,23 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
     P.pr_t[i] = static_cast<uint8_t>(S.products[i].t);
   }
   for (size_t c = 0; c < S.chunks.size(); ++c) P.c_g[c] = static_cast<uint8_t>(S.chunks[c].g);
+  for (size_t q = 0; q < S.passes.size(); ++q) {
+    P.p_g0[q] = static_cast<uint16_t>(S.passes[q].g0);
+    P.p_g1[q] = static_cast<uint16_t>(S.passes[q].g1);
+  }
+  for (size_t g = 0; g < S.agroups.size(); ++g) {
+    P.ag_s[g] = static_cast<uint8_t>(S.agroups[g].s);
+    P.ag_p0[g] = static_cast<uint16_t>(S.agroups[g].p0);
+    P.ag_p1[g] = static_cast<uint16_t>(S.agroups[g].p1);
+  }
 }
 
 bool schedule_fits(const ozb::Schedule& S) {
   return S.batches.size() <= static_cast<size_t>(ozb::kMaxBatches) &&
          S.passes.size() <= static_cast<size_t>(ozb::kMaxPasses) &&
          S.products.size() <= static_cast<size_t>(ozb::kMaxProducts) &&
-         S.chunks.size() <= static_cast<size_t>(ozb::kMaxChunks);
+         S.chunks.size() <= static_cast<size_t>(ozb::kMaxChunks) &&
+         S.agroups.size() <= static_cast<size_t>(ozb::kMaxAGroups);
 }
 
 // Single-CTA kernel: 128 x kBN tile per CTA.
@@ -280,28 +295,32 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
                      const double* Cin, double* Cout, int64_t ldc, int32_t* dump) {
   using Cfg = ozb::PairCfg<kBN>;
   const size_t budget = h->smem_optin - kSmemReserve - kBN * sizeof(double);
-  const int64_t max_stage = static_cast<int64_t>(budget / 3);
-  auto slot_bytes = [](int a, int b) {
-    return static_cast<int64_t>(a) * Cfg::kATile + static_cast<int64_t>(b) * Cfg::kBTile;
-  };
-  const ozb::Schedule S = ozb::make_schedule(k, r, Cfg::kNAcc, max_stage, slot_bytes);
+  // passes are limited by the resident B slices per K block (A slices stream)
+  auto slot_bytes = [](int, int b) { return static_cast<int64_t>(b) * Cfg::kBTile; };
+  const ozb::Schedule S = ozb::make_schedule(k, r, Cfg::kNAcc,
+                                             static_cast<int64_t>(Cfg::kMaxBSlots) * Cfg::kBTile,
+                                             slot_bytes);
   if (!schedule_fits(S))
     return set_err(h, OZMM_ERR_UNSUPPORTED, "schedule too large (k=%d, r=%lld)", k,
                    static_cast<long long>(r));
-  const size_t stage_bytes = slot_bytes(S.a_slots, S.b_slots);
-  const int stages = static_cast<int>(std::min<size_t>(8, budget / stage_bytes));
+  const size_t fixed = ozb::kBBufs * Cfg::kBBuf;
+  const int stages = static_cast<int>(std::min<size_t>(8, (budget - fixed) / Cfg::kATile));
   if (stages < 2)
-    return set_err(h, OZMM_ERR_UNSUPPORTED, "pipeline stage (%zu B) exceeds smem budget",
-                   stage_bytes);
+    return set_err(h, OZMM_ERR_UNSUPPORTED, "A ring does not fit shared memory");
   ozb::GemmParams P;
   const int tiles_m = static_cast<int>((m + 2 * ozb::kBM - 1) / (2 * ozb::kBM));
   const int tiles_n = static_cast<int>((p + kBN - 1) / kBN);
   fill_params(P, S, m, p, lds_a, lds_b, tiles_m, tiles_n, beta_bits, stages, alpha, beta, mu, nu,
               Cin, Cout, ldc, dump);
+  P.n_kb = static_cast<int>((std::max(lds_a, lds_b) + ozb::kKB - 1) / ozb::kKB);
   CUtensorMap map_a, map_b;
-  if (int rc = make_slice_map(h, &map_a, As, lds_a, m, plane_a, k, ozb::kBM)) return rc;
-  if (int rc = make_slice_map(h, &map_b, Bs, lds_b, p, plane_b, k, Cfg::kBHalf)) return rc;
-  const size_t smem = stages * stage_bytes + kSmemReserve + kBN * sizeof(double);
+  if (int rc = make_slice_map(h, &map_a, As, lds_a, m, plane_a, k, ozb::kBM, ozb::kKB,
+                              CU_TENSOR_MAP_SWIZZLE_128B))
+    return rc;
+  if (int rc = make_slice_map(h, &map_b, Bs, lds_b, p, plane_b, k, Cfg::kBHalf, ozb::kKB,
+                              CU_TENSOR_MAP_SWIZZLE_128B))
+    return rc;
+  const size_t smem = fixed + stages * Cfg::kATile + kSmemReserve + kBN * sizeof(double);
   if (!h->pair_attr_set) {
     CUDA_TRY(h, cudaFuncSetAttribute(ozb::ozimmu_gemm_pair_kernel<kBN>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -488,7 +507,7 @@ int ozmm_debug_schedule(int k, int64_t r, int cta_pair, int tile_n, int* rows, i
     bn = 128;
     n_acc = ozb::PairCfg<128>::kNAcc;
     a_tile = ozb::PairCfg<128>::kATile;
-    b_tile = ozb::PairCfg<128>::kBTile;
+    b_tile = ozb::PairCfg<128>::kBTile;  // per CTA, 128-byte K block
   } else {
     bn = tile_n ? tile_n : 64;
     if (bn != 32 && bn != 64 && bn != 128) return set_err(nullptr, OZMM_ERR_ARG, "tile_n");
@@ -497,10 +516,14 @@ int ozmm_debug_schedule(int k, int64_t r, int cta_pair, int tile_n, int* rows, i
     b_tile = bn * ozb::kBK;
   }
   const size_t budget = 232448 - kSmemReserve - bn * sizeof(double);
+  const bool pair_kernel = cta_pair == 2 || (cta_pair == 0 && tile_n == 0);
   auto slot_bytes = [&](int a, int b) {
-    return static_cast<int64_t>(a) * a_tile + static_cast<int64_t>(b) * b_tile;
+    return (pair_kernel ? 0 : static_cast<int64_t>(a) * a_tile) + static_cast<int64_t>(b) * b_tile;
   };
-  const ozb::Schedule S = ozb::make_schedule(k, r, n_acc, static_cast<int64_t>(budget / 3), slot_bytes);
+  const int64_t max_stage = pair_kernel
+                                ? static_cast<int64_t>(ozb::PairCfg<128>::kMaxBSlots) * b_tile
+                                : static_cast<int64_t>(budget / 3);
+  const ozb::Schedule S = ozb::make_schedule(k, r, n_acc, max_stage, slot_bytes);
   const int np = static_cast<int>(S.products.size());
   if (np > cap) return set_err(nullptr, OZMM_ERR_ARG, "debug_schedule: cap too small");
   for (int q = 0; q < static_cast<int>(S.passes.size()); ++q) {
@@ -520,12 +543,14 @@ int ozmm_debug_schedule(int k, int64_t r, int cta_pair, int tile_n, int* rows, i
       row[7] = (pr.s >= ps.alo && pr.s <= ps.ahi && pr.t >= ps.blo && pr.t <= ps.bhi) ? 1 : 0;
     }
   }
-  const size_t stage_bytes = slot_bytes(S.a_slots, S.b_slots);
+  const size_t stage_bytes =
+      pair_kernel ? static_cast<size_t>(a_tile) : static_cast<size_t>(slot_bytes(S.a_slots, S.b_slots));
+  const size_t fixed = pair_kernel ? ozb::kBBufs * ozb::PairCfg<128>::kBBuf : 0;
   info[0] = np;
   info[1] = static_cast<int>(S.chunks.size());
   info[2] = static_cast<int>(S.batches.size());
   info[3] = static_cast<int>(S.passes.size());
-  info[4] = static_cast<int>(std::min<size_t>(8, budget / stage_bytes));  // stages
+  info[4] = static_cast<int>(std::min<size_t>(8, (budget - fixed) / stage_bytes));  // stages
   info[5] = S.a_slots;
   info[6] = S.b_slots;
   return OZMM_OK;

@@ -35,6 +35,14 @@ struct Pass {
   int batch;
   int alo, ahi, blo, bhi;
   int p0, p1;  // product range [p0, p1)
+  int g0, g1;  // A-slice group range [g0, g1) (products sorted by A slice)
+};
+
+// Products of one pass that share an A slice (the CTA-pair kernel streams A
+// slices one at a time and issues each group when its A tile lands).
+struct AGroup {
+  int s;
+  int p0, p1;
 };
 
 struct Batch {
@@ -47,6 +55,7 @@ struct Schedule {
   std::vector<Batch> batches;
   std::vector<Pass> passes;
   std::vector<Product> products;
+  std::vector<AGroup> agroups;
   int a_slots = 0, b_slots = 0;  // max slice tiles per stage over passes
 };
 
@@ -125,20 +134,30 @@ inline Schedule make_schedule(int k, int64_t r, int n_acc, int64_t max_stage_byt
       ps.batch = static_cast<int>(S.batches.size());
       ps.alo = ps.ahi = prods[i].s;
       ps.blo = ps.bhi = prods[i].t;
-      ps.p0 = static_cast<int>(S.products.size());
       size_t j = i;
       while (j < prods.size()) {
         const int alo = std::min(ps.alo, prods[j].s), ahi = std::max(ps.ahi, prods[j].s);
         const int blo = std::min(ps.blo, prods[j].t), bhi = std::max(ps.bhi, prods[j].t);
         if (j > i && stage_slot_bytes(ahi - alo + 1, bhi - blo + 1) > max_stage_bytes) break;
         ps.alo = alo, ps.ahi = ahi, ps.blo = blo, ps.bhi = bhi;
-        Product pr = prods[j];
-        pr.first = !seen[pr.ci];
-        seen[pr.ci] = true;
-        S.products.push_back(pr);
         ++j;
       }
+      // issue order inside the pass: by A slice (integer sums are order-free)
+      std::vector<Product> pass_prods(prods.begin() + i, prods.begin() + j);
+      std::stable_sort(pass_prods.begin(), pass_prods.end(),
+                       [](const Product& x, const Product& y) { return x.s < y.s; });
+      ps.p0 = static_cast<int>(S.products.size());
+      ps.g0 = static_cast<int>(S.agroups.size());
+      for (Product pr : pass_prods) {
+        pr.first = !seen[pr.ci];
+        seen[pr.ci] = true;
+        if (S.agroups.size() == static_cast<size_t>(ps.g0) || S.agroups.back().s != pr.s)
+          S.agroups.push_back({pr.s, static_cast<int>(S.products.size()), 0});
+        S.products.push_back(pr);
+        S.agroups.back().p1 = static_cast<int>(S.products.size());
+      }
       ps.p1 = static_cast<int>(S.products.size());
+      ps.g1 = static_cast<int>(S.agroups.size());
       S.a_slots = std::max(S.a_slots, ps.ahi - ps.alo + 1);
       S.b_slots = std::max(S.b_slots, ps.bhi - ps.blo + 1);
       S.passes.push_back(ps);
