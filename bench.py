@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cublas", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--grid", action="store_true",
+                    help="use the 2-D sharded path (grid2d) even at N=1")
     ap.add_argument("--cpu-sample", type=int, default=1024,
                     help="rows of A / columns of B in the CPU-baseline sub-block")
     return ap.parse_args()
@@ -194,7 +196,12 @@ def main():
     from paper_2409_13313_b200 import ozmm
 
     torch.cuda.set_device(local)
-    if world > 1:
+    use_grid = world > 1 or args.grid
+    if use_grid:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     m, n, p, k, phi = args.m, args.n, args.p, args.k, args.phi
     dev = torch.device("cuda", local)
@@ -203,7 +210,7 @@ def main():
     cfg = ozmm.config_for(ozmm.Method.ozIMMU_H, k)
 
     def barrier():
-        if world > 1:
+        if use_grid:
             dist.barrier(device_ids=[local])
 
     def max_over_ranks(x: float) -> float:
@@ -214,7 +221,7 @@ def main():
         return float(t.item())
 
     t_gen = time.perf_counter()
-    if world == 1:
+    if not use_grid:
         hA = torch.from_numpy(ozmm.gen_phi_block(m, n, phi, seed_a)).pin_memory()
         hB = torch.from_numpy(ozmm.gen_phi_block(n, p, phi, seed_b)).pin_memory()
         hC = torch.zeros((m, p), dtype=torch.float64).pin_memory()
@@ -270,7 +277,7 @@ def main():
     value = flops / (t_step * 1e-3) / 1e12
 
     # dominant kernel time (the fused GEMM) for the roofline
-    if world > 1:
+    if use_grid:
         torch.cuda.synchronize()
         for _ in range(2):
             G.backend.split(A, k, "L", False, G.beta_bits, G.a_loc, G.mu_loc)
@@ -305,7 +312,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         es = max(1, args.e2e_steps)
-        if world == 1:
+        if not use_grid:
             npA, npB, npC = hA.numpy(), hB.numpy(), hC.numpy()
             opt = ozmm.Options()
             cnt, tim = ozmm.Counts(), ozmm.Timings()
@@ -345,7 +352,7 @@ def main():
         t_e2e = max_over_ranks(t_e2e)
         e2e = {"value": flops / t_e2e / 1e12, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e * 1e3,
-               "api": "ozmm_dgemm_host (host pointers, pinned)" if world == 1 else
+               "api": "ozmm_dgemm_host (host pointers, pinned)" if not use_grid else
                       "per-rank pinned H2D of the shard + Grid2DGemm.step + D2H of the C block"}
 
     # ---- context: native cuBLAS DGEMM on the same device buffers
@@ -391,7 +398,7 @@ def main():
                    "sample": f"unavailable: {ex}"[:200]}
 
     if rank == 0:
-        pr, pc = (1, 1) if world == 1 else (G.L.pr, G.L.pc)
+        pr, pc = (G.L.pr, G.L.pc) if use_grid else (1, 1)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
@@ -402,7 +409,7 @@ def main():
                                    f"phi={phi}, alpha=1, beta=0" if (m, n, p) == (16384,) * 3 else
                                    f"m={m} n={n} p={p} ozIMMU_H k={k} phi={phi}",
                        "m": m, "n": n, "p": p, "k": k, "phi": phi,
-                       "parallelism": f"grid{pr}x{pc}" if world > 1 else "single",
+                       "parallelism": f"grid{pr}x{pc}" if use_grid else "single",
                        "l2": "inputs larger than L2 (3 x 8*16384^2 B = 6.4 GB vs 126 MB)",
                        "tile_n": args.tile_n or 64},
             "e2e": e2e,
@@ -423,7 +430,7 @@ def main():
             "host_input_gen_s": t_gen,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_grid:
         dist.destroy_process_group()
 
 
