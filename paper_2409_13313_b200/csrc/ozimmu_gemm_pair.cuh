@@ -35,9 +35,11 @@ constexpr int kPairEpiWarps = 8;  // per CTA
 constexpr int kKB = 128;          // bytes of K per block (= one 128B swizzle row)
 constexpr int kBBufs = 2;
 
-template <int kBN>
+template <int kBN, int kPairs = 1>
 struct PairCfg {
   static constexpr int kNAcc = 512 / kBN;
+  static constexpr int kCluster = 2 * kPairs;             // CTAs per cluster
+  static constexpr int kBPart = kBN / 2 / kPairs;         // B rows each CTA loads (multicast)
   static constexpr int kBHalf = kBN / 2;                  // B rows loaded per CTA
   static constexpr uint32_t kATile = kBM * kKB;           // 16 KB
   static constexpr uint32_t kBTile = kBHalf * kKB;        // bytes per CTA per B slice
@@ -46,12 +48,16 @@ struct PairCfg {
   static constexpr uint32_t kIdesc = ptx::idesc_i8(2 * kBM, kBN);
 };
 
-template <int kBN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
+// kPairs = 2: a 4-CTA cluster of two CTA pairs stacked along M that share the
+// B tiles: each CTA loads 1/kPairs of its B half and TMA-multicasts it to the
+// same-half CTA of the other pair, halving B's L2->SM traffic and keeping the
+// pairs in lockstep (their B stages are released by both pairs' MMAs).
+template <int kBN, int kPairs>
+__global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThreads, 1)
     ozimmu_gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                             const __grid_constant__ CUtensorMap map_b,
                             const __grid_constant__ GemmParams P) {
-  using Cfg = PairCfg<kBN>;
+  using Cfg = PairCfg<kBN, kPairs>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -70,16 +76,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = ptx::cluster_ctarank();
-  const bool leader = rank == 0;
+  const uint32_t lead_rank = rank & ~1u;      // leader of this CTA's pair
+  const uint32_t pp = rank >> 1;              // pair index in the cluster
+  const bool leader = rank == lead_rank;
+  const uint16_t pair_mask = static_cast<uint16_t>(0x3u << (2 * pp));
+  const uint16_t all_mask = static_cast<uint16_t>((1u << Cfg::kCluster) - 1);
 
-  // grouped raster over pair tiles (256 rows x kBN columns)
-  const int bid = blockIdx.x >> 1;
+  // grouped raster over cluster tiles (256*kPairs rows x kBN columns)
+  const int bid = blockIdx.x / Cfg::kCluster;
   const int per_group = P.group_m * P.tiles_n;
   const int first_m = (bid / per_group) * P.group_m;
   const int gm = min(P.group_m, P.tiles_m - first_m);
   const int tm = first_m + (bid % per_group) % gm;  // pair row-block (256 rows)
   const int tn = (bid % per_group) / gm;
-  const int row_base = tm * 2 * kBM + static_cast<int>(rank) * kBM;
+  const int row_base = tm * Cfg::kCluster * kBM + static_cast<int>(rank) * kBM;
   const int n_kb = P.n_kb;  // 128-byte K blocks
 
   if (warp == 0 && lane == 0) {
@@ -87,7 +97,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     ptx::tma_prefetch_desc(&map_b);
     for (int s = 0; s < kBBufs; ++s) {
       ptx::mbar_init(b_full + s, 1);
-      ptx::mbar_init(b_empty + s, 1);
+      ptx::mbar_init(b_empty + s, kPairs);  // released by every pair that reads it
     }
     for (int s = 0; s < n_a; ++s) {
       ptx::mbar_init(a_full + s, 1);
@@ -112,7 +122,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     if (ptx::elect_one()) {
       int bi = 0, ai = 0;
       uint32_t bph = 0, aph = 0;
-      const int b_row = tn * kBN + static_cast<int>(rank) * Cfg::kBHalf;
+      const int b_row = tn * kBN + static_cast<int>(rank & 1u) * Cfg::kBHalf +
+                        static_cast<int>(pp) * Cfg::kBPart;
+      const uint16_t b_mask = static_cast<uint16_t>(kPairs == 1 ? 0 : (0x5u << (rank & 1u)));
       const uint64_t pol_a = ptx::l2_policy(P.hint_a), pol_b = ptx::l2_policy(P.hint_b);
       for (int q = 0; q < P.npass; ++q) {
         const int blo = P.p_blo[q], bhi = P.p_bhi[q], g0 = P.p_g0[q], g1 = P.p_g1[q];
@@ -120,12 +132,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         for (int kb = 0; kb < n_kb; ++kb) {
           ptx::mbar_wait(b_empty + bi, bph ^ 1);
           {
-            const uint32_t fb = ptx::mapa_shared(b_full + bi, 0);
+            const uint32_t fb = ptx::mapa_shared(b_full + bi, lead_rank);
             if (leader) ptx::mbar_arrive_expect_tx(b_full + bi, btx);
-            uint8_t* dst = bbuf + bi * Cfg::kBBuf;
-            for (int t = blo; t <= bhi; ++t)
-              ptx::tma_load_3d_pair_hint(dst + (t - blo) * Cfg::kBTile, &map_b, fb, kb * kKB,
-                                         b_row, t - 1, pol_b);
+            uint8_t* dst = bbuf + bi * Cfg::kBBuf + pp * Cfg::kBPart * kKB;
+            for (int t = blo; t <= bhi; ++t) {
+              if constexpr (kPairs == 1)
+                ptx::tma_load_3d_pair_hint(dst + (t - blo) * Cfg::kBTile, &map_b, fb, kb * kKB,
+                                           b_row, t - 1, pol_b);
+              else
+                ptx::tma_load_3d_pair_mc(dst + (t - blo) * Cfg::kBTile, &map_b, b_full + bi,
+                                         kb * kKB, b_row, t - 1, b_mask, pol_b);
+            }
           }
           if (++bi == kBBufs) {
             bi = 0;
@@ -133,7 +150,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           }
           for (int g = g0; g < g1; ++g) {
             ptx::mbar_wait(a_empty + ai, aph ^ 1);
-            const uint32_t fa = ptx::mapa_shared(a_full + ai, 0);
+            const uint32_t fa = ptx::mapa_shared(a_full + ai, lead_rank);
             if (leader) ptx::mbar_arrive_expect_tx(a_full + ai, 2u * Cfg::kATile);
             ptx::tma_load_3d_pair_hint(aring + ai * Cfg::kATile, &map_a, fa, kb * kKB, row_base,
                                        P.ag_s[g] - 1, pol_a);
@@ -175,7 +192,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, Cfg::kIdesc,
                                      (first && j == 0) ? 0u : 1u);
                 }
-                ptx::mma_commit_pair(a_empty + ai, 0x3);  // A stage free in both CTAs
+                ptx::mma_commit_pair(a_empty + ai, pair_mask);  // A stage free in the pair
               }
               __syncwarp();
               if (++ai == n_a) {
@@ -183,7 +200,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 aph ^= 1;
               }
             }
-            if (ptx::elect_one()) ptx::mma_commit_pair(b_empty + bi, 0x3);
+            if (ptx::elect_one()) ptx::mma_commit_pair(b_empty + bi, all_mask);
             __syncwarp();
             if (++bi == kBBufs) {
               bi = 0;
@@ -191,7 +208,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             }
           }
         }
-        if (ptx::elect_one()) ptx::mma_commit_pair(tmem_full, 0x3);
+        if (ptx::elect_one()) ptx::mma_commit_pair(tmem_full, pair_mask);
         __syncwarp();
       }
     }
@@ -205,7 +222,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     const int col0 = tn * kBN + cslice * kCols;
     const bool row_ok = row < P.m;
     const double mu = row_ok ? P.mu[row] : 0.0;
-    const uint32_t empty_leader = ptx::mapa_shared(tmem_empty, 0);
+    const uint32_t empty_leader = ptx::mapa_shared(tmem_empty, lead_rank);
     double d[kCols];
 #pragma unroll
     for (int j = 0; j < kCols; ++j) d[j] = 0.0;

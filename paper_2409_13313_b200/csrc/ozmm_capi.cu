@@ -57,7 +57,7 @@ struct Handle {
   cudaStream_t s_in = nullptr, s_out = nullptr;  // copy streams of the host entry
   cudaEvent_t ev[5] = {};
   bool gemm_attr_set[3] = {false, false, false};
-  bool pair_attr_set = false;
+  bool pair_attr_set[2] = {false, false};
   int num_sms = 148;
   size_t smem_optin = 232448;
 };
@@ -144,17 +144,50 @@ int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const doubl
                  int k, int beta, int8_t* S, int64_t lds, int64_t plane, double* shift) {
   if (row_mode) {
     const bool vec = (reinterpret_cast<uintptr_t>(X) % 16 == 0) && (ldx % 2 == 0);
-    // one CTA per row, 16 elements per thread (whole row in registers up to 16384)
-    const int64_t want = (lds / 16 + 31) / 32 * 32;
-    const int threads = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(32, want)));
-    const dim3 grid(static_cast<unsigned>(lines));
-    if (vec)
-      ozb::slice_rows_kernel<true><<<grid, threads, 0, h->stream>>>(X, ldx, lines, n, lds, k, beta,
-                                                                    S, plane, shift, h->flags);
-    else
-      ozb::slice_rows_kernel<false><<<grid, threads, 0, h->stream>>>(X, ldx, lines, n, lds, k,
-                                                                     beta, S, plane, shift,
-                                                                     h->flags);
+    // Whole row in registers, 16 elements per thread.  Rows up to 8 x 512 x 16
+    // elements are split over a cluster of up to 8 CTAs (256 or 512 threads);
+    // longer rows use one 1024-thread CTA with a second pass.
+    const int64_t chunks = (lds + 15) / 16;  // 16-element chunks per row
+    int csize = 0, cthreads = 256;
+    for (int t : {256, 512}) {
+      const int64_t c = (chunks + t - 1) / t;
+      if (c <= 8) {
+        csize = static_cast<int>(c);
+        cthreads = t;
+        break;
+      }
+    }
+    if (csize >= 2) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(static_cast<unsigned>(lines * csize));
+      cfg.blockDim = dim3(static_cast<unsigned>(cthreads));
+      cfg.stream = h->stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = csize;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      if (vec)
+        CUDA_TRY(h, cudaLaunchKernelEx(&cfg, ozb::slice_rows_cluster_kernel<true>, X, ldx, lines, n,
+                                       lds, k, beta, S, plane, shift, h->flags));
+      else
+        CUDA_TRY(h, cudaLaunchKernelEx(&cfg, ozb::slice_rows_cluster_kernel<false>, X, ldx, lines,
+                                       n, lds, k, beta, S, plane, shift, h->flags));
+    } else {
+      const int64_t want = (chunks + 31) / 32 * 32;
+      const int threads = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(32, want)));
+      const dim3 grid(static_cast<unsigned>(lines));
+      if (vec)
+        ozb::slice_rows_kernel<true><<<grid, threads, 0, h->stream>>>(X, ldx, lines, n, lds, k,
+                                                                      beta, S, plane, shift,
+                                                                      h->flags);
+      else
+        ozb::slice_rows_kernel<false><<<grid, threads, 0, h->stream>>>(X, ldx, lines, n, lds, k,
+                                                                       beta, S, plane, shift,
+                                                                       h->flags);
+    }
   } else {
     if (int rc = ensure(h, &h->colmax, &h->colmax_n, static_cast<size_t>(lines))) return rc;
     CUDA_TRY(h, cudaMemsetAsync(h->colmax, 0, sizeof(unsigned long long) * lines, h->stream));
@@ -288,12 +321,12 @@ int launch_gemm_bn(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_b
 }
 
 // CTA-pair kernel: 256 x kBN tile per 2-CTA cluster (cta_group::2).
-template <int kBN>
+template <int kBN, int kPairs>
 int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_bits, int64_t r,
                      const int8_t* As, int64_t lds_a, int64_t plane_a, const double* mu, const int8_t* Bs,
                      int64_t lds_b, int64_t plane_b, const double* nu, double alpha, double beta,
                      const double* Cin, double* Cout, int64_t ldc, int32_t* dump) {
-  using Cfg = ozb::PairCfg<kBN>;
+  using Cfg = ozb::PairCfg<kBN, kPairs>;
   const size_t budget = h->smem_optin - kSmemReserve - kBN * sizeof(double);
   // passes are limited by the resident B slices per K block (A slices stream)
   auto slot_bytes = [](int, int b) { return static_cast<int64_t>(b) * Cfg::kBTile; };
@@ -308,27 +341,30 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   if (stages < 2)
     return set_err(h, OZMM_ERR_UNSUPPORTED, "A ring does not fit shared memory");
   ozb::GemmParams P;
-  const int tiles_m = static_cast<int>((m + 2 * ozb::kBM - 1) / (2 * ozb::kBM));
+  const int rows_per_tile = Cfg::kCluster * ozb::kBM;
+  const int tiles_m = static_cast<int>((m + rows_per_tile - 1) / rows_per_tile);
   const int tiles_n = static_cast<int>((p + kBN - 1) / kBN);
   fill_params(P, S, m, p, lds_a, lds_b, tiles_m, tiles_n, beta_bits, stages, alpha, beta, mu, nu,
               Cin, Cout, ldc, dump);
+  if (kPairs > 1 && !std::getenv("OZMM_GROUP_M")) P.group_m = 1;
   P.n_kb = static_cast<int>((std::max(lds_a, lds_b) + ozb::kKB - 1) / ozb::kKB);
   CUtensorMap map_a, map_b;
   if (int rc = make_slice_map(h, &map_a, As, lds_a, m, plane_a, k, ozb::kBM, ozb::kKB,
                               CU_TENSOR_MAP_SWIZZLE_128B))
     return rc;
-  if (int rc = make_slice_map(h, &map_b, Bs, lds_b, p, plane_b, k, Cfg::kBHalf, ozb::kKB,
+  if (int rc = make_slice_map(h, &map_b, Bs, lds_b, p, plane_b, k, Cfg::kBPart, ozb::kKB,
                               CU_TENSOR_MAP_SWIZZLE_128B))
     return rc;
   const size_t smem = fixed + stages * Cfg::kATile + kSmemReserve + kBN * sizeof(double);
-  if (!h->pair_attr_set) {
-    CUDA_TRY(h, cudaFuncSetAttribute(ozb::ozimmu_gemm_pair_kernel<kBN>,
+  if (!h->pair_attr_set[kPairs - 1]) {
+    CUDA_TRY(h, cudaFuncSetAttribute(ozb::ozimmu_gemm_pair_kernel<kBN, kPairs>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(h->smem_optin)));
-    h->pair_attr_set = true;
+    h->pair_attr_set[kPairs - 1] = true;
   }
-  const dim3 grid(static_cast<unsigned>(2 * tiles_m * tiles_n));
-  ozb::ozimmu_gemm_pair_kernel<kBN><<<grid, ozb::kPairThreads, smem, h->stream>>>(map_a, map_b, P);
+  const dim3 grid(static_cast<unsigned>(Cfg::kCluster * tiles_m * tiles_n));
+  ozb::ozimmu_gemm_pair_kernel<kBN, kPairs>
+      <<<grid, ozb::kPairThreads, smem, h->stream>>>(map_a, map_b, P);
   CUDA_TRY(h, cudaGetLastError());
   return OZMM_OK;
 }
@@ -340,8 +376,11 @@ int launch_gemm(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_bits
   int32_t* dump = opt ? opt->chunk_dump : nullptr;
   const int tile_n = opt ? opt->tile_n : 0;
   const int pair = opt ? opt->cta_pair : 0;
+  if (pair == 3 || (pair == 0 && tile_n == 0 && std::getenv("OZMM_QUAD")))
+    return launch_gemm_pair<128, 2>(h, m, n, p, k, beta_bits, r, As, lds_a, plane_a, mu, Bs, lds_b,
+                                    plane_b, nu, alpha, beta, Cin, Cout, ldc, dump);
   if (pair == 2 || (pair == 0 && tile_n == 0))
-    return launch_gemm_pair<128>(h, m, n, p, k, beta_bits, r, As, lds_a, plane_a, mu, Bs, lds_b, plane_b, nu, alpha,
+    return launch_gemm_pair<128, 1>(h, m, n, p, k, beta_bits, r, As, lds_a, plane_a, mu, Bs, lds_b, plane_b, nu, alpha,
                                  beta, Cin, Cout, ldc, dump);
   switch (tile_n ? tile_n : 64) {
     case 32:
@@ -505,9 +544,9 @@ int ozmm_debug_schedule(int k, int64_t r, int cta_pair, int tile_n, int* rows, i
   int n_acc, a_tile, b_tile, bn;
   if (cta_pair == 2 || (cta_pair == 0 && tile_n == 0)) {
     bn = 128;
-    n_acc = ozb::PairCfg<128>::kNAcc;
-    a_tile = ozb::PairCfg<128>::kATile;
-    b_tile = ozb::PairCfg<128>::kBTile;  // per CTA, 128-byte K block
+    n_acc = ozb::PairCfg<128, 1>::kNAcc;
+    a_tile = ozb::PairCfg<128, 1>::kATile;
+    b_tile = ozb::PairCfg<128, 1>::kBTile;  // per CTA, 128-byte K block
   } else {
     bn = tile_n ? tile_n : 64;
     if (bn != 32 && bn != 64 && bn != 128) return set_err(nullptr, OZMM_ERR_ARG, "tile_n");
@@ -521,7 +560,7 @@ int ozmm_debug_schedule(int k, int64_t r, int cta_pair, int tile_n, int* rows, i
     return (pair_kernel ? 0 : static_cast<int64_t>(a) * a_tile) + static_cast<int64_t>(b) * b_tile;
   };
   const int64_t max_stage = pair_kernel
-                                ? static_cast<int64_t>(ozb::PairCfg<128>::kMaxBSlots) * b_tile
+                                ? static_cast<int64_t>(ozb::PairCfg<128, 1>::kMaxBSlots) * b_tile
                                 : static_cast<int64_t>(budget / 3);
   const ozb::Schedule S = ozb::make_schedule(k, r, n_acc, max_stage, slot_bytes);
   const int np = static_cast<int>(S.products.size());
@@ -545,7 +584,7 @@ int ozmm_debug_schedule(int k, int64_t r, int cta_pair, int tile_n, int* rows, i
   }
   const size_t stage_bytes =
       pair_kernel ? static_cast<size_t>(a_tile) : static_cast<size_t>(slot_bytes(S.a_slots, S.b_slots));
-  const size_t fixed = pair_kernel ? ozb::kBBufs * ozb::PairCfg<128>::kBBuf : 0;
+  const size_t fixed = pair_kernel ? ozb::kBBufs * ozb::PairCfg<128, 1>::kBBuf : 0;
   info[0] = np;
   info[1] = static_cast<int>(S.chunks.size());
   info[2] = static_cast<int>(S.batches.size());

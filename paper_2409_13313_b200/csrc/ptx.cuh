@@ -214,6 +214,22 @@ __device__ __forceinline__ void tma_load_3d_pair_hint(void* smem_dst, const CUte
       : "memory");
 }
 
+// 2-CTA TMA with multicast: the tile lands at the same smem offset in every CTA
+// of `mask`; the transaction bytes are counted on the barrier of each
+// destination's pair leader (the barrier address has the peer bit cleared,
+// the convention of CUTLASS's SM100_TMA_2SM_LOAD_MULTICAST).
+__device__ __forceinline__ void tma_load_3d_pair_mc(void* smem_dst, const CUtensorMap* map,
+                                                    uint64_t* bar_local, int32_t c0, int32_t c1,
+                                                    int32_t c2, uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster.L2::cache_hint [%0], [%1, {%4, %5, %6}], [%2], %3, %7;" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar_local) & 0xFEFFFFFFu), "h"(mask),
+      "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+      : "memory");
+}
+
 // L2 eviction policies: 0 = normal, 1 = evict_first, 2 = evict_last.
 __device__ __forceinline__ uint64_t l2_policy(int kind) {
   uint64_t pol;

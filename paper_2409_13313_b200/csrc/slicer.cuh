@@ -156,6 +156,51 @@ __global__ void __launch_bounds__(1024) slice_rows_kernel(const double* __restri
   }
 }
 
+// Cluster variant: a row is split over the `csize` CTAs of a thread-block
+// cluster (16 elements per thread, whole row in registers); the CTA maxima
+// are exchanged through distributed shared memory.  Small CTAs let several
+// rows share an SM, so one row's loads overlap another row's slicing.
+template <bool kVec>
+__global__ void __launch_bounds__(512) slice_rows_cluster_kernel(
+    const double* __restrict__ X, int64_t ld, int64_t rows, int64_t len, int64_t lds, int k,
+    int beta, int8_t* __restrict__ S, int64_t plane, double* __restrict__ shift,
+    int* __restrict__ flags) {
+  __shared__ double red[32];
+  __shared__ double cmax[8];  // one slot per CTA of the cluster
+  uint32_t crank, csize;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
+  const int64_t row = blockIdx.x / csize;
+  const double* x = X + row * ld;
+  int8_t* out = S + row * lds;
+  const int64_t base0 = 16 * (static_cast<int64_t>(crank) * blockDim.x + threadIdx.x);
+  // every CTA of the cluster must be running before its shared memory is written
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  double w[16];
+  load16(x, base0, len, kVec, w);
+  double rm = 0.0;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) rm = fmax(rm, fabs(w[e]));
+  rm = block_max(rm, red);
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  if (threadIdx.x < csize) {  // publish this CTA's max into every CTA's slot crank
+    uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(&cmax[crank]));
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(threadIdx.x));
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(rm) : "memory");
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  for (uint32_t c = 0; c < csize; ++c) rm = fmax(rm, cmax[c]);
+  bool under = false, range = false;
+  const int PE = line_pe(rm, beta, &under, &range);
+  if (crank == 0 && threadIdx.x == 0) {
+    shift[row] = PE == INT32_MIN ? 0.0 : pow2(PE);
+    report_flags(flags, under, range);
+  }
+  if (base0 < lds) emit16(w, PE, beta, k, out + base0, plane);
+}
+
 // Column maxima of |X| for X: len x cols (row stride ld).  colmax holds the
 // IEEE bit pattern of the max (must be zeroed first).  Block 32 x 8 threads.
 __global__ void __launch_bounds__(256) colmax_kernel(const double* __restrict__ X, int64_t ld,
@@ -180,8 +225,11 @@ __global__ void __launch_bounds__(256) colmax_kernel(const double* __restrict__ 
 }
 
 // Slices of the columns of X (len x cols, row stride ld) written as the rows
-// of the transposed planes S[s][col][0..lds).  Block 32 x 8: thread (tx, ty)
-// owns column c0+tx and the 16 rows n0 + 16*ty .. +16 of a 128-row tile.
+// of the transposed planes S[s][col][0..lds).  A CTA of 8 warps covers 32
+// columns x 128 rows; lane l of warp w owns column 4w + (l & 3) and the 16
+// rows 16*(l >> 2) .. +16.  Each warp load then touches 8 fully used 32-byte
+// sectors (4 adjacent columns x 8 rows) and, per slice, each column's 8
+// chunks form one contiguous 128-byte line of the output plane.
 __global__ void __launch_bounds__(256) slice_cols_kernel(const double* __restrict__ X, int64_t ld,
                                                          int64_t len, int64_t cols, int64_t lds,
                                                          int k, int beta,
@@ -189,14 +237,14 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(const double* __restric
                                                          int8_t* __restrict__ S, int64_t plane,
                                                          double* __restrict__ shift,
                                                          int* __restrict__ flags) {
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int64_t col = static_cast<int64_t>(blockIdx.x) * 32 + tx;
-  const int64_t base = static_cast<int64_t>(blockIdx.y) * 128 + 16 * ty;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t col = static_cast<int64_t>(blockIdx.x) * 32 + warp * 4 + (lane & 3);
+  const int64_t base = static_cast<int64_t>(blockIdx.y) * 128 + 16 * (lane >> 2);
   if (col >= cols || base >= lds) return;
   const double rm = __longlong_as_double(static_cast<long long>(colmax[col]));
   bool under = false, range = false;
   const int PE = line_pe(rm, beta, &under, &range);
-  if (blockIdx.y == 0 && ty == 0) {
+  if (blockIdx.y == 0 && (lane >> 2) == 0) {
     shift[col] = PE == INT32_MIN ? 0.0 : pow2(PE);
     report_flags(flags, under, range);
   }
