@@ -103,8 +103,25 @@ typedef struct {
   int tile_n;              /* 0 = auto; 32/64/128: single-CTA kernel with that many
                               output columns per CTA (forces cta_pair = 1) */
   int cta_pair;            /* 0 = auto (CTA-pair kernel, M = 256 x N = 128 per 2-CTA
-                              cluster), 1 = single-CTA kernel, 2 = CTA-pair kernel */
+                              cluster), 1 = single-CTA kernel, 2 = CTA-pair kernel,
+                              3 = experimental 4-CTA cluster sharing B by TMA multicast */
+  int method;              /* OZMM_METHOD_*: 0 = ozIMMU_H (the hot path, default) */
 } ozmm_options_t;
+
+/* Scheme presets (config_for, scheme.cpp:137-159) plus the two other valid
+ * (strategy, accumulation) pairs.  ozIMMU_H is the hot path; the others are
+ * the paper's comparison methods. */
+enum {
+  OZMM_METHOD_OZIMMU_H = 0,            /* RN const shift + group-wise */
+  OZMM_METHOD_OZIMMU = 1,              /* bitmask + per-product FP64 accumulation */
+  OZMM_METHOD_OZIMMU_RN = 2,           /* RN per slice + per-product */
+  OZMM_METHOD_OZIMMU_EF = 3,           /* bitmask + group-wise */
+  OZMM_METHOD_RN_CONST_PER_PRODUCT = 4,/* RN const shift + per-product */
+  OZMM_METHOD_OZIMMU_H_SIMPLE = 5      /* RN const shift + GroupwiseSimple (needs r >= k) */
+};
+
+/* Splitting strategies of ozmm_split_ex (SliceStrategy, split.hpp:11-15). */
+enum { OZMM_SPLIT_RN_CONST_SHIFT = 0, OZMM_SPLIT_BITMASK = 1, OZMM_SPLIT_RN_PER_SLICE = 2 };
 
 /* ---- handle ------------------------------------------------------------- */
 int ozmm_create(ozmm_handle_t* handle, int device);
@@ -160,6 +177,13 @@ int64_t ozmm_slice_ld(int64_t n);
 int ozmm_split(ozmm_handle_t h, char side, char trans, int64_t lines, int64_t n,
                const double* X, int64_t ldx, int k, int beta, int8_t* slices, int64_t lds,
                double* shift);
+
+/* ozmm_split for any strategy.  out: the const shift [lines] for
+ * OZMM_SPLIT_RN_CONST_SHIFT / OZMM_SPLIT_BITMASK, the per-slice units
+ * [k][lines] for OZMM_SPLIT_RN_PER_SLICE (slice_units, split.hpp:38). */
+int ozmm_split_ex(ozmm_handle_t h, char side, char trans, int64_t lines, int64_t n,
+                  const double* X, int64_t ldx, int k, int beta, int strategy, int8_t* slices,
+                  int64_t lds, double* out);
 
 /* K2+K3 over already-split operands: C <- alpha * D + beta * C with D the
  * group-wise ozIMMU_H accumulation of A slices [k][m][lds_a] / mu [m] and

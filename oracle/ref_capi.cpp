@@ -169,6 +169,30 @@ int ozref_split_rn_const_shift(const double* a, std::int64_t rows, std::int64_t 
   });
 }
 
+// Any splitting strategy: 0 = RN const shift, 1 = bitmask, 2 = RN per slice
+// (split.cpp:223-237).  out: const shift [rows or cols] (0, 1) or per-slice
+// units [k][rows or cols] (2).
+int ozref_split_any(int strategy, const double* a, std::int64_t rows, std::int64_t cols, int k,
+                    int side, int force_beta, std::int8_t* slices, double* out) {
+  return guard([&] {
+    const MatrixF64 A = load(a, rows, cols);
+    const Side sd = side ? Side::Right : Side::Left;
+    const SplitMatrix s = strategy == 1   ? split_bitmask(A, k, sd, force_beta)
+                          : strategy == 2 ? split_round_nearest(A, k, sd, force_beta)
+                                          : split_rn_const_shift(A, k, sd, force_beta);
+    for (int t = 0; t < k; ++t)
+      std::memcpy(slices + static_cast<std::int64_t>(t) * rows * cols, s.slices[t].data(),
+                  static_cast<std::size_t>(rows * cols));
+    if (strategy == 2) {
+      const std::int64_t lines = side ? cols : rows;
+      for (int t = 0; t < k; ++t)
+        std::memcpy(out + t * lines, s.slice_units[t].data(), sizeof(double) * lines);
+    } else {
+      std::memcpy(out, s.const_shift.data(), sizeof(double) * s.const_shift.size());
+    }
+  });
+}
+
 // The INT32 chunk sums of the ozIMMU_H group-wise schedule, in flush order,
 // produced by the reference's own splitter and i8_gemm_accumulate following
 // the loop of groupwise_impl (scheme.cpp:81-101).  acc_out receives w

@@ -58,6 +58,13 @@ struct GemmParams {
   int a_slots, b_slots;  // slice tiles per stage (max over passes)
   int n_chunks;
   int hint_a, hint_b;  // L2 policies of the A / B slice loads (0 normal, 1 evict_first, 2 evict_last)
+  // FP64 flush scaling (scheme.cpp:29-41 with the caller's unit vectors):
+  //   0 group-wise        ru = mu_i 2^(2-beta g),   cv = nu_j                (:93-94)
+  //   1 per-product const ru = mu_i 2^(1-beta s),   cv = nu_j 2^(1-beta t)   (:205, units_of)
+  //   2 per-product units ru = units_a[s-1][i],     cv = units_b[t-1][j]     (RN per slice)
+  int scale_mode;
+  const double* units_a;  // [k][m] per-slice row units (scale_mode 2)
+  const double* units_b;  // [k][p] per-slice column units (scale_mode 2)
   double alpha, beta_c;
   const double* mu;    // [m] row shifts of op(A)
   const double* nu;    // [p] column shifts of op(B)
@@ -72,8 +79,9 @@ struct GemmParams {
   uint16_t p_p0[kMaxPasses], p_p1[kMaxPasses];
   // per product: accumulator slot | first-product flag (bit 7), A slice, B slice
   uint8_t pr_ci[kMaxProducts], pr_s[kMaxProducts], pr_t[kMaxProducts];
-  // per chunk in flush order: group g
+  // per chunk in flush order: group g and first A slice s0
   uint8_t c_g[kMaxChunks];
+  uint8_t c_s[kMaxChunks];
   // CTA-pair kernel: per pass the A-slice groups [p_g0, p_g1); per group the
   // A slice and its product range (products are sorted by A slice in a pass)
   uint16_t p_g0[kMaxPasses], p_g1[kMaxPasses];
@@ -88,6 +96,23 @@ struct GemmCfg {
   static constexpr uint32_t kBTile = kBN * kBK;         // bytes per B slice tile
   static constexpr uint32_t kIdesc = ptx::idesc_i8(kBM, kBN);
 };
+
+// Row factor of chunk c's flush for row `row` (mu = the row's shift).
+__device__ __forceinline__ double flush_row_scale(const GemmParams& P, int c, int row,
+                                                  double mu) {
+  if (P.scale_mode == 0) return __dmul_rn(mu, pow2(2 - P.beta * P.c_g[c]));  // ldexp(mu, 2-beta g)
+  if (P.scale_mode == 1) return __dmul_rn(mu, pow2(1 - P.beta * P.c_s[c]));  // unit(s-1, i)
+  return row < P.m ? P.units_a[static_cast<int64_t>(P.c_s[c] - 1) * P.m + row] : 0.0;
+}
+
+// Column factor of chunk c's flush for column `col` (nu = the column's shift).
+__device__ __forceinline__ double flush_col_scale(const GemmParams& P, int c, int col,
+                                                  double nu) {
+  if (P.scale_mode == 0) return nu;
+  const int t = P.c_g[c] - P.c_s[c];
+  if (P.scale_mode == 1) return __dmul_rn(nu, pow2(1 - P.beta * t));  // unit(t-1, j)
+  return col < P.p ? P.units_b[static_cast<int64_t>(t - 1) * P.p + col] : 0.0;
+}
 
 // Dynamic smem: [stages x (a_slots*ATile + b_slots*BTile)] tiles (1024-aligned)
 // then barriers and the nu cache.
@@ -223,7 +248,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int c0 = P.b_c0[b], nc = P.b_nc[b];
       for (int ci = 0; ci < nc; ++ci) {
         const int c = c0 + ci;
-        const double ru = __dmul_rn(mu, pow2(2 - P.beta * P.c_g[c]));  // ldexp(mu, 2-beta*g)
+        const double ru = flush_row_scale(P, c, row, mu);
 #pragma unroll
         for (int cc = 0; cc < kHalf; cc += kLd) {
           uint32_t v[kLd];
@@ -239,8 +264,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
 #pragma unroll
           for (int j = 0; j < kLd; ++j) {
-            const double t = __dmul_rn(__dmul_rn(ru, static_cast<double>(static_cast<int32_t>(v[j]))),
-                                       nu_s[half * kHalf + cc + j]);
+            const double cv = flush_col_scale(P, c, col0 + cc + j, nu_s[half * kHalf + cc + j]);
+            const double t = __dmul_rn(__dmul_rn(ru, static_cast<double>(static_cast<int32_t>(v[j]))), cv);
             d[cc + j] = __dadd_rn(d[cc + j], t);
           }
         }

@@ -233,7 +233,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
       const int c0 = P.b_c0[b], nc = P.b_nc[b];
       for (int ci = 0; ci < nc; ++ci) {
         const int c = c0 + ci;
-        const double ru = __dmul_rn(mu, pow2(2 - P.beta * P.c_g[c]));  // ldexp(mu, 2-beta*g)
+        const double ru = flush_row_scale(P, c, row, mu);
 #pragma unroll
         for (int cc = 0; cc < kCols; cc += kLd) {
           uint32_t v[kLd];
@@ -249,9 +249,9 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
           }
 #pragma unroll
           for (int j = 0; j < kLd; ++j) {
+            const double cv = flush_col_scale(P, c, col0 + cc + j, nu_s[cslice * kCols + cc + j]);
             const double t =
-                __dmul_rn(__dmul_rn(ru, static_cast<double>(static_cast<int32_t>(v[j]))),
-                          nu_s[cslice * kCols + cc + j]);
+                __dmul_rn(__dmul_rn(ru, static_cast<double>(static_cast<int32_t>(v[j]))), cv);
             d[cc + j] = __dadd_rn(d[cc + j], t);
           }
         }

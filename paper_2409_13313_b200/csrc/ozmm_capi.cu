@@ -24,10 +24,39 @@
 #include "ozimmu_gemm_pair.cuh"
 #include "schedule.hpp"
 #include "slicer.cuh"
+#include "slicer_methods.cuh"
 
 namespace {
 
 thread_local std::string g_thread_err;
+
+// Splitting strategy (SliceStrategy, split.hpp:11-15) and FP64 flush scaling of
+// the fused GEMM (GemmParams::scale_mode).
+enum Strategy { kRNConstShift = 0, kBitMask = 1, kRNPerSlice = 2 };
+struct FlushCfg {
+  int scale_mode = 0;
+  const double* units_a = nullptr;
+  const double* units_b = nullptr;
+  bool per_product = false;  // chunks of one product (accumulate_per_product)
+};
+
+// method code of ozmm_options_t -> (strategy, per-product accumulation)
+struct MethodCfg {
+  Strategy strategy;
+  bool per_product;
+  bool simple;  // GroupwiseSimple: requires r >= k
+};
+bool method_cfg(int method, MethodCfg* out) {
+  switch (method) {
+    case OZMM_METHOD_OZIMMU_H: *out = {kRNConstShift, false, false}; return true;
+    case OZMM_METHOD_OZIMMU: *out = {kBitMask, true, false}; return true;
+    case OZMM_METHOD_OZIMMU_RN: *out = {kRNPerSlice, true, false}; return true;
+    case OZMM_METHOD_OZIMMU_EF: *out = {kBitMask, false, false}; return true;
+    case OZMM_METHOD_RN_CONST_PER_PRODUCT: *out = {kRNConstShift, true, false}; return true;
+    case OZMM_METHOD_OZIMMU_H_SIMPLE: *out = {kRNConstShift, false, true}; return true;
+    default: return false;
+  }
+}
 
 struct Handle {
   int device = 0;
@@ -45,6 +74,12 @@ struct Handle {
   unsigned long long* colmax = nullptr;
   size_t colmax_n = 0;
   int* flags = nullptr;  // [0] underflow, [1] range
+  double* units_a = nullptr;  // per-slice units (RN per slice) [k][m] / [k][p]
+  size_t units_a_n = 0;
+  double* units_b = nullptr;
+  size_t units_b_n = 0;
+  double* tscratch = nullptr;  // transposed operand for per-slice RN column splits
+  size_t tscratch_n = 0;
   // device staging for the host-pointer entry (grown lazily, reused)
   double* host_a = nullptr;
   size_t host_a_n = 0;
@@ -203,6 +238,88 @@ int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const doubl
   return OZMM_OK;
 }
 
+// Cluster split of a row over up to 8 CTAs of 256/512 threads (16 elements per
+// thread, whole row in registers).  Returns false when the row is too long.
+bool cluster_rows_config(int64_t lds, int* csize, int* threads) {
+  const int64_t chunks = (lds + 15) / 16;
+  for (int t : {256, 512, 1024}) {
+    const int64_t c = (chunks + t - 1) / t;
+    if (c <= 8) {
+      *csize = static_cast<int>(c);
+      *threads = t;
+      return true;
+    }
+  }
+  return false;
+}
+
+template <class Kern, class... Args>
+int launch_cluster_rows(Handle* h, Kern kern, int64_t lines, int csize, int threads,
+                        Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(lines * csize));
+  cfg.blockDim = dim3(static_cast<unsigned>(threads));
+  cfg.stream = h->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = csize;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(h, cudaLaunchKernelEx(&cfg, kern, args...));
+  return OZMM_OK;
+}
+
+// K1 for any strategy.  out = const shift [lines] (RN const shift, bitmask) or
+// per-slice units [k][lines] (RN per slice).
+int launch_split_m(Handle* h, Strategy st, bool row_mode, int64_t lines, int64_t n,
+                   const double* X, int64_t ldx, int k, int beta, int8_t* S, int64_t lds,
+                   int64_t plane, double* out) {
+  if (st == kRNConstShift)
+    return launch_split(h, row_mode, lines, n, X, ldx, k, beta, S, lds, plane, out);
+  if (st == kRNPerSlice && !row_mode) {
+    // per-slice grids need several reductions per line: transpose to contiguous lines
+    if (int rc = ensure(h, &h->tscratch, &h->tscratch_n, static_cast<size_t>(lines) * n)) return rc;
+    const dim3 g(static_cast<unsigned>((lines + 31) / 32), static_cast<unsigned>((n + 31) / 32));
+    ozb::transpose_f64_kernel<<<g, 256, 0, h->stream>>>(X, ldx, n, lines, h->tscratch);
+    CUDA_TRY(h, cudaGetLastError());
+    X = h->tscratch;
+    ldx = n;
+    row_mode = true;
+  }
+  const bool vec = (reinterpret_cast<uintptr_t>(X) % 16 == 0) && (ldx % 2 == 0);
+  if (row_mode) {
+    int csize, threads;
+    if (!cluster_rows_config(lds, &csize, &threads))
+      return set_err(h, OZMM_ERR_UNSUPPORTED, "inner dimension too long for this splitter");
+    if (st == kBitMask)
+      return vec ? launch_cluster_rows(h, ozb::slice_rows_bitmask_kernel<true>, lines, csize,
+                                       threads, X, ldx, lines, n, lds, k, beta, S, plane, out,
+                                       h->flags)
+                 : launch_cluster_rows(h, ozb::slice_rows_bitmask_kernel<false>, lines, csize,
+                                       threads, X, ldx, lines, n, lds, k, beta, S, plane, out,
+                                       h->flags);
+    return vec ? launch_cluster_rows(h, ozb::slice_rows_rnps_kernel<true>, lines, csize, threads,
+                                     X, ldx, lines, n, lds, k, beta, S, plane, out, h->flags)
+               : launch_cluster_rows(h, ozb::slice_rows_rnps_kernel<false>, lines, csize,
+                                     threads, X, ldx, lines, n, lds, k, beta, S, plane, out,
+                                     h->flags);
+  }
+  // bitmask, column lines
+  if (int rc = ensure(h, &h->colmax, &h->colmax_n, static_cast<size_t>(lines))) return rc;
+  CUDA_TRY(h, cudaMemsetAsync(h->colmax, 0, sizeof(unsigned long long) * lines, h->stream));
+  const int64_t rows_per_block = 512;
+  const dim3 g1(static_cast<unsigned>((lines + 31) / 32),
+                static_cast<unsigned>((n + rows_per_block - 1) / rows_per_block));
+  ozb::colmax_kernel<<<g1, 256, 0, h->stream>>>(X, ldx, n, lines, rows_per_block, h->colmax);
+  const dim3 g2(static_cast<unsigned>((lines + 31) / 32), static_cast<unsigned>((lds + 127) / 128));
+  ozb::slice_cols_bitmask_kernel<<<g2, 256, 0, h->stream>>>(X, ldx, n, lines, lds, k, beta,
+                                                             h->colmax, S, plane, out, h->flags);
+  CUDA_TRY(h, cudaGetLastError());
+  return OZMM_OK;
+}
+
 // ---- K2+K3 launch -------------------------------------------------------------
 constexpr size_t kSmemReserve = 2048;  // barriers, tmem slot, alignment slack (+ nu cache)
 
@@ -210,8 +327,11 @@ constexpr size_t kSmemReserve = 2048;  // barriers, tmem slot, alignment slack (
 void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t p, int64_t lds_a,
                  int64_t lds_b, int tiles_m, int tiles_n, int beta_bits, int stages, double alpha,
                  double beta, const double* mu, const double* nu, const double* Cin, double* Cout,
-                 int64_t ldc, int32_t* dump) {
+                 int64_t ldc, int32_t* dump, const FlushCfg& fl) {
   std::memset(&P, 0, sizeof P);
+  P.scale_mode = fl.scale_mode;
+  P.units_a = fl.units_a;
+  P.units_b = fl.units_b;
   P.m = static_cast<int>(m);
   P.p = static_cast<int>(p);
   P.n_kb = static_cast<int>((std::max(lds_a, lds_b) + ozb::kBK - 1) / ozb::kBK);
@@ -257,7 +377,10 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
     P.pr_s[i] = static_cast<uint8_t>(S.products[i].s);
     P.pr_t[i] = static_cast<uint8_t>(S.products[i].t);
   }
-  for (size_t c = 0; c < S.chunks.size(); ++c) P.c_g[c] = static_cast<uint8_t>(S.chunks[c].g);
+  for (size_t c = 0; c < S.chunks.size(); ++c) {
+    P.c_g[c] = static_cast<uint8_t>(S.chunks[c].g);
+    P.c_s[c] = static_cast<uint8_t>(S.chunks[c].s0);
+  }
   for (size_t q = 0; q < S.passes.size(); ++q) {
     P.p_g0[q] = static_cast<uint16_t>(S.passes[q].g0);
     P.p_g1[q] = static_cast<uint16_t>(S.passes[q].g1);
@@ -282,14 +405,15 @@ template <int kBN>
 int launch_gemm_bn(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_bits, int64_t r,
                    const int8_t* As, int64_t lds_a, int64_t plane_a, const double* mu, const int8_t* Bs,
                    int64_t lds_b, int64_t plane_b, const double* nu, double alpha, double beta, const double* Cin,
-                   double* Cout, int64_t ldc, int32_t* dump) {
+                   double* Cout, int64_t ldc, int32_t* dump, const FlushCfg& fl) {
   using Cfg = ozb::GemmCfg<kBN>;
   const size_t budget = h->smem_optin - kSmemReserve - kBN * sizeof(double);
   const int64_t max_stage = static_cast<int64_t>(budget / 3);
   auto slot_bytes = [](int a, int b) {
     return static_cast<int64_t>(a) * Cfg::kATile + static_cast<int64_t>(b) * Cfg::kBTile;
   };
-  const ozb::Schedule S = ozb::make_schedule(k, r, Cfg::kNAcc, max_stage, slot_bytes);
+  const ozb::Schedule S =
+      ozb::make_schedule(k, fl.per_product ? 1 : r, Cfg::kNAcc, max_stage, slot_bytes);
   if (!schedule_fits(S))
     return set_err(h, OZMM_ERR_UNSUPPORTED, "schedule too large (k=%d, r=%lld)", k,
                    static_cast<long long>(r));
@@ -302,7 +426,7 @@ int launch_gemm_bn(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_b
   const int tiles_m = static_cast<int>((m + ozb::kBM - 1) / ozb::kBM);
   const int tiles_n = static_cast<int>((p + kBN - 1) / kBN);
   fill_params(P, S, m, p, lds_a, lds_b, tiles_m, tiles_n, beta_bits, stages, alpha, beta, mu, nu,
-              Cin, Cout, ldc, dump);
+              Cin, Cout, ldc, dump, fl);
   CUtensorMap map_a, map_b;
   if (int rc = make_slice_map(h, &map_a, As, lds_a, m, plane_a, k, ozb::kBM)) return rc;
   if (int rc = make_slice_map(h, &map_b, Bs, lds_b, p, plane_b, k, kBN)) return rc;
@@ -325,12 +449,13 @@ template <int kBN, int kPairs>
 int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_bits, int64_t r,
                      const int8_t* As, int64_t lds_a, int64_t plane_a, const double* mu, const int8_t* Bs,
                      int64_t lds_b, int64_t plane_b, const double* nu, double alpha, double beta,
-                     const double* Cin, double* Cout, int64_t ldc, int32_t* dump) {
+                     const double* Cin, double* Cout, int64_t ldc, int32_t* dump,
+                     const FlushCfg& fl) {
   using Cfg = ozb::PairCfg<kBN, kPairs>;
   const size_t budget = h->smem_optin - kSmemReserve - kBN * sizeof(double);
   // passes are limited by the resident B slices per K block (A slices stream)
   auto slot_bytes = [](int, int b) { return static_cast<int64_t>(b) * Cfg::kBTile; };
-  const ozb::Schedule S = ozb::make_schedule(k, r, Cfg::kNAcc,
+  const ozb::Schedule S = ozb::make_schedule(k, fl.per_product ? 1 : r, Cfg::kNAcc,
                                              static_cast<int64_t>(Cfg::kMaxBSlots) * Cfg::kBTile,
                                              slot_bytes);
   if (!schedule_fits(S))
@@ -345,7 +470,7 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   const int tiles_m = static_cast<int>((m + rows_per_tile - 1) / rows_per_tile);
   const int tiles_n = static_cast<int>((p + kBN - 1) / kBN);
   fill_params(P, S, m, p, lds_a, lds_b, tiles_m, tiles_n, beta_bits, stages, alpha, beta, mu, nu,
-              Cin, Cout, ldc, dump);
+              Cin, Cout, ldc, dump, fl);
   if (kPairs > 1 && !std::getenv("OZMM_GROUP_M")) P.group_m = 1;
   P.n_kb = static_cast<int>((std::max(lds_a, lds_b) + ozb::kKB - 1) / ozb::kKB);
   CUtensorMap map_a, map_b;
@@ -372,26 +497,26 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
 int launch_gemm(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_bits, int64_t r,
                 const int8_t* As, int64_t lds_a, int64_t plane_a, const double* mu, const int8_t* Bs,
                 int64_t lds_b, int64_t plane_b, const double* nu, double alpha, double beta, const double* Cin, double* Cout,
-                int64_t ldc, const ozmm_options_t* opt) {
+                int64_t ldc, const ozmm_options_t* opt, const FlushCfg& fl = FlushCfg{}) {
   int32_t* dump = opt ? opt->chunk_dump : nullptr;
   const int tile_n = opt ? opt->tile_n : 0;
   const int pair = opt ? opt->cta_pair : 0;
   if (pair == 3 || (pair == 0 && tile_n == 0 && std::getenv("OZMM_QUAD")))
     return launch_gemm_pair<128, 2>(h, m, n, p, k, beta_bits, r, As, lds_a, plane_a, mu, Bs, lds_b,
-                                    plane_b, nu, alpha, beta, Cin, Cout, ldc, dump);
+                                    plane_b, nu, alpha, beta, Cin, Cout, ldc, dump, fl);
   if (pair == 2 || (pair == 0 && tile_n == 0))
     return launch_gemm_pair<128, 1>(h, m, n, p, k, beta_bits, r, As, lds_a, plane_a, mu, Bs, lds_b, plane_b, nu, alpha,
-                                 beta, Cin, Cout, ldc, dump);
+                                 beta, Cin, Cout, ldc, dump, fl);
   switch (tile_n ? tile_n : 64) {
     case 32:
       return launch_gemm_bn<32>(h, m, n, p, k, beta_bits, r, As, lds_a, plane_a, mu, Bs, lds_b, plane_b, nu, alpha,
-                                beta, Cin, Cout, ldc, dump);
+                                beta, Cin, Cout, ldc, dump, fl);
     case 64:
       return launch_gemm_bn<64>(h, m, n, p, k, beta_bits, r, As, lds_a, plane_a, mu, Bs, lds_b, plane_b, nu, alpha,
-                                beta, Cin, Cout, ldc, dump);
+                                beta, Cin, Cout, ldc, dump, fl);
     case 128:
       return launch_gemm_bn<128>(h, m, n, p, k, beta_bits, r, As, lds_a, plane_a, mu, Bs, lds_b, plane_b, nu,
-                                 alpha, beta, Cin, Cout, ldc, dump);
+                                 alpha, beta, Cin, Cout, ldc, dump, fl);
     default:
       return set_err(h, OZMM_ERR_ARG, "tile_n must be 32, 64 or 128 (got %d)", tile_n);
   }
@@ -455,6 +580,9 @@ int ozmm_destroy(ozmm_handle_t handle) {
   cudaFree(h->nu);
   cudaFree(h->colmax);
   cudaFree(h->flags);
+  cudaFree(h->units_a);
+  cudaFree(h->units_b);
+  cudaFree(h->tscratch);
   cudaFree(h->host_a);
   cudaFree(h->host_b);
   cudaFree(h->host_c);
@@ -619,6 +747,33 @@ int ozmm_split(ozmm_handle_t handle, char side, char trans, int64_t lines, int64
   return launch_split(h, row_mode, lines, n, X, ldx, k, beta, slices, lds, lines * lds, shift);
 }
 
+int ozmm_split_ex(ozmm_handle_t handle, char side, char trans, int64_t lines, int64_t n,
+                  const double* X, int64_t ldx, int k, int beta, int strategy, int8_t* slices,
+                  int64_t lds, double* out) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return set_err(nullptr, OZMM_ERR_ARG, "null handle");
+  if (strategy < 0 || strategy > 2) return set_err(h, OZMM_ERR_ARG, "unknown split strategy");
+  if (side != 'L' && side != 'R') return set_err(h, OZMM_ERR_ARG, "side must be 'L' or 'R'");
+  if (!valid_trans(trans)) return set_err(h, OZMM_ERR_ARG, "trans must be 'N' or 'T'");
+  if (lines < 1 || n < 1) return set_err(h, OZMM_ERR_ARG, "split: empty matrix");
+  if (k < 1 || k > ozb::kMaxK) return set_err(h, OZMM_ERR_ARG, "split: k must be in 1..%d", ozb::kMaxK);
+  if (lds < ozmm_slice_ld(n) || lds % 16) return set_err(h, OZMM_ERR_ARG, "split: lds too small or not a multiple of 16");
+  if (beta == 0) {
+    beta = ozb::compute_beta_host(n);
+    if (beta < 0) return set_err(h, OZMM_ERR_ARG, "compute_beta: n out of range");
+  } else if (beta < 1 || beta > 7) {
+    return set_err(h, OZMM_ERR_ARG, "split: forced beta outside 1..7");
+  }
+  const bool row_mode = (side == 'L') != is_trans(trans);
+  if (ldx < (row_mode ? n : lines)) return set_err(h, OZMM_ERR_ARG, "split: leading dimension too small");
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  if (strategy == 2)  // per-slice units start at zero (rows that vanish keep 0)
+    CUDA_TRY(h, cudaMemsetAsync(out, 0, sizeof(double) * k * lines, h->stream));
+  return launch_split_m(h, static_cast<Strategy>(strategy == 0 ? kRNConstShift
+                                                 : strategy == 1 ? kBitMask : kRNPerSlice),
+                        row_mode, lines, n, X, ldx, k, beta, slices, lds, lines * lds, out);
+}
+
 int ozmm_gemm_slices(ozmm_handle_t handle, int64_t m, int64_t n, int64_t p, int k, int beta_bits,
                      int64_t r, const int8_t* As, int64_t lds_a, const double* mu, const int8_t* Bs,
                      int64_t lds_b, const double* nu, double alpha, double beta, double* C,
@@ -665,6 +820,10 @@ int ozmm_dgemm_ex(ozmm_handle_t handle, char transa, char transb, int64_t m, int
   const int64_t fr = opt ? opt->force_r : 0;
   if (fr < 0) return set_err(h, OZMM_ERR_CONFIG, "force_r must be >= 1");
   const int64_t r = fr ? fr : ozb::compute_r_host(n, beta_bits);
+  MethodCfg mc;
+  if (!method_cfg(opt ? opt->method : 0, &mc)) return set_err(h, OZMM_ERR_CONFIG, "unknown method");
+  if (mc.simple && r < k)  // validate_config, scheme.cpp:169-173
+    return set_err(h, OZMM_ERR_CONFIG, "simple group-wise accumulation requires r >= k");
   const int64_t lda_need = is_trans(transa) ? m : n, ldb_need = is_trans(transb) ? n : p;
   if (lda < lda_need || ldb < ldb_need || ldc < p)
     return set_err(h, OZMM_ERR_ARG, "leading dimension too small");
@@ -678,14 +837,27 @@ int ozmm_dgemm_ex(ozmm_handle_t handle, char transa, char transb, int64_t m, int
 
   const bool want_t = (opt && opt->timings) || timings;
   if (want_t) CUDA_TRY(h, cudaEventRecord(h->ev[0], h->stream));
+  FlushCfg fl;
+  fl.per_product = mc.per_product;
+  fl.scale_mode = !mc.per_product ? 0 : (mc.strategy == kRNPerSlice ? 2 : 1);
+  double* out_a = h->mu;
+  double* out_b = h->nu;
+  if (mc.strategy == kRNPerSlice) {
+    if (int rc = ensure(h, &h->units_a, &h->units_a_n, static_cast<size_t>(k) * m)) return rc;
+    if (int rc = ensure(h, &h->units_b, &h->units_b_n, static_cast<size_t>(k) * p)) return rc;
+    CUDA_TRY(h, cudaMemsetAsync(h->units_a, 0, sizeof(double) * k * m, h->stream));
+    CUDA_TRY(h, cudaMemsetAsync(h->units_b, 0, sizeof(double) * k * p, h->stream));
+    fl.units_a = out_a = h->units_a;
+    fl.units_b = out_b = h->units_b;
+  }
   // split A (Left, rows of op(A)) -- split.cpp:233 via scheme.cpp:248
-  if (int rc = launch_split(h, !is_trans(transa), m, n, A, lda, k, beta_bits, h->slices_a, lds,
-                           m * lds, h->mu))
+  if (int rc = launch_split_m(h, mc.strategy, !is_trans(transa), m, n, A, lda, k, beta_bits,
+                              h->slices_a, lds, m * lds, out_a))
     return rc;
   if (want_t) CUDA_TRY(h, cudaEventRecord(h->ev[1], h->stream));
   // split B (Right, columns of op(B)) -- scheme.cpp:251
-  if (int rc = launch_split(h, is_trans(transb), p, n, B, ldb, k, beta_bits, h->slices_b, lds,
-                           p * lds, h->nu))
+  if (int rc = launch_split_m(h, mc.strategy, is_trans(transb), p, n, B, ldb, k, beta_bits,
+                              h->slices_b, lds, p * lds, out_b))
     return rc;
   if (want_t) CUDA_TRY(h, cudaEventRecord(h->ev[2], h->stream));
   if (opt && opt->sync_check)
@@ -693,14 +865,15 @@ int ozmm_dgemm_ex(ozmm_handle_t handle, char transa, char transb, int64_t m, int
   // fused group-wise accumulation + epilogue -- scheme.cpp:261-263, :286-287
   if (int rc = launch_gemm(h, m, n, p, k, beta_bits, r, h->slices_a, lds, m * lds, h->mu,
                            h->slices_b, lds, p * lds,
-                           h->nu, alpha, beta, C, C, ldc, opt))
+                           h->nu, alpha, beta, C, C, ldc, opt, fl))
     return rc;
   if (want_t) CUDA_TRY(h, cudaEventRecord(h->ev[3], h->stream));
   if (counts) {
     counts->int8_gemms = static_cast<int64_t>(k) * (k + 1) / 2;
     counts->r = r;
     counts->w = ozb::flush_count_w_host(k, r);
-    counts->fp64_flushes = static_cast<int64_t>(ozb::make_chunks(k, r).size());
+    counts->fp64_flushes =
+        mc.per_product ? counts->int8_gemms : static_cast<int64_t>(ozb::make_chunks(k, r).size());
   }
   if (timings) {
     CUDA_TRY(h, cudaEventSynchronize(h->ev[3]));
@@ -724,6 +897,38 @@ int ozmm_dgemm(ozmm_handle_t h, char transa, char transb, int64_t m, int64_t n, 
                        nullptr, nullptr);
 }
 
+// Host entry for the comparison methods: copy in, ozmm_dgemm_ex, copy out
+// (only ozIMMU_H, the hot path, gets the pipelined host entry below).
+int dgemm_host_simple(Handle* h, char transa, char transb, int64_t m, int64_t n, int64_t p,
+                      double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+                      double beta, double* C, int64_t ldc, int k, const ozmm_options_t* opt,
+                      ozmm_counts_t* counts, ozmm_timings_t* timings) {
+  const bool ta = is_trans(transa), tb = is_trans(transb);
+  const int64_t arows = ta ? n : m, brows = tb ? p : n, acols = ta ? m : n, bcols = tb ? n : p;
+  if (lda < acols || ldb < bcols || ldc < p) return set_err(h, OZMM_ERR_ARG, "leading dimension too small");
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  if (int rc = ensure(h, &h->host_a, &h->host_a_n, static_cast<size_t>(arows) * acols)) return rc;
+  if (int rc = ensure(h, &h->host_b, &h->host_b_n, static_cast<size_t>(brows) * bcols)) return rc;
+  if (int rc = ensure(h, &h->host_c, &h->host_c_n, static_cast<size_t>(m) * p)) return rc;
+  const size_t D = sizeof(double);
+  CUDA_TRY(h, cudaMemcpy2DAsync(h->host_a, D * acols, A, D * lda, D * acols, arows,
+                                cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, cudaMemcpy2DAsync(h->host_b, D * bcols, B, D * ldb, D * bcols, brows,
+                                cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, cudaMemcpy2DAsync(h->host_c, D * p, C, D * ldc, D * p, m, cudaMemcpyHostToDevice,
+                                h->stream));
+  ozmm_options_t o = opt ? *opt : ozmm_options_t{};
+  o.sync_check = 1;
+  if (int rc = ozmm_dgemm_ex(reinterpret_cast<ozmm_handle_t>(h), transa, transb, m, n, p, alpha,
+                             h->host_a, acols, h->host_b, bcols, beta, h->host_c, p, k, &o,
+                             counts, timings))
+    return rc;
+  CUDA_TRY(h, cudaMemcpy2DAsync(C, D * ldc, h->host_c, D * p, D * p, m, cudaMemcpyDeviceToHost,
+                                h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  return OZMM_OK;
+}
+
 int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, int64_t n,
                     int64_t p, double alpha, const double* A, int64_t lda, const double* B,
                     int64_t ldb, double beta, double* C, int64_t ldc, int k,
@@ -743,6 +948,9 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   if (k > ozb::kMaxK) return set_err(h, OZMM_ERR_UNSUPPORTED, "k > %d not supported on the GPU path", ozb::kMaxK);
   if (m < 1 || n < 1 || p < 1) return set_err(h, OZMM_ERR_ARG, "split: empty matrix");
   if (m > INT32_MAX || p > INT32_MAX) return set_err(h, OZMM_ERR_ARG, "m, p must fit int32");
+  if (opt && opt->method != OZMM_METHOD_OZIMMU_H)
+    return dgemm_host_simple(h, transa, transb, m, n, p, alpha, A, lda, B, ldb, beta, C, ldc, k,
+                             opt, counts, timings);
   const bool ta = is_trans(transa), tb = is_trans(transb);
   const int64_t arows = ta ? n : m, brows = tb ? p : n;
   const int64_t acols = ta ? m : n, bcols = tb ? n : p;

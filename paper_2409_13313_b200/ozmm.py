@@ -68,7 +68,7 @@ class Timings(C.Structure):
 class Options(C.Structure):
     _fields_ = [("force_beta", C.c_int), ("force_r", C.c_int64), ("timings", C.c_int),
                 ("sync_check", C.c_int), ("chunk_dump", C.c_void_p), ("tile_n", C.c_int),
-                ("cta_pair", C.c_int)]
+                ("cta_pair", C.c_int), ("method", C.c_int)]
 
 
 _SIG = {
@@ -93,6 +93,8 @@ _SIG = {
     "ozmm_slice_ld": ([_i64], _i64),
     "ozmm_split": ([_vp, C.c_char, C.c_char, _i64, _i64, _vp, _i64, C.c_int, C.c_int, _vp, _i64,
                     _vp], C.c_int),
+    "ozmm_split_ex": ([_vp, C.c_char, C.c_char, _i64, _i64, _vp, _i64, C.c_int, C.c_int, C.c_int,
+                       _vp, _i64, _vp], C.c_int),
     "ozmm_gemm_slices": ([_vp, _i64, _i64, _i64, C.c_int, C.c_int, _i64, _vp, _i64, _vp, _vp,
                           _i64, _vp, C.c_double, C.c_double, _vp, _i64, C.POINTER(Options)],
                          C.c_int),
@@ -309,6 +311,7 @@ def _options(cfg: SchemeConfig | None, timings: bool = False, dump=None, tile_n:
     if cfg is not None:
         o.force_beta = cfg.force_beta
         o.force_r = cfg.force_r
+        o.method = _method_code(cfg)
     o.timings = int(timings)
     o.sync_check = int(sync_check)
     o.chunk_dump = dump.data_ptr() if dump is not None else None
@@ -317,18 +320,32 @@ def _options(cfg: SchemeConfig | None, timings: bool = False, dump=None, tile_n:
     return o
 
 
+# (strategy, accumulation) -> OZMM_METHOD_* (include/ozmm_b200.h)
+_METHOD_CODES = {
+    (SliceStrategy.RoundNearestConstShift, Accumulation.Groupwise): 0,        # ozIMMU_H
+    (SliceStrategy.BitMask, Accumulation.PerProduct): 1,                      # ozIMMU
+    (SliceStrategy.RoundNearestPerSlice, Accumulation.PerProduct): 2,         # ozIMMU_RN
+    (SliceStrategy.BitMask, Accumulation.Groupwise): 3,                       # ozIMMU_EF
+    (SliceStrategy.RoundNearestConstShift, Accumulation.PerProduct): 4,
+    (SliceStrategy.RoundNearestConstShift, Accumulation.GroupwiseSimple): 5,
+}
+
+
+def _method_code(cfg: SchemeConfig) -> int:
+    return _METHOD_CODES[(cfg.strategy, cfg.accumulation)]
+
+
 def _validate(cfg: SchemeConfig):
-    # validate_config (scheme.cpp:161-174) + the GPU scope: ozIMMU_H only.
+    # validate_config (scheme.cpp:161-174); the r >= k rule of GroupwiseSimple is
+    # checked by the library once n is known.
     if cfg.k < 1:
         raise ConfigError("k must be >= 1")
     if cfg.strategy == SliceStrategy.RoundNearestPerSlice and \
             cfg.accumulation != Accumulation.PerProduct:
         raise ConfigError("per-slice round-to-nearest shifts are only valid with per-product "
                           "accumulation")
-    if (cfg.strategy, cfg.accumulation) != (SliceStrategy.RoundNearestConstShift,
-                                            Accumulation.Groupwise):
-        raise ConfigError("the B200 path implements the ozIMMU_H preset "
-                          "(RoundNearestConstShift + Groupwise) only")
+    if (cfg.strategy, cfg.accumulation) not in _METHOD_CODES:
+        raise ConfigError(f"unsupported scheme {cfg.strategy.name} + {cfg.accumulation.name}")
 
 
 def _to_result(counts: Counts, tim: Timings, d) -> OzakiResult:
@@ -462,6 +479,35 @@ def split_rn_const_shift(x, k: int, side: str = "L", *, trans: bool = False, for
     h.check(lib.ozmm_split(h.h, side.encode(), b"T" if trans else b"N", lines, n, x.data_ptr(),
                            x.stride(0), k, beta, sl.data_ptr(), lds, sh.data_ptr()))
     return SplitMatrix(side, k, beta, sl, sh, n)
+
+
+def split(x, k: int, side: str = "L", strategy: SliceStrategy = SliceStrategy.RoundNearestConstShift,
+          *, trans: bool = False, force_beta: int = 0, handle: Handle | None = None):
+    """Any strategy (split_bitmask / split_round_nearest / split_rn_const_shift,
+    split.cpp:223-237).  Returns SplitMatrix; for RoundNearestPerSlice its
+    ``shift`` holds the per-slice units [k][lines] (slice_units, split.hpp:38)."""
+    torch = _torch()
+    if not (_is_cuda_tensor(x) and x.dtype == torch.float64 and x.stride(-1) == 1):
+        raise ValueError("split needs a row-major float64 CUDA tensor")
+    side = side.upper()
+    rows, cols = x.shape
+    if side == "L":
+        lines, n = (cols, rows) if trans else (rows, cols)
+    else:
+        n, lines = (cols, rows) if trans else (rows, cols)
+    beta = force_beta or compute_beta(n)
+    lds = slice_ld(n)
+    h = handle or default_handle(x.device.index or 0)
+    h.set_stream(torch.cuda.current_stream(x.device).cuda_stream)
+    code = {SliceStrategy.RoundNearestConstShift: 0, SliceStrategy.BitMask: 1,
+            SliceStrategy.RoundNearestPerSlice: 2}[strategy]
+    sl = torch.empty((k, lines, lds), dtype=torch.int8, device=x.device)
+    out = torch.empty((k, lines) if code == 2 else (lines,), dtype=torch.float64,
+                      device=x.device)
+    h.check(lib.ozmm_split_ex(h.h, side.encode(), b"T" if trans else b"N", lines, n,
+                              x.data_ptr(), x.stride(0), k, beta, code, sl.data_ptr(), lds,
+                              out.data_ptr()))
+    return SplitMatrix(side, k, beta, sl, out, n)
 
 
 def gemm_slices(sa: SplitMatrix, sb: SplitMatrix, alpha: float, beta: float, c, *, r: int = 0,

@@ -90,10 +90,32 @@ def main() -> None:
         out[pre + "beta_underflow"] = np.array([sa.beta, int(sa.underflow), int(sb.underflow)])
         out[pre + "chunk_acc"] = ch.acc
         out[pre + "chunk_gs"] = np.stack([ch.g, ch.s0, ch.s1])
+    # comparison methods (config_for presets, scheme.cpp:137-159) on three cases
+    for name in ("phi1_k9_ab", "special_k8", "phi2_k8_r2"):
+        pre = f"{name}/"
+        m, n, p, k, fb, fr = (int(v) for v in out[pre + "params"])
+        phi, alpha, beta = (float(v) for v in out[pre + "scalars"])
+        a, b, c = out[pre + "A"], out[pre + "B"], out[pre + "C"]
+        for meth in ("ozIMMU", "ozIMMU_RN", "ozIMMU_EF"):
+            d, info = ref.gemm(alpha, a, b, beta, c, k=k, method=meth, force_beta=fb,
+                               force_r=fr, with_info=True)
+            out[pre + meth + "/out"] = d
+            out[pre + meth + "/counts"] = np.array(
+                [info["int8_gemms"], info["fp64_flushes"], info["r"], info["w"]], np.int64)
+        for strat in ("bitmask", "rn_per_slice"):
+            sa, ua = ref.split_any(a, k, strat, "left", force_beta=fb)
+            sb, ub = ref.split_any(b, k, strat, "right", force_beta=fb)
+            out[pre + strat + "/sliceA"], out[pre + strat + "/outA"] = sa, ua
+            out[pre + strat + "/sliceB"], out[pre + strat + "/outB"] = sb, ub
     # SPEC known answer: 351 = (101011111)_2, beta forced to 3
     s = ref.split(np.array([[351.0]]), 3, "left", force_beta=3, residual=True)
     out["spec351/slices"] = s.slices.ravel()
     out["spec351/shift"] = s.shift
+    sl, sh = ref.split_any(np.array([[351.0]]), 3, "bitmask", "left", force_beta=3)
+    out["spec351/bitmask_slices"] = sl.ravel()  # [5, 3, 7]
+    sl, un = ref.split_any(np.array([[351.0]]), 3, "rn_per_slice", "left", force_beta=3)
+    out["spec351/rnps_slices"] = sl.ravel()
+    out["spec351/rnps_units"] = un.ravel()
     # closed forms (AC4)
     ns = np.array([1, 2, 3, 1000, 1024, 1025, 8192, 16384, 65536, 2 ** 17, 2 ** 17 + 1,
                    2 ** 18, 2 ** 29], np.int64)
