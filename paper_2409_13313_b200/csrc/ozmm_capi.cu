@@ -457,7 +457,7 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   auto slot_bytes = [](int, int b) { return static_cast<int64_t>(b) * Cfg::kBTile; };
   const ozb::Schedule S = ozb::make_schedule(k, fl.per_product ? 1 : r, Cfg::kNAcc,
                                              static_cast<int64_t>(Cfg::kMaxBSlots) * Cfg::kBTile,
-                                             slot_bytes);
+                                             slot_bytes, Cfg::kMaxBSlots);
   if (!schedule_fits(S))
     return set_err(h, OZMM_ERR_UNSUPPORTED, "schedule too large (k=%d, r=%lld)", k,
                    static_cast<long long>(r));
@@ -690,7 +690,8 @@ int ozmm_debug_schedule(int k, int64_t r, int cta_pair, int tile_n, int* rows, i
   const int64_t max_stage = pair_kernel
                                 ? static_cast<int64_t>(ozb::PairCfg<128, 1>::kMaxBSlots) * b_tile
                                 : static_cast<int64_t>(budget / 3);
-  const ozb::Schedule S = ozb::make_schedule(k, r, n_acc, max_stage, slot_bytes);
+  const ozb::Schedule S = ozb::make_schedule(k, r, n_acc, max_stage, slot_bytes,
+                                             pair_kernel ? ozb::PairCfg<128, 1>::kMaxBSlots : 0);
   const int np = static_cast<int>(S.products.size());
   if (np > cap) return set_err(nullptr, OZMM_ERR_ARG, "debug_schedule: cap too small");
   for (int q = 0; q < static_cast<int>(S.passes.size()); ++q) {

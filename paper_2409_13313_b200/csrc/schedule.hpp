@@ -110,9 +110,16 @@ inline std::vector<Chunk> make_chunks(int k, int64_t r) {
 
 // stage_slot_bytes(a, b) must be <= max_stage_bytes for every pass (a single
 // product always fits: 1 A tile + 1 B tile).
+//
+// b_windows > 0 (the CTA-pair kernel, whose A slices stream through a ring and
+// only the B slices of a K block are resident): a batch's products are split
+// into passes by windows of at most b_windows consecutive B slices, so every
+// pass issues all products of its B window and each streamed A tile feeds as
+// many products as possible.  Otherwise passes are cut greedily in flush order
+// under stage_slot_bytes (the single-CTA kernels stage every slice of a pass).
 template <class SlotBytes>
 inline Schedule make_schedule(int k, int64_t r, int n_acc, int64_t max_stage_bytes,
-                              SlotBytes stage_slot_bytes) {
+                              SlotBytes stage_slot_bytes, int b_windows = 0) {
   Schedule S;
   S.chunks = make_chunks(k, r);
   const int w = static_cast<int>(S.chunks.size());
@@ -128,6 +135,10 @@ inline Schedule make_schedule(int k, int64_t r, int n_acc, int64_t max_stage_byt
       for (int s = c.s0; s <= c.s1; ++s) prods.push_back({ci, s, c.g - s, false});
     }
     std::vector<bool> seen(b.nc, false);
+    if (b_windows > 0) {
+      std::stable_sort(prods.begin(), prods.end(),
+                       [](const Product& x, const Product& y) { return x.t < y.t; });
+    }
     size_t i = 0;
     while (i < prods.size()) {
       Pass ps;
@@ -138,7 +149,11 @@ inline Schedule make_schedule(int k, int64_t r, int n_acc, int64_t max_stage_byt
       while (j < prods.size()) {
         const int alo = std::min(ps.alo, prods[j].s), ahi = std::max(ps.ahi, prods[j].s);
         const int blo = std::min(ps.blo, prods[j].t), bhi = std::max(ps.bhi, prods[j].t);
-        if (j > i && stage_slot_bytes(ahi - alo + 1, bhi - blo + 1) > max_stage_bytes) break;
+        if (b_windows > 0) {
+          if (bhi - blo + 1 > b_windows) break;
+        } else if (j > i && stage_slot_bytes(ahi - alo + 1, bhi - blo + 1) > max_stage_bytes) {
+          break;
+        }
         ps.alo = alo, ps.ahi = ahi, ps.blo = blo, ps.bhi = bhi;
         ++j;
       }
