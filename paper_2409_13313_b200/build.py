@@ -18,6 +18,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libozmm_b200.so")
+CLI = os.path.join(PKG, "ozmm_b200_cli")
+CLI_SRC = os.path.join(PKG, "cli", "ozmm_cli.cpp")
 SOURCES = [os.path.join(CSRC, "ozmm_capi.cu"), os.path.join(CSRC, "host_generate.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp"))] + [
     os.path.join(ROOT, "include", "ozmm_b200.h")]
@@ -58,8 +60,20 @@ def up_to_date(out: str = LIB) -> bool:
     return all(os.path.getmtime(d) <= t for d in DEPS if os.path.exists(d))
 
 
+def build_cli() -> str:
+    """The reference-CLI-compatible front end (gemm / counts) over the C ABI."""
+    cmd = [_host_cxx(), "-std=c++17", "-O2", "-Wall", "-o", CLI, CLI_SRC, f"-L{PKG}",
+           "-l:libozmm_b200.so", "-Wl,-rpath,$ORIGIN"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("CLI build failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
+    return CLI
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
+        if not os.path.exists(CLI) or os.path.getmtime(CLI) < os.path.getmtime(CLI_SRC):
+            build_cli()
         return LIB
     cmd = command(verbose_ptxas=verbose)
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -67,6 +81,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc build failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
     if verbose:
         sys.stderr.write(res.stdout + res.stderr)
+    build_cli()
     return LIB
 
 

@@ -39,3 +39,21 @@ import os as _os
 
 ROOT_HEADER = _os.path.join(_os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))),
                             "include", "ozmm_b200.h")
+
+
+def save_ozmm(path, m, kind=0):
+    """OZMM container (proj/src/io.cpp:16-18, :56-70): magic, version 1, kind, 6 zero
+    bytes, u64 LE rows, u64 LE cols, row-major LE payload."""
+    import struct
+    m = np.ascontiguousarray(m)
+    with open(path, "wb") as f:
+        f.write(b"OZMM" + bytes([1, kind]) + bytes(6) + struct.pack("<QQ", *m.shape))
+        f.write(m.tobytes())
+
+
+def load_ozmm(path):
+    import struct
+    raw = open(path, "rb").read()
+    assert raw[:4] == b"OZMM" and raw[4] == 1 and raw[5] == 0
+    rows, cols = struct.unpack("<QQ", raw[12:28])
+    return np.frombuffer(raw[28:], dtype="<f8").reshape(rows, cols)
