@@ -227,6 +227,17 @@ class RefLib(_Base):
         super().__init__(path)
         self.lib.ozref_split_any.argtypes = [C.c_int, _dp, _i64, _i64, C.c_int, C.c_int, C.c_int,
                                              _i8p, _dp]
+        self.lib.ozref_total_bound.argtypes = [C.c_int, C.c_int, C.c_int, _i64, _dp, _i64, _i64,
+                                               _dp, _i64, _dp]
+
+    def total_bound(self, a, b, k, method="ozIMMU_H", force_beta=0, force_r=0):
+        """The reference's section-5 elementwise bound (analysis.cpp:73-100)."""
+        a, b = _f64(a), _f64(b)
+        out = np.empty((a.shape[0], b.shape[1]), np.float64)
+        self._check(self.lib.ozref_total_bound(METHODS[method], k, force_beta, force_r,
+                                               _ptr(a, _dp), a.shape[0], a.shape[1],
+                                               _ptr(b, _dp), b.shape[1], _ptr(out, _dp)))
+        return out
 
     def split_any(self, a, k, strategy, side="left", force_beta=0):
         """strategy: "rn_const" | "bitmask" | "rn_per_slice".  Returns (slices, shift or units)."""

@@ -13,6 +13,7 @@
 //   exact_gemm_oracle / fp64_gemm_reference / max_rel_err  proj/src/oracle.cpp:276-335
 // Exceptions never cross this boundary: they become status codes plus a
 // thread-local message, mirroring the GPU library's error convention.
+#include "ozmm/analysis.hpp"
 #include "ozmm/generate.hpp"
 #include "ozmm/int_gemm.hpp"
 #include "ozmm/oracle.hpp"
@@ -229,6 +230,23 @@ int ozref_groupwise_chunks(const double* a, std::int64_t m, std::int64_t n, cons
       }
     }
     *w_out = w;
+  });
+}
+
+// total_bound (analysis.cpp:73-100) of ozaki_mm(A, B, config_for(method, k))
+// with |A||B| from exact_gemm_oracle(|A|, |B|), as verify_bounds does
+// (harness.cpp:156-157).  out: m x p elementwise bound.
+int ozref_total_bound(int method, int k, int force_beta, std::int64_t force_r, const double* a,
+                      std::int64_t m, std::int64_t n, const double* b, std::int64_t p,
+                      double* out) {
+  return guard([&] {
+    SchemeConfig cfg = config_for(method_of(method), k);
+    cfg.force_beta = force_beta;
+    cfg.force_r = force_r;
+    const MatrixF64 A = load(a, m, n), B = load(b, n, p);
+    const MatrixF64 absAB = exact_gemm_oracle(A.cwiseAbs(), B.cwiseAbs());
+    const ErrorBundle eb = total_bound(A, B, cfg, absAB);
+    std::memcpy(out, eb.total_bound.data(), sizeof(double) * m * p);
   });
 }
 
