@@ -39,7 +39,7 @@ template <int kBN, int kPairs = 1>
 struct PairCfg {
   static constexpr int kNAcc = 512 / kBN;
   static constexpr int kCluster = 2 * kPairs;             // CTAs per cluster
-  static constexpr int kBPart = kBN / 2 / kPairs;         // B rows each CTA loads (multicast)
+  static constexpr int kAPart = kBM / kPairs;             // A rows each CTA loads (multicast)
   static constexpr int kBHalf = kBN / 2;                  // B rows loaded per CTA
   static constexpr uint32_t kATile = kBM * kKB;           // 16 KB
   static constexpr uint32_t kBTile = kBHalf * kKB;        // bytes per CTA per B slice
@@ -48,10 +48,11 @@ struct PairCfg {
   static constexpr uint32_t kIdesc = ptx::idesc_i8(2 * kBM, kBN);
 };
 
-// kPairs = 2: a 4-CTA cluster of two CTA pairs stacked along M that share the
-// B tiles: each CTA loads 1/kPairs of its B half and TMA-multicasts it to the
-// same-half CTA of the other pair, halving B's L2->SM traffic and keeping the
-// pairs in lockstep (their B stages are released by both pairs' MMAs).
+// kPairs = 2: a 4-CTA cluster of two CTA pairs side by side along N that share
+// the A tiles (same 256 rows): each CTA loads half of its 128-row A tile and
+// TMA-multicasts it to the same-half CTA of the other pair, halving A's L2->SM
+// traffic (A is 2/3 of it).  An A stage is released by both pairs' MMAs, so the
+// pairs are coupled through the 6-deep A ring only; B stays per pair.
 template <int kBN, int kPairs>
 __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThreads, 1)
     ozimmu_gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a,
@@ -82,14 +83,15 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
   const uint16_t pair_mask = static_cast<uint16_t>(0x3u << (2 * pp));
   const uint16_t all_mask = static_cast<uint16_t>((1u << Cfg::kCluster) - 1);
 
-  // grouped raster over cluster tiles (256*kPairs rows x kBN columns)
+  // grouped raster over cluster tiles (256 rows x kPairs*kBN columns)
   const int bid = blockIdx.x / Cfg::kCluster;
   const int per_group = P.group_m * P.tiles_n;
   const int first_m = (bid / per_group) * P.group_m;
   const int gm = min(P.group_m, P.tiles_m - first_m);
   const int tm = first_m + (bid % per_group) % gm;  // pair row-block (256 rows)
   const int tn = (bid % per_group) / gm;
-  const int row_base = tm * Cfg::kCluster * kBM + static_cast<int>(rank) * kBM;
+  const int row_base = tm * 2 * kBM + static_cast<int>(rank & 1u) * kBM;
+  const int col_tile = tn * kPairs + static_cast<int>(pp);  // this pair's kBN-column tile
   const int n_kb = P.n_kb;  // 128-byte K blocks
 
   if (warp == 0 && lane == 0) {
@@ -97,11 +99,11 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
     ptx::tma_prefetch_desc(&map_b);
     for (int s = 0; s < kBBufs; ++s) {
       ptx::mbar_init(b_full + s, 1);
-      ptx::mbar_init(b_empty + s, kPairs);  // released by every pair that reads it
+      ptx::mbar_init(b_empty + s, 1);
     }
     for (int s = 0; s < n_a; ++s) {
       ptx::mbar_init(a_full + s, 1);
-      ptx::mbar_init(a_empty + s, 1);
+      ptx::mbar_init(a_empty + s, kPairs);  // released by every pair that reads it
     }
     ptx::mbar_init(tmem_full, 1);
     ptx::mbar_init(tmem_empty, 2 * kPairEpiWarps);
@@ -109,7 +111,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
   }
   if (warp == 1) ptx::tmem_alloc_pair<512>(tmem_base_smem);
   for (int j = threadIdx.x; j < kBN; j += blockDim.x) {
-    const int col = tn * kBN + j;
+    const int col = col_tile * kBN + j;
     nu_s[j] = col < P.p ? P.nu[col] : 0.0;
   }
   ptx::tc_fence_before();
@@ -122,9 +124,9 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
     if (ptx::elect_one()) {
       int bi = 0, ai = 0;
       uint32_t bph = 0, aph = 0;
-      const int b_row = tn * kBN + static_cast<int>(rank & 1u) * Cfg::kBHalf +
-                        static_cast<int>(pp) * Cfg::kBPart;
-      const uint16_t b_mask = static_cast<uint16_t>(kPairs == 1 ? 0 : (0x5u << (rank & 1u)));
+      const int b_row = col_tile * kBN + static_cast<int>(rank & 1u) * Cfg::kBHalf;
+      const int a_row = row_base + static_cast<int>(pp) * Cfg::kAPart;
+      const uint16_t a_mask = static_cast<uint16_t>(kPairs == 1 ? 0 : (0x5u << (rank & 1u)));
       const uint64_t pol_a = ptx::l2_policy(P.hint_a), pol_b = ptx::l2_policy(P.hint_b);
       for (int q = 0; q < P.npass; ++q) {
         const int blo = P.p_blo[q], bhi = P.p_bhi[q], g0 = P.p_g0[q], g1 = P.p_g1[q];
@@ -134,15 +136,10 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
           {
             const uint32_t fb = ptx::mapa_shared(b_full + bi, lead_rank);
             if (leader) ptx::mbar_arrive_expect_tx(b_full + bi, btx);
-            uint8_t* dst = bbuf + bi * Cfg::kBBuf + pp * Cfg::kBPart * kKB;
-            for (int t = blo; t <= bhi; ++t) {
-              if constexpr (kPairs == 1)
-                ptx::tma_load_3d_pair_hint(dst + (t - blo) * Cfg::kBTile, &map_b, fb, kb * kKB,
-                                           b_row, t - 1, pol_b);
-              else
-                ptx::tma_load_3d_pair_mc(dst + (t - blo) * Cfg::kBTile, &map_b, b_full + bi,
-                                         kb * kKB, b_row, t - 1, b_mask, pol_b);
-            }
+            uint8_t* dst = bbuf + bi * Cfg::kBBuf;
+            for (int t = blo; t <= bhi; ++t)
+              ptx::tma_load_3d_pair_hint(dst + (t - blo) * Cfg::kBTile, &map_b, fb, kb * kKB,
+                                         b_row, t - 1, pol_b);
           }
           if (++bi == kBBufs) {
             bi = 0;
@@ -152,8 +149,12 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
             ptx::mbar_wait(a_empty + ai, aph ^ 1);
             const uint32_t fa = ptx::mapa_shared(a_full + ai, lead_rank);
             if (leader) ptx::mbar_arrive_expect_tx(a_full + ai, 2u * Cfg::kATile);
-            ptx::tma_load_3d_pair_hint(aring + ai * Cfg::kATile, &map_a, fa, kb * kKB, row_base,
-                                       P.ag_s[g] - 1, pol_a);
+            if constexpr (kPairs == 1)
+              ptx::tma_load_3d_pair_hint(aring + ai * Cfg::kATile, &map_a, fa, kb * kKB, a_row,
+                                         P.ag_s[g] - 1, pol_a);
+            else
+              ptx::tma_load_3d_pair_mc(aring + ai * Cfg::kATile + pp * Cfg::kAPart * kKB, &map_a,
+                                       a_full + ai, kb * kKB, a_row, P.ag_s[g] - 1, a_mask, pol_a);
             if (++ai == n_a) {
               ai = 0;
               aph ^= 1;
@@ -192,7 +193,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
                     ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, Cfg::kIdesc,
                                      (first && j == 0) ? 0u : 1u);
                 }
-                ptx::mma_commit_pair(a_empty + ai, pair_mask);  // A stage free in the pair
+                ptx::mma_commit_pair(a_empty + ai, all_mask);  // A stage free (all sharers)
               }
               __syncwarp();
               if (++ai == n_a) {
@@ -200,7 +201,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
                 aph ^= 1;
               }
             }
-            if (ptx::elect_one()) ptx::mma_commit_pair(b_empty + bi, all_mask);
+            if (ptx::elect_one()) ptx::mma_commit_pair(b_empty + bi, pair_mask);
             __syncwarp();
             if (++bi == kBBufs) {
               bi = 0;
@@ -219,7 +220,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
     constexpr int kCols = kBN / 2;         // columns per epilogue warp
     constexpr int kLd = 16;
     const int row = row_base + quarter * 32 + lane;
-    const int col0 = tn * kBN + cslice * kCols;
+    const int col0 = col_tile * kBN + cslice * kCols;
     const bool row_ok = row < P.m;
     const double mu = row_ok ? P.mu[row] : 0.0;
     const uint32_t empty_leader = ptx::mapa_shared(tmem_empty, lead_rank);

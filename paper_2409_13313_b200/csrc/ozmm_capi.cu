@@ -179,17 +179,21 @@ int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const doubl
                  int k, int beta, int8_t* S, int64_t lds, int64_t plane, double* shift) {
   if (row_mode) {
     const bool vec = (reinterpret_cast<uintptr_t>(X) % 16 == 0) && (ldx % 2 == 0);
-    // Whole row in registers, 16 elements per thread.  Rows up to 8 x 512 x 16
-    // elements are split over a cluster of up to 8 CTAs (256 or 512 threads);
-    // longer rows use one 1024-thread CTA with a second pass.
+    // Whole row in registers, 16 elements per thread, split over a cluster of up
+    // to 8 CTAs (smallest CTAs first: more rows in flight per SM); longer rows
+    // use one 1024-thread CTA with a second pass.
     const int64_t chunks = (lds + 15) / 16;  // 16-element chunks per row
-    int csize = 0, cthreads = 256;
-    for (int t : {256, 512}) {
-      const int64_t c = (chunks + t - 1) / t;
-      if (c <= 8) {
-        csize = static_cast<int>(c);
-        cthreads = t;
-        break;
+    int csize = 0, cthreads = 128;
+    {
+      int t0 = 128;
+      if (const char* e = std::getenv("OZMM_ROW_CTA")) t0 = std::atoi(e);
+      for (int t : {t0, 256, 512}) {
+        const int64_t c = (chunks + t - 1) / t;
+        if (c <= 8) {
+          csize = static_cast<int>(c);
+          cthreads = t;
+          break;
+        }
       }
     }
     if (csize >= 2) {
@@ -466,18 +470,16 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   if (stages < 2)
     return set_err(h, OZMM_ERR_UNSUPPORTED, "A ring does not fit shared memory");
   ozb::GemmParams P;
-  const int rows_per_tile = Cfg::kCluster * ozb::kBM;
-  const int tiles_m = static_cast<int>((m + rows_per_tile - 1) / rows_per_tile);
-  const int tiles_n = static_cast<int>((p + kBN - 1) / kBN);
+  const int tiles_m = static_cast<int>((m + 2 * ozb::kBM - 1) / (2 * ozb::kBM));
+  const int tiles_n = static_cast<int>((p + kPairs * kBN - 1) / (kPairs * kBN));
   fill_params(P, S, m, p, lds_a, lds_b, tiles_m, tiles_n, beta_bits, stages, alpha, beta, mu, nu,
               Cin, Cout, ldc, dump, fl);
-  if (kPairs > 1 && !std::getenv("OZMM_GROUP_M")) P.group_m = 1;
   P.n_kb = static_cast<int>((std::max(lds_a, lds_b) + ozb::kKB - 1) / ozb::kKB);
   CUtensorMap map_a, map_b;
-  if (int rc = make_slice_map(h, &map_a, As, lds_a, m, plane_a, k, ozb::kBM, ozb::kKB,
+  if (int rc = make_slice_map(h, &map_a, As, lds_a, m, plane_a, k, Cfg::kAPart, ozb::kKB,
                               CU_TENSOR_MAP_SWIZZLE_128B))
     return rc;
-  if (int rc = make_slice_map(h, &map_b, Bs, lds_b, p, plane_b, k, Cfg::kBPart, ozb::kKB,
+  if (int rc = make_slice_map(h, &map_b, Bs, lds_b, p, plane_b, k, Cfg::kBHalf, ozb::kKB,
                               CU_TENSOR_MAP_SWIZZLE_128B))
     return rc;
   const size_t smem = fixed + stages * Cfg::kATile + kSmemReserve + kBN * sizeof(double);
