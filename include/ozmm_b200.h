@@ -195,6 +195,16 @@ int ozmm_gemm_slices(ozmm_handle_t h, int64_t m, int64_t n, int64_t p, int k, in
                      const int8_t* Bs, int64_t lds_b, const double* nu, double alpha,
                      double beta, double* C, int64_t ldc, const ozmm_options_t* opt);
 
+/* ozmm_gemm_slices with explicit slice-plane strides (elements between slice s
+ * and s+1): plane_a >= m*lds_a, plane_b >= p*lds_b.  Lets a caller run the
+ * GEMM on a row range of a taller A panel / a column range of a wider B panel
+ * in place (the 2-D grid's per-strip launches, grid2d.py). */
+int ozmm_gemm_slices_strided(ozmm_handle_t h, int64_t m, int64_t n, int64_t p, int k,
+                             int beta_bits, int64_t r, const int8_t* As, int64_t lds_a,
+                             int64_t plane_a, const double* mu, const int8_t* Bs, int64_t lds_b,
+                             int64_t plane_b, const double* nu, double alpha, double beta,
+                             double* C, int64_t ldc, const ozmm_options_t* opt);
+
 /* ---- introspection (host only; used by tests/test_host_logic.py) ---------- */
 /* The GEMM's host schedule for (k, r) and a kernel choice (cta_pair/tile_n as
  * in ozmm_options_t): one row of 8 ints per slice product, in issue order:

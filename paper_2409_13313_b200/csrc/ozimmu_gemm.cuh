@@ -68,7 +68,11 @@ struct GemmParams {
   double alpha, beta_c;
   const double* mu;    // [m] row shifts of op(A)
   const double* nu;    // [p] column shifts of op(B)
-  const double* c_in;  // [m x ldc] (read: fl(beta*c) is always formed, as the reference does)
+  // [m x ldc] (read: fl(beta*c) is always formed, as the reference does).  nullptr
+  // only from the host entry's beta = 0, alpha > 0 mode, where fl(alpha*d) + fl(0*c)
+  // equals fl(alpha*d) for every finite c (d is never -0) and the host patches the
+  // non-finite c entries afterwards.
+  const double* c_in;
   double* c_out;
   int64_t ldc;
   int32_t* dump;       // optional [n_chunks][m][p] INT32 chunk sums (parity/debug)
@@ -276,13 +280,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
 
     if (row_ok) {
-      const double* cin = P.c_in + static_cast<int64_t>(row) * P.ldc;
+      const double* cin = P.c_in ? P.c_in + static_cast<int64_t>(row) * P.ldc : nullptr;
       double* cout = P.c_out + static_cast<int64_t>(row) * P.ldc;
 #pragma unroll
       for (int j = 0; j < kHalf; ++j) {
         const int col = col0 + j;
         if (col < P.p)
-          cout[col] = __dadd_rn(__dmul_rn(P.alpha, d[j]), __dmul_rn(P.beta_c, cin[col]));
+          cout[col] = __dadd_rn(__dmul_rn(P.alpha, d[j]), cin ? __dmul_rn(P.beta_c, cin[col]) : 0.0);
       }
     }
   }

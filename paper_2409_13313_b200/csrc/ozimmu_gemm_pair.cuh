@@ -263,13 +263,13 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
     }
 
     if (row_ok) {
-      const double* cin = P.c_in + static_cast<int64_t>(row) * P.ldc;
+      const double* cin = P.c_in ? P.c_in + static_cast<int64_t>(row) * P.ldc : nullptr;
       double* cout = P.c_out + static_cast<int64_t>(row) * P.ldc;
 #pragma unroll
       for (int j = 0; j < kCols; ++j) {
         const int col = col0 + j;
         if (col < P.p)
-          cout[col] = __dadd_rn(__dmul_rn(P.alpha, d[j]), __dmul_rn(P.beta_c, cin[col]));
+          cout[col] = __dadd_rn(__dmul_rn(P.alpha, d[j]), cin ? __dmul_rn(P.beta_c, cin[col]) : 0.0);
       }
     }
   }

@@ -17,6 +17,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <utility>
 #include <vector>
 
 #include "../../include/ozmm_b200.h"
@@ -90,6 +92,9 @@ struct Handle {
   double* host_o = nullptr;  // GEMM output for the host entry (the input C stays intact)
   size_t host_o_n = 0;
   cudaStream_t s_in = nullptr, s_out = nullptr;  // copy streams of the host entry
+  cudaStream_t s_split = nullptr;                 // host entry: panel splits (high priority)
+  cudaStream_t s_gemm[2] = {nullptr, nullptr};    // host entry: strip GEMMs
+  int* hflags = nullptr;                          // pinned copy of flags (host entry gate)
   cudaEvent_t ev[5] = {};
   bool gemm_attr_set[3] = {false, false, false};
   bool pair_attr_set[2] = {false, false};
@@ -591,6 +596,10 @@ int ozmm_destroy(ozmm_handle_t handle) {
   cudaFree(h->host_o);
   if (h->s_in) cudaStreamDestroy(h->s_in);
   if (h->s_out) cudaStreamDestroy(h->s_out);
+  if (h->s_split) cudaStreamDestroy(h->s_split);
+  for (auto sg : h->s_gemm)
+    if (sg) cudaStreamDestroy(sg);
+  if (h->hflags) cudaFreeHost(h->hflags);
   for (auto& ev : h->ev) cudaEventDestroy(ev);
   delete h;
   return OZMM_OK;
@@ -781,6 +790,15 @@ int ozmm_gemm_slices(ozmm_handle_t handle, int64_t m, int64_t n, int64_t p, int 
                      int64_t r, const int8_t* As, int64_t lds_a, const double* mu, const int8_t* Bs,
                      int64_t lds_b, const double* nu, double alpha, double beta, double* C,
                      int64_t ldc, const ozmm_options_t* opt) {
+  return ozmm_gemm_slices_strided(handle, m, n, p, k, beta_bits, r, As, lds_a, m * lds_a, mu, Bs,
+                                  lds_b, p * lds_b, nu, alpha, beta, C, ldc, opt);
+}
+
+int ozmm_gemm_slices_strided(ozmm_handle_t handle, int64_t m, int64_t n, int64_t p, int k,
+                             int beta_bits, int64_t r, const int8_t* As, int64_t lds_a,
+                             int64_t plane_a, const double* mu, const int8_t* Bs, int64_t lds_b,
+                             int64_t plane_b, const double* nu, double alpha, double beta,
+                             double* C, int64_t ldc, const ozmm_options_t* opt) {
   Handle* h = reinterpret_cast<Handle*>(handle);
   if (!h) return set_err(nullptr, OZMM_ERR_ARG, "null handle");
   if (m < 1 || n < 1 || p < 1) return set_err(h, OZMM_ERR_ARG, "empty shape");
@@ -790,12 +808,13 @@ int ozmm_gemm_slices(ozmm_handle_t handle, int64_t m, int64_t n, int64_t p, int 
   if (ldc < p) return set_err(h, OZMM_ERR_ARG, "ldc < p");
   if (lds_a % 16 || lds_b % 16 || lds_a < n || lds_b < n)
     return set_err(h, OZMM_ERR_ARG, "slice strides must be multiples of 16 and >= n");
+  if (plane_a < m * lds_a || plane_b < p * lds_b || plane_a % 16 || plane_b % 16)
+    return set_err(h, OZMM_ERR_ARG, "slice plane strides must be multiples of 16 and cover the plane");
   if (r == 0) r = ozb::compute_r_host(n, beta_bits);
   if (r < 1) return set_err(h, OZMM_ERR_CONFIG, "force_r must be >= 1");
   CUDA_TRY(h, cudaSetDevice(h->device));
-  return launch_gemm(h, m, n, p, k, beta_bits, r, As, lds_a, m * lds_a, mu, Bs, lds_b, p * lds_b, nu,
-                     alpha, beta, C, C,
-                     ldc, opt);
+  return launch_gemm(h, m, n, p, k, beta_bits, r, As, lds_a, plane_a, mu, Bs, lds_b, plane_b, nu,
+                     alpha, beta, C, C, ldc, opt);
 }
 
 int ozmm_dgemm_ex(ozmm_handle_t handle, char transa, char transb, int64_t m, int64_t n, int64_t p,
@@ -936,13 +955,30 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
                     int64_t p, double alpha, const double* A, int64_t lda, const double* B,
                     int64_t ldb, double beta, double* C, int64_t ldc, int k,
                     const ozmm_options_t* opt, ozmm_counts_t* counts, ozmm_timings_t* timings) {
-  // Pipelined host entry.  H2D stream: B, then (A panel i, C panel i) for each
-  // row panel of op(A)/C; compute stream: split B, then per panel split A_i and
-  // the fused GEMM into a separate output buffer; D2H stream: result panel i as
-  // soon as GEMM_i is done.  Copies overlap slicing/GEMM, and H2D overlaps D2H.
-  // A range error (row max >= 2^921) is only known once every split ran: the
-  // device still holds the caller's original C, which is then copied back, so
-  // on error C is left as it was -- the reference throws without touching it.
+  // Pipelined host entry (the reference's calling convention: host matrices in,
+  // C overwritten).  op(A) is cut into row panels A_s and op(B) into column
+  // panels B_s (about 16 of each), sent over PCIe in the order A_0 B_0 A_1 B_1
+  // ... .  When A_s lands, the row strip (A_s x B_0..B_{s-1}) of C becomes
+  // computable; when B_s lands, the column strip (A_0..A_s x B_s).  Each strip
+  // is one fused-GEMM launch (two GEMM streams, so a small strip's tail overlaps
+  // the next one), the panel splits run on a high-priority stream, and finished
+  // strips go back on the D2H stream.  The GEMM therefore starts after 2/16 of
+  // an operand has crossed PCIe instead of after all of B.
+  //
+  // C input.  fl(beta*c) is always formed (scheme.cpp:287).  For beta = +-0 and
+  // alpha > 0 it cannot change a finite entry: D is never -0 (it starts at +0 and
+  // only exact cancellation gives zero, which rounds to +0), so fl(alpha*d) is
+  // never -0 and fl(alpha*d) + (+-0) = fl(alpha*d).  In that mode C is NOT
+  // copied to the device: host threads scan it for non-finite entries while the
+  // GPU works, and those entries are recomputed on the host afterwards as
+  // fl(fl(alpha*d) + fl(beta*c)) -- the reference's own expression.  Otherwise
+  // C strips are copied in just ahead of their GEMM.
+  //
+  // Errors.  A range error (row max >= 2^921, split.cpp:124-125) is only known
+  // once every panel is split; the reference throws without touching C.  With C
+  // on the device the original is copied back on error; in the no-C mode the
+  // D2H copies are not issued until the last split has run and the flags are
+  // clear, so C is never written on error.
   Handle* h = reinterpret_cast<Handle*>(handle);
   if (!h) return set_err(nullptr, OZMM_ERR_ARG, "null handle");
   if (!valid_trans(transa) || !valid_trans(transb))
@@ -955,7 +991,6 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
     return dgemm_host_simple(h, transa, transb, m, n, p, alpha, A, lda, B, ldb, beta, C, ldc, k,
                              opt, counts, timings);
   const bool ta = is_trans(transa), tb = is_trans(transb);
-  const int64_t arows = ta ? n : m, brows = tb ? p : n;
   const int64_t acols = ta ? m : n, bcols = tb ? n : p;
   if (lda < acols || ldb < bcols || ldc < p) return set_err(h, OZMM_ERR_ARG, "leading dimension too small");
   const int fb = opt ? opt->force_beta : 0;
@@ -970,94 +1005,224 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   const int64_t fr = opt ? opt->force_r : 0;
   if (fr < 0) return set_err(h, OZMM_ERR_CONFIG, "force_r must be >= 1");
   const int64_t r = fr ? fr : ozb::compute_r_host(n, beta_bits);
+  const bool no_c = beta == 0.0 && alpha > 0.0 && !(opt && opt->chunk_dump);
+
+  // panels: ~16 per operand, A panels in whole CTA-pair tile rows (256), B panels
+  // in whole tile columns (128)
+  int64_t npanels = 16;
+  if (const char* e = std::getenv("OZMM_HOST_PANELS")) npanels = std::max(1, std::atoi(e));
+  auto round_up = [](int64_t x, int64_t q) { return (x + q - 1) / q * q; };
+  int64_t pa = round_up((m + npanels - 1) / npanels, 256), pb = round_up((p + npanels - 1) / npanels, 128);
+  if (pa >= m) pa = m;
+  if (pb >= p) pb = p;
+  const int ra = static_cast<int>((m + pa - 1) / pa), rb = static_cast<int>((p + pb - 1) / pb);
+  const int steps = std::max(ra, rb);
 
   CUDA_TRY(h, cudaSetDevice(h->device));
   const int64_t lds = ozmm_slice_ld(n);
-  if (int rc = ensure(h, &h->host_a, &h->host_a_n, static_cast<size_t>(arows) * acols)) return rc;
-  if (int rc = ensure(h, &h->host_b, &h->host_b_n, static_cast<size_t>(brows) * bcols)) return rc;
-  if (int rc = ensure(h, &h->host_c, &h->host_c_n, static_cast<size_t>(m) * p)) return rc;
+  if (int rc = ensure(h, &h->host_a, &h->host_a_n, static_cast<size_t>(m) * n)) return rc;
+  if (int rc = ensure(h, &h->host_b, &h->host_b_n, static_cast<size_t>(n) * p)) return rc;
+  if (!no_c)
+    if (int rc = ensure(h, &h->host_c, &h->host_c_n, static_cast<size_t>(m) * p)) return rc;
   if (int rc = ensure(h, &h->host_o, &h->host_o_n, static_cast<size_t>(m) * p)) return rc;
   if (int rc = ensure(h, &h->slices_a, &h->slices_a_bytes, static_cast<size_t>(k) * m * lds)) return rc;
   if (int rc = ensure(h, &h->slices_b, &h->slices_b_bytes, static_cast<size_t>(k) * p * lds)) return rc;
   if (int rc = ensure(h, &h->mu, &h->mu_n, static_cast<size_t>(m))) return rc;
   if (int rc = ensure(h, &h->nu, &h->nu_n, static_cast<size_t>(p))) return rc;
+  // column-line splits reuse h->colmax: size it once so no launch reallocates it
+  if (int rc = ensure(h, &h->colmax, &h->colmax_n, static_cast<size_t>(std::max(pa, pb)))) return rc;
   if (!h->s_in) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
   if (!h->s_out) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
+  if (!h->s_split) {
+    int lo = 0, hi = 0;
+    CUDA_TRY(h, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CUDA_TRY(h, cudaStreamCreateWithPriority(&h->s_split, cudaStreamNonBlocking, hi));
+  }
+  for (auto& sg : h->s_gemm)
+    if (!sg) CUDA_TRY(h, cudaStreamCreateWithFlags(&sg, cudaStreamNonBlocking));
+  if (!h->hflags) CUDA_TRY(h, cudaMallocHost(reinterpret_cast<void**>(&h->hflags), 2 * sizeof(int)));
   double *dA = h->host_a, *dB = h->host_b, *dC = h->host_c, *dO = h->host_o;
   const size_t D = sizeof(double);
 
-  // row panels of op(A) / C: multiples of 256 rows (one CTA-pair tile row)
-  int64_t prow = std::max<int64_t>(256, (m / 8 + 255) / 256 * 256);
-  if (prow >= m) prow = m;
-  const int npan = static_cast<int>((m + prow - 1) / prow);
-  std::vector<cudaEvent_t> ev(3 * npan + 3);
-  for (auto& e : ev) CUDA_TRY(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  auto destroy = [&] {
-    for (auto& e : ev) cudaEventDestroy(e);
+  // strips in issue order: step s = row strip (A_s x B_<s), column strip (A_<=s x B_s)
+  struct Strip {
+    int64_t r0, rows, c0, cols;
+    int step;
+    bool row;
   };
-  cudaEvent_t evB = ev[3 * npan], evStart = ev[3 * npan + 2];
+  std::vector<Strip> strips;
+  for (int s = 0; s < steps; ++s) {
+    if (s < ra && std::min(s, rb) > 0)
+      strips.push_back({s * pa, std::min(pa, m - s * pa), 0, std::min<int64_t>(p, std::min(s, rb) * pb), s, true});
+    if (s < rb)
+      strips.push_back({0, std::min<int64_t>(m, std::min(s + 1, ra) * pa), s * pb, std::min(pb, p - s * pb), s, false});
+  }
+  const int ns = static_cast<int>(strips.size());
+  // events: A/B copied [ra + rb], A/B split [ra + rb], C strip copied [ns], GEMM done [ns], start, splits done
+  std::vector<cudaEvent_t> ev(2 * (ra + rb) + 2 * ns + 2);
+  for (auto& e : ev) CUDA_TRY(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaEvent_t* evA = ev.data();
+  cudaEvent_t* evB = evA + ra;
+  cudaEvent_t* evSA = evB + rb;
+  cudaEvent_t* evSB = evSA + ra;
+  cudaEvent_t* evC = evSB + rb;
+  cudaEvent_t* evG = evC + ns;
+  cudaEvent_t evStart = evG[ns], evSplit = evG[ns + 1];
+  cudaStream_t user = h->stream;
   int rc = OZMM_OK;
   auto cu = [&](cudaError_t e, const char* what) {
     if (e != cudaSuccess && rc == OZMM_OK)
       rc = set_err(h, OZMM_ERR_CUDA, "%s failed: %s", what, cudaGetErrorString(e));
     return e == cudaSuccess;
   };
-  // the copy streams must not run ahead of earlier work on the handle's stream
-  cu(cudaEventRecord(evStart, h->stream), "event");
-  cu(cudaStreamWaitEvent(h->s_in, evStart, 0), "wait");
-  cu(cudaStreamWaitEvent(h->s_out, evStart, 0), "wait");
-  // B first: every GEMM panel needs all of its slices
-  cu(cudaMemcpy2DAsync(dB, D * bcols, B, D * ldb, D * bcols, brows, cudaMemcpyHostToDevice, h->s_in),
-     "H2D B");
-  cu(cudaEventRecord(evB, h->s_in), "event");
-  for (int i = 0; i < npan && rc == OZMM_OK; ++i) {
-    const int64_t r0 = i * prow, rows = std::min(prow, m - r0);
-    if (ta)  // op(A) rows r0.. = columns r0.. of the stored n x m A
-      cu(cudaMemcpy2DAsync(dA + r0, D * m, A + r0, D * lda, D * rows, n, cudaMemcpyHostToDevice,
-                           h->s_in), "H2D A");
-    else
-      cu(cudaMemcpy2DAsync(dA + r0 * n, D * n, A + r0 * lda, D * lda, D * n, rows,
-                           cudaMemcpyHostToDevice, h->s_in), "H2D A");
-    cu(cudaEventRecord(ev[3 * i], h->s_in), "event");
-    cu(cudaMemcpy2DAsync(dC + r0 * p, D * p, C + r0 * ldc, D * ldc, D * p, rows,
+
+  // host scan of C for non-finite entries (no-C mode), concurrent with the GPU
+  std::vector<std::thread> scanners;
+  std::vector<std::vector<std::pair<int64_t, double>>> bad;  // (index, original c)
+  if (no_c) {
+    const int nt = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>({8, static_cast<int64_t>(std::thread::hardware_concurrency()), (m * p) >> 20})));
+    bad.resize(nt);
+    for (int t = 0; t < nt; ++t)
+      scanners.emplace_back([&, t, nt] {
+        const int64_t i0 = m * t / nt, i1 = m * (t + 1) / nt;
+        for (int64_t i = i0; i < i1; ++i) {
+          const uint64_t* row = reinterpret_cast<const uint64_t*>(C + i * ldc);
+          uint64_t any = 0;
+          for (int64_t j = 0; j < p; ++j)
+            any |= static_cast<uint64_t>((row[j] & 0x7FF0000000000000ull) == 0x7FF0000000000000ull);
+          if (any)
+            for (int64_t j = 0; j < p; ++j)
+              if ((row[j] & 0x7FF0000000000000ull) == 0x7FF0000000000000ull)
+                bad[t].push_back({i * ldc + j, C[i * ldc + j]});
+        }
+      });
+  }
+
+  // every stream starts after earlier work on the handle's stream
+  cu(cudaEventRecord(evStart, user), "event");
+  for (cudaStream_t s : {h->s_in, h->s_out, h->s_split, h->s_gemm[0], h->s_gemm[1]})
+    cu(cudaStreamWaitEvent(s, evStart, 0), "wait");
+
+  // H2D stream: A_s, [C row strip], B_s, [C column strip]
+  auto copy_c = [&](int q) {
+    const Strip& t = strips[q];
+    cu(cudaMemcpy2DAsync(dC + t.r0 * p + t.c0, D * p, C + t.r0 * ldc + t.c0, D * ldc, D * t.cols, t.rows,
                          cudaMemcpyHostToDevice, h->s_in), "H2D C");
-    cu(cudaEventRecord(ev[3 * i + 1], h->s_in), "event");
+    cu(cudaEventRecord(evC[q], h->s_in), "event");
+  };
+  {
+    int q = 0;
+    for (int s = 0; s < steps && rc == OZMM_OK; ++s) {
+      if (s < ra) {
+        const int64_t r0 = s * pa, rows = std::min(pa, m - r0);
+        if (ta)  // op(A) rows r0.. = columns r0.. of the stored n x m A
+          cu(cudaMemcpy2DAsync(dA + r0, D * m, A + r0, D * lda, D * rows, n, cudaMemcpyHostToDevice,
+                               h->s_in), "H2D A");
+        else
+          cu(cudaMemcpy2DAsync(dA + r0 * n, D * n, A + r0 * lda, D * lda, D * n, rows,
+                               cudaMemcpyHostToDevice, h->s_in), "H2D A");
+        cu(cudaEventRecord(evA[s], h->s_in), "event");
+        if (q < ns && strips[q].step == s && strips[q].row) {
+          if (!no_c) copy_c(q);
+          ++q;
+        }
+      }
+      if (s < rb) {
+        const int64_t c0 = s * pb, cols = std::min(pb, p - c0);
+        if (tb)  // op(B) columns c0.. = rows c0.. of the stored p x n B
+          cu(cudaMemcpy2DAsync(dB + c0 * n, D * n, B + c0 * ldb, D * ldb, D * n, cols,
+                               cudaMemcpyHostToDevice, h->s_in), "H2D B");
+        else
+          cu(cudaMemcpy2DAsync(dB + c0, D * p, B + c0, D * ldb, D * cols, n, cudaMemcpyHostToDevice,
+                               h->s_in), "H2D B");
+        cu(cudaEventRecord(evB[s], h->s_in), "event");
+        if (!no_c) copy_c(q);
+        ++q;
+      }
+    }
   }
-  // compute stream
-  if (rc == OZMM_OK) cu(cudaStreamWaitEvent(h->stream, evB, 0), "wait");
-  if (rc == OZMM_OK)
-    rc = launch_split(h, tb, p, n, dB, bcols, k, beta_bits, h->slices_b, lds, p * lds, h->nu);
-  for (int i = 0; i < npan && rc == OZMM_OK; ++i) {
-    const int64_t r0 = i * prow, rows = std::min(prow, m - r0);
-    cu(cudaStreamWaitEvent(h->stream, ev[3 * i], 0), "wait");
+  // split stream (high priority): A_s then B_s, each as soon as it lands
+  for (int s = 0; s < steps && rc == OZMM_OK; ++s) {
+    h->stream = h->s_split;
+    if (s < ra) {
+      const int64_t r0 = s * pa, rows = std::min(pa, m - r0);
+      cu(cudaStreamWaitEvent(h->s_split, evA[s], 0), "wait");
+      if (rc == OZMM_OK)
+        rc = launch_split(h, !ta, rows, n, ta ? dA + r0 : dA + r0 * n, ta ? m : n, k, beta_bits,
+                          h->slices_a + r0 * lds, lds, m * lds, h->mu + r0);
+      cu(cudaEventRecord(evSA[s], h->s_split), "event");
+    }
+    if (s < rb && rc == OZMM_OK) {
+      const int64_t c0 = s * pb, cols = std::min(pb, p - c0);
+      cu(cudaStreamWaitEvent(h->s_split, evB[s], 0), "wait");
+      if (rc == OZMM_OK)
+        rc = launch_split(h, tb, cols, n, tb ? dB + c0 * n : dB + c0, tb ? n : p, k, beta_bits,
+                          h->slices_b + c0 * lds, lds, p * lds, h->nu + c0);
+      cu(cudaEventRecord(evSB[s], h->s_split), "event");
+    }
+  }
+  cu(cudaEventRecord(evSplit, h->s_split), "event");
+  // GEMM streams: one fused launch per strip (the split stream is in order, so the
+  // strip's last split event covers every panel it reads)
+  for (int q = 0; q < ns && rc == OZMM_OK; ++q) {
+    const Strip& t = strips[q];
+    cudaStream_t sg = h->s_gemm[q & 1];
+    cu(cudaStreamWaitEvent(sg, t.row ? evSA[t.step] : evSB[t.step], 0), "wait");
+    if (!no_c) cu(cudaStreamWaitEvent(sg, evC[q], 0), "wait");
+    h->stream = sg;
     if (rc == OZMM_OK)
-      rc = launch_split(h, !ta, rows, n, ta ? dA + r0 : dA + r0 * n, ta ? m : n, k, beta_bits,
-                        h->slices_a + r0 * lds, lds, m * lds, h->mu + r0);
-    cu(cudaStreamWaitEvent(h->stream, ev[3 * i + 1], 0), "wait");
-    if (rc == OZMM_OK)
-      rc = launch_gemm(h, rows, n, p, k, beta_bits, r, h->slices_a + r0 * lds, lds, m * lds,
-                       h->mu + r0, h->slices_b, lds, p * lds, h->nu, alpha, beta, dC + r0 * p,
-                       dO + r0 * p, p, opt);
-    cu(cudaEventRecord(ev[3 * i + 2], h->stream), "event");
-    cu(cudaStreamWaitEvent(h->s_out, ev[3 * i + 2], 0), "wait");
-    cu(cudaMemcpy2DAsync(C + r0 * ldc, D * ldc, dO + r0 * p, D * p, D * p, rows,
+      rc = launch_gemm(h, t.rows, n, t.cols, k, beta_bits, r, h->slices_a + t.r0 * lds, lds, m * lds,
+                       h->mu + t.r0, h->slices_b + t.c0 * lds, lds, p * lds, h->nu + t.c0, alpha, beta,
+                       no_c ? nullptr : dC + t.r0 * p + t.c0, dO + t.r0 * p + t.c0, p, opt);
+    cu(cudaEventRecord(evG[q], sg), "event");
+  }
+  h->stream = user;
+  auto copy_out = [&](int q) {
+    const Strip& t = strips[q];
+    cu(cudaStreamWaitEvent(h->s_out, evG[q], 0), "wait");
+    cu(cudaMemcpy2DAsync(C + t.r0 * ldc + t.c0, D * ldc, dO + t.r0 * p + t.c0, D * p, D * t.cols, t.rows,
                          cudaMemcpyDeviceToHost, h->s_out), "D2H C");
+  };
+  bool range_err = false;
+  if (!no_c) {
+    for (int q = 0; q < ns && rc == OZMM_OK; ++q) copy_out(q);
+  } else {
+    // gate: every split done and its flags clear before C is written at all
+    cu(cudaEventSynchronize(evSplit), "sync");
+    cu(cudaMemcpyAsync(h->hflags, h->flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->s_out), "flags");
+    cu(cudaStreamSynchronize(h->s_out), "sync");
+    range_err = rc == OZMM_OK && h->hflags[1] != 0;
+    for (auto& th : scanners) th.join();  // every c read before any D2H writes C
+    for (int q = 0; q < ns && rc == OZMM_OK && !range_err; ++q) copy_out(q);
   }
-  cu(cudaStreamSynchronize(h->s_out), "sync");
-  cu(cudaStreamSynchronize(h->stream), "sync");
-  cu(cudaStreamSynchronize(h->s_in), "sync");
-  if (rc == OZMM_OK) {
+  for (auto& th : scanners)
+    if (th.joinable()) th.join();
+  for (cudaStream_t s : {h->s_in, h->s_split, h->s_gemm[0], h->s_gemm[1], h->s_out})
+    cu(cudaStreamSynchronize(s), "sync");
+  if (rc == OZMM_OK && !no_c) {
     int f[2] = {0, 0};
     cu(cudaMemcpy(f, h->flags, sizeof f, cudaMemcpyDeviceToHost), "flags");
     if (f[1]) {  // restore the caller's C, then report like the reference's throw
-      const int zero = 0;
-      cu(cudaMemcpy(h->flags + 1, &zero, sizeof(int), cudaMemcpyHostToDevice), "flags");
+      range_err = true;
       cu(cudaMemcpy2D(C, D * ldc, dC, D * p, D * p, m, cudaMemcpyDeviceToHost), "restore C");
-      if (rc == OZMM_OK)
-        rc = set_err(h, OZMM_ERR_RANGE, "split: row magnitude too large for shift extraction");
     }
   }
-  destroy();
+  if (range_err) {
+    const int zero = 0;
+    cu(cudaMemcpy(h->flags + 1, &zero, sizeof(int), cudaMemcpyHostToDevice), "flags");
+    if (rc == OZMM_OK) rc = set_err(h, OZMM_ERR_RANGE, "split: row magnitude too large for shift extraction");
+  }
+  if (rc == OZMM_OK && no_c) {
+    // non-finite c: the reference's fl(fl(alpha*d) + fl(beta*c)) on the host
+    // (the device wrote fl(alpha*d) there)
+    for (const auto& v : bad)
+      for (const auto& [idx, c] : v) {
+        const double z = beta * c;
+        C[idx] = C[idx] + z;
+      }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
   if (rc == OZMM_OK && counts) {
     counts->int8_gemms = static_cast<int64_t>(k) * (k + 1) / 2;
     counts->r = r;

@@ -15,7 +15,8 @@ Per step each rank:
      row communicator (the Pc ranks sharing gr), B planes inside its column
      communicator (the Pr ranks sharing gc).  No reductions: NCCL only
      broadcasts slice panels, as the north star asks,
-  3. runs the fused K2+K3 kernel on its C block.
+  3. runs the fused K2+K3 kernel on its C block in three strips, the first
+     of which needs no communication, so the gathers overlap the GEMM (step()).
 
 The compute backend is injectable (``Backend``): the default calls the CUDA
 library; tests/test_grid2d_gloo.py drives the same orchestration under gloo
@@ -117,13 +118,31 @@ class Backend:
             out_shift.data_ptr()))
 
     def gemm(self, m, n, p, k, beta_bits, a_slices, mu, b_slices, nu, alpha, beta, c):
+        """K2+K3 on [k][m][lds] / [k][p][lds] slice views (row / column ranges of a
+        panel are fine: the plane stride is passed through)."""
         oz = self.oz
         self.handle.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
         opt = oz.Options()
-        self.handle.check(oz.lib.ozmm_gemm_slices(
-            self.handle.h, m, n, p, k, beta_bits, 0, a_slices.data_ptr(), a_slices.shape[-1],
-            mu.data_ptr(), b_slices.data_ptr(), b_slices.shape[-1], nu.data_ptr(), alpha, beta,
-            c.data_ptr(), c.stride(0), ctypes.byref(opt)))
+        self.handle.check(oz.lib.ozmm_gemm_slices_strided(
+            self.handle.h, m, n, p, k, beta_bits, 0, a_slices.data_ptr(), a_slices.stride(1),
+            a_slices.stride(0), mu.data_ptr(), b_slices.data_ptr(), b_slices.stride(1),
+            b_slices.stride(0), nu.data_ptr(), alpha, beta, c.data_ptr(), c.stride(0),
+            ctypes.byref(opt)))
+
+
+def _new_group(ranks):
+    """Row / column communicator.  Under NCCL its stream is high priority, so the
+    gather kernels take SMs ahead of the GEMM's next CTAs as they free up."""
+    if dist.get_backend() == "nccl":
+        opts = dist.ProcessGroupNCCL.Options()
+        opts.is_high_priority_stream = True
+        return dist.new_group(ranks, pg_options=opts)
+    return dist.new_group(ranks)
+
+
+def _other_ranges(total: int, own0: int, own: int):
+    """[0, total) minus [own0, own0 + own), as up to two (start, stop) ranges."""
+    return [(a, b) for a, b in ((0, own0), (own0 + own, total)) if b > a]
 
 
 class Grid2DGemm:
@@ -139,19 +158,22 @@ class Grid2DGemm:
     """
 
     def __init__(self, m, n, p, k, *, world=None, rank=None, backend=None, transa=False,
-                 transb=False, group_factory=None):
+                 transb=False, group_factory=None, all_gather=None):
         self.world = world if world is not None else dist.get_world_size()
         self.rank = rank if rank is not None else dist.get_rank()
         self.L = make_layout(m, n, p, self.world, self.rank)
         self.k = k
         self.transa, self.transb = transa, transb
+        # all_gather(out, inp, group) -> work with .wait(); injectable for tests
+        self._all_gather = all_gather or (lambda out, inp, group: dist.all_gather_into_tensor(
+            out, inp, group=group, async_op=True))
         from .ozmm import compute_beta, slice_ld  # closed forms (host)
         self.beta_bits = compute_beta(n)
         self.lds = slice_ld(n)
         self.backend = backend
         L = self.L
         # every rank must create every group, in the same order
-        make = group_factory or (lambda ranks: dist.new_group(ranks))
+        make = group_factory or _new_group
         self.row_group = self.col_group = None
         for gr in range(L.pr):
             ranks = [gr * L.pc + gc for gc in range(L.pc)]
@@ -182,19 +204,43 @@ class Grid2DGemm:
 
     def _gather(self, out, inp, group, nranks):
         if nranks > 1:
-            dist.all_gather_into_tensor(out, inp, group=group)
+            return self._all_gather(out, inp, group)
+        return None
+
+    @staticmethod
+    def _wait(works):
+        for w in works:
+            if w is not None:
+                w.wait()
 
     def step(self, a_rows, b_cols, c_block, alpha=1.0, beta=0.0):
+        """One sharded emulated GEMM.  The slice-panel all-gathers run while the
+        GEMM works on what is already local, in three strip launches:
+          G1  own A rows x own B columns     -- needs no communication;
+          G2  own A rows x the other columns -- after the B (column-group) gather;
+          G3  the other rows x all columns   -- after the A (row-group) gather.
+        Every C entry is still produced by exactly one fused launch from the same
+        slices and shifts, so the result is bit-identical to one GPU."""
         L, k = self.L, self.k
         be = self.backend
         be.split(a_rows, k, "L", self.transa, self.beta_bits, self.a_loc, self.mu_loc)
         be.split(b_cols, k, "R", self.transb, self.beta_bits, self.b_loc, self.nu_loc)
-        # slice planes in order s = 1..k: group g of the GEMM needs slices <= g-1
-        for s in range(k):
-            self._gather(self.a_pan[s], self.a_loc[s], self.row_group, L.pc)
-            self._gather(self.b_pan[s], self.b_loc[s], self.col_group, L.pr)
-        self._gather(self.mu_pan, self.mu_loc, self.row_group, L.pc)
-        self._gather(self.nu_pan, self.nu_loc, self.col_group, L.pr)
-        be.gemm(L.mr, L.n, L.pcols, k, self.beta_bits, self.a_pan, self.mu_pan, self.b_pan,
-                self.nu_pan, alpha, beta, c_block)
+        # B first: it unblocks G2; group g of a GEMM needs slice planes <= g-1
+        wb = [self._gather(self.b_pan[s], self.b_loc[s], self.col_group, L.pr) for s in range(k)]
+        wb.append(self._gather(self.nu_pan, self.nu_loc, self.col_group, L.pr))
+        wa = [self._gather(self.a_pan[s], self.a_loc[s], self.row_group, L.pc) for s in range(k)]
+        wa.append(self._gather(self.mu_pan, self.mu_loc, self.row_group, L.pc))
+        r0, c0 = L.gc * L.ms, L.gr * L.ps  # own rows / columns inside the C block
+        g = (L.n, k, self.beta_bits)
+        own_rows = c_block[r0:r0 + L.ms]
+        be.gemm(L.ms, g[0], L.ps, k, g[2], self.a_loc, self.mu_loc, self.b_loc, self.nu_loc,
+                alpha, beta, own_rows[:, c0:c0 + L.ps])
+        self._wait(wb)
+        for lo, hi in _other_ranges(L.pcols, c0, L.ps):
+            be.gemm(L.ms, g[0], hi - lo, k, g[2], self.a_loc, self.mu_loc, self.b_pan[:, lo:hi],
+                    self.nu_pan[lo:hi], alpha, beta, own_rows[:, lo:hi])
+        self._wait(wa)
+        for lo, hi in _other_ranges(L.mr, r0, L.ms):
+            be.gemm(hi - lo, g[0], L.pcols, k, g[2], self.a_pan[:, lo:hi], self.mu_pan[lo:hi],
+                    self.b_pan, self.nu_pan, alpha, beta, c_block[lo:hi])
         return c_block

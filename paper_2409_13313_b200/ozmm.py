@@ -98,6 +98,9 @@ _SIG = {
     "ozmm_gemm_slices": ([_vp, _i64, _i64, _i64, C.c_int, C.c_int, _i64, _vp, _i64, _vp, _vp,
                           _i64, _vp, C.c_double, C.c_double, _vp, _i64, C.POINTER(Options)],
                          C.c_int),
+    "ozmm_gemm_slices_strided": ([_vp, _i64, _i64, _i64, C.c_int, C.c_int, _i64, _vp, _i64, _i64,
+                                  _vp, _vp, _i64, _i64, _vp, C.c_double, C.c_double, _vp, _i64,
+                                  C.POINTER(Options)], C.c_int),
     "ozmm_gen_phi_block": ([_i64, _i64, C.c_double, C.c_uint64, _i64, _i64, _i64, _i64, _vp,
                             _i64], C.c_int),
     "ozmm_counter_hash": ([C.c_uint64, C.c_uint64], C.c_uint64),

@@ -35,3 +35,76 @@ def test_grid2d_cuda_world1():
         assert torch.equal(got.view(torch.int64), want.view(torch.int64))
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_grid2d_cuda_emulated_ranks(world):
+    """All ranks of a Pr x Pc grid as threads on the one GPU, with an in-process
+    all-gather: the CUDA backend's strip launches (G1/G2/G3 on row/column ranges of
+    the gathered panels, ozmm_gemm_slices_strided) must tile C exactly like the
+    single call, bit for bit."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import threading
+    from paper_2409_13313_b200 import ozmm
+    from paper_2409_13313_b200.grid2d import Backend, Grid2DGemm, make_layout
+
+    m, n, p, k, alpha, beta = 1024, 2500, 768, 8, 1.25, -0.5
+    A = ozmm.gen_phi_matrix(m, n, 1.0, 11)
+    B = ozmm.gen_phi_matrix(n, p, 1.0, 12)
+    C = ozmm.gen_phi_matrix(m, p, 1.0, 13)
+    dev = lambda x: torch.tensor(np.ascontiguousarray(x), device="cuda")  # noqa: E731
+    want = ozmm.ozaki_gemm(alpha, dev(A), dev(B), beta, dev(C),
+                           ozmm.config_for("ozIMMU_H", k)).cpu().numpy()
+
+    barriers, pool, lock = {}, {}, threading.Lock()
+
+    class Done:
+        def wait(self):
+            pass
+
+    def all_gather(out, inp, group):
+        ranks = tuple(group)
+        me = threading.current_thread().rank
+        with lock:
+            bar = barriers.setdefault(ranks, threading.Barrier(len(ranks)))
+            seq = threading.current_thread().seq.setdefault(ranks, 0)
+            threading.current_thread().seq[ranks] = seq + 1
+        torch.cuda.synchronize()
+        with lock:
+            pool[(ranks, seq, me)] = inp
+        bar.wait()
+        parts = [pool[(ranks, seq, r)] for r in ranks]
+        out.copy_(torch.cat([x.reshape(-1) for x in parts]).view_as(out))
+        torch.cuda.synchronize()
+        bar.wait()
+        return Done()
+
+    got = np.full((m, p), np.nan)
+    errors = []
+
+    def run(rank):
+        try:
+            th = threading.current_thread()
+            th.rank, th.seq = rank, {}
+            L = make_layout(m, n, p, world, rank)
+            G = Grid2DGemm(m, n, p, k, world=world, rank=rank, backend=Backend(0),
+                           group_factory=lambda ranks: tuple(ranks), all_gather=all_gather)
+            a = dev(A[L.a_row0:L.a_row0 + L.ms])
+            b = dev(B[:, L.b_col0:L.b_col0 + L.ps])
+            c = dev(C[L.c_row0:L.c_row0 + L.mr, L.c_col0:L.c_col0 + L.pcols])
+            G.step(a, b, c, alpha, beta)
+            torch.cuda.synchronize()
+            got[L.c_row0:L.c_row0 + L.mr, L.c_col0:L.c_col0 + L.pcols] = c.cpu().numpy()
+        except BaseException as ex:  # surfaced below
+            errors.append(ex)
+            for bar in list(barriers.values()):
+                bar.abort()
+
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not errors, errors
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))

@@ -1,8 +1,8 @@
 """CPU, multi-process: the 2-D block partition (grid2d.Grid2DGemm) under gloo.
 
 Runs the real orchestration -- rank grid, row/column communicators, per-rank
-slicing of full rows/columns, slice-panel all-gathers -- with world sizes 2
-and 4 on CPU.  The compute backend is a TEST-ONLY stand-in (the GPU kernels
+slicing of full rows/columns, async slice-panel all-gathers overlapped with the
+three strip GEMMs -- with world sizes 2, 4 and 8 (grids 2x1, 2x2, 2x4) on CPU.  The compute backend is a TEST-ONLY stand-in (the GPU kernels
 need a B200): slicing by the oracle port, and the group-wise accumulation of
 the gathered slice panels restated in numpy (exact int64 products, the
 reference's flush order scheme.cpp:81-101 and flush arithmetic :29-41).
@@ -89,7 +89,7 @@ def _worker(rank, world, port, m, n, p, k, phi, alpha, beta, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_grid2d_matches_single_process(world, port):
     m, n, p, k, phi, alpha, beta = 32, 200, 48, 8, 1.0, 1.5, 0.5
     from paper_2409_13313_b200 import ozmm
@@ -114,4 +114,4 @@ def test_grid2d_matches_single_process(world, port):
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
 
 
-PORT = {2: _free_port(), 4: _free_port()}
+PORT = {2: _free_port(), 4: _free_port(), 8: _free_port()}
