@@ -464,9 +464,15 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   const size_t budget = h->smem_optin - kSmemReserve - kBN * sizeof(double);
   // passes are limited by the resident B slices per K block (A slices stream)
   auto slot_bytes = [](int, int b) { return static_cast<int64_t>(b) * Cfg::kBTile; };
+  ozb::PassCost cm;
+  cm.a_tile /= kPairs;  // the 4-CTA variant multicasts A: each CTA fills half
+  if (const char* e = std::getenv("OZMM_SCHED_BATCH")) cm.batch = std::atof(e);
+  if (const char* e = std::getenv("OZMM_SCHED_FILL"))  // scale of the fill terms
+    cm.a_tile *= std::atof(e), cm.b_tile *= std::atof(e);
+  if (const char* e = std::getenv("OZMM_SCHED")) cm.greedy = std::string(e) == "greedy";
   const ozb::Schedule S = ozb::make_schedule(k, fl.per_product ? 1 : r, Cfg::kNAcc,
                                              static_cast<int64_t>(Cfg::kMaxBSlots) * Cfg::kBTile,
-                                             slot_bytes, Cfg::kMaxBSlots);
+                                             slot_bytes, Cfg::kMaxBSlots, cm);
   if (!schedule_fits(S))
     return set_err(h, OZMM_ERR_UNSUPPORTED, "schedule too large (k=%d, r=%lld)", k,
                    static_cast<long long>(r));

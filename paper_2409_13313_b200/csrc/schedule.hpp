@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <utility>
 #include <vector>
 
 namespace ozb {
@@ -108,57 +109,158 @@ inline std::vector<Chunk> make_chunks(int k, int64_t r) {
   return out;
 }
 
+// Per-K-block cost model of one pass of the CTA-pair kernel, in SM clocks:
+// the tensor core needs `prod` per product (4 MMAs of K = 32), and the pass's
+// slice tiles must be filled from L2 (`a_tile` / `b_tile` per distinct A / B
+// slice).  A pass runs at the slower of the two.  Fitted on B200 (C3 vs C4,
+// profiles/r1/configs.csv): an SM fills about 48 B/clk while the GEMM runs.
+struct PassCost {
+  double prod = 256.0;    // 4 x (M=256, N=128, K=32) MMAs per CTA pair at 8192 MAC/clk/SM
+  double a_tile = 341.0;  // 16 KB A tile per CTA
+  double b_tile = 171.0;  // 8 KB B tile per CTA
+  double batch = 24.0;    // per-batch drain/refill, amortised per K block
+  bool greedy = false;    // n_acc chunks per batch, B windows cut every b_windows slices
+};
+
+namespace detail {
+
+// Products of a batch (chunks [c0, c0 + nc)) in flush order.
+inline std::vector<Product> batch_products(const std::vector<Chunk>& chunks, int c0, int nc) {
+  std::vector<Product> prods;
+  for (int ci = 0; ci < nc; ++ci) {
+    const Chunk& c = chunks[c0 + ci];
+    for (int s = c.s0; s <= c.s1; ++s) prods.push_back({ci, s, c.g - s, false});
+  }
+  return prods;
+}
+
+inline double pass_cost(const std::vector<Product>& prods, int u, int v, const PassCost& cm) {
+  int np = 0, tlo = 1 << 20, thi = -1;
+  uint64_t amask[4] = {0, 0, 0, 0};
+  for (const Product& p : prods)
+    if (p.t >= u && p.t <= v) {
+      ++np;
+      tlo = std::min(tlo, p.t);
+      thi = std::max(thi, p.t);
+      amask[p.s >> 6] |= uint64_t(1) << (p.s & 63);
+    }
+  if (np == 0) return 0.0;
+  int na = 0;
+  for (uint64_t m : amask) na += __builtin_popcountll(m);
+  return std::max(cm.prod * np, cm.a_tile * na + cm.b_tile * (thi - tlo + 1));
+}
+
+// Best split of the batch's B-slice range into windows of <= b_windows slices:
+// returns the window boundaries [u, v] and the cost.
+inline double best_windows(const std::vector<Product>& prods, int b_windows, const PassCost& cm,
+                           std::vector<std::pair<int, int>>* out) {
+  int blo = 1 << 20, bhi = -1;
+  for (const Product& p : prods) blo = std::min(blo, p.t), bhi = std::max(bhi, p.t);
+  const int nb = bhi - blo + 1;
+  std::vector<double> best(nb + 1, 1e300);
+  std::vector<int> from(nb + 1, 0);
+  best[0] = 0.0;
+  for (int e = 1; e <= nb; ++e)
+    for (int b = std::max(0, e - b_windows); b < e; ++b) {
+      const double c = best[b] + pass_cost(prods, blo + b, blo + e - 1, cm);
+      if (c < best[e] - 1e-9) best[e] = c, from[e] = b;
+    }
+  if (out) {
+    out->clear();
+    for (int e = nb; e > 0; e = from[e]) out->push_back({blo + from[e], blo + e - 1});
+    std::reverse(out->begin(), out->end());
+  }
+  return best[nb];
+}
+
+}  // namespace detail
+
 // stage_slot_bytes(a, b) must be <= max_stage_bytes for every pass (a single
 // product always fits: 1 A tile + 1 B tile).
 //
 // b_windows > 0 (the CTA-pair kernel, whose A slices stream through a ring and
-// only the B slices of a K block are resident): a batch's products are split
-// into passes by windows of at most b_windows consecutive B slices, so every
-// pass issues all products of its B window and each streamed A tile feeds as
-// many products as possible.  Otherwise passes are cut greedily in flush order
-// under stage_slot_bytes (the single-CTA kernels stage every slice of a pass).
+// only the B slices of a K block are resident): batches are cut by dynamic
+// programming over the chunk sequence (consecutive chunks, at most n_acc per
+// batch, minimising the PassCost model), and each batch's products are split
+// into passes by windows of at most b_windows consecutive B slices (again the
+// cheapest split), so every streamed A tile feeds as many products as possible
+// and no batch degenerates into a fill-bound sweep.  Otherwise batches take
+// n_acc chunks in turn and passes are cut greedily in flush order under
+// stage_slot_bytes (the single-CTA kernels stage every slice of a pass).
 template <class SlotBytes>
 inline Schedule make_schedule(int k, int64_t r, int n_acc, int64_t max_stage_bytes,
-                              SlotBytes stage_slot_bytes, int b_windows = 0) {
+                              SlotBytes stage_slot_bytes, int b_windows = 0,
+                              const PassCost& cm = PassCost{}) {
   Schedule S;
   S.chunks = make_chunks(k, r);
   const int w = static_cast<int>(S.chunks.size());
-  for (int c0 = 0; c0 < w; c0 += n_acc) {
+  // batch boundaries
+  std::vector<int> starts;
+  if (b_windows > 0 && !cm.greedy) {
+    std::vector<double> best(w + 1, 1e300);
+    std::vector<int> from(w + 1, 0);
+    best[0] = 0.0;
+    for (int e = 1; e <= w; ++e)
+      for (int b = std::max(0, e - n_acc); b < e; ++b) {
+        const auto prods = detail::batch_products(S.chunks, b, e - b);
+        const double c = best[b] + cm.batch + detail::best_windows(prods, b_windows, cm, nullptr);
+        if (c < best[e] - 1e-9) best[e] = c, from[e] = b;
+      }
+    for (int e = w; e > 0; e = from[e]) starts.push_back(from[e]);
+    std::reverse(starts.begin(), starts.end());
+  } else {
+    for (int c0 = 0; c0 < w; c0 += n_acc) starts.push_back(c0);
+  }
+  for (size_t bi = 0; bi < starts.size(); ++bi) {
     Batch b;
-    b.c0 = c0;
-    b.nc = std::min(n_acc, w - c0);
+    b.c0 = starts[bi];
+    b.nc = (bi + 1 < starts.size() ? starts[bi + 1] : w) - b.c0;
     b.pass0 = static_cast<int>(S.passes.size());
-    // products of the batch in flush order
-    std::vector<Product> prods;
-    for (int ci = 0; ci < b.nc; ++ci) {
-      const Chunk& c = S.chunks[c0 + ci];
-      for (int s = c.s0; s <= c.s1; ++s) prods.push_back({ci, s, c.g - s, false});
-    }
+    const std::vector<Product> prods = detail::batch_products(S.chunks, b.c0, b.nc);
     std::vector<bool> seen(b.nc, false);
+    // the passes, as product subsets
+    std::vector<std::vector<Product>> pass_sets;
     if (b_windows > 0) {
-      std::stable_sort(prods.begin(), prods.end(),
-                       [](const Product& x, const Product& y) { return x.t < y.t; });
+      std::vector<std::pair<int, int>> wins;
+      if (cm.greedy) {
+        int blo = 1 << 20, bhi = -1;
+        for (const Product& p : prods) blo = std::min(blo, p.t), bhi = std::max(bhi, p.t);
+        for (int u = blo; u <= bhi; u += b_windows) wins.push_back({u, std::min(bhi, u + b_windows - 1)});
+      } else {
+        detail::best_windows(prods, b_windows, cm, &wins);
+      }
+      for (const auto& [u, v] : wins) {
+        std::vector<Product> ps;
+        for (const Product& p : prods)
+          if (p.t >= u && p.t <= v) ps.push_back(p);
+        if (!ps.empty()) pass_sets.push_back(std::move(ps));
+      }
+    } else {
+      size_t i = 0;
+      while (i < prods.size()) {
+        int alo = prods[i].s, ahi = alo, blo = prods[i].t, bhi = blo;
+        size_t j = i + 1;
+        while (j < prods.size()) {
+          const int a0 = std::min(alo, prods[j].s), a1 = std::max(ahi, prods[j].s);
+          const int b0 = std::min(blo, prods[j].t), b1 = std::max(bhi, prods[j].t);
+          if (stage_slot_bytes(a1 - a0 + 1, b1 - b0 + 1) > max_stage_bytes) break;
+          alo = a0, ahi = a1, blo = b0, bhi = b1;
+          ++j;
+        }
+        pass_sets.emplace_back(prods.begin() + i, prods.begin() + j);
+        i = j;
+      }
     }
-    size_t i = 0;
-    while (i < prods.size()) {
+    for (auto& pass_prods : pass_sets) {
       Pass ps;
       ps.batch = static_cast<int>(S.batches.size());
-      ps.alo = ps.ahi = prods[i].s;
-      ps.blo = ps.bhi = prods[i].t;
-      size_t j = i;
-      while (j < prods.size()) {
-        const int alo = std::min(ps.alo, prods[j].s), ahi = std::max(ps.ahi, prods[j].s);
-        const int blo = std::min(ps.blo, prods[j].t), bhi = std::max(ps.bhi, prods[j].t);
-        if (b_windows > 0) {
-          if (bhi - blo + 1 > b_windows) break;
-        } else if (j > i && stage_slot_bytes(ahi - alo + 1, bhi - blo + 1) > max_stage_bytes) {
-          break;
-        }
-        ps.alo = alo, ps.ahi = ahi, ps.blo = blo, ps.bhi = bhi;
-        ++j;
+      ps.alo = ps.ahi = pass_prods[0].s;
+      ps.blo = ps.bhi = pass_prods[0].t;
+      for (const Product& p : pass_prods) {
+        ps.alo = std::min(ps.alo, p.s), ps.ahi = std::max(ps.ahi, p.s);
+        ps.blo = std::min(ps.blo, p.t), ps.bhi = std::max(ps.bhi, p.t);
       }
       // issue order inside the pass: by A slice (integer sums are order-free)
-      std::vector<Product> pass_prods(prods.begin() + i, prods.begin() + j);
       std::stable_sort(pass_prods.begin(), pass_prods.end(),
                        [](const Product& x, const Product& y) { return x.s < y.s; });
       ps.p0 = static_cast<int>(S.products.size());
@@ -176,7 +278,6 @@ inline Schedule make_schedule(int k, int64_t r, int n_acc, int64_t max_stage_byt
       S.a_slots = std::max(S.a_slots, ps.ahi - ps.alo + 1);
       S.b_slots = std::max(S.b_slots, ps.bhi - ps.blo + 1);
       S.passes.push_back(ps);
-      i = j;
     }
     b.pass1 = static_cast<int>(S.passes.size());
     S.batches.push_back(b);
