@@ -44,6 +44,22 @@ sys.path.insert(0, ROOT)
 METRIC = "emulated DGEMM TFLOPS (2mnp/t) at n=16384 vs cuBLAS DGEMM; max rel err vs phi"
 UNIT = "TFLOPS"
 SPEC_INT8_TOPS = 4500.0
+SPEC_HBM_GBS = 8000.0
+
+
+def step_roofline(m, n, p, k, beta_nonzero, t_step_ms, int8_peak_tops, hbm_gbs):
+    """Whole-step roofline as the north star states it: INT8 products / INT8 peak
+    plus slice and epilogue bytes / HBM bandwidth.
+      ops   = k(k+1)/2 * 2mnp
+      bytes = 8(mn+np) FP64 read + k(mn+np) INT8 slices written + 8(m+p) shifts
+              + 8mp C written (+ 8mp C read when beta != 0)
+    frac = t_roof / t_step."""
+    ops = k * (k + 1) / 2 * 2.0 * m * n * p
+    byts = 8.0 * (m * n + n * p) + k * (m * n + n * p) + 8.0 * (m + p) + 8.0 * m * p * (
+        2 if beta_nonzero else 1)
+    t_roof = ops / (int8_peak_tops * 1e12) + byts / (hbm_gbs * 1e9)
+    return {"int8_ops": ops, "hbm_bytes": byts, "t_roof_ms": t_roof * 1e3,
+            "frac": t_roof * 1e3 / t_step_ms}
 
 
 def parse():
@@ -427,6 +443,12 @@ def main():
                                         " a long power-capped loop",
                          "frac_of_burst": achieved / int8_peak_burst,
                          "frac_of_spec_4500": achieved / SPEC_INT8_TOPS},
+            "step_roofline": {
+                "spec": step_roofline(m, n, p, k, False, t_step, SPEC_INT8_TOPS, SPEC_HBM_GBS),
+                "measured": step_roofline(m, n, p, k, False, t_step, int8_peak, pk["hbm_gbs"]),
+                "note": "t_roof = INT8 ops / INT8 peak + (slice + epilogue bytes) / HBM BW; "
+                        "spec = 4.5 POPS dense + 8 TB/s, measured = 2 x sustained bf16 + "
+                        "measured copy BW (MEASURED_PEAKS.json); frac = t_roof / ms_per_step"},
             "cpu_baseline": cpu,
             "cublas_dgemm": cublas,
             "clocks": clk,

@@ -17,6 +17,9 @@ Per step each rank:
      broadcasts slice panels, as the north star asks,
   3. runs the fused K2+K3 kernel on its C block in three strips, the first
      of which needs no communication, so the gathers overlap the GEMM (step()).
+     The first strip runs on a side stream: the other two wait only on the
+     gathers, so their CTAs take the SMs the first strip's last partial wave
+     leaves idle (no wave-quantisation gap between strips).
 
 The compute backend is injectable (``Backend``): the default calls the CUDA
 library; tests/test_grid2d_gloo.py drives the same orchestration under gloo
@@ -24,6 +27,7 @@ on CPU with a test-only backend to check the gather/partition logic.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import math
 from dataclasses import dataclass
@@ -103,6 +107,21 @@ class Backend:
 
     def empty(self, shape, dtype):
         return torch.empty(shape, dtype=dtype, device=self.device)
+
+    def side_stream(self):
+        """Context for the communication-free strip G1: a second stream that
+        starts after the current one, so G2/G3 (which wait only on the gathers)
+        fill the SMs G1's last partial wave leaves idle.  join_side() puts the
+        current stream back behind it."""
+        if not hasattr(self, "_side"):
+            self._side = torch.cuda.Stream(self.device)
+        cur = torch.cuda.current_stream(self.device)
+        self._side.wait_stream(cur)
+        return torch.cuda.stream(self._side)
+
+    def join_side(self):
+        if hasattr(self, "_side"):
+            torch.cuda.current_stream(self.device).wait_stream(self._side)
 
     def split(self, x, k: int, side: str, trans: bool, beta: int, out_slices, out_shift):
         oz = self.oz
@@ -233,8 +252,10 @@ class Grid2DGemm:
         r0, c0 = L.gc * L.ms, L.gr * L.ps  # own rows / columns inside the C block
         g = (L.n, k, self.beta_bits)
         own_rows = c_block[r0:r0 + L.ms]
-        be.gemm(L.ms, g[0], L.ps, k, g[2], self.a_loc, self.mu_loc, self.b_loc, self.nu_loc,
-                alpha, beta, own_rows[:, c0:c0 + L.ps])
+        side = getattr(be, "side_stream", None)
+        with side() if side else contextlib.nullcontext():
+            be.gemm(L.ms, g[0], L.ps, k, g[2], self.a_loc, self.mu_loc, self.b_loc, self.nu_loc,
+                    alpha, beta, own_rows[:, c0:c0 + L.ps])
         self._wait(wb)
         for lo, hi in _other_ranges(L.pcols, c0, L.ps):
             be.gemm(L.ms, g[0], hi - lo, k, g[2], self.a_loc, self.mu_loc, self.b_pan[:, lo:hi],
@@ -243,4 +264,6 @@ class Grid2DGemm:
         for lo, hi in _other_ranges(L.mr, r0, L.ms):
             be.gemm(hi - lo, g[0], L.pcols, k, g[2], self.a_pan[:, lo:hi], self.mu_pan[lo:hi],
                     self.b_pan, self.nu_pan, alpha, beta, c_block[lo:hi])
+        if side:
+            be.join_side()
         return c_block
