@@ -57,6 +57,7 @@ struct GemmParams {
   int stages;          // smem pipeline depth
   int a_slots, b_slots;  // slice tiles per stage (max over passes)
   int n_chunks;
+  uint32_t idesc_xor;  // experiment hook (OZMM_IDESC_XOR): flips instruction-descriptor bits
   int hint_a, hint_b;  // L2 policies of the A / B slice loads (0 normal, 1 evict_first, 2 evict_last)
   // FP64 flush scaling (scheme.cpp:29-41 with the caller's unit vectors):
   //   0 group-wise        ru = mu_i 2^(2-beta g),   cv = nu_j                (:93-94)

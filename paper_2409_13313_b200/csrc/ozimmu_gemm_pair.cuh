@@ -190,7 +190,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
                   const bool first = kb == 0 && (ci & 0x80u);
 #pragma unroll
                   for (int j = 0; j < kKB / kBK; ++j)  // K = 32 per MMA: +32 B = +2 in desc.lo
-                    ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, Cfg::kIdesc,
+                    ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, Cfg::kIdesc ^ P.idesc_xor,
                                      (first && j == 0) ? 0u : 1u);
                 }
                 ptx::mma_commit_pair(a_empty + ai, all_mask);  // A stage free (all sharers)
