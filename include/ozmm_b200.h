@@ -106,6 +106,11 @@ typedef struct {
                               cluster), 1 = single-CTA kernel, 2 = CTA-pair kernel,
                               3 = experimental 4-CTA cluster sharing B by TMA multicast */
   int method;              /* OZMM_METHOD_*: 0 = ozIMMU_H (the hot path, default) */
+  int signed_slices;       /* 0 = auto: when the CTA-pair kernel runs ozIMMU_H, the
+                              internal slice planes are offset-binary (slice + o_s
+                              as u8, u8 x u8 MMAs, offsets removed exactly in the
+                              epilogue; same results, less tensor-core power);
+                              1 = keep the reference's signed int8 planes */
 } ozmm_options_t;
 
 /* Scheme presets (config_for, scheme.cpp:137-159) plus the two other valid

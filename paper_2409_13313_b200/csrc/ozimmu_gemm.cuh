@@ -58,6 +58,16 @@ struct GemmParams {
   int a_slots, b_slots;  // slice tiles per stage (max over passes)
   int n_chunks;
   uint32_t idesc_xor;  // experiment hook (OZMM_IDESC_XOR): flips instruction-descriptor bits
+  // Offset-binary operands (CTA-pair kernel only; slicer.cuh): the slice planes
+  // hold slice + o_s (o_1 = 2^beta - 1, o_s = 2^(beta-1)) as u8 and the MMAs run
+  // u8 x u8.  For a chunk c the accumulator then holds, mod 2^32,
+  //   acc_c + sum_{(s,t) in c} [ o_t lsa[s][i] + o_s lsb[t][j] + o_s o_t n ]
+  // and the epilogue subtracts that exactly (lsa / lsb = signed line sums).
+  int bias;
+  int64_t n_inner;
+  const int32_t* lsa;  // [k][lsa_plane] row sums of the signed A slices
+  const int32_t* lsb;  // [k][lsb_plane] column sums of the signed B slices
+  int64_t lsa_plane, lsb_plane;
   int hint_a, hint_b;  // L2 policies of the A / B slice loads (0 normal, 1 evict_first, 2 evict_last)
   // FP64 flush scaling (scheme.cpp:29-41 with the caller's unit vectors):
   //   0 group-wise        ru = mu_i 2^(2-beta g),   cv = nu_j                (:93-94)
@@ -87,6 +97,7 @@ struct GemmParams {
   // per chunk in flush order: group g and first A slice s0
   uint8_t c_g[kMaxChunks];
   uint8_t c_s[kMaxChunks];
+  uint8_t c_e[kMaxChunks];  // last A slice of chunk c (products s = c_s .. c_e, t = g - s)
   // CTA-pair kernel: per pass the A-slice groups [p_g0, p_g1); per group the
   // A slice and its product range (products are sorted by A slice in a pass)
   uint16_t p_g0[kMaxPasses], p_g1[kMaxPasses];

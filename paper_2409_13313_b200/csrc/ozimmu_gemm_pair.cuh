@@ -65,7 +65,9 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
   const int n_a = P.stages;  // A ring depth
   uint8_t* bbuf = smem;
   uint8_t* aring = smem + kBBufs * Cfg::kBBuf;
-  uint64_t* b_full = reinterpret_cast<uint64_t*>(aring + n_a * Cfg::kATile);
+  // offset mode: the batch's per-column corrections [kNAcc][kBN] (int32)
+  uint32_t* ccol = reinterpret_cast<uint32_t*>(aring + n_a * Cfg::kATile);
+  uint64_t* b_full = reinterpret_cast<uint64_t*>(ccol + (P.bias ? Cfg::kNAcc * kBN : 0));
   uint64_t* b_empty = b_full + kBBufs;
   uint64_t* a_full = b_empty + kBBufs;
   uint64_t* a_empty = a_full + n_a;
@@ -165,6 +167,8 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
     }
   } else if (warp == 1) {
     // ------------------------------------------- MMA issuer (leader CTA)
+    // u8 x u8 for offset-binary planes (instruction-descriptor bits 7 / 10)
+    const uint32_t idesc = (P.bias ? (Cfg::kIdesc & ~((1u << 7) | (1u << 10))) : Cfg::kIdesc) ^ P.idesc_xor;
     if (leader) {
       int bi = 0, ai = 0;
       uint32_t bph = 0, aph = 0;
@@ -190,7 +194,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
                   const bool first = kb == 0 && (ci & 0x80u);
 #pragma unroll
                   for (int j = 0; j < kKB / kBK; ++j)  // K = 32 per MMA: +32 B = +2 in desc.lo
-                    ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, Cfg::kIdesc ^ P.idesc_xor,
+                    ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, idesc,
                                      (first && j == 0) ? 0u : 1u);
                 }
                 ptx::mma_commit_pair(a_empty + ai, all_mask);  // A stage free (all sharers)
@@ -228,13 +232,38 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
 #pragma unroll
     for (int j = 0; j < kCols; ++j) d[j] = 0.0;
 
+    const uint32_t o1 = (1u << P.beta) - 1u, os = 1u << (P.beta - 1);  // slice offsets
     for (int b = 0; b < P.nbatch; ++b) {
+      const int c0 = P.b_c0[b], nc = P.b_nc[b];
+      if (P.bias) {
+        // per-column part of the batch's offset corrections, while its MMAs run:
+        // ccol[ci][j] = sum_{(s,t) in chunk} o_s lsb[t][col] + o_s o_t n
+        asm volatile("bar.sync 1, %0;" ::"r"(kPairEpiWarps * 32) : "memory");  // previous batch done
+        for (int idx = threadIdx.x - 4 * 32; idx < nc * kBN; idx += kPairEpiWarps * 32) {
+          const int ci = idx / kBN, j = idx % kBN, c = c0 + ci, g = P.c_g[c];
+          const int col = col_tile * kBN + j;
+          uint32_t acc = 0;
+          for (int s = P.c_s[c]; s <= P.c_e[c]; ++s) {
+            const int t = g - s;
+            const uint32_t oa = s == 1 ? o1 : os, ob = t == 1 ? o1 : os;
+            const uint32_t ls = col < P.p ? static_cast<uint32_t>(P.lsb[(t - 1) * P.lsb_plane + col]) : 0u;
+            acc += oa * ls + oa * ob * static_cast<uint32_t>(P.n_inner);
+          }
+          ccol[ci * kBN + j] = acc;
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(kPairEpiWarps * 32) : "memory");
+      }
       ptx::mbar_wait(tmem_full, b & 1);
       ptx::tc_fence_after();
-      const int c0 = P.b_c0[b], nc = P.b_nc[b];
       for (int ci = 0; ci < nc; ++ci) {
         const int c = c0 + ci;
         const double ru = flush_row_scale(P, c, row, mu);
+        uint32_t rrow = 0;  // per-row part: sum_{(s,t)} o_t lsa[s][row]
+        if (P.bias && row_ok)
+          for (int s = P.c_s[c]; s <= P.c_e[c]; ++s) {
+            const int t = P.c_g[c] - s;
+            rrow += (t == 1 ? o1 : os) * static_cast<uint32_t>(P.lsa[(s - 1) * P.lsa_plane + row]);
+          }
 #pragma unroll
         for (int cc = 0; cc < kCols; cc += kLd) {
           uint32_t v[kLd];
@@ -242,6 +271,10 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
                                        ci * kBN + cslice * kCols + cc,
                                    v);
           ptx::tmem_ld_wait();
+          if (P.bias) {
+#pragma unroll
+            for (int j = 0; j < kLd; ++j) v[j] -= rrow + ccol[ci * kBN + cslice * kCols + cc + j];
+          }
           if (P.dump != nullptr && row_ok) {
             int32_t* dst = P.dump + (static_cast<int64_t>(c) * P.m + row) * P.p;
 #pragma unroll

@@ -40,6 +40,12 @@ struct FlushCfg {
   const double* units_a = nullptr;
   const double* units_b = nullptr;
   bool per_product = false;  // chunks of one product (accumulate_per_product)
+  // offset-binary slice planes (CTA-pair kernel only): signed line sums [k][plane]
+  const int32_t* lsa = nullptr;
+  const int32_t* lsb = nullptr;
+  int64_t lsa_plane = 0, lsb_plane = 0;
+  int64_t n = 0;
+  bool biased() const { return lsa != nullptr; }
 };
 
 // method code of ozmm_options_t -> (strategy, per-product accumulation)
@@ -80,6 +86,10 @@ struct Handle {
   size_t units_a_n = 0;
   double* units_b = nullptr;
   size_t units_b_n = 0;
+  int32_t* lsa = nullptr;  // offset-binary planes: signed line sums [k][m] / [k][p]
+  size_t lsa_n = 0;
+  int32_t* lsb = nullptr;
+  size_t lsb_n = 0;
   double* tscratch = nullptr;  // transposed operand for per-slice RN column splits
   size_t tscratch_n = 0;
   // device staging for the host-pointer entry (grown lazily, reused)
@@ -180,8 +190,11 @@ bool valid_trans(char t) { return is_trans(t) || t == 'N' || t == 'n'; }
 
 // ---- K1 launch ----------------------------------------------------------------
 // Lines of op(X): row mode when the line is contiguous in memory.
+// lsum != nullptr: offset-binary planes + signed line sums lsum[s][line] (plane
+// stride lsum_plane; zeroed by the caller), the fused pair GEMM's operand format.
 int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const double* X, int64_t ldx,
-                 int k, int beta, int8_t* S, int64_t lds, int64_t plane, double* shift) {
+                 int k, int beta, int8_t* S, int64_t lds, int64_t plane, double* shift,
+                 int* lsum = nullptr, int64_t lsum_plane = 0) {
   if (row_mode) {
     const bool vec = (reinterpret_cast<uintptr_t>(X) % 16 == 0) && (ldx % 2 == 0);
     // Whole row in registers, 16 elements per thread, split over a cluster of up
@@ -215,10 +228,11 @@ int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const doubl
       cfg.numAttrs = 1;
       if (vec)
         CUDA_TRY(h, cudaLaunchKernelEx(&cfg, ozb::slice_rows_cluster_kernel<true>, X, ldx, lines, n,
-                                       lds, k, beta, S, plane, shift, h->flags));
+                                       lds, k, beta, S, plane, shift, h->flags, lsum, lsum_plane));
       else
         CUDA_TRY(h, cudaLaunchKernelEx(&cfg, ozb::slice_rows_cluster_kernel<false>, X, ldx, lines,
-                                       n, lds, k, beta, S, plane, shift, h->flags));
+                                       n, lds, k, beta, S, plane, shift, h->flags, lsum,
+                                       lsum_plane));
     } else {
       const int64_t want = (chunks + 31) / 32 * 32;
       const int threads = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(32, want)));
@@ -226,11 +240,11 @@ int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const doubl
       if (vec)
         ozb::slice_rows_kernel<true><<<grid, threads, 0, h->stream>>>(X, ldx, lines, n, lds, k,
                                                                       beta, S, plane, shift,
-                                                                      h->flags);
+                                                                      h->flags, lsum, lsum_plane);
       else
         ozb::slice_rows_kernel<false><<<grid, threads, 0, h->stream>>>(X, ldx, lines, n, lds, k,
                                                                        beta, S, plane, shift,
-                                                                       h->flags);
+                                                                       h->flags, lsum, lsum_plane);
     }
   } else {
     if (int rc = ensure(h, &h->colmax, &h->colmax_n, static_cast<size_t>(lines))) return rc;
@@ -239,9 +253,14 @@ int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const doubl
     const dim3 g1(static_cast<unsigned>((lines + 31) / 32),
                   static_cast<unsigned>((n + rows_per_block - 1) / rows_per_block));
     ozb::colmax_kernel<<<g1, 256, 0, h->stream>>>(X, ldx, n, lines, rows_per_block, h->colmax);
-    const dim3 g2(static_cast<unsigned>((lines + 31) / 32), static_cast<unsigned>((lds + 127) / 128));
+    // offset planes: 8 row tiles per CTA (column sums leave with one atomic per
+    // column, slice and CTA); signed planes: one tile per CTA
+    const int tpc = lsum ? 8 : 1;
+    const dim3 g2(static_cast<unsigned>((lines + 31) / 32),
+                  static_cast<unsigned>((lds + 128 * tpc - 1) / (128 * tpc)));
     ozb::slice_cols_kernel<<<g2, 256, 0, h->stream>>>(X, ldx, n, lines, lds, k, beta, h->colmax,
-                                                       S, plane, shift, h->flags);
+                                                       S, plane, shift, h->flags, lsum, lsum_plane,
+                                                       tpc);
   }
   CUDA_TRY(h, cudaGetLastError());
   return OZMM_OK;
@@ -339,6 +358,12 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
                  int64_t ldc, int32_t* dump, const FlushCfg& fl) {
   std::memset(&P, 0, sizeof P);
   P.scale_mode = fl.scale_mode;
+  P.bias = fl.biased() ? 1 : 0;
+  P.n_inner = fl.n;
+  P.lsa = fl.lsa;
+  P.lsb = fl.lsb;
+  P.lsa_plane = fl.lsa_plane;
+  P.lsb_plane = fl.lsb_plane;
   P.units_a = fl.units_a;
   P.units_b = fl.units_b;
   P.m = static_cast<int>(m);
@@ -390,6 +415,7 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
   for (size_t c = 0; c < S.chunks.size(); ++c) {
     P.c_g[c] = static_cast<uint8_t>(S.chunks[c].g);
     P.c_s[c] = static_cast<uint8_t>(S.chunks[c].s0);
+    P.c_e[c] = static_cast<uint8_t>(S.chunks[c].s1);
   }
   for (size_t q = 0; q < S.passes.size(); ++q) {
     P.p_g0[q] = static_cast<uint16_t>(S.passes[q].g0);
@@ -477,7 +503,8 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   if (!schedule_fits(S))
     return set_err(h, OZMM_ERR_UNSUPPORTED, "schedule too large (k=%d, r=%lld)", k,
                    static_cast<long long>(r));
-  const size_t fixed = ozb::kBBufs * Cfg::kBBuf;
+  const size_t ccol_bytes = fl.biased() ? sizeof(uint32_t) * Cfg::kNAcc * kBN : 0;
+  const size_t fixed = ozb::kBBufs * Cfg::kBBuf + ccol_bytes;
   // A-ring depth.  When each A tile feeds >= 2.5 products on average (tensor-bound
   // schedules, e.g. C3), 4 stages, not the 6 that fit: a deeper ring lets each
   // CTA pair run further ahead along K, the tiles of a wave drift apart and stop
@@ -507,6 +534,8 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   if (int rc = make_slice_map(h, &map_b, Bs, lds_b, p, plane_b, k, Cfg::kBHalf, ozb::kKB,
                               CU_TENSOR_MAP_SWIZZLE_128B))
     return rc;
+  if (fl.biased() && (kPairs != 1 || fl.per_product || fl.scale_mode != 0))
+    return set_err(h, OZMM_ERR_UNSUPPORTED, "offset-binary slices need the CTA-pair ozIMMU_H kernel");
   const size_t smem = fixed + stages * Cfg::kATile + kSmemReserve + kBN * sizeof(double);
   if (!h->pair_attr_set[kPairs - 1]) {
     CUDA_TRY(h, cudaFuncSetAttribute(ozb::ozimmu_gemm_pair_kernel<kBN, kPairs>,
@@ -521,11 +550,30 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   return OZMM_OK;
 }
 
+// The kernel launch_gemm picks for these options is the CTA-pair <128, 1> one.
+bool pair_kernel_selected(const ozmm_options_t* opt) {
+  const int tile_n = opt ? opt->tile_n : 0;
+  const int pair = opt ? opt->cta_pair : 0;
+  if (pair == 3 || (pair == 0 && tile_n == 0 && std::getenv("OZMM_QUAD"))) return false;
+  return pair == 2 || (pair == 0 && tile_n == 0);
+}
+
+// Offset-binary planes for the ozIMMU_H hot path unless the caller asks for
+// the signed ones (options / OZMM_SIGNED=1) or another kernel runs.
+bool use_offset_planes(const ozmm_options_t* opt, const MethodCfg& mc) {
+  if (opt && opt->signed_slices) return false;
+  if (const char* e = std::getenv("OZMM_SIGNED"))
+    if (std::atoi(e) != 0) return false;
+  return mc.strategy == kRNConstShift && !mc.per_product && pair_kernel_selected(opt);
+}
+
 int launch_gemm(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_bits, int64_t r,
                 const int8_t* As, int64_t lds_a, int64_t plane_a, const double* mu, const int8_t* Bs,
                 int64_t lds_b, int64_t plane_b, const double* nu, double alpha, double beta, const double* Cin, double* Cout,
                 int64_t ldc, const ozmm_options_t* opt, const FlushCfg& fl = FlushCfg{}) {
   int32_t* dump = opt ? opt->chunk_dump : nullptr;
+  if (fl.biased() && !pair_kernel_selected(opt))
+    return set_err(h, OZMM_ERR_UNSUPPORTED, "offset-binary slices need the CTA-pair kernel");
   const int tile_n = opt ? opt->tile_n : 0;
   const int pair = opt ? opt->cta_pair : 0;
   if (pair == 3 || (pair == 0 && tile_n == 0 && std::getenv("OZMM_QUAD")))
@@ -610,6 +658,8 @@ int ozmm_destroy(ozmm_handle_t handle) {
   cudaFree(h->units_a);
   cudaFree(h->units_b);
   cudaFree(h->tscratch);
+  cudaFree(h->lsa);
+  cudaFree(h->lsb);
   cudaFree(h->host_a);
   cudaFree(h->host_b);
   cudaFree(h->host_c);
@@ -892,15 +942,37 @@ int ozmm_dgemm_ex(ozmm_handle_t handle, char transa, char transb, int64_t m, int
     fl.units_a = out_a = h->units_a;
     fl.units_b = out_b = h->units_b;
   }
+  const bool offset = use_offset_planes(opt, mc);
+  if (offset) {
+    if (int rc = ensure(h, &h->lsa, &h->lsa_n, static_cast<size_t>(k) * m)) return rc;
+    if (int rc = ensure(h, &h->lsb, &h->lsb_n, static_cast<size_t>(k) * p)) return rc;
+    CUDA_TRY(h, cudaMemsetAsync(h->lsa, 0, sizeof(int32_t) * k * m, h->stream));
+    CUDA_TRY(h, cudaMemsetAsync(h->lsb, 0, sizeof(int32_t) * k * p, h->stream));
+    fl.lsa = h->lsa;
+    fl.lsb = h->lsb;
+    fl.lsa_plane = m;
+    fl.lsb_plane = p;
+    fl.n = n;
+  }
   // split A (Left, rows of op(A)) -- split.cpp:233 via scheme.cpp:248
-  if (int rc = launch_split_m(h, mc.strategy, !is_trans(transa), m, n, A, lda, k, beta_bits,
-                              h->slices_a, lds, m * lds, out_a))
+  if (offset) {
+    if (int rc = launch_split(h, !is_trans(transa), m, n, A, lda, k, beta_bits, h->slices_a, lds,
+                              m * lds, out_a, h->lsa, m))
+      return rc;
+  } else if (int rc = launch_split_m(h, mc.strategy, !is_trans(transa), m, n, A, lda, k, beta_bits,
+                                     h->slices_a, lds, m * lds, out_a)) {
     return rc;
+  }
   if (want_t) CUDA_TRY(h, cudaEventRecord(h->ev[1], h->stream));
   // split B (Right, columns of op(B)) -- scheme.cpp:251
-  if (int rc = launch_split_m(h, mc.strategy, is_trans(transb), p, n, B, ldb, k, beta_bits,
-                              h->slices_b, lds, p * lds, out_b))
+  if (offset) {
+    if (int rc = launch_split(h, is_trans(transb), p, n, B, ldb, k, beta_bits, h->slices_b, lds,
+                              p * lds, out_b, h->lsb, p))
+      return rc;
+  } else if (int rc = launch_split_m(h, mc.strategy, is_trans(transb), p, n, B, ldb, k, beta_bits,
+                                     h->slices_b, lds, p * lds, out_b)) {
     return rc;
+  }
   if (want_t) CUDA_TRY(h, cudaEventRecord(h->ev[2], h->stream));
   if (opt && opt->sync_check)
     if (int rc = check_range_sync(h)) return rc;
@@ -1119,6 +1191,21 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
       });
   }
 
+  // offset-binary slice planes (the fused pair kernel's operand format)
+  MethodCfg mch;
+  method_cfg(OZMM_METHOD_OZIMMU_H, &mch);
+  const bool offset = use_offset_planes(opt, mch);
+  FlushCfg fl;
+  if (offset && rc == OZMM_OK) {
+    if ((rc = ensure(h, &h->lsa, &h->lsa_n, static_cast<size_t>(k) * m)) == OZMM_OK &&
+        (rc = ensure(h, &h->lsb, &h->lsb_n, static_cast<size_t>(k) * p)) == OZMM_OK) {
+      cu(cudaMemsetAsync(h->lsa, 0, sizeof(int32_t) * k * m, user), "memset");
+      cu(cudaMemsetAsync(h->lsb, 0, sizeof(int32_t) * k * p, user), "memset");
+    }
+    fl.lsa_plane = m;
+    fl.lsb_plane = p;
+    fl.n = n;
+  }
   // every stream starts after earlier work on the handle's stream
   cu(cudaEventRecord(evStart, user), "event");
   for (cudaStream_t s : {h->s_in, h->s_out, h->s_split, h->s_gemm[0], h->s_gemm[1]})
@@ -1170,7 +1257,8 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
       cu(cudaStreamWaitEvent(h->s_split, evA[s], 0), "wait");
       if (rc == OZMM_OK)
         rc = launch_split(h, !ta, rows, n, ta ? dA + r0 : dA + r0 * n, ta ? m : n, k, beta_bits,
-                          h->slices_a + r0 * lds, lds, m * lds, h->mu + r0);
+                          h->slices_a + r0 * lds, lds, m * lds, h->mu + r0,
+                          offset ? h->lsa + r0 : nullptr, m);
       cu(cudaEventRecord(evSA[s], h->s_split), "event");
     }
     if (s < rb && rc == OZMM_OK) {
@@ -1178,7 +1266,8 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
       cu(cudaStreamWaitEvent(h->s_split, evB[s], 0), "wait");
       if (rc == OZMM_OK)
         rc = launch_split(h, tb, cols, n, tb ? dB + c0 * n : dB + c0, tb ? n : p, k, beta_bits,
-                          h->slices_b + c0 * lds, lds, p * lds, h->nu + c0);
+                          h->slices_b + c0 * lds, lds, p * lds, h->nu + c0,
+                          offset ? h->lsb + c0 : nullptr, p);
       cu(cudaEventRecord(evSB[s], h->s_split), "event");
     }
   }
@@ -1191,10 +1280,14 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
     cu(cudaStreamWaitEvent(sg, t.row ? evSA[t.step] : evSB[t.step], 0), "wait");
     if (!no_c) cu(cudaStreamWaitEvent(sg, evC[q], 0), "wait");
     h->stream = sg;
+    if (offset) {
+      fl.lsa = h->lsa + t.r0;
+      fl.lsb = h->lsb + t.c0;
+    }
     if (rc == OZMM_OK)
       rc = launch_gemm(h, t.rows, n, t.cols, k, beta_bits, r, h->slices_a + t.r0 * lds, lds, m * lds,
                        h->mu + t.r0, h->slices_b + t.c0 * lds, lds, p * lds, h->nu + t.c0, alpha, beta,
-                       no_c ? nullptr : dC + t.r0 * p + t.c0, dO + t.r0 * p + t.c0, p, opt);
+                       no_c ? nullptr : dC + t.r0 * p + t.c0, dO + t.r0 * p + t.c0, p, opt, fl);
     cu(cudaEventRecord(evG[q], sg), "event");
   }
   h->stream = user;

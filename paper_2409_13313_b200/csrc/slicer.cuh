@@ -13,6 +13,15 @@
 // so every line starts 16-byte aligned for TMA; bytes [n, lds) are written as
 // zeros.  The shift vector is written as doubles (const_shift, split.hpp:37).
 //
+// Offset-binary planes (`lsum != nullptr`, the fused GEMM's operand format):
+// byte = slice + o_s with o_1 = 2^beta - 1 and o_s = 2^(beta-1) for s >= 2, so
+// every byte is an unsigned value in [0, 2^(beta+1) - 2] (|slice_1| <= 2^beta - 1
+// by rn_unit's bump rule, |slice_s| <= 2^(beta-1) after round-to-nearest);
+// padding bytes stay 0.  lsum[s][line] (zeroed by the caller) receives the
+// line's sum of the SIGNED slice values (mod 2^32), from which the GEMM removes
+// the offsets' contribution exactly (ozimmu_gemm_pair.cuh).  The signed planes
+// (lsum == nullptr) are the reference's SplitMatrix slices, bit for bit.
+//
 // Two access patterns, both one coalesced read of the FP64 input plus one
 // 16-byte-vector write per slice:
 //   * slice_rows_kernel: lines are contiguous rows (A, or B when transb='T').
@@ -33,6 +42,7 @@
 namespace ozb {
 
 constexpr double kSigmaScale = 6755399441055744.0;  // 0.75 * 2^53 (split.cpp:16)
+constexpr int kMaxSlices = 22;  // = kMaxK of the GEMM (line-sum scratch in shared memory)
 
 // flags[0] |= underflow (pe < -1000), flags[1] |= range (pe > 920).
 __device__ __forceinline__ void report_flags(int* flags, bool under, bool range) {
@@ -50,10 +60,25 @@ __device__ __forceinline__ void report_flags(int* flags, bool under, bool range)
 // is unit, so bits(t) - bits(sigma) == x / unit exactly (no division, no
 // float->int conversion).  Valid for every unit >= 2^-1074 (sigma is then
 // normal); unit == 0 (underflowed grid) is handled separately.
+//
+// Offset mode (lsum != nullptr): the `nvalid` leading elements get the slice
+// offset; the per-slice sums of the signed values are reduced over the lanes
+// that share the line (kLaneGroup: 32 = the whole warp is one line, 8 = lanes
+// l, l^4, l^8, .. of slice_cols_kernel) and added into lsum[s-1][0] by the
+// group's first lane.  Every lane of the warp must call it (nvalid = 0 and
+// store = false for lanes without data).
+template <int kLaneGroup = 32>
 __device__ __forceinline__ void emit16(double (&w)[16], int PE, int beta, int k,
-                                       int8_t* dst, int64_t plane) {
+                                       int8_t* dst, int64_t plane, int nvalid = 16,
+                                       bool store = true, int* lsum = nullptr,
+                                       int64_t lsum_plane = 0) {
   for (int s = 1; s <= k; ++s) {
-    uint32_t packed[4] = {0u, 0u, 0u, 0u};
+    // offset of this slice (0 for the signed planes); the byte (q + off) & 0xFF
+    // is slice + off because slice + off lies in [0, 254]
+    const uint32_t off = lsum == nullptr ? 0u : (s == 1 ? (1u << beta) - 1u : 1u << (beta - 1));
+    const uint32_t off4 = off * 0x01010101u;
+    uint32_t packed[4] = {off4, off4, off4, off4};  // zero line / underflowed grid: slice 0
+    int qsum = 0;
     if (PE != INT32_MIN) {
       const int ue = PE + 1 - beta * s;
       const double unit = pow2(ue);
@@ -61,12 +86,15 @@ __device__ __forceinline__ void emit16(double (&w)[16], int PE, int beta, int k,
         const double sigma = __dmul_rn(kSigmaScale, unit);  // exact
         const long long sbits = __double_as_longlong(sigma);
 #pragma unroll
+        for (int e = 0; e < 4; ++e) packed[e] = 0u;
+#pragma unroll
         for (int e = 0; e < 16; ++e) {
           const double t = __dadd_rn(w[e], sigma);
           const double x = __dadd_rn(t, -sigma);
           const uint32_t q = static_cast<uint32_t>(__double_as_longlong(t) - sbits);
           w[e] = __dadd_rn(w[e], -x);
-          packed[e >> 2] |= (q & 0xFFu) << (8 * (e & 3));
+          packed[e >> 2] |= ((q + off) & 0xFFu) << (8 * (e & 3));
+          qsum += static_cast<int>(q);  // padding elements are 0 (w = 0 there)
         }
       } else {
         // unit underflowed to 0: the reference computes x = w, int8(w/0) = 0
@@ -75,9 +103,32 @@ __device__ __forceinline__ void emit16(double (&w)[16], int PE, int beta, int k,
         for (int e = 0; e < 16; ++e) w[e] = __dadd_rn(w[e], -w[e]);
       }
     }
-    *reinterpret_cast<uint4*>(dst + static_cast<int64_t>(s - 1) * plane) =
-        make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    if (lsum != nullptr) {
+      if (nvalid < 16) {  // padding bytes stay 0
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          if (e >= nvalid) packed[e >> 2] &= ~(0xFFu << (8 * (e & 3)));
+      }
+      if constexpr (kLaneGroup == 32) {
+        qsum = __reduce_add_sync(0xffffffffu, qsum);
+        if ((threadIdx.x & 31) == 0 && qsum != 0)
+          atomicAdd(lsum + static_cast<int64_t>(s - 1) * lsum_plane, qsum);
+      } else {
+#pragma unroll
+        for (int o = 32 / kLaneGroup; o < 32; o <<= 1) qsum += __shfl_xor_sync(0xffffffffu, qsum, o);
+        if ((threadIdx.x & 31) < 32 / kLaneGroup && store && qsum != 0)
+          atomicAdd(lsum + static_cast<int64_t>(s - 1) * lsum_plane, qsum);
+      }
+    }
+    if (store)
+      *reinterpret_cast<uint4*>(dst + static_cast<int64_t>(s - 1) * plane) =
+          make_uint4(packed[0], packed[1], packed[2], packed[3]);
   }
+}
+
+// Number of valid elements in a 16-element run with `rest` elements left in the line.
+__device__ __forceinline__ int valid16(int64_t rest) {
+  return rest <= 0 ? 0 : (rest >= 16 ? 16 : static_cast<int>(rest));
 }
 
 __device__ __forceinline__ void load16(const double* x, int64_t base, int64_t len, bool vec,
@@ -119,8 +170,11 @@ __global__ void __launch_bounds__(1024) slice_rows_kernel(const double* __restri
                                                           int k, int beta,
                                                           int8_t* __restrict__ S, int64_t plane,
                                                           double* __restrict__ shift,
-                                                          int* __restrict__ flags) {
+                                                          int* __restrict__ flags,
+                                                          int* __restrict__ lsum, int64_t lsum_plane) {
   __shared__ double red[32];
+  __shared__ int lsum_s[kMaxSlices];  // offset mode: the row's per-slice sums
+  if (threadIdx.x < kMaxSlices) lsum_s[threadIdx.x] = 0;  // ordered by block_max's barrier
   const int64_t row = blockIdx.x;
   const double* x = X + row * ld;
   int8_t* out = S + row * lds;
@@ -146,13 +200,26 @@ __global__ void __launch_bounds__(1024) slice_rows_kernel(const double* __restri
     shift[row] = PE == INT32_MIN ? 0.0 : pow2(PE);
     report_flags(flags, under, range);
   }
+  int* ls = lsum ? lsum_s : nullptr;
+  auto nval = [&](int64_t base) { return valid16(len - base); };
   if (lds <= step) {
-    if (base0 < lds) emit16(w, PE, beta, k, out + base0, plane);
+    if (ls)  // every lane takes part in the line-sum reduction
+      emit16(w, PE, beta, k, out + base0, plane, nval(base0), base0 < lds, ls, 1);
+    else if (base0 < lds)
+      emit16(w, PE, beta, k, out + base0, plane);
   } else {
-    for (int64_t base = base0; base < lds; base += step) {
+    for (int64_t it = 0; it * step < lds; ++it) {  // same trip count in every thread
+      const int64_t base = base0 + it * step;
       load16(x, base, len, kVec, w);
-      emit16(w, PE, beta, k, out + base, plane);
+      if (ls)
+        emit16(w, PE, beta, k, out + base, plane, nval(base), base < lds, ls, 1);
+      else if (base < lds)
+        emit16(w, PE, beta, k, out + base, plane);
     }
+  }
+  if (lsum) {  // one CTA owns the row: plain stores
+    __syncthreads();
+    if (threadIdx.x < k) lsum[threadIdx.x * lsum_plane + row] = lsum_s[threadIdx.x];
   }
 }
 
@@ -164,9 +231,11 @@ template <bool kVec>
 __global__ void __launch_bounds__(512) slice_rows_cluster_kernel(
     const double* __restrict__ X, int64_t ld, int64_t rows, int64_t len, int64_t lds, int k,
     int beta, int8_t* __restrict__ S, int64_t plane, double* __restrict__ shift,
-    int* __restrict__ flags) {
+    int* __restrict__ flags, int* __restrict__ lsum, int64_t lsum_plane) {
   __shared__ double red[32];
   __shared__ double cmax[8];  // one slot per CTA of the cluster
+  __shared__ int lsum_s[kMaxSlices];  // offset mode: this CTA's part of the row sums
+  if (threadIdx.x < kMaxSlices) lsum_s[threadIdx.x] = 0;  // ordered by block_max's barrier
   uint32_t crank, csize;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
   asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
@@ -198,7 +267,14 @@ __global__ void __launch_bounds__(512) slice_rows_cluster_kernel(
     shift[row] = PE == INT32_MIN ? 0.0 : pow2(PE);
     report_flags(flags, under, range);
   }
-  if (base0 < lds) emit16(w, PE, beta, k, out + base0, plane);
+  if (lsum) {
+    emit16(w, PE, beta, k, out + base0, plane, valid16(len - base0), base0 < lds, lsum_s, 1);
+    __syncthreads();
+    if (threadIdx.x < k && lsum_s[threadIdx.x] != 0)
+      atomicAdd(lsum + threadIdx.x * lsum_plane + row, lsum_s[threadIdx.x]);
+  } else if (base0 < lds) {
+    emit16(w, PE, beta, k, out + base0, plane);
+  }
 }
 
 // Column maxima of |X| for X: len x cols (row stride ld).  colmax holds the
@@ -236,22 +312,56 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(const double* __restric
                                                          const unsigned long long* __restrict__ colmax,
                                                          int8_t* __restrict__ S, int64_t plane,
                                                          double* __restrict__ shift,
-                                                         int* __restrict__ flags) {
+                                                         int* __restrict__ flags,
+                                                         int* __restrict__ lsum, int64_t lsum_plane,
+                                                         int tiles_per_cta) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t col = static_cast<int64_t>(blockIdx.x) * 32 + warp * 4 + (lane & 3);
-  const int64_t base = static_cast<int64_t>(blockIdx.y) * 128 + 16 * (lane >> 2);
-  if (col >= cols || base >= lds) return;
-  const double rm = __longlong_as_double(static_cast<long long>(colmax[col]));
+  if (lsum == nullptr) {  // signed planes: one 128-row tile per CTA
+    const int64_t base = static_cast<int64_t>(blockIdx.y) * 128 + 16 * (lane >> 2);
+    if (col >= cols || base >= lds) return;
+    const double rm = __longlong_as_double(static_cast<long long>(colmax[col]));
+    bool under = false, range = false;
+    const int PE = line_pe(rm, beta, &under, &range);
+    if (blockIdx.y == 0 && (lane >> 2) == 0) {
+      shift[col] = PE == INT32_MIN ? 0.0 : pow2(PE);
+      report_flags(flags, under, range);
+    }
+    double w[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) w[e] = base + e < len ? __ldg(X + (base + e) * ld + col) : 0.0;
+    emit16(w, PE, beta, k, S + col * lds + base, plane);
+    return;
+  }
+  // offset planes: `tiles_per_cta` 128-row tiles per CTA; the column sums
+  // collect in shared memory and leave with one atomic per column and slice
+  __shared__ int lsum_s[kMaxSlices][32];
+  for (int i = threadIdx.x; i < kMaxSlices * 32; i += blockDim.x) lsum_s[i / 32][i % 32] = 0;
+  __syncthreads();
+  const double rm = col < cols ? __longlong_as_double(static_cast<long long>(colmax[col])) : 0.0;
   bool under = false, range = false;
   const int PE = line_pe(rm, beta, &under, &range);
-  if (blockIdx.y == 0 && (lane >> 2) == 0) {
+  if (col < cols && blockIdx.y == 0 && (lane >> 2) == 0) {
     shift[col] = PE == INT32_MIN ? 0.0 : pow2(PE);
     report_flags(flags, under, range);
   }
-  double w[16];
+  for (int it = 0; it < tiles_per_cta; ++it) {  // uniform trip count: every lane reduces
+    const int64_t base =
+        (static_cast<int64_t>(blockIdx.y) * tiles_per_cta + it) * 128 + 16 * (lane >> 2);
+    const bool valid = col < cols && base < lds;
+    double w[16];
 #pragma unroll
-  for (int e = 0; e < 16; ++e) w[e] = base + e < len ? __ldg(X + (base + e) * ld + col) : 0.0;
-  emit16(w, PE, beta, k, S + col * lds + base, plane);
+    for (int e = 0; e < 16; ++e)
+      w[e] = valid && base + e < len ? __ldg(X + (base + e) * ld + col) : 0.0;
+    emit16<8>(w, PE, beta, k, S + col * lds + base, plane, valid ? valid16(len - base) : 0, valid,
+              &lsum_s[0][warp * 4 + (lane & 3)], 32);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < k * 32; i += blockDim.x) {
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * 32 + (i % 32);
+    if (c < cols && lsum_s[i / 32][i % 32] != 0)
+      atomicAdd(lsum + (i / 32) * lsum_plane + c, lsum_s[i / 32][i % 32]);
+  }
 }
 
 }  // namespace ozb

@@ -68,7 +68,7 @@ class Timings(C.Structure):
 class Options(C.Structure):
     _fields_ = [("force_beta", C.c_int), ("force_r", C.c_int64), ("timings", C.c_int),
                 ("sync_check", C.c_int), ("chunk_dump", C.c_void_p), ("tile_n", C.c_int),
-                ("cta_pair", C.c_int), ("method", C.c_int)]
+                ("cta_pair", C.c_int), ("method", C.c_int), ("signed_slices", C.c_int)]
 
 
 _SIG = {
@@ -309,7 +309,7 @@ def _is_cuda_tensor(x) -> bool:
 
 
 def _options(cfg: SchemeConfig | None, timings: bool = False, dump=None, tile_n: int = 0,
-             sync_check: bool = False, cta_pair: int = 0) -> Options:
+             sync_check: bool = False, cta_pair: int = 0, signed_slices: bool = False) -> Options:
     o = Options()
     if cfg is not None:
         o.force_beta = cfg.force_beta
@@ -320,6 +320,7 @@ def _options(cfg: SchemeConfig | None, timings: bool = False, dump=None, tile_n:
     o.chunk_dump = dump.data_ptr() if dump is not None else None
     o.tile_n = tile_n
     o.cta_pair = cta_pair
+    o.signed_slices = int(signed_slices)
     return o
 
 
@@ -360,12 +361,14 @@ def _to_result(counts: Counts, tim: Timings, d) -> OzakiResult:
 def ozaki_gemm_ex(alpha: float, a, b, beta: float, c, cfg: SchemeConfig | None = None, *,
                   transa: bool = False, transb: bool = False, handle: Handle | None = None,
                   out=None, timings: bool = True, chunk_dump=None,
-                  tile_n: int = 0) -> OzakiResult:
+                  tile_n: int = 0, signed_slices: bool = False) -> OzakiResult:
     """Emulated DGEMM: alpha * op(A) op(B) + beta * C (scheme.cpp:274-291).
 
     Returns OzakiResult(d=new matrix, counts, timings); C is not modified
     unless it is passed as ``out`` too.  Shapes: op(A) m x n, op(B) n x p,
-    C m x p, all row-major.
+    C m x p, all row-major.  ``signed_slices`` keeps the reference's signed
+    int8 planes inside the fused GEMM instead of the default offset-binary ones
+    (same results; include/ozmm_b200.h).
     """
     cfg = cfg or config_for(Method.ozIMMU_H, 8)
     _validate(cfg)
@@ -390,7 +393,7 @@ def ozaki_gemm_ex(alpha: float, a, b, beta: float, c, cfg: SchemeConfig | None =
             out = c.clone()
         elif out.data_ptr() != c.data_ptr():
             out.copy_(c)
-        opt = _options(cfg, timings, chunk_dump, tile_n)
+        opt = _options(cfg, timings, chunk_dump, tile_n, signed_slices=signed_slices)
         h.check(lib.ozmm_dgemm_ex(h.h, b"T" if transa else b"N", b"T" if transb else b"N", m, n,
                                   p, alpha, a.data_ptr(), a.stride(0), b.data_ptr(),
                                   b.stride(0), beta, out.data_ptr(), out.stride(0), cfg.k,
@@ -410,7 +413,7 @@ def ozaki_gemm_ex(alpha: float, a, b, beta: float, c, cfg: SchemeConfig | None =
     res = c.copy() if out is None else out
     if out is not None:
         np.copyto(res, c)
-    opt = _options(cfg, timings, None, tile_n, sync_check=True)
+    opt = _options(cfg, timings, None, tile_n, sync_check=True, signed_slices=signed_slices)
     h.set_stream(None)
     h.check(lib.ozmm_dgemm_host(h.h, b"T" if transa else b"N", b"T" if transb else b"N", m, n,
                                 p, alpha, a.ctypes.data, a.shape[1], b.ctypes.data, b.shape[1],
