@@ -527,6 +527,10 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   fill_params(P, S, m, p, lds_a, lds_b, tiles_m, tiles_n, beta_bits, stages, alpha, beta, mu, nu,
               Cin, Cout, ldc, dump, fl);
   P.n_kb = static_cast<int>((std::max(lds_a, lds_b) + ozb::kKB - 1) / ozb::kKB);
+  // raster: tensor-bound schedules visit 4 pair-row-blocks per group (a wave of
+  // 74 tiles then spans ~4 x 18 tiles and re-reads less of B from DRAM: C3 DRAM
+  // 135 -> 82 GB, +3 %; tools/group_ncu.sh); L2-bound ones (C4) keep 2
+  if (!std::getenv("OZMM_GROUP_M")) P.group_m = dense ? 4 : 2;
   CUtensorMap map_a, map_b;
   if (int rc = make_slice_map(h, &map_a, As, lds_a, m, plane_a, k, Cfg::kAPart, ozb::kKB,
                               CU_TENSOR_MAP_SWIZZLE_128B))
