@@ -17,6 +17,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <atomic>
+#include <chrono>
 #include <thread>
 #include <utility>
 #include <vector>
@@ -1156,7 +1158,12 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   const int ns = static_cast<int>(strips.size());
   // events: A/B copied [ra + rb], A/B split [ra + rb], C strip copied [ns], GEMM done [ns], start, splits done
   std::vector<cudaEvent_t> ev(2 * (ra + rb) + 2 * ns + 2);
-  for (auto& e : ev) CUDA_TRY(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  // OZMM_TRACE=1: timed events and a per-panel / per-strip timeline on stderr
+  const bool trace = std::getenv("OZMM_TRACE") != nullptr;
+  for (auto& e : ev) CUDA_TRY(h, cudaEventCreateWithFlags(&e, trace ? 0 : cudaEventDisableTiming));
+  std::vector<cudaEvent_t> evGs(trace ? ns : 0), evO(trace ? ns : 0);
+  for (auto& e : evGs) CUDA_TRY(h, cudaEventCreate(&e));
+  for (auto& e : evO) CUDA_TRY(h, cudaEventCreate(&e));
   cudaEvent_t* evA = ev.data();
   cudaEvent_t* evB = evA + ra;
   cudaEvent_t* evSA = evB + rb;
@@ -1284,6 +1291,7 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
     cu(cudaStreamWaitEvent(sg, t.row ? evSA[t.step] : evSB[t.step], 0), "wait");
     if (!no_c) cu(cudaStreamWaitEvent(sg, evC[q], 0), "wait");
     h->stream = sg;
+    if (trace) cu(cudaEventRecord(evGs[q], sg), "event");
     if (offset) {
       fl.lsa = h->lsa + t.r0;
       fl.lsb = h->lsb + t.c0;
@@ -1300,18 +1308,55 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
     cu(cudaStreamWaitEvent(h->s_out, evG[q], 0), "wait");
     cu(cudaMemcpy2DAsync(C + t.r0 * ldc + t.c0, D * ldc, dO + t.r0 * p + t.c0, D * p, D * t.cols, t.rows,
                          cudaMemcpyDeviceToHost, h->s_out), "D2H C");
+    if (trace) cu(cudaEventRecord(evO[q], h->s_out), "event");
   };
   bool range_err = false;
   if (!no_c) {
     for (int q = 0; q < ns && rc == OZMM_OK; ++q) copy_out(q);
   } else {
+    for (auto& th : scanners) th.join();  // every c read before any D2H writes C
+    if (trace) {
+      float t_gpu = -1.f;
+      cudaEvent_t now;
+      cudaEventCreate(&now);
+      cudaEventRecord(now, h->s_in);  // H2D stream: how far the copies are
+      cudaEventSynchronize(now);
+      cudaEventElapsedTime(&t_gpu, evStart, now);
+      cudaEventDestroy(now);
+      std::fprintf(stderr, "[ozmm trace] host scan joined; H2D stream at %.2f ms\n", t_gpu);
+    }
     // gate: every split done and its flags clear before C is written at all
     cu(cudaEventSynchronize(evSplit), "sync");
     cu(cudaMemcpyAsync(h->hflags, h->flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->s_out), "flags");
     cu(cudaStreamSynchronize(h->s_out), "sync");
     range_err = rc == OZMM_OK && h->hflags[1] != 0;
-    for (auto& th : scanners) th.join();  // every c read before any D2H writes C
-    for (int q = 0; q < ns && rc == OZMM_OK && !range_err; ++q) copy_out(q);
+    // The strips already finished by now form (typically) the square
+    // [0, X) x [0, Y): it goes back as ONE copy with X-wide host rows -- host
+    // writes in narrow 8 KB row pieces drop to ~31 GB/s while the GEMM runs,
+    // full rows keep ~52-57 GB/s (tools/d2h_2d.py).  The rest goes per strip.
+    int q0 = 0;
+    if (rc == OZMM_OK && !range_err) {
+      int qd = 0;
+      while (qd < ns && cudaEventQuery(evG[qd]) == cudaSuccess) ++qd;
+      for (; qd > 1; --qd) {
+        int64_t R = 0, Cc = 0, area = 0;
+        for (int q = 0; q < qd; ++q) {
+          R = std::max(R, strips[q].r0 + strips[q].rows);
+          Cc = std::max(Cc, strips[q].c0 + strips[q].cols);
+          area += strips[q].rows * strips[q].cols;
+        }
+        if (area == R * Cc) {
+          for (int q = 0; q < qd; ++q) cu(cudaStreamWaitEvent(h->s_out, evG[q], 0), "wait");
+          cu(cudaMemcpy2DAsync(C, D * ldc, dO, D * p, D * Cc, R, cudaMemcpyDeviceToHost, h->s_out),
+             "D2H C");
+          if (trace)
+            for (int q = 0; q < qd; ++q) cu(cudaEventRecord(evO[q], h->s_out), "event");
+          q0 = qd;
+          break;
+        }
+      }
+    }
+    for (int q = q0; q < ns && rc == OZMM_OK && !range_err; ++q) copy_out(q);
   }
   for (auto& th : scanners)
     if (th.joinable()) th.join();
@@ -1339,6 +1384,23 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
         C[idx] = C[idx] + z;
       }
   }
+  if (trace && rc == OZMM_OK) {
+    auto ms = [&](cudaEvent_t e) {
+      float t = -1.f;
+      cudaEventElapsedTime(&t, evStart, e);
+      return t;
+    };
+    for (int s = 0; s < steps; ++s)
+      std::fprintf(stderr, "[ozmm trace] step %2d  A copied %7.2f split %7.2f | B copied %7.2f split %7.2f\n",
+                   s, s < ra ? ms(evA[s]) : -1.f, s < ra ? ms(evSA[s]) : -1.f,
+                   s < rb ? ms(evB[s]) : -1.f, s < rb ? ms(evSB[s]) : -1.f);
+    for (int q = 0; q < ns; ++q)
+      std::fprintf(stderr, "[ozmm trace] strip %2d %s %6lld x %6lld  gemm %7.2f -> %7.2f  d2h done %7.2f\n", q,
+                   strips[q].row ? "row" : "col", static_cast<long long>(strips[q].rows),
+                   static_cast<long long>(strips[q].cols), ms(evGs[q]), ms(evG[q]), ms(evO[q]));
+  }
+  for (auto& e : evGs) cudaEventDestroy(e);
+  for (auto& e : evO) cudaEventDestroy(e);
   for (auto& e : ev) cudaEventDestroy(e);
   if (rc == OZMM_OK && counts) {
     counts->int8_gemms = static_cast<int64_t>(k) * (k + 1) / 2;
