@@ -499,6 +499,7 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   if (const char* e = std::getenv("OZMM_SCHED_FILL"))  // scale of the fill terms
     cm.a_tile *= std::atof(e), cm.b_tile *= std::atof(e);
   if (const char* e = std::getenv("OZMM_SCHED")) cm.greedy = std::string(e) == "greedy";
+  if (const char* e = std::getenv("OZMM_AORDER")) cm.interleave = std::string(e) == "interleave";
   const ozb::Schedule S = ozb::make_schedule(k, fl.per_product ? 1 : r, Cfg::kNAcc,
                                              static_cast<int64_t>(Cfg::kMaxBSlots) * Cfg::kBTile,
                                              slot_bytes, Cfg::kMaxBSlots, cm);
@@ -540,7 +541,7 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   if (int rc = make_slice_map(h, &map_b, Bs, lds_b, p, plane_b, k, Cfg::kBHalf, ozb::kKB,
                               CU_TENSOR_MAP_SWIZZLE_128B))
     return rc;
-  if (fl.biased() && (kPairs != 1 || fl.per_product || fl.scale_mode != 0))
+  if (fl.biased() && (fl.per_product || fl.scale_mode != 0))
     return set_err(h, OZMM_ERR_UNSUPPORTED, "offset-binary slices need the CTA-pair ozIMMU_H kernel");
   const size_t smem = fixed + stages * Cfg::kATile + kSmemReserve + kBN * sizeof(double);
   if (!h->pair_attr_set[kPairs - 1]) {
@@ -556,12 +557,12 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   return OZMM_OK;
 }
 
-// The kernel launch_gemm picks for these options is the CTA-pair <128, 1> one.
+// The kernel launch_gemm picks for these options is a CTA-pair one (<128, 1>
+// or the 4-CTA <128, 2>), which can run on offset-binary planes.
 bool pair_kernel_selected(const ozmm_options_t* opt) {
   const int tile_n = opt ? opt->tile_n : 0;
   const int pair = opt ? opt->cta_pair : 0;
-  if (pair == 3 || (pair == 0 && tile_n == 0 && std::getenv("OZMM_QUAD"))) return false;
-  return pair == 2 || (pair == 0 && tile_n == 0);
+  return pair == 2 || pair == 3 || (pair == 0 && tile_n == 0);
 }
 
 // Offset-binary planes for the ozIMMU_H hot path unless the caller asks for

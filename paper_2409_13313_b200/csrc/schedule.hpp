@@ -120,6 +120,7 @@ struct PassCost {
   double b_tile = 171.0;  // 8 KB B tile per CTA
   double batch = 24.0;    // per-batch drain/refill, amortised per K block
   bool greedy = false;    // n_acc chunks per batch, B windows cut every b_windows slices
+  bool interleave = false; // A groups in large/small alternation (see make_schedule)
 };
 
 namespace detail {
@@ -260,9 +261,33 @@ inline Schedule make_schedule(int k, int64_t r, int n_acc, int64_t max_stage_byt
         ps.alo = std::min(ps.alo, p.s), ps.ahi = std::max(ps.ahi, p.s);
         ps.blo = std::min(ps.blo, p.t), ps.bhi = std::max(ps.bhi, p.t);
       }
-      // issue order inside the pass: by A slice (integer sums are order-free)
+      // issue order inside the pass: grouped by A slice (integer sums are
+      // order-free), slices ascending.  Optionally (PassCost::interleave) the
+      // groups alternate large and small (8, 1, 7, 2, ...) so the A ring's lead
+      // time never drops to a run of one-product stages: measured at C3 it keeps
+      // the tensor pipe busier (87.2 vs 85.5 %) but lets the tiles of a wave
+      // drift apart, DRAM reads rise 90 -> 162 GB and the capped clock falls --
+      // net 4 % slower, so it is off (tools/aorder_ab.sh).
       std::stable_sort(pass_prods.begin(), pass_prods.end(),
                        [](const Product& x, const Product& y) { return x.s < y.s; });
+      if (b_windows > 0 && cm.interleave) {
+        std::vector<std::vector<Product>> groups;
+        for (const Product& p : pass_prods) {
+          if (groups.empty() || groups.back()[0].s != p.s) groups.emplace_back();
+          groups.back().push_back(p);
+        }
+        std::stable_sort(groups.begin(), groups.end(),
+                         [](const auto& x, const auto& y) { return x.size() > y.size(); });
+        pass_prods.clear();
+        for (size_t lo = 0, hi = groups.size(); lo < hi;) {
+          for (const Product& p : groups[lo]) pass_prods.push_back(p);
+          ++lo;
+          if (lo < hi) {
+            --hi;
+            for (const Product& p : groups[hi]) pass_prods.push_back(p);
+          }
+        }
+      }
       ps.p0 = static_cast<int>(S.products.size());
       ps.g0 = static_cast<int>(S.agroups.size());
       for (Product pr : pass_prods) {
