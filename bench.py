@@ -219,6 +219,8 @@ def main():
         os.environ.setdefault("MASTER_PORT", "29517")
         os.environ.setdefault("RANK", str(rank))
         os.environ.setdefault("WORLD_SIZE", str(world))
+        # NCCL's version banner goes to stdout; keep stdout to the one JSON line
+        os.environ["NCCL_DEBUG"] = os.environ.get("OZMM_NCCL_DEBUG", "WARN")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     m, n, p, k, phi = args.m, args.n, args.p, args.k, args.phi
     dev = torch.device("cuda", local)

@@ -210,6 +210,27 @@ int ozmm_gemm_slices_strided(ozmm_handle_t h, int64_t m, int64_t n, int64_t p, i
                              int64_t plane_b, const double* nu, double alpha, double beta,
                              double* C, int64_t ldc, const ozmm_options_t* opt);
 
+/* Offset-binary halves (the fused GEMM's fast operand format, see
+ * ozmm_options_t.signed_slices).  ozmm_split_offset writes byte = slice + o_s
+ * (o_1 = 2^beta - 1, o_s = 2^(beta-1) for s >= 2; padding bytes 0) and the
+ * line sums of the SIGNED slices (mod 2^32) at
+ *   lsum[s * lsum_plane + line * lsum_lstride],  s = 0..k-1
+ * -- [k][lines] (lsum_lstride = 1, lsum_plane >= lines) or [lines][k]
+ * (lsum_plane = 1, lsum_lstride >= k); it zeroes them first.
+ * ozmm_gemm_slices_offset consumes such planes with their line sums (row sums
+ * of A lsa, column sums of B lsb, same indexing) and returns exactly what
+ * ozmm_gemm_slices_strided returns for the signed planes. */
+int ozmm_split_offset(ozmm_handle_t h, char side, char trans, int64_t lines, int64_t n,
+                      const double* X, int64_t ldx, int k, int beta, int8_t* slices, int64_t lds,
+                      double* shift, int32_t* lsum, int64_t lsum_plane, int64_t lsum_lstride);
+int ozmm_gemm_slices_offset(ozmm_handle_t h, int64_t m, int64_t n, int64_t p, int k,
+                            int beta_bits, int64_t r, const int8_t* As, int64_t lds_a,
+                            int64_t plane_a, const double* mu, const int32_t* lsa,
+                            int64_t lsa_plane, int64_t lsa_lstride, const int8_t* Bs,
+                            int64_t lds_b, int64_t plane_b, const double* nu, const int32_t* lsb,
+                            int64_t lsb_plane, int64_t lsb_lstride, double alpha, double beta,
+                            double* C, int64_t ldc, const ozmm_options_t* opt);
+
 /* ---- introspection (host only; used by tests/test_host_logic.py) ---------- */
 /* The GEMM's host schedule for (k, r) and a kernel choice (cta_pair/tile_n as
  * in ozmm_options_t): one row of 8 ints per slice product, in issue order:

@@ -65,9 +65,9 @@ struct GemmParams {
   // and the epilogue subtracts that exactly (lsa / lsb = signed line sums).
   int bias;
   int64_t n_inner;
-  const int32_t* lsa;  // [k][lsa_plane] row sums of the signed A slices
-  const int32_t* lsb;  // [k][lsb_plane] column sums of the signed B slices
-  int64_t lsa_plane, lsb_plane;
+  const int32_t* lsa;  // row sums of the signed A slices: lsa[(s-1)*lsa_plane + i*lsa_lstride]
+  const int32_t* lsb;  // column sums of the signed B slices (same indexing)
+  int64_t lsa_plane, lsb_plane, lsa_lstride, lsb_lstride;
   int hint_a, hint_b;  // L2 policies of the A / B slice loads (0 normal, 1 evict_first, 2 evict_last)
   // FP64 flush scaling (scheme.cpp:29-41 with the caller's unit vectors):
   //   0 group-wise        ru = mu_i 2^(2-beta g),   cv = nu_j                (:93-94)

@@ -246,7 +246,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
           for (int s = P.c_s[c]; s <= P.c_e[c]; ++s) {
             const int t = g - s;
             const uint32_t oa = s == 1 ? o1 : os, ob = t == 1 ? o1 : os;
-            const uint32_t ls = col < P.p ? static_cast<uint32_t>(P.lsb[(t - 1) * P.lsb_plane + col]) : 0u;
+            const uint32_t ls = col < P.p ? static_cast<uint32_t>(P.lsb[(t - 1) * P.lsb_plane + col * P.lsb_lstride]) : 0u;
             acc += oa * ls + oa * ob * static_cast<uint32_t>(P.n_inner);
           }
           ccol[ci * kBN + j] = acc;
@@ -262,7 +262,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
         if (P.bias && row_ok)
           for (int s = P.c_s[c]; s <= P.c_e[c]; ++s) {
             const int t = P.c_g[c] - s;
-            rrow += (t == 1 ? o1 : os) * static_cast<uint32_t>(P.lsa[(s - 1) * P.lsa_plane + row]);
+            rrow += (t == 1 ? o1 : os) * static_cast<uint32_t>(P.lsa[(s - 1) * P.lsa_plane + row * P.lsa_lstride]);
           }
 #pragma unroll
         for (int cc = 0; cc < kCols; cc += kLd) {

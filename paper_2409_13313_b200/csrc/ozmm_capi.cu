@@ -45,7 +45,7 @@ struct FlushCfg {
   // offset-binary slice planes (CTA-pair kernel only): signed line sums [k][plane]
   const int32_t* lsa = nullptr;
   const int32_t* lsb = nullptr;
-  int64_t lsa_plane = 0, lsb_plane = 0;
+  int64_t lsa_plane = 0, lsb_plane = 0, lsa_lstride = 1, lsb_lstride = 1;
   int64_t n = 0;
   bool biased() const { return lsa != nullptr; }
 };
@@ -196,7 +196,7 @@ bool valid_trans(char t) { return is_trans(t) || t == 'N' || t == 'n'; }
 // stride lsum_plane; zeroed by the caller), the fused pair GEMM's operand format.
 int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const double* X, int64_t ldx,
                  int k, int beta, int8_t* S, int64_t lds, int64_t plane, double* shift,
-                 int* lsum = nullptr, int64_t lsum_plane = 0) {
+                 int* lsum = nullptr, int64_t lsum_plane = 0, int64_t lsum_lstride = 1) {
   if (row_mode) {
     const bool vec = (reinterpret_cast<uintptr_t>(X) % 16 == 0) && (ldx % 2 == 0);
     // Whole row in registers, 16 elements per thread, split over a cluster of up
@@ -230,11 +230,11 @@ int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const doubl
       cfg.numAttrs = 1;
       if (vec)
         CUDA_TRY(h, cudaLaunchKernelEx(&cfg, ozb::slice_rows_cluster_kernel<true>, X, ldx, lines, n,
-                                       lds, k, beta, S, plane, shift, h->flags, lsum, lsum_plane));
+                                       lds, k, beta, S, plane, shift, h->flags, lsum, lsum_plane, lsum_lstride));
       else
         CUDA_TRY(h, cudaLaunchKernelEx(&cfg, ozb::slice_rows_cluster_kernel<false>, X, ldx, lines,
                                        n, lds, k, beta, S, plane, shift, h->flags, lsum,
-                                       lsum_plane));
+                                       lsum_plane, lsum_lstride));
     } else {
       const int64_t want = (chunks + 31) / 32 * 32;
       const int threads = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(32, want)));
@@ -242,11 +242,11 @@ int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const doubl
       if (vec)
         ozb::slice_rows_kernel<true><<<grid, threads, 0, h->stream>>>(X, ldx, lines, n, lds, k,
                                                                       beta, S, plane, shift,
-                                                                      h->flags, lsum, lsum_plane);
+                                                                      h->flags, lsum, lsum_plane, lsum_lstride);
       else
         ozb::slice_rows_kernel<false><<<grid, threads, 0, h->stream>>>(X, ldx, lines, n, lds, k,
                                                                        beta, S, plane, shift,
-                                                                       h->flags, lsum, lsum_plane);
+                                                                       h->flags, lsum, lsum_plane, lsum_lstride);
     }
   } else {
     if (int rc = ensure(h, &h->colmax, &h->colmax_n, static_cast<size_t>(lines))) return rc;
@@ -262,7 +262,7 @@ int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const doubl
                   static_cast<unsigned>((lds + 128 * tpc - 1) / (128 * tpc)));
     ozb::slice_cols_kernel<<<g2, 256, 0, h->stream>>>(X, ldx, n, lines, lds, k, beta, h->colmax,
                                                        S, plane, shift, h->flags, lsum, lsum_plane,
-                                                       tpc);
+                                                       lsum_lstride, tpc);
   }
   CUDA_TRY(h, cudaGetLastError());
   return OZMM_OK;
@@ -366,6 +366,8 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
   P.lsb = fl.lsb;
   P.lsa_plane = fl.lsa_plane;
   P.lsb_plane = fl.lsb_plane;
+  P.lsa_lstride = fl.lsa_lstride;
+  P.lsb_lstride = fl.lsb_lstride;
   P.units_a = fl.units_a;
   P.units_b = fl.units_b;
   P.m = static_cast<int>(m);
@@ -615,6 +617,12 @@ int check_range_sync(Handle* h) {
   return OZMM_OK;
 }
 
+int gemm_slices_checked(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_bits,
+                        int64_t r, const int8_t* As, int64_t lds_a, int64_t plane_a,
+                        const double* mu, const int8_t* Bs, int64_t lds_b, int64_t plane_b,
+                        const double* nu, double alpha, double beta, double* C, int64_t ldc,
+                        const ozmm_options_t* opt, const FlushCfg& fl);
+
 }  // namespace
 
 // =============================================================================
@@ -836,6 +844,63 @@ int ozmm_split(ozmm_handle_t handle, char side, char trans, int64_t lines, int64
   return launch_split(h, row_mode, lines, n, X, ldx, k, beta, slices, lds, lines * lds, shift);
 }
 
+int ozmm_split_offset(ozmm_handle_t handle, char side, char trans, int64_t lines, int64_t n,
+                      const double* X, int64_t ldx, int k, int beta, int8_t* slices, int64_t lds,
+                      double* shift, int32_t* lsum, int64_t lsum_plane, int64_t lsum_lstride) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return set_err(nullptr, OZMM_ERR_ARG, "null handle");
+  if (side != 'L' && side != 'R') return set_err(h, OZMM_ERR_ARG, "side must be 'L' or 'R'");
+  if (!valid_trans(trans)) return set_err(h, OZMM_ERR_ARG, "trans must be 'N' or 'T'");
+  if (lines < 1 || n < 1) return set_err(h, OZMM_ERR_ARG, "split: empty matrix");
+  if (k < 1 || k > ozb::kMaxK) return set_err(h, OZMM_ERR_ARG, "split: k must be in 1..%d", ozb::kMaxK);
+  if (lds < ozmm_slice_ld(n) || lds % 16) return set_err(h, OZMM_ERR_ARG, "split: lds too small or not a multiple of 16");
+  if (!lsum || lsum_plane < 1 || lsum_lstride < 1 ||
+      !((lsum_lstride == 1 && lsum_plane >= lines) || (lsum_plane == 1 && lsum_lstride >= k)))
+    return set_err(h, OZMM_ERR_ARG, "split: line sums need [k][>=lines] or [lines][>=k] strides");
+  if (beta == 0) {
+    beta = ozb::compute_beta_host(n);
+    if (beta < 0) return set_err(h, OZMM_ERR_ARG, "compute_beta: n out of range");
+  } else if (beta < 1 || beta > 7) {
+    return set_err(h, OZMM_ERR_ARG, "split: forced beta outside 1..7");
+  }
+  const bool row_mode = (side == 'L') != is_trans(trans);
+  if (ldx < (row_mode ? n : lines)) return set_err(h, OZMM_ERR_ARG, "split: leading dimension too small");
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  if (lsum_lstride == 1)
+    CUDA_TRY(h, cudaMemset2DAsync(lsum, sizeof(int32_t) * lsum_plane, 0, sizeof(int32_t) * lines, k,
+                                  h->stream));
+  else
+    CUDA_TRY(h, cudaMemset2DAsync(lsum, sizeof(int32_t) * lsum_lstride, 0, sizeof(int32_t) * k, lines,
+                                  h->stream));
+  return launch_split(h, row_mode, lines, n, X, ldx, k, beta, slices, lds, lines * lds, shift,
+                      lsum, lsum_plane, lsum_lstride);
+}
+
+int ozmm_gemm_slices_offset(ozmm_handle_t handle, int64_t m, int64_t n, int64_t p, int k,
+                            int beta_bits, int64_t r, const int8_t* As, int64_t lds_a,
+                            int64_t plane_a, const double* mu, const int32_t* lsa,
+                            int64_t lsa_plane, int64_t lsa_lstride, const int8_t* Bs, int64_t lds_b,
+                            int64_t plane_b, const double* nu, const int32_t* lsb,
+                            int64_t lsb_plane, int64_t lsb_lstride, double alpha, double beta,
+                            double* C, int64_t ldc, const ozmm_options_t* opt) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return set_err(nullptr, OZMM_ERR_ARG, "null handle");
+  if (!lsa || !lsb || lsa_plane < 1 || lsb_plane < 1 || lsa_lstride < 1 || lsb_lstride < 1)
+    return set_err(h, OZMM_ERR_ARG, "line sums missing or bad strides");
+  if (!pair_kernel_selected(opt))
+    return set_err(h, OZMM_ERR_UNSUPPORTED, "offset-binary slices need the CTA-pair kernel");
+  FlushCfg fl;
+  fl.lsa = lsa;
+  fl.lsb = lsb;
+  fl.lsa_plane = lsa_plane;
+  fl.lsb_plane = lsb_plane;
+  fl.lsa_lstride = lsa_lstride;
+  fl.lsb_lstride = lsb_lstride;
+  fl.n = n;
+  return gemm_slices_checked(h, m, n, p, k, beta_bits, r, As, lds_a, plane_a, mu, Bs, lds_b,
+                             plane_b, nu, alpha, beta, C, ldc, opt, fl);
+}
+
 int ozmm_split_ex(ozmm_handle_t handle, char side, char trans, int64_t lines, int64_t n,
                   const double* X, int64_t ldx, int k, int beta, int strategy, int8_t* slices,
                   int64_t lds, double* out) {
@@ -878,6 +943,19 @@ int ozmm_gemm_slices_strided(ozmm_handle_t handle, int64_t m, int64_t n, int64_t
                              double* C, int64_t ldc, const ozmm_options_t* opt) {
   Handle* h = reinterpret_cast<Handle*>(handle);
   if (!h) return set_err(nullptr, OZMM_ERR_ARG, "null handle");
+  return gemm_slices_checked(h, m, n, p, k, beta_bits, r, As, lds_a, plane_a, mu, Bs, lds_b,
+                             plane_b, nu, alpha, beta, C, ldc, opt, FlushCfg{});
+}
+
+}  // extern "C"
+
+namespace {
+// argument checks shared by the two slice-level GEMM entries
+int gemm_slices_checked(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_bits,
+                        int64_t r, const int8_t* As, int64_t lds_a, int64_t plane_a,
+                        const double* mu, const int8_t* Bs, int64_t lds_b, int64_t plane_b,
+                        const double* nu, double alpha, double beta, double* C, int64_t ldc,
+                        const ozmm_options_t* opt, const FlushCfg& fl) {
   if (m < 1 || n < 1 || p < 1) return set_err(h, OZMM_ERR_ARG, "empty shape");
   if (m > INT32_MAX || p > INT32_MAX) return set_err(h, OZMM_ERR_ARG, "m, p must fit int32");
   if (k < 1 || k > ozb::kMaxK) return set_err(h, OZMM_ERR_CONFIG, "k must be in 1..%d", ozb::kMaxK);
@@ -891,8 +969,11 @@ int ozmm_gemm_slices_strided(ozmm_handle_t handle, int64_t m, int64_t n, int64_t
   if (r < 1) return set_err(h, OZMM_ERR_CONFIG, "force_r must be >= 1");
   CUDA_TRY(h, cudaSetDevice(h->device));
   return launch_gemm(h, m, n, p, k, beta_bits, r, As, lds_a, plane_a, mu, Bs, lds_b, plane_b, nu,
-                     alpha, beta, C, C, ldc, opt);
+                     alpha, beta, C, C, ldc, opt, fl);
 }
+}  // namespace
+
+extern "C" {
 
 int ozmm_dgemm_ex(ozmm_handle_t handle, char transa, char transb, int64_t m, int64_t n, int64_t p,
                   double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,

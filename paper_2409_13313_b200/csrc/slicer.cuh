@@ -17,8 +17,8 @@
 // byte = slice + o_s with o_1 = 2^beta - 1 and o_s = 2^(beta-1) for s >= 2, so
 // every byte is an unsigned value in [0, 2^(beta+1) - 2] (|slice_1| <= 2^beta - 1
 // by rn_unit's bump rule, |slice_s| <= 2^(beta-1) after round-to-nearest);
-// padding bytes stay 0.  lsum[s][line] (zeroed by the caller) receives the
-// line's sum of the SIGNED slice values (mod 2^32), from which the GEMM removes
+// padding bytes stay 0.  lsum[s * lsum_plane + line * lsum_lstride] (zeroed by
+// the caller) receives the line's sum of the SIGNED slice values (mod 2^32), from which the GEMM removes
 // the offsets' contribution exactly (ozimmu_gemm_pair.cuh).  The signed planes
 // (lsum == nullptr) are the reference's SplitMatrix slices, bit for bit.
 //
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(1024) slice_rows_kernel(const double* __restri
                                                           int8_t* __restrict__ S, int64_t plane,
                                                           double* __restrict__ shift,
                                                           int* __restrict__ flags,
-                                                          int* __restrict__ lsum, int64_t lsum_plane) {
+                                                          int* __restrict__ lsum, int64_t lsum_plane, int64_t lsum_lstride) {
   __shared__ double red[32];
   __shared__ int lsum_s[kMaxSlices];  // offset mode: the row's per-slice sums
   if (threadIdx.x < kMaxSlices) lsum_s[threadIdx.x] = 0;  // ordered by block_max's barrier
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(1024) slice_rows_kernel(const double* __restri
   }
   if (lsum) {  // one CTA owns the row: plain stores
     __syncthreads();
-    if (threadIdx.x < k) lsum[threadIdx.x * lsum_plane + row] = lsum_s[threadIdx.x];
+    if (threadIdx.x < k) lsum[threadIdx.x * lsum_plane + row * lsum_lstride] = lsum_s[threadIdx.x];
   }
 }
 
@@ -231,7 +231,7 @@ template <bool kVec>
 __global__ void __launch_bounds__(512) slice_rows_cluster_kernel(
     const double* __restrict__ X, int64_t ld, int64_t rows, int64_t len, int64_t lds, int k,
     int beta, int8_t* __restrict__ S, int64_t plane, double* __restrict__ shift,
-    int* __restrict__ flags, int* __restrict__ lsum, int64_t lsum_plane) {
+    int* __restrict__ flags, int* __restrict__ lsum, int64_t lsum_plane, int64_t lsum_lstride) {
   __shared__ double red[32];
   __shared__ double cmax[8];  // one slot per CTA of the cluster
   __shared__ int lsum_s[kMaxSlices];  // offset mode: this CTA's part of the row sums
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(512) slice_rows_cluster_kernel(
     emit16(w, PE, beta, k, out + base0, plane, valid16(len - base0), base0 < lds, lsum_s, 1);
     __syncthreads();
     if (threadIdx.x < k && lsum_s[threadIdx.x] != 0)
-      atomicAdd(lsum + threadIdx.x * lsum_plane + row, lsum_s[threadIdx.x]);
+      atomicAdd(lsum + threadIdx.x * lsum_plane + row * lsum_lstride, lsum_s[threadIdx.x]);
   } else if (base0 < lds) {
     emit16(w, PE, beta, k, out + base0, plane);
   }
@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(const double* __restric
                                                          double* __restrict__ shift,
                                                          int* __restrict__ flags,
                                                          int* __restrict__ lsum, int64_t lsum_plane,
-                                                         int tiles_per_cta) {
+                                                         int64_t lsum_lstride, int tiles_per_cta) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t col = static_cast<int64_t>(blockIdx.x) * 32 + warp * 4 + (lane & 3);
   if (lsum == nullptr) {  // signed planes: one 128-row tile per CTA
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(const double* __restric
   for (int i = threadIdx.x; i < k * 32; i += blockDim.x) {
     const int64_t c = static_cast<int64_t>(blockIdx.x) * 32 + (i % 32);
     if (c < cols && lsum_s[i / 32][i % 32] != 0)
-      atomicAdd(lsum + (i / 32) * lsum_plane + c, lsum_s[i / 32][i % 32]);
+      atomicAdd(lsum + (i / 32) * lsum_plane + c * lsum_lstride, lsum_s[i / 32][i % 32]);
   }
 }
 

@@ -11,7 +11,8 @@ the group-wise accumulation is entry-local (proj/src/scheme.cpp:81-101).
 Per step each rank:
   1. slices m/(Pr*Pc) FULL rows of op(A) from its row panel and p/(Pr*Pc)
      FULL columns of op(B) from its column panel (K1; row maxima are local),
-  2. all-gathers the INT8 slice planes + shift vectors: A planes inside its
+  2. all-gathers the INT8 slice planes + shift vectors (+ the int32 line sums
+     of the offset-binary planes the CUDA backend uses): A planes inside its
      row communicator (the Pc ranks sharing gr), B planes inside its column
      communicator (the Pr ranks sharing gc).  No reductions: NCCL only
      broadcasts slice panels, as the north star asks,
@@ -97,7 +98,13 @@ def make_layout(m: int, n: int, p: int, world: int, rank: int) -> Layout:
 
 
 class Backend:
-    """CUDA backend: K1 / K2+K3 through the C ABI (no CPU fallback)."""
+    """CUDA backend: K1 / K2+K3 through the C ABI (no CPU fallback).
+
+    ``offset_planes``: the slice planes are the fused GEMM's offset-binary
+    format (ozmm_split_offset / ozmm_gemm_slices_offset) and travel with their
+    int32 line sums, which the grid gathers alongside the shift vectors."""
+
+    offset_planes = True
 
     def __init__(self, device: int):
         from . import ozmm
@@ -123,7 +130,10 @@ class Backend:
         if hasattr(self, "_side"):
             torch.cuda.current_stream(self.device).wait_stream(self._side)
 
-    def split(self, x, k: int, side: str, trans: bool, beta: int, out_slices, out_shift):
+    def split(self, x, k: int, side: str, trans: bool, beta: int, out_slices, out_shift,
+              lsum=None):
+        """lsum ([lines][k] int32 view): offset-binary planes plus their line sums;
+        None: the reference's signed planes."""
         oz = self.oz
         rows, cols = x.shape
         if side == "L":
@@ -131,22 +141,36 @@ class Backend:
         else:
             n, lines = (cols, rows) if trans else (rows, cols)
         self.handle.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
-        self.handle.check(oz.lib.ozmm_split(
-            self.handle.h, side.encode(), b"T" if trans else b"N", lines, n, x.data_ptr(),
-            x.stride(0), k, beta, out_slices.data_ptr(), out_slices.shape[-1],
-            out_shift.data_ptr()))
+        args = (self.handle.h, side.encode(), b"T" if trans else b"N", lines, n, x.data_ptr(),
+                x.stride(0), k, beta, out_slices.data_ptr(), out_slices.shape[-1],
+                out_shift.data_ptr())
+        if lsum is None:
+            self.handle.check(oz.lib.ozmm_split(*args))
+        else:
+            self.handle.check(oz.lib.ozmm_split_offset(*args, lsum.data_ptr(), lsum.stride(1),
+                                                       lsum.stride(0)))
 
-    def gemm(self, m, n, p, k, beta_bits, a_slices, mu, b_slices, nu, alpha, beta, c):
+    def gemm(self, m, n, p, k, beta_bits, a_slices, mu, b_slices, nu, alpha, beta, c,
+             lsa=None, lsb=None):
         """K2+K3 on [k][m][lds] / [k][p][lds] slice views (row / column ranges of a
-        panel are fine: the plane stride is passed through)."""
+        panel are fine: the plane stride is passed through); lsa / lsb: the line
+        sums of offset-binary planes ([m][k] / [p][k] views)."""
         oz = self.oz
         self.handle.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
         opt = oz.Options()
-        self.handle.check(oz.lib.ozmm_gemm_slices_strided(
-            self.handle.h, m, n, p, k, beta_bits, 0, a_slices.data_ptr(), a_slices.stride(1),
-            a_slices.stride(0), mu.data_ptr(), b_slices.data_ptr(), b_slices.stride(1),
-            b_slices.stride(0), nu.data_ptr(), alpha, beta, c.data_ptr(), c.stride(0),
-            ctypes.byref(opt)))
+        if lsa is None:
+            self.handle.check(oz.lib.ozmm_gemm_slices_strided(
+                self.handle.h, m, n, p, k, beta_bits, 0, a_slices.data_ptr(), a_slices.stride(1),
+                a_slices.stride(0), mu.data_ptr(), b_slices.data_ptr(), b_slices.stride(1),
+                b_slices.stride(0), nu.data_ptr(), alpha, beta, c.data_ptr(), c.stride(0),
+                ctypes.byref(opt)))
+        else:
+            self.handle.check(oz.lib.ozmm_gemm_slices_offset(
+                self.handle.h, m, n, p, k, beta_bits, 0, a_slices.data_ptr(), a_slices.stride(1),
+                a_slices.stride(0), mu.data_ptr(), lsa.data_ptr(), lsa.stride(1), lsa.stride(0),
+                b_slices.data_ptr(), b_slices.stride(1), b_slices.stride(0), nu.data_ptr(),
+                lsb.data_ptr(), lsb.stride(1), lsb.stride(0), alpha, beta, c.data_ptr(),
+                c.stride(0), ctypes.byref(opt)))
 
 
 def _new_group(ranks):
@@ -220,6 +244,15 @@ class Grid2DGemm:
         else:
             self.b_pan = be.empty((k, L.pcols, self.lds), torch.int8)
             self.nu_pan = be.empty((L.pcols,), torch.float64)
+        # offset-binary planes travel with their int32 line sums, [lines][k] so that
+        # one all-gather along the lines moves them
+        self.offset = bool(getattr(be, "offset_planes", False))
+        self.lsa_loc = self.lsa_pan = self.lsb_loc = self.lsb_pan = None
+        if self.offset:
+            self.lsa_loc = be.empty((L.ms, k), torch.int32)
+            self.lsb_loc = be.empty((L.ps, k), torch.int32)
+            self.lsa_pan = self.lsa_loc if L.pc == 1 else be.empty((L.mr, k), torch.int32)
+            self.lsb_pan = self.lsb_loc if L.pr == 1 else be.empty((L.pcols, k), torch.int32)
 
     def _gather(self, out, inp, group, nranks):
         if nranks > 1:
@@ -242,28 +275,40 @@ class Grid2DGemm:
         slices and shifts, so the result is bit-identical to one GPU."""
         L, k = self.L, self.k
         be = self.backend
-        be.split(a_rows, k, "L", self.transa, self.beta_bits, self.a_loc, self.mu_loc)
-        be.split(b_cols, k, "R", self.transb, self.beta_bits, self.b_loc, self.nu_loc)
+        off = self.offset
+        ls = (lambda *a: dict(lsum=a[0])) if off else (lambda *a: {})
+        be.split(a_rows, k, "L", self.transa, self.beta_bits, self.a_loc, self.mu_loc,
+                 **ls(self.lsa_loc))
+        be.split(b_cols, k, "R", self.transb, self.beta_bits, self.b_loc, self.nu_loc,
+                 **ls(self.lsb_loc))
         # B first: it unblocks G2; group g of a GEMM needs slice planes <= g-1
         wb = [self._gather(self.b_pan[s], self.b_loc[s], self.col_group, L.pr) for s in range(k)]
         wb.append(self._gather(self.nu_pan, self.nu_loc, self.col_group, L.pr))
         wa = [self._gather(self.a_pan[s], self.a_loc[s], self.row_group, L.pc) for s in range(k)]
         wa.append(self._gather(self.mu_pan, self.mu_loc, self.row_group, L.pc))
+        if off:
+            wb.append(self._gather(self.lsb_pan, self.lsb_loc, self.col_group, L.pr))
+            wa.append(self._gather(self.lsa_pan, self.lsa_loc, self.row_group, L.pc))
+
+        def sums(a_sl, b_sl):  # line sums of the operand rows / columns a strip reads
+            return dict(lsa=a_sl, lsb=b_sl) if off else {}
         r0, c0 = L.gc * L.ms, L.gr * L.ps  # own rows / columns inside the C block
         g = (L.n, k, self.beta_bits)
         own_rows = c_block[r0:r0 + L.ms]
         side = getattr(be, "side_stream", None)
         with side() if side else contextlib.nullcontext():
             be.gemm(L.ms, g[0], L.ps, k, g[2], self.a_loc, self.mu_loc, self.b_loc, self.nu_loc,
-                    alpha, beta, own_rows[:, c0:c0 + L.ps])
+                    alpha, beta, own_rows[:, c0:c0 + L.ps], **sums(self.lsa_loc, self.lsb_loc))
         self._wait(wb)
         for lo, hi in _other_ranges(L.pcols, c0, L.ps):
             be.gemm(L.ms, g[0], hi - lo, k, g[2], self.a_loc, self.mu_loc, self.b_pan[:, lo:hi],
-                    self.nu_pan[lo:hi], alpha, beta, own_rows[:, lo:hi])
+                    self.nu_pan[lo:hi], alpha, beta, own_rows[:, lo:hi],
+                    **sums(self.lsa_loc, self.lsb_pan[lo:hi] if off else None))
         self._wait(wa)
         for lo, hi in _other_ranges(L.mr, r0, L.ms):
             be.gemm(hi - lo, g[0], L.pcols, k, g[2], self.a_pan[:, lo:hi], self.mu_pan[lo:hi],
-                    self.b_pan, self.nu_pan, alpha, beta, c_block[lo:hi])
+                    self.b_pan, self.nu_pan, alpha, beta, c_block[lo:hi],
+                    **sums(self.lsa_pan[lo:hi] if off else None, self.lsb_pan))
         if side:
             be.join_side()
         return c_block

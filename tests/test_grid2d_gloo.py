@@ -62,13 +62,49 @@ class OracleBackend:
         c.copy_(torch.from_numpy(alpha * D + beta * c.numpy()))
 
 
+class OffsetOracleBackend(OracleBackend):
+    """Test stand-in with the CUDA backend's offset-binary contract: split()
+    emits byte = slice + o_s (o_1 = 2^beta - 1, o_s = 2^(beta-1); padding 0) and
+    the signed line sums into lsum ([lines][k]); gemm() recovers the signed
+    planes from the bytes, checks the line sums that travelled through the
+    gathers against them, then accumulates like OracleBackend."""
+
+    offset_planes = True
+
+    @staticmethod
+    def _offsets(k, beta):
+        return np.array([(1 << beta) - 1] + [1 << (beta - 1)] * (k - 1), np.int64)
+
+    def split(self, x, k, side, trans, beta, out_slices, out_shift, lsum=None):
+        super().split(x, k, side, trans, beta, out_slices, out_shift)
+        a = x.numpy().T if trans else x.numpy()
+        n = a.shape[1] if side == "L" else a.shape[0]
+        sl = out_slices.numpy()[:, :, :n].astype(np.int64)
+        lsum.copy_(torch.from_numpy(sl.sum(axis=2).T.astype(np.int32)))
+        biased = (sl + self._offsets(k, beta)[:, None, None]).astype(np.uint8).view(np.int8)
+        out_slices[:, :, :n] = torch.from_numpy(np.ascontiguousarray(biased))
+
+    def gemm(self, m, n, p, k, beta_bits, a_slices, mu, b_slices, nu, alpha, beta, c,
+             lsa=None, lsb=None):
+        off = self._offsets(k, beta_bits)
+
+        def unbias(planes, sums):
+            u = planes.numpy()[:, :, :n].view(np.uint8).astype(np.int64) - off[:, None, None]
+            assert np.array_equal(u.sum(axis=2).T.astype(np.int32), sums.numpy())
+            out = torch.zeros_like(planes)
+            out[:, :, :n] = torch.from_numpy(u.astype(np.int8))
+            return out
+        super().gemm(m, n, p, k, beta_bits, unbias(a_slices, lsa), mu, unbias(b_slices, lsb),
+                     nu, alpha, beta, c)
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, m, n, p, k, phi, alpha, beta, q):
+def _worker(rank, world, port, m, n, p, k, phi, alpha, beta, q, offset=False):
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -76,7 +112,7 @@ def _worker(rank, world, port, m, n, p, k, phi, alpha, beta, q):
     try:
         from paper_2409_13313_b200 import ozmm
         from paper_2409_13313_b200.grid2d import Grid2DGemm
-        G = Grid2DGemm(m, n, p, k, backend=OracleBackend())
+        G = Grid2DGemm(m, n, p, k, backend=OffsetOracleBackend() if offset else OracleBackend())
         L = G.L
         sa, sb, sc = (ozmm.counter_hash(5, i) for i in (1, 2, 3))
         a_rows = torch.from_numpy(ozmm.gen_phi_block(m, n, phi, sa, L.a_row0, L.ms, 0, n))
@@ -89,8 +125,9 @@ def _worker(rank, world, port, m, n, p, k, phi, alpha, beta, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4, 8])
-def test_grid2d_matches_single_process(world, port):
+@pytest.mark.parametrize("world,offset", [(2, False), (4, False), (8, False), (4, True),
+                                          (8, True)])
+def test_grid2d_matches_single_process(world, offset, port):
     m, n, p, k, phi, alpha, beta = 32, 200, 48, 8, 1.0, 1.5, 0.5
     from paper_2409_13313_b200 import ozmm
     A = ozmm.gen_phi_block(m, n, phi, ozmm.counter_hash(5, 1))
@@ -99,8 +136,8 @@ def test_grid2d_matches_single_process(world, port):
     want = port.gemm(alpha, A, B, beta, C, k=k)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, PORT[world],
-                                               m, n, p, k, phi, alpha, beta, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, PORT[(world, offset)],
+                                               m, n, p, k, phi, alpha, beta, q, offset))
              for r in range(world)]
     for pr in procs:
         pr.start()
@@ -114,4 +151,4 @@ def test_grid2d_matches_single_process(world, port):
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
 
 
-PORT = {2: _free_port(), 4: _free_port(), 8: _free_port()}
+PORT = {(w, o): _free_port() for w in (2, 4, 8) for o in (False, True)}
