@@ -425,6 +425,22 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
     P.p_g0[q] = static_cast<uint16_t>(S.passes[q].g0);
     P.p_g1[q] = static_cast<uint16_t>(S.passes[q].g1);
   }
+  // timing experiment only (results are wrong): OZMM_ONLY_BATCH=b runs batch b alone
+  if (const char* e = std::getenv("OZMM_ONLY_BATCH")) {
+    const int b = std::atoi(e);
+    if (b >= 0 && b < P.nbatch) {
+      const int q0 = P.b_pass0[b], q1 = P.b_pass1[b];
+      for (int q = q0; q < q1; ++q) {
+        P.p_alo[q - q0] = P.p_alo[q], P.p_ahi[q - q0] = P.p_ahi[q];
+        P.p_blo[q - q0] = P.p_blo[q], P.p_bhi[q - q0] = P.p_bhi[q];
+        P.p_p0[q - q0] = P.p_p0[q], P.p_p1[q - q0] = P.p_p1[q];
+        P.p_g0[q - q0] = P.p_g0[q], P.p_g1[q - q0] = P.p_g1[q];
+      }
+      P.b_c0[0] = P.b_c0[b], P.b_nc[0] = P.b_nc[b];
+      P.b_pass0[0] = 0, P.b_pass1[0] = static_cast<uint8_t>(q1 - q0);
+      P.nbatch = 1, P.npass = q1 - q0;
+    }
+  }
   for (size_t g = 0; g < S.agroups.size(); ++g) {
     P.ag_s[g] = static_cast<uint8_t>(S.agroups[g].s);
     P.ag_p0[g] = static_cast<uint16_t>(S.agroups[g].p0);
