@@ -1258,6 +1258,7 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   std::vector<cudaEvent_t> ev(2 * (ra + rb) + 2 * ns + 2);
   // OZMM_TRACE=1: timed events and a per-panel / per-strip timeline on stderr
   const bool trace = std::getenv("OZMM_TRACE") != nullptr;
+  const auto t_entry = std::chrono::steady_clock::now();
   for (auto& e : ev) CUDA_TRY(h, cudaEventCreateWithFlags(&e, trace ? 0 : cudaEventDisableTiming));
   std::vector<cudaEvent_t> evGs(trace ? ns : 0), evO(trace ? ns : 0);
   for (auto& e : evGs) CUDA_TRY(h, cudaEventCreate(&e));
@@ -1281,18 +1282,22 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   std::vector<std::thread> scanners;
   std::vector<std::vector<std::pair<int64_t, double>>> bad;  // (index, original c)
   if (no_c) {
+    int64_t want = 8;
+    if (const char* e = std::getenv("OZMM_SCAN_THREADS")) want = std::max(1, std::atoi(e));
     const int nt = static_cast<int>(std::max<int64_t>(
-        1, std::min<int64_t>({8, static_cast<int64_t>(std::thread::hardware_concurrency()), (m * p) >> 20})));
+        1, std::min<int64_t>({want, static_cast<int64_t>(std::thread::hardware_concurrency()), (m * p) >> 20})));
     bad.resize(nt);
     for (int t = 0; t < nt; ++t)
       scanners.emplace_back([&, t, nt] {
         const int64_t i0 = m * t / nt, i1 = m * (t + 1) / nt;
+        constexpr uint64_t kExp = 0x7FF0000000000000ull, kOne = 0x0010000000000000ull;
         for (int64_t i = i0; i < i1; ++i) {
           const uint64_t* row = reinterpret_cast<const uint64_t*>(C + i * ldc);
+          // (x & kExp) + kOne carries into bit 63 exactly when the exponent field is
+          // all ones (inf / NaN): and + add + or per element, which vectorises
           uint64_t any = 0;
-          for (int64_t j = 0; j < p; ++j)
-            any |= static_cast<uint64_t>((row[j] & 0x7FF0000000000000ull) == 0x7FF0000000000000ull);
-          if (any)
+          for (int64_t j = 0; j < p; ++j) any |= (row[j] & kExp) + kOne;
+          if (any >> 63)
             for (int64_t j = 0; j < p; ++j)
               if ((row[j] & 0x7FF0000000000000ull) == 0x7FF0000000000000ull)
                 bad[t].push_back({i * ldc + j, C[i * ldc + j]});
@@ -1413,16 +1418,10 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
     for (int q = 0; q < ns && rc == OZMM_OK; ++q) copy_out(q);
   } else {
     for (auto& th : scanners) th.join();  // every c read before any D2H writes C
-    if (trace) {
-      float t_gpu = -1.f;
-      cudaEvent_t now;
-      cudaEventCreate(&now);
-      cudaEventRecord(now, h->s_in);  // H2D stream: how far the copies are
-      cudaEventSynchronize(now);
-      cudaEventElapsedTime(&t_gpu, evStart, now);
-      cudaEventDestroy(now);
-      std::fprintf(stderr, "[ozmm trace] host scan joined; H2D stream at %.2f ms\n", t_gpu);
-    }
+    if (trace)
+      std::fprintf(stderr, "[ozmm trace] host C scan joined %.2f ms after entry\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_entry)
+                       .count());
     // gate: every split done and its flags clear before C is written at all
     cu(cudaEventSynchronize(evSplit), "sync");
     cu(cudaMemcpyAsync(h->hflags, h->flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->s_out), "flags");
