@@ -18,6 +18,7 @@
 #include <mutex>
 #include <string>
 #include <atomic>
+#include <memory>
 #include <chrono>
 #include <thread>
 #include <utility>
@@ -1240,18 +1241,52 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   double *dA = h->host_a, *dB = h->host_b, *dC = h->host_c, *dO = h->host_o;
   const size_t D = sizeof(double);
 
-  // strips in issue order: step s = row strip (A_s x B_<s), column strip (A_<=s x B_s)
+  // Panel arrival order over PCIe: A_s then B_s per step, except that the last
+  // step sends B first, so the final strip is a row strip -- full-width host
+  // rows, whose D2H is the tail of the call (a narrow column strip's D2H runs
+  // at ~31 GB/s while the GEMM is busy, full rows at ~52+).
+  struct Arrival {
+    bool is_a;
+    int idx;
+  };
+  std::vector<Arrival> order;
+  for (int s = 0; s < steps; ++s) {
+    if (s == steps - 1 && s < ra && s < rb) {
+      order.push_back({false, s});
+      order.push_back({true, s});
+      continue;
+    }
+    if (s < ra) order.push_back({true, s});
+    if (s < rb) order.push_back({false, s});
+  }
+  // strips in issue order: each arrival makes one block of C computable, A_s x
+  // (the B panels so far) or (the A panels so far) x B_s; it waits on the split
+  // of that arrival (the split stream is in order, so that covers every panel)
   struct Strip {
     int64_t r0, rows, c0, cols;
-    int step;
-    bool row;
+    bool trig_a;
+    int trig;
   };
   std::vector<Strip> strips;
-  for (int s = 0; s < steps; ++s) {
-    if (s < ra && std::min(s, rb) > 0)
-      strips.push_back({s * pa, std::min(pa, m - s * pa), 0, std::min<int64_t>(p, std::min(s, rb) * pb), s, true});
-    if (s < rb)
-      strips.push_back({0, std::min<int64_t>(m, std::min(s + 1, ra) * pa), s * pb, std::min(pb, p - s * pb), s, false});
+  std::vector<int> strip_of(order.size(), -1);
+  {
+    int64_t na_arr = 0, nb_arr = 0;
+    for (size_t o = 0; o < order.size(); ++o) {
+      const int i = order[o].idx;
+      if (order[o].is_a) {
+        if (nb_arr > 0) {
+          strip_of[o] = static_cast<int>(strips.size());
+          strips.push_back({i * pa, std::min(pa, m - i * pa), 0, std::min<int64_t>(p, nb_arr * pb), true, i});
+        }
+        ++na_arr;
+      } else {
+        if (na_arr > 0) {
+          strip_of[o] = static_cast<int>(strips.size());
+          strips.push_back({0, std::min<int64_t>(m, na_arr * pa), i * pb, std::min(pb, p - i * pb), false, i});
+        }
+        ++nb_arr;
+      }
+    }
   }
   const int ns = static_cast<int>(strips.size());
   // events: A/B copied [ra + rb], A/B split [ra + rb], C strip copied [ns], GEMM done [ns], start, splits done
@@ -1278,15 +1313,48 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
     return e == cudaSuccess;
   };
 
-  // host scan of C for non-finite entries (no-C mode), concurrent with the GPU
+  // Host scans (no-C mode), concurrent with the GPU:
+  //  1. C for non-finite entries (patched on the host afterwards, see below);
+  //  2. then the A and B panels of the LAST steps, backwards, for any element
+  //     with |x| >= 2^921 (exponent field >= 1944, incl. inf / NaN).  A line
+  //     max >= 2^921 is the only range error (split.cpp:124-125), so a clean
+  //     scan of a panel proves its split cannot raise the range flag.  The D2H
+  //     gate then opens as soon as the GPU has split every earlier step with
+  //     clean flags -- the GPU-split prefix meets the host-scanned suffix at
+  //     ~55 ms at C3 instead of the last split at ~81 ms.
   std::vector<std::thread> scanners;
   std::vector<std::vector<std::pair<int64_t, double>>> bad;  // (index, original c)
+  std::atomic<int> c_scans_left{0}, next_tail{steps - 1}, tail_hit{0}, stop_tail{0};
+  std::unique_ptr<std::atomic<int>[]> tail_done(new std::atomic<int>[steps]);
+  for (int s0 = 0; s0 < steps; ++s0) tail_done[s0] = 0;
+  auto any_big = [](const double* x, int64_t rows, int64_t cols, int64_t ld) {
+    constexpr uint64_t kExp = 0x7FF0000000000000ull, kBias = uint64_t(2048 - 1944) << 52;
+    uint64_t any = 0;
+    for (int64_t i = 0; i < rows; ++i) {
+      const uint64_t* row = reinterpret_cast<const uint64_t*>(x + i * ld);
+      for (int64_t j = 0; j < cols; ++j) any |= (row[j] & kExp) + kBias;  // bit 63: exp >= 1944
+    }
+    return (any >> 63) != 0;
+  };
+  auto scan_step = [&](int st) {  // A panel st and B panel st of op(A) / op(B)
+    bool big = false;
+    if (st < ra) {
+      const int64_t r0 = st * pa, rows = std::min(pa, m - r0);
+      big = ta ? any_big(A + r0, n, rows, lda) : any_big(A + r0 * lda, rows, n, lda);
+    }
+    if (!big && st < rb) {
+      const int64_t c0 = st * pb, cols = std::min(pb, p - c0);
+      big = tb ? any_big(B + c0 * ldb, cols, n, ldb) : any_big(B + c0, n, cols, ldb);
+    }
+    return big;
+  };
   if (no_c) {
     int64_t want = 8;
     if (const char* e = std::getenv("OZMM_SCAN_THREADS")) want = std::max(1, std::atoi(e));
     const int nt = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>({want, static_cast<int64_t>(std::thread::hardware_concurrency()), (m * p) >> 20})));
     bad.resize(nt);
+    c_scans_left = nt;
     for (int t = 0; t < nt; ++t)
       scanners.emplace_back([&, t, nt] {
         const int64_t i0 = m * t / nt, i1 = m * (t + 1) / nt;
@@ -1301,6 +1369,14 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
             for (int64_t j = 0; j < p; ++j)
               if ((row[j] & 0x7FF0000000000000ull) == 0x7FF0000000000000ull)
                 bad[t].push_back({i * ldc + j, C[i * ldc + j]});
+        }
+        --c_scans_left;
+        // tail scan: claim steps from the last one backwards until the gate opens
+        while (!stop_tail.load() && !tail_hit.load()) {
+          const int st = next_tail.fetch_sub(1);
+          if (st < 0) break;
+          if (scan_step(st)) tail_hit = 1;
+          tail_done[st] = 1;
         }
       });
   }
@@ -1325,64 +1401,56 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   for (cudaStream_t s : {h->s_in, h->s_out, h->s_split, h->s_gemm[0], h->s_gemm[1]})
     cu(cudaStreamWaitEvent(s, evStart, 0), "wait");
 
-  // H2D stream: A_s, [C row strip], B_s, [C column strip]
+  // H2D stream: the panels in arrival order, each followed by the C block its strip reads
   auto copy_c = [&](int q) {
     const Strip& t = strips[q];
     cu(cudaMemcpy2DAsync(dC + t.r0 * p + t.c0, D * p, C + t.r0 * ldc + t.c0, D * ldc, D * t.cols, t.rows,
                          cudaMemcpyHostToDevice, h->s_in), "H2D C");
     cu(cudaEventRecord(evC[q], h->s_in), "event");
   };
-  {
-    int q = 0;
-    for (int s = 0; s < steps && rc == OZMM_OK; ++s) {
-      if (s < ra) {
-        const int64_t r0 = s * pa, rows = std::min(pa, m - r0);
-        if (ta)  // op(A) rows r0.. = columns r0.. of the stored n x m A
-          cu(cudaMemcpy2DAsync(dA + r0, D * m, A + r0, D * lda, D * rows, n, cudaMemcpyHostToDevice,
-                               h->s_in), "H2D A");
-        else
-          cu(cudaMemcpy2DAsync(dA + r0 * n, D * n, A + r0 * lda, D * lda, D * n, rows,
-                               cudaMemcpyHostToDevice, h->s_in), "H2D A");
-        cu(cudaEventRecord(evA[s], h->s_in), "event");
-        if (q < ns && strips[q].step == s && strips[q].row) {
-          if (!no_c) copy_c(q);
-          ++q;
-        }
-      }
-      if (s < rb) {
-        const int64_t c0 = s * pb, cols = std::min(pb, p - c0);
-        if (tb)  // op(B) columns c0.. = rows c0.. of the stored p x n B
-          cu(cudaMemcpy2DAsync(dB + c0 * n, D * n, B + c0 * ldb, D * ldb, D * n, cols,
-                               cudaMemcpyHostToDevice, h->s_in), "H2D B");
-        else
-          cu(cudaMemcpy2DAsync(dB + c0, D * p, B + c0, D * ldb, D * cols, n, cudaMemcpyHostToDevice,
-                               h->s_in), "H2D B");
-        cu(cudaEventRecord(evB[s], h->s_in), "event");
-        if (!no_c) copy_c(q);
-        ++q;
-      }
+  for (size_t o = 0; o < order.size() && rc == OZMM_OK; ++o) {
+    const int s0 = order[o].idx;
+    if (order[o].is_a) {
+      const int64_t r0 = s0 * pa, rows = std::min(pa, m - r0);
+      if (ta)  // op(A) rows r0.. = columns r0.. of the stored n x m A
+        cu(cudaMemcpy2DAsync(dA + r0, D * m, A + r0, D * lda, D * rows, n, cudaMemcpyHostToDevice,
+                             h->s_in), "H2D A");
+      else
+        cu(cudaMemcpy2DAsync(dA + r0 * n, D * n, A + r0 * lda, D * lda, D * n, rows,
+                             cudaMemcpyHostToDevice, h->s_in), "H2D A");
+      cu(cudaEventRecord(evA[s0], h->s_in), "event");
+    } else {
+      const int64_t c0 = s0 * pb, cols = std::min(pb, p - c0);
+      if (tb)  // op(B) columns c0.. = rows c0.. of the stored p x n B
+        cu(cudaMemcpy2DAsync(dB + c0 * n, D * n, B + c0 * ldb, D * ldb, D * n, cols,
+                             cudaMemcpyHostToDevice, h->s_in), "H2D B");
+      else
+        cu(cudaMemcpy2DAsync(dB + c0, D * p, B + c0, D * ldb, D * cols, n, cudaMemcpyHostToDevice,
+                             h->s_in), "H2D B");
+      cu(cudaEventRecord(evB[s0], h->s_in), "event");
     }
+    if (!no_c && strip_of[o] >= 0) copy_c(strip_of[o]);
   }
-  // split stream (high priority): A_s then B_s, each as soon as it lands
-  for (int s = 0; s < steps && rc == OZMM_OK; ++s) {
-    h->stream = h->s_split;
-    if (s < ra) {
-      const int64_t r0 = s * pa, rows = std::min(pa, m - r0);
-      cu(cudaStreamWaitEvent(h->s_split, evA[s], 0), "wait");
+  // split stream (high priority): each panel as soon as it lands
+  h->stream = h->s_split;
+  for (size_t o = 0; o < order.size() && rc == OZMM_OK; ++o) {
+    const int s0 = order[o].idx;
+    if (order[o].is_a) {
+      const int64_t r0 = s0 * pa, rows = std::min(pa, m - r0);
+      cu(cudaStreamWaitEvent(h->s_split, evA[s0], 0), "wait");
       if (rc == OZMM_OK)
         rc = launch_split(h, !ta, rows, n, ta ? dA + r0 : dA + r0 * n, ta ? m : n, k, beta_bits,
                           h->slices_a + r0 * lds, lds, m * lds, h->mu + r0,
                           offset ? h->lsa + r0 : nullptr, m);
-      cu(cudaEventRecord(evSA[s], h->s_split), "event");
-    }
-    if (s < rb && rc == OZMM_OK) {
-      const int64_t c0 = s * pb, cols = std::min(pb, p - c0);
-      cu(cudaStreamWaitEvent(h->s_split, evB[s], 0), "wait");
+      cu(cudaEventRecord(evSA[s0], h->s_split), "event");
+    } else {
+      const int64_t c0 = s0 * pb, cols = std::min(pb, p - c0);
+      cu(cudaStreamWaitEvent(h->s_split, evB[s0], 0), "wait");
       if (rc == OZMM_OK)
         rc = launch_split(h, tb, cols, n, tb ? dB + c0 * n : dB + c0, tb ? n : p, k, beta_bits,
                           h->slices_b + c0 * lds, lds, p * lds, h->nu + c0,
                           offset ? h->lsb + c0 : nullptr, p);
-      cu(cudaEventRecord(evSB[s], h->s_split), "event");
+      cu(cudaEventRecord(evSB[s0], h->s_split), "event");
     }
   }
   cu(cudaEventRecord(evSplit, h->s_split), "event");
@@ -1391,7 +1459,7 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   for (int q = 0; q < ns && rc == OZMM_OK; ++q) {
     const Strip& t = strips[q];
     cudaStream_t sg = h->s_gemm[q & 1];
-    cu(cudaStreamWaitEvent(sg, t.row ? evSA[t.step] : evSB[t.step], 0), "wait");
+    cu(cudaStreamWaitEvent(sg, t.trig_a ? evSA[t.trig] : evSB[t.trig], 0), "wait");
     if (!no_c) cu(cudaStreamWaitEvent(sg, evC[q], 0), "wait");
     h->stream = sg;
     if (trace) cu(cudaEventRecord(evGs[q], sg), "event");
@@ -1417,16 +1485,41 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   if (!no_c) {
     for (int q = 0; q < ns && rc == OZMM_OK; ++q) copy_out(q);
   } else {
-    for (auto& th : scanners) th.join();  // every c read before any D2H writes C
+    // every c read before any D2H writes C
+    while (c_scans_left.load() > 0) std::this_thread::sleep_for(std::chrono::microseconds(100));
     if (trace)
-      std::fprintf(stderr, "[ozmm trace] host C scan joined %.2f ms after entry\n",
+      std::fprintf(stderr, "[ozmm trace] host C scan done %.2f ms after entry\n",
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_entry)
                        .count());
-    // gate: every split done and its flags clear before C is written at all
-    cu(cudaEventSynchronize(evSplit), "sync");
+    // gate: open when the GPU has split steps [0, s) and the host has scanned
+    // steps [s, steps) clean; otherwise (a big element on the host side, or a
+    // device error) after every split, as before
+    bool early = false;
+    for (;;) {
+      if (tail_hit.load() || rc != OZMM_OK) break;
+      int gd = 0;
+      while (gd < steps && (gd >= ra || cudaEventQuery(evSA[gd]) == cudaSuccess) &&
+             (gd >= rb || cudaEventQuery(evSB[gd]) == cudaSuccess))
+        ++gd;
+      int hs = steps;
+      while (hs > 0 && tail_done[hs - 1].load()) --hs;
+      if (gd == steps) break;  // every split already done: the plain gate below
+      if (gd >= hs && !tail_hit.load()) {
+        early = true;
+        break;
+      }
+      std::this_thread::sleep_for(std::chrono::microseconds(200));
+    }
+    stop_tail = 1;
+    if (!early) cu(cudaEventSynchronize(evSplit), "sync");
+    // the flags of the splits that have run (all of them on the plain path)
     cu(cudaMemcpyAsync(h->hflags, h->flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->s_out), "flags");
     cu(cudaStreamSynchronize(h->s_out), "sync");
     range_err = rc == OZMM_OK && h->hflags[1] != 0;
+    if (trace)
+      std::fprintf(stderr, "[ozmm trace] D2H gate open %.2f ms after entry (%s)\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_entry)
+                       .count(), early ? "early: host-scanned tail" : "after the last split");
     // The strips already finished by now form (typically) the square
     // [0, X) x [0, Y): it goes back as ONE copy with X-wide host rows -- host
     // writes in narrow 8 KB row pieces drop to ~31 GB/s while the GEMM runs,
@@ -1459,6 +1552,16 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
     if (th.joinable()) th.join();
   for (cudaStream_t s : {h->s_in, h->s_split, h->s_gemm[0], h->s_gemm[1], h->s_out})
     cu(cudaStreamSynchronize(s), "sync");
+  if (rc == OZMM_OK && no_c && !range_err) {
+    // early gate: the host scan proved the later panels clean; confirm on the device
+    int f[2] = {0, 0};
+    cu(cudaMemcpy(f, h->flags, sizeof f, cudaMemcpyDeviceToHost), "flags");
+    if (f[1]) {
+      const int zero = 0;
+      cu(cudaMemcpy(h->flags + 1, &zero, sizeof(int), cudaMemcpyHostToDevice), "flags");
+      rc = set_err(h, OZMM_ERR_CUDA, "internal: range flag raised on a host-scanned panel");
+    }
+  }
   if (rc == OZMM_OK && !no_c) {
     int f[2] = {0, 0};
     cu(cudaMemcpy(f, h->flags, sizeof f, cudaMemcpyDeviceToHost), "flags");
@@ -1493,7 +1596,7 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
                    s < rb ? ms(evB[s]) : -1.f, s < rb ? ms(evSB[s]) : -1.f);
     for (int q = 0; q < ns; ++q)
       std::fprintf(stderr, "[ozmm trace] strip %2d %s %6lld x %6lld  gemm %7.2f -> %7.2f  d2h done %7.2f\n", q,
-                   strips[q].row ? "row" : "col", static_cast<long long>(strips[q].rows),
+                   strips[q].trig_a ? "row" : "col", static_cast<long long>(strips[q].rows),
                    static_cast<long long>(strips[q].cols), ms(evGs[q]), ms(evG[q]), ms(evO[q]));
   }
   for (auto& e : evGs) cudaEventDestroy(e);
