@@ -437,7 +437,7 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": int8_peak,
                          "unit": "TFLOP/s", "frac": achieved / int8_peak, "traffic": traffic,
-                         "kernel": "ozimmu_gemm_kernel (tcgen05 kind::i8 + fused FP64 epilogue)",
+                         "kernel": "ozimmu_gemm_pair_kernel<128,1> (tcgen05.mma.cta_group::2.kind::i8, offset-binary u8 planes, fused exact FP64 epilogue)",
                          "algorithmic_ops_per_launch": int8_ops,
                          "kernel_ms": t_gemm,
                          "peak_source": f"2 x bf16_tflops_sustained ({pk_src}, MEASURED_PEAKS.json):"
