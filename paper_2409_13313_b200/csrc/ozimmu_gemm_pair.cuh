@@ -182,6 +182,52 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
             ptx::tc_fence_after();
             const uint32_t sb = ptx::smem_u32(bbuf + bi * Cfg::kBBuf);
             for (int g = g0; g < g1; ++g) {
+              if (P.group_pairs > 1 && g + 1 < g1) {
+                // up to group_pairs A stages per barrier round: wait for all, issue
+                // their MMAs in one burst, release all (fewer issue-stream breaks)
+                const int ng = min(P.group_pairs, g1 - g);
+                {
+                  int sl = ai;
+                  uint32_t ph = aph;
+                  for (int h2 = 0; h2 < ng; ++h2) {
+                    ptx::mbar_wait(a_full + sl, ph);
+                    if (++sl == n_a) sl = 0, ph ^= 1;
+                  }
+                }
+                ptx::tc_fence_after();
+                if (ptx::elect_one()) {
+                  int sl = ai;
+                  for (int h2 = 0; h2 < ng; ++h2) {
+                    const int gg = g + h2;
+                    const uint64_t adesc = ptx::smem_desc(ptx::smem_u32(aring + sl * Cfg::kATile), 1024, 2);
+                    for (int pr = P.ag_p0[gg]; pr < P.ag_p1[gg]; ++pr) {
+                      const uint32_t ci = P.pr_ci[pr];
+                      const uint64_t bdesc =
+                          ptx::smem_desc(sb + (P.pr_t[pr] - blo) * Cfg::kBTile, 1024, 2);
+                      const uint32_t d = tmem_base + (ci & 0x7Fu) * kBN;
+                      const bool first = kb == 0 && (ci & 0x80u);
+#pragma unroll
+                      for (int j = 0; j < kKB / kBK; ++j)
+                        ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, idesc,
+                                         (first && j == 0) ? 0u : 1u);
+                    }
+                    if (++sl == n_a) sl = 0;
+                  }
+                  sl = ai;
+                  for (int h2 = 0; h2 < ng; ++h2) {
+                    ptx::mma_commit_pair(a_empty + sl, all_mask);
+                    if (++sl == n_a) sl = 0;
+                  }
+                }
+                __syncwarp();
+                g += ng - 1;
+                for (int h2 = 0; h2 < ng; ++h2)
+                  if (++ai == n_a) {
+                    ai = 0;
+                    aph ^= 1;
+                  }
+                continue;
+              }
               ptx::mbar_wait(a_full + ai, aph);
               ptx::tc_fence_after();
               if (ptx::elect_one()) {
@@ -196,6 +242,9 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
                   for (int j = 0; j < kKB / kBK; ++j)  // K = 32 per MMA: +32 B = +2 in desc.lo
                     ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, idesc,
                                      (first && j == 0) ? 0u : 1u);
+                  for (int x = 0; x < P.dup_mma; ++x)  // timing experiment only (wrong results)
+                    for (int j = 0; j < kKB / kBK; ++j)
+                      ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, idesc, 1u);
                 }
                 ptx::mma_commit_pair(a_empty + ai, all_mask);  // A stage free (all sharers)
               }

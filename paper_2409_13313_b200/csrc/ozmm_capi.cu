@@ -382,6 +382,12 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
   P.hint_b = 0;
   if (const char* g = std::getenv("OZMM_HINT_A")) P.hint_a = std::atoi(g);
   if (const char* g = std::getenv("OZMM_HINT_B")) P.hint_b = std::atoi(g);
+  if (const char* g = std::getenv("OZMM_DUP_MMA")) P.dup_mma = std::atoi(g);
+  // CTA-pair kernel: A groups issued two per barrier round (one wait burst, one
+  // MMA burst, one release burst): C3 +9-12 %, C5 k=12 +7.5 %, C4 +2 % against one
+  // group per round; three per round starve the producer (tools/gpairs_probe*.sh)
+  P.group_pairs = 2;
+  if (const char* g = std::getenv("OZMM_GROUP_PAIRS")) P.group_pairs = std::atoi(g);
   if (const char* g = std::getenv("OZMM_IDESC_XOR")) P.idesc_xor = static_cast<uint32_t>(std::strtoul(g, nullptr, 0));
   P.nbatch = static_cast<int>(S.batches.size());
   P.npass = static_cast<int>(S.passes.size());
@@ -528,17 +534,18 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   const size_t ccol_bytes = fl.biased() ? sizeof(uint32_t) * Cfg::kNAcc * kBN : 0;
   const size_t fixed = ozb::kBBufs * Cfg::kBBuf + ccol_bytes;
   // A-ring depth.  When each A tile feeds >= 2.5 products on average (tensor-bound
-  // schedules, e.g. C3), 4 stages, not the 6 that fit: a deeper ring lets each
-  // CTA pair run further ahead along K, the tiles of a wave drift apart and stop
-  // sharing slice tiles in L2.  At C3, 6 stages read 233 GB from DRAM per launch
-  // (L2 hit 55 %), 4 stages 148 GB (68 %), and the power saved raises the capped
-  // SM clock 1.43 -> 1.55 GHz (+6 %; tools/stage_ncu.sh).  Schedules with few
-  // products per A tile (C4: r = 2, 1.4 per tile) are L2-throughput bound and
-  // need the deeper ring to hide latency (6 stages +7 % there).
+  // schedules, e.g. C3), 5 stages, not the 6 that fit.  With one A group per
+  // barrier round, a deeper ring let each CTA pair run further ahead along K:
+  // the tiles of a wave drifted apart and stopped sharing slice tiles in L2 (C3,
+  // 6 vs 4 stages: 233 vs 148 GB of DRAM reads, clock 1.43 vs 1.55 GHz; 4 was
+  // best, tools/stage_ncu.sh).  With two groups per round (P.group_pairs) a
+  // round holds two slots, and 5 stages beat 4 by 2 % (DRAM 86 GB).  Schedules
+  // with few products per A tile (C4: r = 2, 1.4 per tile) are L2-throughput
+  // bound and keep 6.
   int64_t a_loads = 0;
   for (const auto& q : S.passes) a_loads += q.g1 - q.g0;
   const bool dense = a_loads > 0 && 2 * static_cast<int64_t>(S.products.size()) >= 5 * a_loads;
-  int stages = static_cast<int>(std::min<size_t>(dense ? 4 : 6, (budget - fixed) / Cfg::kATile));
+  int stages = static_cast<int>(std::min<size_t>(dense ? 5 : 6, (budget - fixed) / Cfg::kATile));
   if (const char* e = std::getenv("OZMM_STAGES"))
     stages = static_cast<int>(std::min<size_t>((budget - fixed) / Cfg::kATile, std::max(2, std::atoi(e))));
   if (stages < 2)
