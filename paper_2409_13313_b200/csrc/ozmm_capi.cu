@@ -524,6 +524,11 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   if (const char* e = std::getenv("OZMM_SCHED_FILL"))  // scale of the fill terms
     cm.a_tile *= std::atof(e), cm.b_tile *= std::atof(e);
   if (const char* e = std::getenv("OZMM_SCHED")) cm.greedy = std::string(e) == "greedy";
+  // A groups alternate large and small when every batch is a single pass (k <= 8:
+  // all B slices resident), so that the two-group issue rounds are even (8+1,
+  // 7+2, ... products): C3 +3-4 % (profiles/r1/aorder_g2.txt).  Multi-window
+  // schedules (k >= 9) keep the sorted order (C5 k=12: -1.7 % interleaved).
+  cm.interleave = k <= Cfg::kMaxBSlots;
   if (const char* e = std::getenv("OZMM_AORDER")) cm.interleave = std::string(e) == "interleave";
   const ozb::Schedule S = ozb::make_schedule(k, fl.per_product ? 1 : r, Cfg::kNAcc,
                                              static_cast<int64_t>(Cfg::kMaxBSlots) * Cfg::kBTile,
