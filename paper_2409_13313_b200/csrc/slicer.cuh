@@ -84,17 +84,28 @@ __device__ __forceinline__ void emit16(double (&w)[16], int PE, int beta, int k,
       const double unit = pow2(ue);
       if (unit != 0.0) {
         const double sigma = __dmul_rn(kSigmaScale, unit);  // exact
-        const long long sbits = __double_as_longlong(sigma);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) packed[e] = 0u;
+        // only the low byte of bits(t) - bits(sigma) is kept: the low words suffice
+        const uint32_t slo = static_cast<uint32_t>(__double2loint(sigma));
+        uint32_t q[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const double t = __dadd_rn(w[e], sigma);
           const double x = __dadd_rn(t, -sigma);
-          const uint32_t q = static_cast<uint32_t>(__double_as_longlong(t) - sbits);
+          q[e] = static_cast<uint32_t>(__double2loint(t)) - slo;
           w[e] = __dadd_rn(w[e], -x);
-          packed[e >> 2] |= ((q + off) & 0xFFu) << (8 * (e & 3));
-          qsum += static_cast<int>(q);  // padding elements are 0 (w = 0 there)
+        }
+        // byte-pack 4 slices with two PRMTs + one; the line sum of the signed
+        // bytes with one dp4a per 4; the offset with one per-byte add (the slicer
+        // is issue-bound, ncu: 79 % issue slots busy)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t lo = __byte_perm(q[4 * i], q[4 * i + 1], 0x0040);
+          const uint32_t hi = __byte_perm(q[4 * i + 2], q[4 * i + 3], 0x0040);
+          packed[i] = __byte_perm(lo, hi, 0x5410);
+          if (lsum != nullptr) {
+            qsum = __dp4a(static_cast<int>(packed[i]), 0x01010101, qsum);  // padding bytes are 0
+            packed[i] = __vadd4(packed[i], off4);  // no carries: slice + off in [0, 254]
+          }
         }
       } else {
         // unit underflowed to 0: the reference computes x = w, int8(w/0) = 0
