@@ -37,8 +37,9 @@ def test_grid2d_cuda_world1():
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4, 8])
-def test_grid2d_cuda_emulated_ranks(world):
+@pytest.mark.parametrize("world,trans", [(2, False), (4, False), (8, False), (4, True),
+                                         (8, True)])
+def test_grid2d_cuda_emulated_ranks(world, trans):
     """All ranks of a Pr x Pc grid as threads on the one GPU, with an in-process
     all-gather: the CUDA backend's strip launches (G1/G2/G3 on row/column ranges of
     the gathered panels, ozmm_gemm_slices_strided) must tile C exactly like the
@@ -56,6 +57,8 @@ def test_grid2d_cuda_emulated_ranks(world):
     dev = lambda x: torch.tensor(np.ascontiguousarray(x), device="cuda")  # noqa: E731
     want = ozmm.ozaki_gemm(alpha, dev(A), dev(B), beta, dev(C),
                            ozmm.config_for("ozIMMU_H", k)).cpu().numpy()
+    # transa / transb: each rank holds its shard of the stored transposes
+    At, Bt = np.ascontiguousarray(A.T), np.ascontiguousarray(B.T)
 
     barriers, pool, lock = {}, {}, threading.Lock()
 
@@ -89,9 +92,14 @@ def test_grid2d_cuda_emulated_ranks(world):
             th.rank, th.seq = rank, {}
             L = make_layout(m, n, p, world, rank)
             G = Grid2DGemm(m, n, p, k, world=world, rank=rank, backend=Backend(0),
-                           group_factory=lambda ranks: tuple(ranks), all_gather=all_gather)
-            a = dev(A[L.a_row0:L.a_row0 + L.ms])
-            b = dev(B[:, L.b_col0:L.b_col0 + L.ps])
+                           group_factory=lambda ranks: tuple(ranks), all_gather=all_gather,
+                           transa=trans, transb=trans)
+            if trans:
+                a = dev(At[:, L.a_row0:L.a_row0 + L.ms])
+                b = dev(Bt[L.b_col0:L.b_col0 + L.ps])
+            else:
+                a = dev(A[L.a_row0:L.a_row0 + L.ms])
+                b = dev(B[:, L.b_col0:L.b_col0 + L.ps])
             c = dev(C[L.c_row0:L.c_row0 + L.mr, L.c_col0:L.c_col0 + L.pcols])
             G.step(a, b, c, alpha, beta)
             torch.cuda.synchronize()
