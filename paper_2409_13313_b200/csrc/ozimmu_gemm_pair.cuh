@@ -344,14 +344,32 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
       if (lane == 0) ptx::mbar_arrive_cluster(empty_leader);
     }
 
-    if (row_ok) {
-      const double* cin = P.c_in ? P.c_in + static_cast<int64_t>(row) * P.ldc : nullptr;
-      double* cout = P.c_out + static_cast<int64_t>(row) * P.ldc;
+    // C = fl(fl(alpha*D) + fl(beta*C)).  Each thread holds one row of D, so storing
+    // (and reading C) straight from registers makes every warp access touch 32
+    // rows 128 KB apart: 32 L1 wavefronts per instruction, ~70 us per tile at C3
+    // (a fixed cost independent of n, tools/fixed_cost_probe.sh).  D is staged
+    // in the operand pool instead -- free now: the tile's last MMA has completed
+    // -- and C is read and written row by row with consecutive lanes on
+    // consecutive columns.
+    constexpr int kStageLd = kBN + 1;  // doubles; the pad spreads a row-per-lane write over banks
+    double* stage = reinterpret_cast<double*>(smem);
+    const int lrow = quarter * 32 + lane;
 #pragma unroll
-      for (int j = 0; j < kCols; ++j) {
-        const int col = col0 + j;
+    for (int j = 0; j < kCols; ++j) stage[lrow * kStageLd + cslice * kCols + j] = d[j];
+    asm volatile("bar.sync 1, %0;" ::"r"(kPairEpiWarps * 32) : "memory");
+    const int ew = warp - 4;
+    const int crow0 = row_base;  // this CTA's first row
+    for (int rr = ew; rr < kBM; rr += kPairEpiWarps) {
+      const int grow = crow0 + rr;
+      if (grow >= P.m) break;
+      const double* cin = P.c_in ? P.c_in + static_cast<int64_t>(grow) * P.ldc : nullptr;
+      double* cout = P.c_out + static_cast<int64_t>(grow) * P.ldc;
+#pragma unroll
+      for (int cc = lane; cc < kBN; cc += 32) {
+        const int col = col_tile * kBN + cc;
         if (col < P.p)
-          cout[col] = __dadd_rn(__dmul_rn(P.alpha, d[j]), cin ? __dmul_rn(P.beta_c, cin[col]) : 0.0);
+          cout[col] = __dadd_rn(__dmul_rn(P.alpha, stage[rr * kStageLd + cc]),
+                                cin ? __dmul_rn(P.beta_c, cin[col]) : 0.0);
       }
     }
   }
