@@ -78,6 +78,10 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // diagnostics: stamps 0 start, 1 prologue done, 2 first MMA issued, 3 batch 0
+  // drained, 4 second batch's first MMA, 5 last batch drained, 6 C written, 7 end
+  uint64_t* trace = P.tile_trace ? P.tile_trace + static_cast<int64_t>(blockIdx.x) * 8 : nullptr;
+  if (trace && threadIdx.x == 0) trace[0] = ptx::globaltimer();
   const uint32_t rank = ptx::cluster_ctarank();
   const uint32_t lead_rank = rank & ~1u;      // leader of this CTA's pair
   const uint32_t pp = rank >> 1;              // pair index in the cluster
@@ -120,6 +124,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
   ptx::cluster_sync();  // barrier inits + TMEM address visible cluster-wide
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
+  if (trace && threadIdx.x == 0) trace[1] = ptx::globaltimer();
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
@@ -180,6 +185,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
           for (int kb = 0; kb < n_kb; ++kb) {
             ptx::mbar_wait(b_full + bi, bph);
             ptx::tc_fence_after();
+            if (trace && kb == 0 && q == P.b_pass0[b] && b < 2 && lane == 0) trace[2 + 2 * b] = ptx::globaltimer();
             const uint32_t sb = ptx::smem_u32(bbuf + bi * Cfg::kBBuf);
             for (int g = g0; g < g1; ++g) {
               if (P.group_pairs > 1 && g + 1 < g1) {
@@ -282,6 +288,17 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
     for (int j = 0; j < kCols; ++j) d[j] = 0.0;
 
     const uint32_t o1 = (1u << P.beta) - 1u, os = 1u << (P.beta - 1);  // slice offsets
+    // C is read once, after the last MMA: pull this CTA's 128 rows x kBN columns
+    // into L2 now, while the MMAs run, so that the final pass waits on L2 rather
+    // than HBM (it was 31 us per tile, profiles/r1/tile_trace.txt)
+    if (P.c_in != nullptr) {
+      constexpr int kLines = kBN * 8 / 128;  // 128-byte lines per row
+      for (int i = threadIdx.x - 4 * 32; i < kBM * kLines; i += kPairEpiWarps * 32) {
+        const int r = row_base + i / kLines, c = col_tile * kBN + (i % kLines) * 16;
+        if (r < P.m && c < P.p)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(P.c_in + static_cast<int64_t>(r) * P.ldc + c));
+      }
+    }
     for (int b = 0; b < P.nbatch; ++b) {
       const int c0 = P.b_c0[b], nc = P.b_nc[b];
       if (P.bias) {
@@ -342,6 +359,8 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_cluster(empty_leader);
+      if (trace && warp == 4 && lane == 0 && (b == 0 || b == P.nbatch - 1))
+        trace[b == 0 && P.nbatch > 1 ? 3 : 5] = ptx::globaltimer();
     }
 
     // C = fl(fl(alpha*D) + fl(beta*C)).  Each thread holds one row of D, so storing
@@ -359,19 +378,37 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
     asm volatile("bar.sync 1, %0;" ::"r"(kPairEpiWarps * 32) : "memory");
     const int ew = warp - 4;
     const int crow0 = row_base;  // this CTA's first row
-    for (int rr = ew; rr < kBM; rr += kPairEpiWarps) {
-      const int grow = crow0 + rr;
-      if (grow >= P.m) break;
-      const double* cin = P.c_in ? P.c_in + static_cast<int64_t>(grow) * P.ldc : nullptr;
-      double* cout = P.c_out + static_cast<int64_t>(grow) * P.ldc;
+    // 4 rows per warp per round, all their C loads issued before any store: C is
+    // read and written in place, so a load after a store to the same array
+    // would wait for it (the single-row loop ran at ~13 GB/s per SM)
+    constexpr int kU = kBN / 32;
+    for (int r0 = ew; r0 < kBM; r0 += 4 * kPairEpiWarps) {
+      double cv[4][kU];
 #pragma unroll
-      for (int cc = lane; cc < kBN; cc += 32) {
-        const int col = col_tile * kBN + cc;
-        if (col < P.p)
-          cout[col] = __dadd_rn(__dmul_rn(P.alpha, stage[rr * kStageLd + cc]),
-                                cin ? __dmul_rn(P.beta_c, cin[col]) : 0.0);
+      for (int i = 0; i < 4; ++i) {
+        const int grow = crow0 + r0 + i * kPairEpiWarps;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int col = col_tile * kBN + lane + 32 * u;
+          cv[i][u] = (P.c_in && grow < P.m && col < P.p)
+                         ? P.c_in[static_cast<int64_t>(grow) * P.ldc + col] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int rr = r0 + i * kPairEpiWarps, grow = crow0 + rr;
+        if (grow >= P.m) continue;
+        double* cout = P.c_out + static_cast<int64_t>(grow) * P.ldc;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int cc = lane + 32 * u, col = col_tile * kBN + cc;
+          if (col < P.p)
+            cout[col] = __dadd_rn(__dmul_rn(P.alpha, stage[rr * kStageLd + cc]),
+                                  P.c_in ? __dmul_rn(P.beta_c, cv[i][u]) : 0.0);
+        }
       }
     }
+    if (trace && warp == 4 && lane == 0) trace[6] = ptx::globaltimer();
   }
 
   ptx::tc_fence_before();
@@ -380,6 +417,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
     ptx::tc_fence_after();
     ptx::tmem_dealloc_pair<512>(tmem_base);
   }
+  if (trace && threadIdx.x == 0) trace[7] = ptx::globaltimer();
 }
 
 }  // namespace ozb

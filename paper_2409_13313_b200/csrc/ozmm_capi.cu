@@ -582,9 +582,46 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
     h->pair_attr_set[kPairs - 1] = true;
   }
   const dim3 grid(static_cast<unsigned>(Cfg::kCluster * tiles_m * tiles_n));
+  // OZMM_TILE_TRACE=1 (diagnostics): per-CTA globaltimer stamps, summarised on stderr
+  const bool ttrace = std::getenv("OZMM_TILE_TRACE") != nullptr;
+  uint64_t* tbuf = nullptr;
+  if (ttrace) {
+    CUDA_TRY(h, cudaMalloc(&tbuf, sizeof(uint64_t) * 8 * grid.x));
+    CUDA_TRY(h, cudaMemsetAsync(tbuf, 0, sizeof(uint64_t) * 8 * grid.x, h->stream));
+    P.tile_trace = tbuf;
+  }
   ozb::ozimmu_gemm_pair_kernel<kBN, kPairs>
       <<<grid, ozb::kPairThreads, smem, h->stream>>>(map_a, map_b, P);
   CUDA_TRY(h, cudaGetLastError());
+  if (ttrace) {
+    std::vector<uint64_t> t(8 * static_cast<size_t>(grid.x));
+    CUDA_TRY(h, cudaMemcpyAsync(t.data(), tbuf, t.size() * 8, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    cudaFree(tbuf);
+    // mean interval between consecutive stamps over leader CTAs (us)
+    double sum[8] = {}, tot = 0;
+    int cnt = 0;
+    uint64_t t_min = ~0ull, t_max = 0;
+    for (unsigned c = 0; c < grid.x; c += Cfg::kCluster) {
+      const uint64_t* r = t.data() + 8 * c;
+      if (!r[0] || !r[7]) continue;
+      ++cnt;
+      t_min = std::min(t_min, r[0]);
+      t_max = std::max(t_max, r[7]);
+      uint64_t prev = r[0];
+      for (int i = 1; i < 8; ++i)
+        if (r[i]) {
+          sum[i] += static_cast<double>(r[i] - prev) * 1e-3;
+          prev = r[i];
+        }
+      tot += static_cast<double>(r[7] - r[0]) * 1e-3;
+    }
+    std::fprintf(stderr,
+                 "[ozmm tile trace] %d tiles, launch span %.2f ms, mean tile %.1f us: prologue %.1f | to 1st MMA %.1f |"
+                 " batch0 %.1f | to next MMA %.1f | rest %.1f | C write %.1f | teardown %.1f\n",
+                 cnt, (t_max - t_min) * 1e-6, cnt ? tot / cnt : 0.0, sum[1] / cnt, sum[2] / cnt,
+                 sum[3] / cnt, sum[4] / cnt, sum[5] / cnt, sum[6] / cnt, sum[7] / cnt);
+  }
   return OZMM_OK;
 }
 
