@@ -530,6 +530,9 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   // schedules (k >= 9) keep the sorted order (C5 k=12: -1.7 % interleaved).
   cm.interleave = k <= Cfg::kMaxBSlots;
   if (const char* e = std::getenv("OZMM_AORDER")) cm.interleave = std::string(e) == "interleave";
+  // ... and no two consecutive products into one accumulator (C3 +1 %)
+  cm.avoid_raw = cm.interleave;
+  if (const char* e = std::getenv("OZMM_AVOID_RAW")) cm.avoid_raw = std::atoi(e) != 0;
   const ozb::Schedule S = ozb::make_schedule(k, fl.per_product ? 1 : r, Cfg::kNAcc,
                                              static_cast<int64_t>(Cfg::kMaxBSlots) * Cfg::kBTile,
                                              slot_bytes, Cfg::kMaxBSlots, cm);

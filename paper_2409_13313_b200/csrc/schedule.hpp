@@ -121,6 +121,7 @@ struct PassCost {
   double batch = 24.0;    // per-batch drain/refill, amortised per K block
   bool greedy = false;    // n_acc chunks per batch, B windows cut every b_windows slices
   bool interleave = false; // A groups in large/small alternation (see make_schedule)
+  bool avoid_raw = false;  // no back-to-back products into one accumulator
 };
 
 namespace detail {
@@ -270,23 +271,38 @@ inline Schedule make_schedule(int k, int64_t r, int n_acc, int64_t max_stage_byt
       // net 4 % slower, so it is off (tools/aorder_ab.sh).
       std::stable_sort(pass_prods.begin(), pass_prods.end(),
                        [](const Product& x, const Product& y) { return x.s < y.s; });
-      if (b_windows > 0 && cm.interleave) {
+      if (b_windows > 0 && (cm.interleave || cm.avoid_raw)) {
         std::vector<std::vector<Product>> groups;
         for (const Product& p : pass_prods) {
           if (groups.empty() || groups.back()[0].s != p.s) groups.emplace_back();
           groups.back().push_back(p);
         }
-        std::stable_sort(groups.begin(), groups.end(),
-                         [](const auto& x, const auto& y) { return x.size() > y.size(); });
-        pass_prods.clear();
-        for (size_t lo = 0, hi = groups.size(); lo < hi;) {
-          for (const Product& p : groups[lo]) pass_prods.push_back(p);
-          ++lo;
-          if (lo < hi) {
-            --hi;
-            for (const Product& p : groups[hi]) pass_prods.push_back(p);
+        if (cm.interleave) {
+          std::stable_sort(groups.begin(), groups.end(),
+                           [](const auto& x, const auto& y) { return x.size() > y.size(); });
+          std::vector<std::vector<Product>> il;
+          for (size_t lo = 0, hi = groups.size(); lo < hi;) {
+            il.push_back(groups[lo++]);
+            if (lo < hi) il.push_back(groups[--hi]);
           }
+          groups.swap(il);
         }
+        if (cm.avoid_raw) {
+          // no two consecutive products into the same accumulator, also across the
+          // wrap to the next K block: rotate a group whose first product would
+          // follow one into the same chunk
+          for (int sweep = 0; sweep < 2; ++sweep)
+            for (size_t i = 0; i < groups.size(); ++i) {
+              const auto& prev = groups[(i + groups.size() - 1) % groups.size()];
+              auto& gr = groups[i];
+              if (groups.size() < 2 && gr.size() < 2) break;
+              for (size_t rot = 0; rot < gr.size() && gr[0].ci == prev.back().ci; ++rot)
+                std::rotate(gr.begin(), gr.begin() + 1, gr.end());
+            }
+        }
+        pass_prods.clear();
+        for (const auto& gr : groups)
+          for (const Product& p : gr) pass_prods.push_back(p);
       }
       ps.p0 = static_cast<int>(S.products.size());
       ps.g0 = static_cast<int>(S.agroups.size());
