@@ -97,6 +97,9 @@ struct GemmParams {
   uint16_t p_p0[kMaxPasses], p_p1[kMaxPasses];
   // per product: accumulator slot | first-product flag (bit 7), A slice, B slice
   uint8_t pr_ci[kMaxProducts], pr_s[kMaxProducts], pr_t[kMaxProducts];
+  // CTA-pair kernel, per product: B tile offset within its pass's B buffer in
+  // smem-descriptor units (bytes >> 4) | accumulator << 16 | first << 24
+  uint32_t pr_info[kMaxProducts];
   // per chunk in flush order: group g and first A slice s0
   uint8_t c_g[kMaxChunks];
   uint8_t c_s[kMaxChunks];

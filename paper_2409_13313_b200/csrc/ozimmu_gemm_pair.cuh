@@ -187,6 +187,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
             ptx::tc_fence_after();
             if (trace && kb == 0 && q == P.b_pass0[b] && b < 2 && lane == 0) trace[2 + 2 * b] = ptx::globaltimer();
             const uint32_t sb = ptx::smem_u32(bbuf + bi * Cfg::kBBuf);
+            const uint64_t bdesc0 = ptx::smem_desc(sb, 1024, 2);
             for (int g = g0; g < g1; ++g) {
               if (P.group_pairs > 1 && g + 1 < g1) {
                 // up to group_pairs A stages per barrier round: wait for all, issue
@@ -207,11 +208,13 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
                     const int gg = g + h2;
                     const uint64_t adesc = ptx::smem_desc(ptx::smem_u32(aring + sl * Cfg::kATile), 1024, 2);
                     for (int pr = P.ag_p0[gg]; pr < P.ag_p1[gg]; ++pr) {
-                      const uint32_t ci = P.pr_ci[pr];
-                      const uint64_t bdesc =
-                          ptx::smem_desc(sb + (P.pr_t[pr] - blo) * Cfg::kBTile, 1024, 2);
-                      const uint32_t d = tmem_base + (ci & 0x7Fu) * kBN;
-                      const bool first = kb == 0 && (ci & 0x80u);
+                      // one 32-bit word per product (host-packed): B tile offset in
+                      // descriptor units | accumulator << 16 | first << 24 -- the
+                      // issuing thread was the bottleneck of thin batches
+                      const uint32_t info = P.pr_info[pr];
+                      const uint64_t bdesc = bdesc0 + (info & 0xFFFFu);
+                      const uint32_t d = tmem_base + ((info >> 16) & 0x7Fu) * kBN;
+                      const bool first = kb == 0 && (info >> 24);
 #pragma unroll
                       for (int j = 0; j < kKB / kBK; ++j)
                         ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, idesc,
@@ -239,11 +242,10 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
               if (ptx::elect_one()) {
                 const uint64_t adesc = ptx::smem_desc(ptx::smem_u32(aring + ai * Cfg::kATile), 1024, 2);
                 for (int pr = P.ag_p0[g]; pr < P.ag_p1[g]; ++pr) {
-                  const uint32_t ci = P.pr_ci[pr];
-                  const uint64_t bdesc =
-                      ptx::smem_desc(sb + (P.pr_t[pr] - blo) * Cfg::kBTile, 1024, 2);
-                  const uint32_t d = tmem_base + (ci & 0x7Fu) * kBN;
-                  const bool first = kb == 0 && (ci & 0x80u);
+                  const uint32_t info = P.pr_info[pr];
+                  const uint64_t bdesc = bdesc0 + (info & 0xFFFFu);
+                  const uint32_t d = tmem_base + ((info >> 16) & 0x7Fu) * kBN;
+                  const bool first = kb == 0 && (info >> 24);
 #pragma unroll
                   for (int j = 0; j < kKB / kBK; ++j)  // K = 32 per MMA: +32 B = +2 in desc.lo
                     ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, idesc,

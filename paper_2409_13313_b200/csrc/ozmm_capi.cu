@@ -564,6 +564,12 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   fill_params(P, S, m, p, lds_a, lds_b, tiles_m, tiles_n, beta_bits, stages, alpha, beta, mu, nu,
               Cin, Cout, ldc, dump, fl);
   P.n_kb = static_cast<int>((std::max(lds_a, lds_b) + ozb::kKB - 1) / ozb::kKB);
+  for (const auto& ps : S.passes)
+    for (int i = ps.p0; i < ps.p1; ++i) {
+      const auto& pr = S.products[i];
+      P.pr_info[i] = static_cast<uint32_t>(((pr.t - ps.blo) * Cfg::kBTile) >> 4) |
+                     (static_cast<uint32_t>(pr.ci) << 16) | (pr.first ? 1u << 24 : 0u);
+    }
   // raster: tensor-bound schedules visit 4 pair-row-blocks per group (a wave of
   // 74 tiles then spans ~4 x 18 tiles and re-reads less of B from DRAM: C3 DRAM
   // 135 -> 82 GB, +3 %; tools/group_ncu.sh); L2-bound ones (C4) keep 2
