@@ -111,6 +111,10 @@ typedef struct {
                               as u8, u8 x u8 MMAs, offsets removed exactly in the
                               epilogue; same results, less tensor-core power);
                               1 = keep the reference's signed int8 planes */
+  int c_write_only;        /* slice-level GEMMs only: C is output only (not read).
+                              Valid only with beta == 0 and a C free of inf/NaN, where
+                              fl(beta*c) = 0 changes nothing; ozmm_gemm_slices*
+                              reject it with beta != 0 */
 } ozmm_options_t;
 
 /* Scheme presets (config_for, scheme.cpp:137-159) plus the two other valid

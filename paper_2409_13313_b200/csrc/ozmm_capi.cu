@@ -1043,8 +1043,11 @@ int gemm_slices_checked(Handle* h, int64_t m, int64_t n, int64_t p, int k, int b
   if (r == 0) r = ozb::compute_r_host(n, beta_bits);
   if (r < 1) return set_err(h, OZMM_ERR_CONFIG, "force_r must be >= 1");
   CUDA_TRY(h, cudaSetDevice(h->device));
+  const bool write_only = opt && opt->c_write_only;
+  if (write_only && beta != 0.0)
+    return set_err(h, OZMM_ERR_ARG, "c_write_only needs beta == 0");
   return launch_gemm(h, m, n, p, k, beta_bits, r, As, lds_a, plane_a, mu, Bs, lds_b, plane_b, nu,
-                     alpha, beta, C, C, ldc, opt, fl);
+                     alpha, beta, write_only ? nullptr : C, C, ldc, opt, fl);
 }
 }  // namespace
 

@@ -151,13 +151,14 @@ class Backend:
                                                        lsum.stride(0)))
 
     def gemm(self, m, n, p, k, beta_bits, a_slices, mu, b_slices, nu, alpha, beta, c,
-             lsa=None, lsb=None):
+             lsa=None, lsb=None, c_write_only=False):
         """K2+K3 on [k][m][lds] / [k][p][lds] slice views (row / column ranges of a
         panel are fine: the plane stride is passed through); lsa / lsb: the line
         sums of offset-binary planes ([m][k] / [p][k] views)."""
         oz = self.oz
         self.handle.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
         opt = oz.Options()
+        opt.c_write_only = int(c_write_only)
         if lsa is None:
             self.handle.check(oz.lib.ozmm_gemm_slices_strided(
                 self.handle.h, m, n, p, k, beta_bits, 0, a_slices.data_ptr(), a_slices.stride(1),
@@ -265,20 +266,35 @@ class Grid2DGemm:
             if w is not None:
                 w.wait()
 
-    def step(self, a_rows, b_cols, c_block, alpha=1.0, beta=0.0):
+    def step(self, a_rows, b_cols, c_block, alpha=1.0, beta=0.0, ready=None,
+             c_write_only=False):
         """One sharded emulated GEMM.  The slice-panel all-gathers run while the
         GEMM works on what is already local, in three strip launches:
           G1  own A rows x own B columns     -- needs no communication;
           G2  own A rows x the other columns -- after the B (column-group) gather;
           G3  the other rows x all columns   -- after the A (row-group) gather.
         Every C entry is still produced by exactly one fused launch from the same
-        slices and shifts, so the result is bit-identical to one GPU."""
+        slices and shifts, so the result is bit-identical to one GPU.
+
+        ready: optional {'a', 'b', 'c'} -> CUDA event of the copy that fills
+        a_rows / b_cols / c_block, for callers that stream the inputs in: each
+        split waits only for its own operand and the GEMMs for C, so the
+        slicing and gathers overlap the rest of the upload.
+        c_write_only: C is not read (beta == 0 and a finite C, where fl(beta*c)
+        = 0), so the caller need not upload it."""
         L, k = self.L, self.k
         be = self.backend
         off = self.offset
+        ready = ready or {}
+
+        def wait(key):
+            if ready.get(key) is not None:
+                torch.cuda.current_stream().wait_event(ready[key])
         ls = (lambda *a: dict(lsum=a[0])) if off else (lambda *a: {})
+        wait("a")
         be.split(a_rows, k, "L", self.transa, self.beta_bits, self.a_loc, self.mu_loc,
                  **ls(self.lsa_loc))
+        wait("b")
         be.split(b_cols, k, "R", self.transb, self.beta_bits, self.b_loc, self.nu_loc,
                  **ls(self.lsb_loc))
         # B first: it unblocks G2; group g of a GEMM needs slice planes <= g-1
@@ -291,11 +307,15 @@ class Grid2DGemm:
             wa.append(self._gather(self.lsa_pan, self.lsa_loc, self.row_group, L.pc))
 
         def sums(a_sl, b_sl):  # line sums of the operand rows / columns a strip reads
-            return dict(lsa=a_sl, lsb=b_sl) if off else {}
+            kw = dict(lsa=a_sl, lsb=b_sl) if off else {}
+            if c_write_only:
+                kw["c_write_only"] = True
+            return kw
         r0, c0 = L.gc * L.ms, L.gr * L.ps  # own rows / columns inside the C block
         g = (L.n, k, self.beta_bits)
         own_rows = c_block[r0:r0 + L.ms]
         side = getattr(be, "side_stream", None)
+        wait("c")  # C block landed (the side stream forks from here)
         with side() if side else contextlib.nullcontext():
             be.gemm(L.ms, g[0], L.ps, k, g[2], self.a_loc, self.mu_loc, self.b_loc, self.nu_loc,
                     alpha, beta, own_rows[:, c0:c0 + L.ps], **sums(self.lsa_loc, self.lsb_loc))

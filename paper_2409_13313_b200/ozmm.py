@@ -68,7 +68,8 @@ class Timings(C.Structure):
 class Options(C.Structure):
     _fields_ = [("force_beta", C.c_int), ("force_r", C.c_int64), ("timings", C.c_int),
                 ("sync_check", C.c_int), ("chunk_dump", C.c_void_p), ("tile_n", C.c_int),
-                ("cta_pair", C.c_int), ("method", C.c_int), ("signed_slices", C.c_int)]
+                ("cta_pair", C.c_int), ("method", C.c_int), ("signed_slices", C.c_int),
+                ("c_write_only", C.c_int)]
 
 
 _SIG = {

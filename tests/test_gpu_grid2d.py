@@ -116,3 +116,35 @@ def test_grid2d_cuda_emulated_ranks(world, trans):
         t.join(timeout=300)
     assert not errors, errors
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+def test_gemm_slices_c_write_only():
+    """c_write_only (beta = 0, finite C): C is not read, the result equals the
+    reference's fl(alpha*D) + fl(0*c); with beta != 0 the option is rejected."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2409_13313_b200 import ozmm
+    from paper_2409_13313_b200.grid2d import Backend
+    m, n, p, k = 300, 1100, 260, 8
+    A = torch.tensor(ozmm.gen_phi_matrix(m, n, 1.0, 21), device="cuda")
+    B = torch.tensor(ozmm.gen_phi_matrix(n, p, 1.0, 22), device="cuda")
+    C0 = torch.tensor(ozmm.gen_phi_matrix(m, p, 1.0, 23), device="cuda")
+    want = ozmm.ozaki_gemm(1.25, A, B, 0.0, C0, ozmm.config_for("ozIMMU_H", k))
+    be = Backend(0)
+    beta_bits, lds = ozmm.compute_beta(n), ozmm.slice_ld(n)
+    sa = torch.empty((k, m, lds), dtype=torch.int8, device="cuda")
+    sb = torch.empty((k, p, lds), dtype=torch.int8, device="cuda")
+    mu = torch.empty(m, dtype=torch.float64, device="cuda")
+    nu = torch.empty(p, dtype=torch.float64, device="cuda")
+    la = torch.empty((m, k), dtype=torch.int32, device="cuda")
+    lb = torch.empty((p, k), dtype=torch.int32, device="cuda")
+    be.split(A, k, "L", False, beta_bits, sa, mu, lsum=la)
+    be.split(B, k, "R", False, beta_bits, sb, nu, lsum=lb)
+    got = torch.full((m, p), float("nan"), dtype=torch.float64, device="cuda")  # never read
+    be.gemm(m, n, p, k, beta_bits, sa, mu, sb, nu, 1.25, 0.0, got, lsa=la, lsb=lb,
+            c_write_only=True)
+    torch.cuda.synchronize()
+    assert torch.equal(got.view(torch.int64), want.view(torch.int64))
+    with pytest.raises(ValueError):
+        be.gemm(m, n, p, k, beta_bits, sa, mu, sb, nu, 1.25, 0.5, got, lsa=la, lsb=lb,
+                c_write_only=True)
