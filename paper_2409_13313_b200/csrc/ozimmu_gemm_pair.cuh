@@ -11,10 +11,13 @@
 // Pipeline (per CTA; K advances in 128-byte blocks, 128-byte swizzle):
 //   * B buffers (2): for the current K block every B slice of the pass
 //     (kBN/2 rows x 128 B each), resident while all of the block's MMAs run;
-//   * A ring (kARing stages): one A slice tile (128 rows x 128 B) per stage,
-//     streamed in pass order; when A_s lands the MMA thread issues every
-//     product of the pass that uses A_s (4 MMAs of K = 32 each) into its
-//     chunk accumulator.
+//   * A ring (P.stages, 5 for tensor-bound schedules): one A slice tile
+//     (128 rows x 128 B) per stage, streamed in pass order; the MMA thread
+//     takes the A groups two per barrier round (P.group_pairs) and issues every
+//     product that uses them (4 MMAs of K = 32 each) into its chunk
+//     accumulator, then releases both stages together.
+//   * Operands are offset-binary u8 planes by default (P.bias): the epilogue
+//     removes the offsets' contribution exactly, see GemmParams.
 // One TMA box per 128-byte row keeps the TMA request count 4x below a
 // 32-byte-row design (ncu: l1tex2xbar request cycles were 87 % busy there).
 //
@@ -52,7 +55,9 @@ struct PairCfg {
 // the A tiles (same 256 rows): each CTA loads half of its 128-row A tile and
 // TMA-multicasts it to the same-half CTA of the other pair, halving A's L2->SM
 // traffic (A is 2/3 of it).  An A stage is released by both pairs' MMAs, so the
-// pairs are coupled through the 6-deep A ring only; B stays per pair.
+// pairs are coupled through the A ring only; B stays per pair.  A 4-CTA cluster
+// can only use 132 of the 148 SMs, which costs more than the L2 traffic saves
+// (profiles/r1/quad_ab.txt): this variant is off by default.
 template <int kBN, int kPairs>
 __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThreads, 1)
     ozimmu_gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a,
