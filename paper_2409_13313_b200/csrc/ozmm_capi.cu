@@ -107,6 +107,8 @@ struct Handle {
   cudaStream_t s_in = nullptr, s_out = nullptr;  // copy streams of the host entry
   cudaStream_t s_split = nullptr;                 // host entry: panel splits (high priority)
   cudaStream_t s_gemm[2] = {nullptr, nullptr};    // host entry: strip GEMMs
+  cudaStream_t s_aux = nullptr;                   // device entry: B's column maxima
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int* hflags = nullptr;                          // pinned copy of flags (host entry gate)
   cudaEvent_t ev[5] = {};
   bool gemm_attr_set[3] = {false, false, false};
@@ -195,9 +197,23 @@ bool valid_trans(char t) { return is_trans(t) || t == 'N' || t == 'n'; }
 // Lines of op(X): row mode when the line is contiguous in memory.
 // lsum != nullptr: offset-binary planes + signed line sums lsum[s][line] (plane
 // stride lsum_plane; zeroed by the caller), the fused pair GEMM's operand format.
+// Column maxima of the `lines` columns of X (n x lines) into h->colmax.
+int launch_colmax(Handle* h, int64_t lines, int64_t n, const double* X, int64_t ldx) {
+  if (int rc = ensure(h, &h->colmax, &h->colmax_n, static_cast<size_t>(lines))) return rc;
+  CUDA_TRY(h, cudaMemsetAsync(h->colmax, 0, sizeof(unsigned long long) * lines, h->stream));
+  const int64_t rows_per_block = 512;
+  const dim3 g1(static_cast<unsigned>((lines + 31) / 32),
+                static_cast<unsigned>((n + rows_per_block - 1) / rows_per_block));
+  ozb::colmax_kernel<<<g1, 256, 0, h->stream>>>(X, ldx, n, lines, rows_per_block, h->colmax);
+  CUDA_TRY(h, cudaGetLastError());
+  return OZMM_OK;
+}
+
+// colmax_ready: column mode only, h->colmax already holds this X's maxima.
 int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const double* X, int64_t ldx,
                  int k, int beta, int8_t* S, int64_t lds, int64_t plane, double* shift,
-                 int* lsum = nullptr, int64_t lsum_plane = 0, int64_t lsum_lstride = 1) {
+                 int* lsum = nullptr, int64_t lsum_plane = 0, int64_t lsum_lstride = 1,
+                 bool colmax_ready = false) {
   if (row_mode) {
     const bool vec = (reinterpret_cast<uintptr_t>(X) % 16 == 0) && (ldx % 2 == 0);
     // Whole row in registers, 16 elements per thread, split over a cluster of up
@@ -250,12 +266,8 @@ int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const doubl
                                                                        h->flags, lsum, lsum_plane, lsum_lstride);
     }
   } else {
-    if (int rc = ensure(h, &h->colmax, &h->colmax_n, static_cast<size_t>(lines))) return rc;
-    CUDA_TRY(h, cudaMemsetAsync(h->colmax, 0, sizeof(unsigned long long) * lines, h->stream));
-    const int64_t rows_per_block = 512;
-    const dim3 g1(static_cast<unsigned>((lines + 31) / 32),
-                  static_cast<unsigned>((n + rows_per_block - 1) / rows_per_block));
-    ozb::colmax_kernel<<<g1, 256, 0, h->stream>>>(X, ldx, n, lines, rows_per_block, h->colmax);
+    if (!colmax_ready)
+      if (int rc = launch_colmax(h, lines, n, X, ldx)) return rc;
     // offset planes: 8 row tiles per CTA (column sums leave with one atomic per
     // column, slice and CTA); signed planes: one tile per CTA
     const int tpc = lsum ? 8 : 1;
@@ -759,6 +771,9 @@ int ozmm_destroy(ozmm_handle_t handle) {
   if (h->s_split) cudaStreamDestroy(h->s_split);
   for (auto sg : h->s_gemm)
     if (sg) cudaStreamDestroy(sg);
+  if (h->s_aux) cudaStreamDestroy(h->s_aux);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->hflags) cudaFreeHost(h->hflags);
   for (auto& ev : h->ev) cudaEventDestroy(ev);
   delete h;
@@ -1120,6 +1135,22 @@ int ozmm_dgemm_ex(ozmm_handle_t handle, char transa, char transb, int64_t m, int
     fl.lsb_plane = p;
     fl.n = n;
   }
+  // B's column maxima (an HBM-bound pass) run on a side stream beside A's row
+  // split (issue-bound) when A is split by rows and B by columns
+  const bool overlap_colmax = offset && !is_trans(transa) && !is_trans(transb);
+  if (overlap_colmax) {
+    if (!h->s_aux) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->s_aux, cudaStreamNonBlocking));
+    if (!h->ev_fork) CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+    if (!h->ev_join) CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+    cudaStream_t user = h->stream;
+    CUDA_TRY(h, cudaEventRecord(h->ev_fork, user));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->s_aux, h->ev_fork, 0));
+    h->stream = h->s_aux;
+    const int rc = launch_colmax(h, p, n, B, ldb);
+    h->stream = user;
+    if (rc) return rc;
+    CUDA_TRY(h, cudaEventRecord(h->ev_join, h->s_aux));
+  }
   // split A (Left, rows of op(A)) -- split.cpp:233 via scheme.cpp:248
   if (offset) {
     if (int rc = launch_split(h, !is_trans(transa), m, n, A, lda, k, beta_bits, h->slices_a, lds,
@@ -1132,8 +1163,9 @@ int ozmm_dgemm_ex(ozmm_handle_t handle, char transa, char transb, int64_t m, int
   if (want_t) CUDA_TRY(h, cudaEventRecord(h->ev[1], h->stream));
   // split B (Right, columns of op(B)) -- scheme.cpp:251
   if (offset) {
+    if (overlap_colmax) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_join, 0));
     if (int rc = launch_split(h, is_trans(transb), p, n, B, ldb, k, beta_bits, h->slices_b, lds,
-                              p * lds, out_b, h->lsb, p))
+                              p * lds, out_b, h->lsb, p, 1, overlap_colmax))
       return rc;
   } else if (int rc = launch_split_m(h, mc.strategy, is_trans(transb), p, n, B, ldb, k, beta_bits,
                                      h->slices_b, lds, p * lds, out_b)) {
