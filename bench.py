@@ -357,24 +357,31 @@ def main():
         else:
             s_in = torch.cuda.Stream(dev)
             ev = {key: torch.cuda.Event() for key in "abc"}
+            # B first, then A in row panels: B's split and gather, and the first
+            # strip of each A panel, run while the rest of A is still crossing PCIe
+            a_pieces = [(lo, min(lo + max(256, L.ms // 4), L.ms))
+                        for lo in range(0, L.ms, max(256, L.ms // 4))]
+            a_ev = [torch.cuda.Event() for _ in a_pieces]
+            ev["a"] = [(lo, hi, e) for (lo, hi), e in zip(a_pieces, a_ev)]
 
             # beta = 0 and a finite C: fl(0*c) = 0, so C need not cross PCIe (the
             # host entry's no-upload mode; no non-finite entries to patch here)
             c_out_only = bool(torch.isfinite(hC).all())
 
             def e2e_call():
-                # the shard streams in on its own stream; G.step waits per operand,
-                # so A's split overlaps B's copy and the gathers overlap C's
+                # the shard streams in on its own stream (B, then A panel by panel);
+                # G.step splits each operand / panel as it lands
                 with torch.cuda.stream(s_in):
-                    A.copy_(hA, non_blocking=True)
-                    ev["a"].record(s_in)
                     B.copy_(hB, non_blocking=True)
                     ev["b"].record(s_in)
+                    for (lo, hi), e in zip(a_pieces, a_ev):
+                        A[lo:hi].copy_(hA[lo:hi], non_blocking=True)
+                        e.record(s_in)
                     if not c_out_only:
                         C.copy_(hC, non_blocking=True)
                     ev["c"].record(s_in)
-                G.step(A, B, C, 1.0, 0.0, ready=ev, c_write_only=c_out_only)
-                hC.copy_(C, non_blocking=True)
+                # finished C rows stream back while later strips still run
+                G.step(A, B, C, 1.0, 0.0, ready=ev, c_write_only=c_out_only, c_host=hC)
                 torch.cuda.synchronize()
             e2e_call()
             barrier()

@@ -227,6 +227,13 @@ int ozmm_gemm_slices_strided(ozmm_handle_t h, int64_t m, int64_t n, int64_t p, i
 int ozmm_split_offset(ozmm_handle_t h, char side, char trans, int64_t lines, int64_t n,
                       const double* X, int64_t ldx, int k, int beta, int8_t* slices, int64_t lds,
                       double* shift, int32_t* lsum, int64_t lsum_plane, int64_t lsum_lstride);
+/* ozmm_split_offset into planes `plane` bytes apart (plane >= lines * lds):
+ * a range of lines of a larger slice array, e.g. one row panel of A split as
+ * soon as it lands (grid2d.Grid2DGemm.step with per-panel ready events). */
+int ozmm_split_offset_strided(ozmm_handle_t h, char side, char trans, int64_t lines, int64_t n,
+                              const double* X, int64_t ldx, int k, int beta, int8_t* slices,
+                              int64_t lds, int64_t plane, double* shift, int32_t* lsum,
+                              int64_t lsum_plane, int64_t lsum_lstride);
 int ozmm_gemm_slices_offset(ozmm_handle_t h, int64_t m, int64_t n, int64_t p, int k,
                             int beta_bits, int64_t r, const int8_t* As, int64_t lds_a,
                             int64_t plane_a, const double* mu, const int32_t* lsa,

@@ -937,6 +937,14 @@ int ozmm_split(ozmm_handle_t handle, char side, char trans, int64_t lines, int64
 int ozmm_split_offset(ozmm_handle_t handle, char side, char trans, int64_t lines, int64_t n,
                       const double* X, int64_t ldx, int k, int beta, int8_t* slices, int64_t lds,
                       double* shift, int32_t* lsum, int64_t lsum_plane, int64_t lsum_lstride) {
+  return ozmm_split_offset_strided(handle, side, trans, lines, n, X, ldx, k, beta, slices, lds,
+                                   lines * lds, shift, lsum, lsum_plane, lsum_lstride);
+}
+
+int ozmm_split_offset_strided(ozmm_handle_t handle, char side, char trans, int64_t lines,
+                              int64_t n, const double* X, int64_t ldx, int k, int beta,
+                              int8_t* slices, int64_t lds, int64_t plane, double* shift,
+                              int32_t* lsum, int64_t lsum_plane, int64_t lsum_lstride) {
   Handle* h = reinterpret_cast<Handle*>(handle);
   if (!h) return set_err(nullptr, OZMM_ERR_ARG, "null handle");
   if (side != 'L' && side != 'R') return set_err(h, OZMM_ERR_ARG, "side must be 'L' or 'R'");
@@ -953,6 +961,7 @@ int ozmm_split_offset(ozmm_handle_t handle, char side, char trans, int64_t lines
   } else if (beta < 1 || beta > 7) {
     return set_err(h, OZMM_ERR_ARG, "split: forced beta outside 1..7");
   }
+  if (plane < lines * lds) return set_err(h, OZMM_ERR_ARG, "split: plane stride below lines * lds");
   const bool row_mode = (side == 'L') != is_trans(trans);
   if (ldx < (row_mode ? n : lines)) return set_err(h, OZMM_ERR_ARG, "split: leading dimension too small");
   CUDA_TRY(h, cudaSetDevice(h->device));
@@ -962,7 +971,7 @@ int ozmm_split_offset(ozmm_handle_t handle, char side, char trans, int64_t lines
   else
     CUDA_TRY(h, cudaMemset2DAsync(lsum, sizeof(int32_t) * lsum_lstride, 0, sizeof(int32_t) * k, lines,
                                   h->stream));
-  return launch_split(h, row_mode, lines, n, X, ldx, k, beta, slices, lds, lines * lds, shift,
+  return launch_split(h, row_mode, lines, n, X, ldx, k, beta, slices, lds, plane, shift,
                       lsum, lsum_plane, lsum_lstride);
 }
 

@@ -31,6 +31,7 @@ from __future__ import annotations
 import contextlib
 import ctypes
 import math
+import os
 from dataclasses import dataclass
 
 import torch
@@ -115,7 +116,7 @@ class Backend:
     def empty(self, shape, dtype):
         return torch.empty(shape, dtype=dtype, device=self.device)
 
-    def side_stream(self):
+    def side_stream(self, after_current=True):
         """Context for the communication-free strip G1: a second stream that
         starts after the current one, so G2/G3 (which wait only on the gathers)
         fill the SMs G1's last partial wave leaves idle.  join_side() puts the
@@ -123,8 +124,23 @@ class Backend:
         if not hasattr(self, "_side"):
             self._side = torch.cuda.Stream(self.device)
         cur = torch.cuda.current_stream(self.device)
-        self._side.wait_stream(cur)
+        if after_current:  # else the caller orders the side stream with events
+            self._side.wait_stream(cur)
         return torch.cuda.stream(self._side)
+
+    def split_stream(self):
+        """Stream for the per-panel A splits (Grid2DGemm.step with A panels); it
+        starts after the current stream."""
+        if not hasattr(self, "_split"):
+            self._split = torch.cuda.Stream(self.device)
+        self._split.wait_stream(torch.cuda.current_stream(self.device))
+        return self._split
+
+    def copy_stream(self):
+        """Stream for the D2H copies of finished C rows (Grid2DGemm.step c_host)."""
+        if not hasattr(self, "_copy"):
+            self._copy = torch.cuda.Stream(self.device)
+        return self._copy
 
     def join_side(self):
         if hasattr(self, "_side"):
@@ -146,9 +162,10 @@ class Backend:
                 out_shift.data_ptr())
         if lsum is None:
             self.handle.check(oz.lib.ozmm_split(*args))
-        else:
-            self.handle.check(oz.lib.ozmm_split_offset(*args, lsum.data_ptr(), lsum.stride(1),
-                                                       lsum.stride(0)))
+        else:  # out_slices may be a line range of a larger [k][lines][lds] array
+            self.handle.check(oz.lib.ozmm_split_offset_strided(
+                *args[:-1], out_slices.stride(0), args[-1], lsum.data_ptr(), lsum.stride(1),
+                lsum.stride(0)))
 
     def gemm(self, m, n, p, k, beta_bits, a_slices, mu, b_slices, nu, alpha, beta, c,
              lsa=None, lsb=None, c_write_only=False):
@@ -187,6 +204,11 @@ def _new_group(ranks):
 def _other_ranges(total: int, own0: int, own: int):
     """[0, total) minus [own0, own0 + own), as up to two (start, stop) ranges."""
     return [(a, b) for a, b in ((0, own0), (own0 + own, total)) if b > a]
+
+
+def _pieces(total: int, size: int):
+    """[0, total) in consecutive pieces of `size` (the last one shorter)."""
+    return [(a, min(a + size, total)) for a in range(0, total, size)]
 
 
 class Grid2DGemm:
@@ -267,7 +289,7 @@ class Grid2DGemm:
                 w.wait()
 
     def step(self, a_rows, b_cols, c_block, alpha=1.0, beta=0.0, ready=None,
-             c_write_only=False):
+             c_write_only=False, c_host=None):
         """One sharded emulated GEMM.  The slice-panel all-gathers run while the
         GEMM works on what is already local, in three strip launches:
           G1  own A rows x own B columns     -- needs no communication;
@@ -279,32 +301,87 @@ class Grid2DGemm:
         ready: optional {'a', 'b', 'c'} -> CUDA event of the copy that fills
         a_rows / b_cols / c_block, for callers that stream the inputs in: each
         split waits only for its own operand and the GEMMs for C, so the
-        slicing and gathers overlap the rest of the upload.
+        slicing and gathers overlap the rest of the upload.  ready['a'] may also
+        be a list of (row0, row1, event) panels of a_rows (not transa): B is then
+        split first, each A panel as soon as it lands, and the first strip runs
+        per panel (upload B first, then A panel by panel).
         c_write_only: C is not read (beta == 0 and a finite C, where fl(beta*c)
-        = 0), so the caller need not upload it."""
+        = 0), so the caller need not upload it.
+        c_host: optional (pinned) host tensor shaped like c_block.  Each finished
+        full-width row range of C goes back on the backend's copy stream as soon
+        as the strips that write it are done: the own rows after G1 and G2, the
+        other rows per peer piece of G3 (pieces alternate between two streams so
+        one's last wave overlaps the next one's first).  Only the last piece's
+        D2H trails the GEMM.  The current stream waits for the copies."""
         L, k = self.L, self.k
         be = self.backend
         off = self.offset
         ready = ready or {}
+        # OZMM_GRID_TRACE=1 (diagnostics, CUDA only): timing events after each
+        # split / strip / copy, printed after a synchronize at the end of the step
+        marks = [] if os.environ.get("OZMM_GRID_TRACE") == "1" else None
+
+        def mark(name):
+            if marks is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                marks.append((name, e))
+        mark("start")
 
         def wait(key):
             if ready.get(key) is not None:
                 torch.cuda.current_stream().wait_event(ready[key])
         ls = (lambda *a: dict(lsum=a[0])) if off else (lambda *a: {})
-        wait("a")
-        be.split(a_rows, k, "L", self.transa, self.beta_bits, self.a_loc, self.mu_loc,
-                 **ls(self.lsa_loc))
-        wait("b")
-        be.split(b_cols, k, "R", self.transb, self.beta_bits, self.b_loc, self.nu_loc,
-                 **ls(self.lsb_loc))
-        # B first: it unblocks G2; group g of a GEMM needs slice planes <= g-1
-        wb = [self._gather(self.b_pan[s], self.b_loc[s], self.col_group, L.pr) for s in range(k)]
-        wb.append(self._gather(self.nu_pan, self.nu_loc, self.col_group, L.pr))
-        wa = [self._gather(self.a_pan[s], self.a_loc[s], self.row_group, L.pc) for s in range(k)]
-        wa.append(self._gather(self.mu_pan, self.mu_loc, self.row_group, L.pc))
-        if off:
-            wb.append(self._gather(self.lsb_pan, self.lsb_loc, self.col_group, L.pr))
-            wa.append(self._gather(self.lsa_pan, self.lsa_loc, self.row_group, L.pc))
+        a_panels = ready.get("a") if isinstance(ready.get("a"), (list, tuple)) else None
+        if a_panels is not None and self.transa:
+            raise ValueError("A panels need row-major op(A) (transa=False)")
+
+        def split_b():
+            wait("b")
+            be.split(b_cols, k, "R", self.transb, self.beta_bits, self.b_loc, self.nu_loc,
+                     **ls(self.lsb_loc))
+            mark("split B")
+        def gather_b():  # B first: it unblocks G2; group g needs slice planes <= g-1
+            wb = [self._gather(self.b_pan[s], self.b_loc[s], self.col_group, L.pr)
+                  for s in range(k)]
+            wb.append(self._gather(self.nu_pan, self.nu_loc, self.col_group, L.pr))
+            if off:
+                wb.append(self._gather(self.lsb_pan, self.lsb_loc, self.col_group, L.pr))
+            return wb
+        a_split = []  # per A panel: (row0, row1, event after its split) when panelled
+        if a_panels is None:
+            wait("a")
+            be.split(a_rows, k, "L", self.transa, self.beta_bits, self.a_loc, self.mu_loc,
+                     **ls(self.lsa_loc))
+            mark("split A")
+            split_b()
+            wb = gather_b()
+        else:
+            split_b()
+            wb = gather_b()  # before the A panels: the collective waits on this stream
+
+        def gather_a():
+            wa = [self._gather(self.a_pan[s], self.a_loc[s], self.row_group, L.pc)
+                  for s in range(k)]
+            wa.append(self._gather(self.mu_pan, self.mu_loc, self.row_group, L.pc))
+            if off:
+                wa.append(self._gather(self.lsa_pan, self.lsa_loc, self.row_group, L.pc))
+            return wa
+        if a_panels is None:
+            wa = gather_a()
+        else:
+            # the A panels are split on their own stream (the strips on the main
+            # and side streams wait per panel), and A's gather follows the last one
+            sp = be.split_stream()
+            with torch.cuda.stream(sp):
+                for lo, hi, ev in a_panels:
+                    sp.wait_event(ev)
+                    be.split(a_rows[lo:hi], k, "L", False, self.beta_bits, self.a_loc[:, lo:hi],
+                             self.mu_loc[lo:hi], **ls(self.lsa_loc[lo:hi] if off else None))
+                    a_split.append((lo, hi, torch.cuda.Event()))
+                    a_split[-1][2].record(sp)
+                    mark(f"split A {lo}:{hi}")
+                wa = gather_a()
 
         def sums(a_sl, b_sl):  # line sums of the operand rows / columns a strip reads
             kw = dict(lsa=a_sl, lsb=b_sl) if off else {}
@@ -315,20 +392,107 @@ class Grid2DGemm:
         g = (L.n, k, self.beta_bits)
         own_rows = c_block[r0:r0 + L.ms]
         side = getattr(be, "side_stream", None)
-        wait("c")  # C block landed (the side stream forks from here)
-        with side() if side else contextlib.nullcontext():
-            be.gemm(L.ms, g[0], L.ps, k, g[2], self.a_loc, self.mu_loc, self.b_loc, self.nu_loc,
-                    alpha, beta, own_rows[:, c0:c0 + L.ps], **sums(self.lsa_loc, self.lsb_loc))
-        self._wait(wb)
-        for lo, hi in _other_ranges(L.pcols, c0, L.ps):
-            be.gemm(L.ms, g[0], hi - lo, k, g[2], self.a_loc, self.mu_loc, self.b_pan[:, lo:hi],
-                    self.nu_pan[lo:hi], alpha, beta, own_rows[:, lo:hi],
-                    **sums(self.lsa_loc, self.lsb_pan[lo:hi] if off else None))
+        if not c_write_only:
+            wait("c")  # C block landed (the side stream forks from here)
+        out_s = be.copy_stream() if c_host is not None else None
+        cur = torch.cuda.current_stream() if out_s is not None else None
+        # streaming C back: the own rows go in pieces too (G1 / G2 per piece)
+        if a_split:
+            own = [(lo, hi) for lo, hi, _ in a_split]
+        else:
+            own = [(0, L.ms)] if out_s is None else _pieces(L.ms, max(256, L.ms // 4))
+
+        def send(lo, hi, waits):  # D2H of C rows [lo, hi) once `waits` are done
+            for w in waits:
+                if isinstance(w, torch.cuda.Event):
+                    out_s.wait_event(w)
+                else:
+                    out_s.wait_stream(w)
+            with torch.cuda.stream(out_s):
+                c_host[lo:hi].copy_(c_block[lo:hi], non_blocking=True)
+                mark(f"D2H {lo}:{hi}")
+
+        def g1(lo, hi):  # own rows x own columns: no communication
+            be.gemm(hi - lo, g[0], L.ps, k, g[2], self.a_loc[:, lo:hi], self.mu_loc[lo:hi],
+                    self.b_loc, self.nu_loc, alpha, beta, own_rows[lo:hi, c0:c0 + L.ps],
+                    **sums(self.lsa_loc[lo:hi] if off else None, self.lsb_loc))
+            mark(f"G1 {lo}:{hi}")
+
+        def g2(lo, hi):  # own rows x the other columns: after the B gather
+            for clo, chi in _other_ranges(L.pcols, c0, L.ps):
+                be.gemm(hi - lo, g[0], chi - clo, k, g[2], self.a_loc[:, lo:hi], self.mu_loc[lo:hi],
+                        self.b_pan[:, clo:chi], self.nu_pan[clo:chi], alpha, beta,
+                        own_rows[lo:hi, clo:chi],
+                        **sums(self.lsa_loc[lo:hi] if off else None,
+                               self.lsb_pan[clo:chi] if off else None))
+            mark(f"G2 {lo}:{hi}")
+        if side and (a_split or out_s is not None):
+            # per piece of the own rows: G1 and G2 back to back, pieces alternating
+            # between the main and the side stream, so the own rows finish (and go
+            # back) piece by piece while the next piece's first wave fills the SMs
+            forked = torch.cuda.Event()
+            forked.record()  # splits, B gather and C's arrival queued on the main stream
+            for i, (lo, hi) in enumerate(own):
+                st = be.side_stream(after_current=False) if i % 2 else contextlib.nullcontext()
+                with st:
+                    if i % 2:
+                        torch.cuda.current_stream().wait_event(forked)
+                    if a_split:
+                        torch.cuda.current_stream().wait_event(a_split[i][2])
+                    g1(lo, hi)
+                    self._wait(wb)
+                    g2(lo, hi)
+                    if out_s is not None:
+                        send(r0 + lo, r0 + hi, [torch.cuda.current_stream()])
+        else:
+            g1_done = []
+            with side() if side else contextlib.nullcontext():
+                for lo, hi in own:
+                    if a_split:
+                        torch.cuda.current_stream().wait_event(a_split[len(g1_done)][2])
+                    g1(lo, hi)
+                    g1_done.append(torch.cuda.Event() if out_s is not None else None)
+                    if out_s is not None:
+                        g1_done[-1].record()
+            self._wait(wb)
+            for i, (lo, hi) in enumerate(own):
+                g2(lo, hi)
+                if out_s is not None:
+                    send(r0 + lo, r0 + hi, [cur, g1_done[i]])
         self._wait(wa)
-        for lo, hi in _other_ranges(L.mr, r0, L.ms):
+        gathered = torch.cuda.Event() if out_s is not None and side else None
+        if gathered is not None:
+            gathered.record(cur)
+
+        def g3(lo, hi):
             be.gemm(hi - lo, g[0], L.pcols, k, g[2], self.a_pan[:, lo:hi], self.mu_pan[lo:hi],
                     self.b_pan, self.nu_pan, alpha, beta, c_block[lo:hi],
                     **sums(self.lsa_pan[lo:hi] if off else None, self.lsb_pan))
+            mark(f"G3 {lo}:{hi}")
+        if out_s is None:
+            for lo, hi in _other_ranges(L.mr, r0, L.ms):
+                g3(lo, hi)
+        else:
+            pieces = [(a, min(a + L.ms, hi)) for lo, hi in _other_ranges(L.mr, r0, L.ms)
+                      for a in range(lo, hi, L.ms)]
+            for i, (lo, hi) in enumerate(pieces):
+                if i % 2 and side:
+                    with be.side_stream(after_current=False):
+                        sst = torch.cuda.current_stream()
+                        sst.wait_event(gathered)  # gathers done, not piece i-1
+                        g3(lo, hi)
+                    send(lo, hi, [sst])
+                else:
+                    g3(lo, hi)
+                    send(lo, hi, [cur])
         if side:
             be.join_side()
+        if out_s is not None:
+            cur.wait_stream(out_s)
+        if marks is not None:
+            mark("end")
+            torch.cuda.synchronize()
+            t0 = marks[0][1]
+            print("grid trace:", ", ".join(f"{n} {t0.elapsed_time(e):.1f}" for n, e in marks),
+                  flush=True)
         return c_block

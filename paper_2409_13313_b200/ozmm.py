@@ -104,6 +104,8 @@ _SIG = {
                                   C.POINTER(Options)], C.c_int),
     "ozmm_split_offset": ([_vp, C.c_char, C.c_char, _i64, _i64, _vp, _i64, C.c_int, C.c_int,
                            _vp, _i64, _vp, _vp, _i64, _i64], C.c_int),
+    "ozmm_split_offset_strided": ([_vp, C.c_char, C.c_char, _i64, _i64, _vp, _i64, C.c_int,
+                                   C.c_int, _vp, _i64, _i64, _vp, _vp, _i64, _i64], C.c_int),
     "ozmm_gemm_slices_offset": ([_vp, _i64, _i64, _i64, C.c_int, C.c_int, _i64, _vp, _i64, _i64,
                                  _vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp, _vp, _i64, _i64,
                                  C.c_double, C.c_double, _vp, _i64, C.POINTER(Options)], C.c_int),

@@ -37,13 +37,20 @@ def test_grid2d_cuda_world1():
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,trans", [(2, False), (4, False), (8, False), (4, True),
-                                         (8, True)])
-def test_grid2d_cuda_emulated_ranks(world, trans):
+@pytest.mark.parametrize("world,trans,host", [(2, False, False), (4, False, False),
+                                              (8, False, False), (4, True, False),
+                                              (8, True, False), (2, False, True),
+                                              (4, False, True), (8, True, True),
+                                              (2, False, "panels"), (4, False, "panels"),
+                                              (8, False, "panels")])
+def test_grid2d_cuda_emulated_ranks(world, trans, host):
     """All ranks of a Pr x Pc grid as threads on the one GPU, with an in-process
     all-gather: the CUDA backend's strip launches (G1/G2/G3 on row/column ranges of
     the gathered panels, ozmm_gemm_slices_strided) must tile C exactly like the
-    single call, bit for bit."""
+    single call, bit for bit.  host: the C rows stream back into a pinned host
+    block piece by piece (step's c_host), which must hold the same result;
+    "panels": A also arrives in row panels with one ready event each, split and
+    multiplied panel by panel."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import threading
@@ -101,9 +108,21 @@ def test_grid2d_cuda_emulated_ranks(world, trans):
                 a = dev(A[L.a_row0:L.a_row0 + L.ms])
                 b = dev(B[:, L.b_col0:L.b_col0 + L.ps])
             c = dev(C[L.c_row0:L.c_row0 + L.mr, L.c_col0:L.c_col0 + L.pcols])
-            G.step(a, b, c, alpha, beta)
+            hc = torch.full(tuple(c.shape), float("nan"), dtype=torch.float64).pin_memory() \
+                if host else None
+            ready = None
+            if host == "panels":
+                cuts = sorted({0, L.ms, *(int(x) for x in np.random.default_rng(rank).integers(
+                    1, L.ms, 2))})
+                ready = {"a": []}
+                for lo, hi in zip(cuts[:-1], cuts[1:]):
+                    e = torch.cuda.Event()
+                    e.record()
+                    ready["a"].append((lo, hi, e))
+            G.step(a, b, c, alpha, beta, c_host=hc, ready=ready)
             torch.cuda.synchronize()
-            got[L.c_row0:L.c_row0 + L.mr, L.c_col0:L.c_col0 + L.pcols] = c.cpu().numpy()
+            got[L.c_row0:L.c_row0 + L.mr, L.c_col0:L.c_col0 + L.pcols] = \
+                (hc if host else c.cpu()).numpy()
         except BaseException as ex:  # surfaced below
             errors.append(ex)
             for bar in list(barriers.values()):

@@ -44,6 +44,10 @@ def main():
     ap.add_argument("--nvlink-gbs", type=float, default=700.0)
     ap.add_argument("--clock-ghz", type=float, default=1.4, help="for the _sleep cycle count")
     ap.add_argument("--no-side", action="store_true", help="G1 on the main stream (old order)")
+    ap.add_argument("--e2e", action="store_true",
+                    help="also time the rank's end-to-end step (pinned H2D of its shard, step, "
+                         "D2H of its C block): C rows streamed back per strip (c_host) against "
+                         "one copy after the step")
     args = ap.parse_args()
 
     from paper_2409_13313_b200 import ozmm
@@ -117,10 +121,50 @@ def main():
         else:
             wire_ns[0] = 0.0
             t = timed(lambda: G.step(A, B, C, 1.0, 0.0), args.reps)
+        e2e = {}
+        if args.e2e and world > 1:
+            hA, hB = A.cpu().pin_memory(), B.cpu().pin_memory()
+            hC = torch.empty(tuple(C.shape), dtype=torch.float64).pin_memory()
+            s_in = torch.cuda.Stream(dev)
+            ev = {key: torch.cuda.Event() for key in "abc"}
+            # B first, then A in row panels: B's split and gather, and the first
+            # strip of each A panel, run while the rest of A is still crossing PCIe
+            a_pieces = [(lo, min(lo + max(256, L.ms // 4), L.ms))
+                        for lo in range(0, L.ms, max(256, L.ms // 4))]
+            a_ev = [torch.cuda.Event() for _ in a_pieces]
+            ev["a"] = [(lo, hi, e) for (lo, hi), e in zip(a_pieces, a_ev)]
+
+            ev1 = torch.cuda.Event()
+
+            def e2e_call(mode):
+                # after: A then B whole, one D2H after the step; streamed: C rows go
+                # back per strip (c_host); panels: + B first, then A panel by panel
+                with torch.cuda.stream(s_in):
+                    if mode == "panels":
+                        B.copy_(hB, non_blocking=True)
+                        ev["b"].record(s_in)
+                        for (lo, hi), e in zip(a_pieces, a_ev):
+                            A[lo:hi].copy_(hA[lo:hi], non_blocking=True)
+                            e.record(s_in)
+                    else:
+                        A.copy_(hA, non_blocking=True)
+                        ev1.record(s_in)
+                        B.copy_(hB, non_blocking=True)
+                        ev["b"].record(s_in)
+                    ev["c"].record(s_in)
+                rd = dict(ev, a=ev["a"] if mode == "panels" else ev1)
+                G.step(A, B, C, 1.0, 0.0, ready=rd, c_write_only=True,
+                       c_host=None if mode == "after" else hC)
+                if mode == "after":
+                    hC.copy_(C, non_blocking=True)
+            for mode in ("after", "streamed", "panels") * 2:
+                e2e.setdefault(mode, []).append(round(timed(lambda: e2e_call(mode), args.reps), 3))
         row = {"world": world, "grid": f"{L.pr}x{L.pc}", "rank_ms": round(t, 3),
                "c_block": [L.mr, L.pcols],
                "modelled_wire_ms_per_step": round(wire_ns[0] / 1e6 / (args.reps + 3), 3)
                if world > 1 else 0.0}
+        if e2e:
+            row["e2e_ms"] = e2e
         if t1:
             row["t1_ms"] = round(t1, 3)
             row["efficiency"] = round(t1 / (world * t), 4)
