@@ -137,6 +137,7 @@ int ozmm_create(ozmm_handle_t* handle, int device);
 int ozmm_destroy(ozmm_handle_t handle);
 /* stream: a cudaStream_t (NULL = legacy default stream). */
 int ozmm_set_stream(ozmm_handle_t handle, void* stream);
+int ozmm_get_stream(ozmm_handle_t handle, void** stream);
 /* Message of the last failing call on this handle (or thread, when handle is NULL). */
 const char* ozmm_last_error(ozmm_handle_t handle);
 const char* ozmm_status_string(int status);
@@ -241,6 +242,42 @@ int ozmm_gemm_slices_offset(ozmm_handle_t h, int64_t m, int64_t n, int64_t p, in
                             int64_t lds_b, int64_t plane_b, const double* nu, const int32_t* lsb,
                             int64_t lsb_plane, int64_t lsb_lstride, double alpha, double beta,
                             double* C, int64_t ldc, const ozmm_options_t* opt);
+
+/* ---- 2-D grid over several GPUs (SURVEY.md 8b "multi-GPU", 8e) -----------
+ * One process and one handle per GPU.  The ranks form a Pr x Pc grid
+ * (ozmm_grid_shape: 1x1, 2x1, 2x2, 2x4, ...); rank (gr, gc) = (rank / Pc,
+ * rank % Pc) owns C block (gr, gc) of (m/Pr) x (p/Pc) and passes
+ *   A: its m/(Pr*Pc) rows of op(A), rows [gr*m/Pr + gc*m/(Pr*Pc), +m/(Pr*Pc))
+ *      -- (m/(Pr*Pc)) x n, or its transpose when transa;
+ *   B: its p/(Pr*Pc) columns of op(B), columns [gc*p/Pc + gr*p/(Pr*Pc), ...)
+ *      -- n x (p/(Pr*Pc)), or its transpose when transb;
+ *   C: its C block (ldc >= p/Pc), overwritten with alpha*D + beta*C.
+ * ozmm_dgemm_2d splits the rank's lines, all-gathers the INT8 slice planes,
+ * shifts and line sums inside the row group (A) and the column group (B) --
+ * broadcasts only -- and runs the fused GEMM on the block in three strips.
+ * The result is bit-identical to ozmm_dgemm on the whole matrices.  It is
+ * stream-ordered on the handle's stream; range errors surface through
+ * ozmm_sync_status on each rank, as for the split halves.
+ * The all-gather is NCCL (every rank passes the same 128-byte id from
+ * ozmm_nccl_unique_id on one rank; libnccl.so.2 is loaded on first use) or,
+ * when `hook` is non-NULL, the caller's: hook(ctx, group, send, recv, bytes,
+ * stream) gathers `bytes` from each member of group 0 (this grid row, member
+ * index gc) or group 1 (this grid column, index gr) into recv, rank-major,
+ * ordered on `stream` (a cudaStream_t); send == recv + index * bytes.
+ * Returns 0 on success. */
+typedef struct ozmm_grid* ozmm_grid_t;
+typedef int (*ozmm_allgather_fn)(void* ctx, int group, const void* send, void* recv,
+                                 int64_t bytes, void* stream);
+int ozmm_grid_shape(int world, int* pr, int* pc);
+int ozmm_nccl_unique_id(void* id128);
+int ozmm_grid_create(ozmm_handle_t h, int device, int world, int rank, const void* nccl_id,
+                     ozmm_allgather_fn hook, void* hook_ctx, ozmm_grid_t* grid);
+int ozmm_grid_destroy(ozmm_grid_t grid);
+int ozmm_grid_coords(ozmm_grid_t grid, int* pr, int* pc, int* gr, int* gc);
+const char* ozmm_grid_last_error(void);
+int ozmm_dgemm_2d(ozmm_grid_t grid, char transa, char transb, int64_t m, int64_t n, int64_t p,
+                  double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+                  double beta, double* C, int64_t ldc, int k);
 
 /* ---- introspection (host only; used by tests/test_host_logic.py) ---------- */
 /* The GEMM's host schedule for (k, r) and a kernel choice (cta_pair/tile_n as

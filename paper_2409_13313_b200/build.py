@@ -20,7 +20,8 @@ ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libozmm_b200.so")
 CLI = os.path.join(PKG, "ozmm_b200_cli")
 CLI_SRC = os.path.join(PKG, "cli", "ozmm_cli.cpp")
-SOURCES = [os.path.join(CSRC, "ozmm_capi.cu"), os.path.join(CSRC, "host_generate.cpp")]
+SOURCES = [os.path.join(CSRC, "ozmm_capi.cu"), os.path.join(CSRC, "host_generate.cpp"),
+           os.path.join(CSRC, "ozmm_grid.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp"))] + [
     os.path.join(ROOT, "include", "ozmm_b200.h")]
 
@@ -46,7 +47,7 @@ def command(out: str = LIB, verbose_ptxas: bool = False) -> list[str]:
         "-gencode", "arch=compute_100a,code=sm_100a",
         "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
         "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off,-O3",
-        "-shared", "-o", out, *SOURCES, "-lgomp",
+        "-shared", "-o", out, *SOURCES, "-lgomp", "-ldl",
     ]
     if verbose_ptxas:
         cmd[1:1] = ["-Xptxas", "-v"]

@@ -787,6 +787,13 @@ int ozmm_set_stream(ozmm_handle_t handle, void* stream) {
   return OZMM_OK;
 }
 
+int ozmm_get_stream(ozmm_handle_t handle, void** stream) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h || !stream) return set_err(h, OZMM_ERR_ARG, "null handle or output");
+  *stream = h->stream;
+  return OZMM_OK;
+}
+
 const char* ozmm_last_error(ozmm_handle_t handle) {
   Handle* h = reinterpret_cast<Handle*>(handle);
   return h ? h->err.c_str() : g_thread_err.c_str();

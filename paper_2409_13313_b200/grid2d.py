@@ -496,3 +496,65 @@ class Grid2DGemm:
             print("grid trace:", ", ".join(f"{n} {t0.elapsed_time(e):.1f}" for n, e in marks),
                   flush=True)
         return c_block
+
+
+class NativeGrid2D:
+    """The same 2-D partition through the C ABI's native entry (ozmm_dgemm_2d,
+    csrc/ozmm_grid.cpp): splits, in-place all-gathers and the three strips are
+    orchestrated in C++ on the handle's stream.  The collective is NCCL -- rank 0
+    makes the id (ozmm_nccl_unique_id) and torch.distributed broadcasts it -- or
+    `hook`, an ozmm.ALLGATHER_FN (the single-GPU tests emulate ranks with it).
+    The shard arguments of step() are those of Grid2DGemm.step."""
+
+    def __init__(self, m: int, n: int, p: int, k: int, world: int | None = None,
+                 rank: int | None = None, device: int = 0, transa: bool = False,
+                 transb: bool = False, hook=None):
+        from . import ozmm
+        self.oz = ozmm
+        if world is None:
+            world = dist.get_world_size() if dist.is_initialized() else 1
+        if rank is None:
+            rank = dist.get_rank() if dist.is_initialized() else 0
+        self.m, self.n, self.p, self.k = m, n, p, k
+        self.transa, self.transb = transa, transb
+        self.L = make_layout(m, n, p, world, rank)
+        self.device = torch.device("cuda", device)
+        self.handle = ozmm.Handle(device)
+        self._hook = hook  # keep the ctypes callback alive
+        nid = None
+        if world > 1 and hook is None:
+            buf = (ctypes.c_char * 128)()
+            if rank == 0:
+                self._check(ozmm.lib.ozmm_nccl_unique_id(buf))
+            obj = [bytes(buf)]
+            dist.broadcast_object_list(obj, src=0)
+            nid = (ctypes.c_char * 128).from_buffer_copy(obj[0])
+        g = ctypes.c_void_p()
+        self._check(ozmm.lib.ozmm_grid_create(self.handle.h, device, world, rank, nid,
+                                              ctypes.cast(hook, ctypes.c_void_p) if hook else None,
+                                              None, ctypes.byref(g)))
+        self.g = g
+
+    def _check(self, rc):
+        if rc != 0:
+            raise RuntimeError(f"ozmm grid: {self.oz.lib.ozmm_grid_last_error().decode()}")
+
+    def step(self, a_rows, b_cols, c_block, alpha=1.0, beta=0.0):
+        self.handle.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
+        self._check(self.oz.lib.ozmm_dgemm_2d(
+            self.g, b"T" if self.transa else b"N", b"T" if self.transb else b"N",
+            self.m, self.n, self.p, alpha, a_rows.data_ptr(), a_rows.stride(0),
+            b_cols.data_ptr(), b_cols.stride(0), beta, c_block.data_ptr(), c_block.stride(0),
+            self.k))
+        return c_block
+
+    def close(self):
+        if getattr(self, "g", None):
+            self.oz.lib.ozmm_grid_destroy(self.g)
+            self.g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

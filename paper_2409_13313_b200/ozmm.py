@@ -112,6 +112,18 @@ _SIG = {
     "ozmm_gen_phi_block": ([_i64, _i64, C.c_double, C.c_uint64, _i64, _i64, _i64, _i64, _vp,
                             _i64], C.c_int),
     "ozmm_counter_hash": ([C.c_uint64, C.c_uint64], C.c_uint64),
+    "ozmm_get_stream": ([_vp, C.POINTER(C.c_void_p)], C.c_int),
+    # 2-D grid (ozmm_dgemm_2d); the hook argument is an ALLGATHER_FN or None
+    "ozmm_grid_shape": ([C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
+    "ozmm_nccl_unique_id": ([_vp], C.c_int),
+    "ozmm_grid_create": ([_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, C.POINTER(C.c_void_p)],
+                         C.c_int),
+    "ozmm_grid_destroy": ([_vp], C.c_int),
+    "ozmm_grid_coords": ([_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                          C.POINTER(C.c_int)], C.c_int),
+    "ozmm_grid_last_error": ([], C.c_char_p),
+    "ozmm_dgemm_2d": ([_vp, C.c_char, C.c_char, _i64, _i64, _i64, C.c_double, _vp, _i64, _vp,
+                       _i64, C.c_double, _vp, _i64, C.c_int], C.c_int),
     "ozmm_debug_schedule": ([C.c_int, _i64, C.c_int, C.c_int, _vp, C.c_int, _vp], C.c_int),
 }
 for _name, (_args, _res) in _SIG.items():
@@ -119,6 +131,9 @@ for _name, (_args, _res) in _SIG.items():
     _f.argtypes, _f.restype = _args, _res
 
 EXPORTED_SYMBOLS = tuple(_SIG)
+
+# ozmm_allgather_fn (include/ozmm_b200.h): (ctx, group, send, recv, bytes, stream) -> int
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, _vp, C.c_int, _vp, _vp, _i64, _vp)
 
 
 # ---------------------------------------------------------------- errors

@@ -167,3 +167,135 @@ def test_gemm_slices_c_write_only():
     with pytest.raises(ValueError):
         be.gemm(m, n, p, k, beta_bits, sa, mu, sb, nu, 1.25, 0.5, got, lsa=la, lsb=lb,
                 c_write_only=True)
+
+
+def _native_case(trans):
+    from paper_2409_13313_b200 import ozmm
+    m, n, p, k, alpha, beta = 1024, 2500, 768, 8, 1.25, -0.5
+    A = ozmm.gen_phi_matrix(m, n, 1.0, 21)
+    B = ozmm.gen_phi_matrix(n, p, 1.0, 22)
+    C = ozmm.gen_phi_matrix(m, p, 1.0, 23)
+    dev = lambda x: torch.tensor(np.ascontiguousarray(x), device="cuda")  # noqa: E731
+    want = ozmm.ozaki_gemm(alpha, dev(A), dev(B), beta, dev(C),
+                           ozmm.config_for("ozIMMU_H", k)).cpu().numpy()
+
+    def shard(L):
+        if trans:
+            a = dev(np.ascontiguousarray(A.T)[:, L.a_row0:L.a_row0 + L.ms])
+            b = dev(np.ascontiguousarray(B.T)[L.b_col0:L.b_col0 + L.ps])
+        else:
+            a = dev(A[L.a_row0:L.a_row0 + L.ms])
+            b = dev(B[:, L.b_col0:L.b_col0 + L.ps])
+        c = dev(C[L.c_row0:L.c_row0 + L.mr, L.c_col0:L.c_col0 + L.pcols])
+        return a, b, c
+    return (m, n, p, k, alpha, beta), want, shard
+
+
+@pytest.mark.parametrize("trans", [False, True])
+def test_native_grid_world1(trans):
+    """ozmm_dgemm_2d on a 1x1 grid (no collective) equals the single call."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2409_13313_b200.grid2d import NativeGrid2D
+    (m, n, p, k, alpha, beta), want, shard = _native_case(trans)
+    G = NativeGrid2D(m, n, p, k, world=1, rank=0, transa=trans, transb=trans)
+    a, b, c = shard(G.L)
+    G.step(a, b, c, alpha, beta)
+    torch.cuda.synchronize()
+    assert np.array_equal(c.cpu().numpy().view(np.uint64), want.view(np.uint64))
+    G.close()
+
+
+def test_native_grid_nccl_init():
+    """The NCCL plumbing of the native grid: unique id, ncclCommInitRank and the
+    two ncclCommSplit calls on a one-rank world, then a bit-exact step."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import ctypes
+    from paper_2409_13313_b200 import ozmm
+    (m, n, p, k, alpha, beta), want, shard = _native_case(False)
+    from paper_2409_13313_b200.grid2d import make_layout
+    h = ozmm.Handle(0)
+    nid = (ctypes.c_char * 128)()
+    assert ozmm.lib.ozmm_nccl_unique_id(nid) == 0, ozmm.lib.ozmm_grid_last_error()
+    g = ctypes.c_void_p()
+    rc = ozmm.lib.ozmm_grid_create(h.h, 0, 1, 0, nid, None, None, ctypes.byref(g))
+    assert rc == 0, ozmm.lib.ozmm_grid_last_error()
+    a, b, c = shard(make_layout(m, n, p, 1, 0))
+    h.set_stream(torch.cuda.current_stream().cuda_stream)
+    assert ozmm.lib.ozmm_dgemm_2d(g, b"N", b"N", m, n, p, alpha, a.data_ptr(), a.stride(0),
+                                  b.data_ptr(), b.stride(0), beta, c.data_ptr(), c.stride(0),
+                                  k) == 0, ozmm.lib.ozmm_grid_last_error()
+    torch.cuda.synchronize()
+    assert np.array_equal(c.cpu().numpy().view(np.uint64), want.view(np.uint64))
+    assert ozmm.lib.ozmm_grid_destroy(g) == 0
+
+
+@pytest.mark.parametrize("world,trans", [(2, False), (4, False), (8, False), (8, True)])
+def test_native_grid_emulated_ranks(world, trans):
+    """ozmm_dgemm_2d with W ranks as threads on the one GPU: the all-gather hook
+    copies the peers' parts (cudaMemcpy) between barriers.  The native split
+    into panel slots, in-place gathers and strips must tile C like the single
+    call, bit for bit."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import ctypes
+    import threading
+    from paper_2409_13313_b200 import ozmm
+    from paper_2409_13313_b200.grid2d import NativeGrid2D, make_layout
+    (m, n, p, k, alpha, beta), want, shard = _native_case(trans)
+    cudart = ctypes.CDLL("libcudart.so.12")
+    cudart.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+    barriers, pool, lock, errors = {}, {}, threading.Lock(), []
+
+    def gather(ctx, group, send, recv, nbytes, stream):
+        try:
+            th = threading.current_thread()
+            L = th.L
+            members = tuple(L.gr * L.pc + c for c in range(L.pc)) if group == 0 else \
+                tuple(r * L.pc + L.gc for r in range(L.pr))
+            with lock:
+                bar = barriers.setdefault(members, threading.Barrier(len(members)))
+                seq = th.seq.setdefault(members, 0)
+                th.seq[members] = seq + 1
+            torch.cuda.synchronize()
+            pool[(members, seq, th.rank)] = send
+            bar.wait()
+            for idx, r in enumerate(members):
+                if r != th.rank:
+                    assert cudart.cudaMemcpy(recv + idx * nbytes, pool[(members, seq, r)],
+                                             nbytes, 3) == 0
+            bar.wait()
+            return 0
+        except BaseException as ex:  # surfaced below
+            errors.append(ex)
+            for b in list(barriers.values()):
+                b.abort()
+            return 1
+    hook = ozmm.ALLGATHER_FN(gather)
+    got = np.full((m, p), np.nan)
+
+    def run(rank):
+        try:
+            th = threading.current_thread()
+            th.rank, th.seq = rank, {}
+            th.L = L = make_layout(m, n, p, world, rank)
+            G = NativeGrid2D(m, n, p, k, world=world, rank=rank, transa=trans, transb=trans,
+                             hook=hook)
+            a, b, c = shard(L)
+            G.step(a, b, c, alpha, beta)
+            torch.cuda.synchronize()
+            got[L.c_row0:L.c_row0 + L.mr, L.c_col0:L.c_col0 + L.pcols] = c.cpu().numpy()
+            G.close()
+        except BaseException as ex:
+            errors.append(ex)
+            for b in list(barriers.values()):
+                b.abort()
+
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not errors, errors
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))

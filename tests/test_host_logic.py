@@ -118,3 +118,14 @@ def test_grid_layout():
             assert L.c_col0 <= L.b_col0 < L.c_col0 + L.pcols
         assert sorted(rows_seen) == list(range(m))      # each row of A sliced once
         assert sorted(cols_seen) == list(range(p))      # each column of B sliced once
+
+
+def test_native_grid_shape_matches_python():
+    """ozmm_grid_shape (native grid) and grid2d.grid_shape pick the same Pr x Pc."""
+    import ctypes
+    from paper_2409_13313_b200 import ozmm
+    from paper_2409_13313_b200.grid2d import grid_shape
+    for w in range(1, 17):
+        pr, pc = ctypes.c_int(), ctypes.c_int()
+        assert ozmm.lib.ozmm_grid_shape(w, ctypes.byref(pr), ctypes.byref(pc)) == 0
+        assert (pr.value, pc.value) == grid_shape(w), w
