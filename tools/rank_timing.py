@@ -44,6 +44,9 @@ def main():
     ap.add_argument("--nvlink-gbs", type=float, default=700.0)
     ap.add_argument("--clock-ghz", type=float, default=1.4, help="for the _sleep cycle count")
     ap.add_argument("--no-side", action="store_true", help="G1 on the main stream (old order)")
+    ap.add_argument("--native", action="store_true",
+                    help="also time the native C-ABI grid entry (ozmm_dgemm_2d) with the same "
+                         "emulated all-gather as a hook")
     ap.add_argument("--e2e", action="store_true",
                     help="also time the rank's end-to-end step (pinned H2D of its shard, step, "
                          "D2H of its C block): C rows streamed back per strip (c_host) against "
@@ -121,6 +124,32 @@ def main():
         else:
             wire_ns[0] = 0.0
             t = timed(lambda: G.step(A, B, C, 1.0, 0.0), args.reps)
+        native = None
+        if args.native and world > 1:
+            import ctypes
+            from paper_2409_13313_b200.grid2d import NativeGrid2D
+            cudart = ctypes.CDLL("libcudart.so.12")
+            cudart.cudaMemcpyAsync.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                               ctypes.c_int, ctypes.c_void_p]
+            Lw = L
+
+            def hook(ctx, group, send, recv, nbytes, stream):
+                # this rank's part into every peer slot (stand-in for the peers' data),
+                # then the modelled wire time of the bytes received, on `stream`
+                nr = Lw.pc if group == 0 else Lw.pr
+                idx = Lw.gc if group == 0 else Lw.gr
+                for i in range(nr):
+                    if i != idx:
+                        cudart.cudaMemcpyAsync(recv + i * nbytes, send, nbytes, 3, stream)
+                ns = nbytes * (nr - 1) / (args.nvlink_gbs * 1e9) * 1e9
+                if ns > 0:
+                    with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+                        torch.cuda._sleep(int(ns * args.clock_ghz))
+                return 0
+            cb = ozmm.ALLGATHER_FN(hook)
+            NG = NativeGrid2D(m, n, p, k, world=world, rank=0, hook=cb)
+            native = timed(lambda: NG.step(A, B, C, 1.0, 0.0), args.reps)
+            NG.close()
         e2e = {}
         if args.e2e and world > 1:
             hA, hB = A.cpu().pin_memory(), B.cpu().pin_memory()
@@ -163,6 +192,8 @@ def main():
                "c_block": [L.mr, L.pcols],
                "modelled_wire_ms_per_step": round(wire_ns[0] / 1e6 / (args.reps + 3), 3)
                if world > 1 else 0.0}
+        if native is not None:
+            row["native_rank_ms"] = round(native, 3)
         if e2e:
             row["e2e_ms"] = e2e
         if t1:
