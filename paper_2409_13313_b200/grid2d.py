@@ -136,6 +136,18 @@ class Backend:
         self._split.wait_stream(torch.cuda.current_stream(self.device))
         return self._split
 
+    def range_error(self) -> int:
+        """1 if a split since the last query saw a line max >= 2^921 (the
+        reference's std::overflow_error, split.cpp:124-125), else 0.  Synchronises
+        the device and clears the flag."""
+        torch.cuda.synchronize(self.device)
+        uf = ctypes.c_int()
+        rc = self.oz.lib.ozmm_sync_status(self.handle.h, ctypes.byref(uf))
+        if rc == self.oz.OZMM_ERR_RANGE:
+            return 1
+        self.handle.check(rc)
+        return 0
+
     def copy_stream(self):
         """Stream for the D2H copies of finished C rows (Grid2DGemm.step c_host)."""
         if not hasattr(self, "_copy"):
@@ -288,8 +300,21 @@ class Grid2DGemm:
             if w is not None:
                 w.wait()
 
+    def _check_range_across_grid(self):
+        L, be = self.L, self.backend
+        flag = be.empty((1,), torch.int32)
+        flag.fill_(be.range_error())
+        for group, nr in ((self.row_group, L.pc), (self.col_group, L.pr)):
+            if nr > 1:
+                out = be.empty((nr,), torch.int32)
+                self._wait([self._gather(out, flag, group, nr)])
+                flag.fill_(int(out.max().item()))
+        if int(flag.item()):
+            raise OverflowError("split: a rank of the grid saw a line magnitude too large for "
+                                "shift extraction (>= 2^921)")
+
     def step(self, a_rows, b_cols, c_block, alpha=1.0, beta=0.0, ready=None,
-             c_write_only=False, c_host=None):
+             c_write_only=False, c_host=None, sync_check=False):
         """One sharded emulated GEMM.  The slice-panel all-gathers run while the
         GEMM works on what is already local, in three strip launches:
           G1  own A rows x own B columns     -- needs no communication;
@@ -312,7 +337,13 @@ class Grid2DGemm:
         as the strips that write it are done: the own rows after G1 and G2, the
         other rows per peer piece of G3 (pieces alternate between two streams so
         one's last wave overlaps the next one's first).  Only the last piece's
-        D2H trails the GEMM.  The current stream waits for the copies."""
+        D2H trails the GEMM.  The current stream waits for the copies.
+        sync_check: the reference's throw-before-write across the grid.  After the
+        local splits every rank reads its range flag (a synchronisation), the
+        flags are max-reduced over the grid by two tiny all-gathers (row group,
+        then column group), and EVERY rank raises OverflowError before any GEMM
+        when any rank saw a line max >= 2^921; C is left untouched.  Without it
+        the flag stays in the backend (Backend.range_error / ozmm_sync_status)."""
         L, k = self.L, self.k
         be = self.backend
         off = self.offset
@@ -359,6 +390,9 @@ class Grid2DGemm:
         else:
             split_b()
             wb = gather_b()  # before the A panels: the collective waits on this stream
+
+        if sync_check:
+            self._check_range_across_grid()
 
         def gather_a():
             wa = [self._gather(self.a_pan[s], self.a_loc[s], self.row_group, L.pc)

@@ -299,3 +299,30 @@ def test_native_grid_emulated_ranks(world, trans):
         t.join(timeout=300)
     assert not errors, errors
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+def test_grid2d_cuda_sync_check_range_error():
+    """Grid2DGemm.step(sync_check=True) on the CUDA backend: a line max >= 2^921
+    raises OverflowError before any GEMM (C untouched), the flag is cleared, and
+    the next clean step is bit-exact."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2409_13313_b200 import ozmm
+    from paper_2409_13313_b200.grid2d import Backend, Grid2DGemm
+    m, n, p, k = 512, 1000, 384, 8
+    A = ozmm.gen_phi_matrix(m, n, 1.0, 31)
+    B = ozmm.gen_phi_matrix(n, p, 1.0, 32)
+    G = Grid2DGemm(m, n, p, k, world=1, rank=0, backend=Backend(0),
+                   group_factory=lambda ranks: tuple(ranks), all_gather=None)
+    bad = A.copy()
+    bad[7, 11] = 2.0 ** 925
+    a, b = torch.tensor(bad, device="cuda"), torch.tensor(B, device="cuda")
+    c = torch.full((m, p), 7.0, dtype=torch.float64, device="cuda")
+    with pytest.raises(OverflowError):
+        G.step(a, b, c, 1.0, 0.0, sync_check=True)
+    assert bool((c == 7.0).all())
+    want = ozmm.ozaki_gemm(1.0, torch.tensor(A, device="cuda"), b, 0.0, torch.zeros_like(c),
+                           ozmm.config_for("ozIMMU_H", k)).cpu().numpy()
+    G.step(torch.tensor(A, device="cuda"), b, c, 1.0, 0.0, sync_check=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(c.cpu().numpy().view(np.uint64), want.view(np.uint64))

@@ -33,13 +33,24 @@ class OracleBackend:
         return torch.zeros(shape, dtype=dtype)
 
     def split(self, x, k, side, trans, beta, out_slices, out_shift):
+        from oracle.oracle import OracleError
         a = x.numpy().T if trans else x.numpy()
-        s = self.port.split(np.ascontiguousarray(a), k, "left" if side == "L" else "right",
-                            force_beta=beta)
+        try:
+            s = self.port.split(np.ascontiguousarray(a), k, "left" if side == "L" else "right",
+                                force_beta=beta)
+        except OracleError:  # line max >= 2^921: flagged like the CUDA backend's split
+            self._range = 1
+            out_slices.zero_()
+            out_shift.zero_()
+            return
         planes = s.slices if side == "L" else s.slices.transpose(0, 2, 1)  # [k][lines][n]
         out_slices.zero_()
         out_slices[:, :, : planes.shape[2]] = torch.from_numpy(np.ascontiguousarray(planes))
         out_shift.copy_(torch.from_numpy(s.shift))
+
+    def range_error(self):
+        r, self._range = getattr(self, "_range", 0), 0
+        return r
 
     def gemm(self, m, n, p, k, beta_bits, a_slices, mu, b_slices, nu, alpha, beta, c):
         from paper_2409_13313_b200.ozmm import compute_r
@@ -152,3 +163,47 @@ def test_grid2d_matches_single_process(world, offset, port):
 
 
 PORT = {(w, o): _free_port() for w in (2, 4, 8) for o in (False, True)}
+
+
+def _range_worker(rank, world, port, bad_rank, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2409_13313_b200.grid2d import Grid2DGemm
+        m, n, p, k = 32, 64, 48, 4
+        G = Grid2DGemm(m, n, p, k, backend=OracleBackend())
+        L = G.L
+        a_rows = torch.ones((L.ms, n), dtype=torch.float64)
+        if rank == bad_rank:
+            a_rows[1, 3] = 2.0 ** 925
+        b_cols = torch.ones((n, L.ps), dtype=torch.float64)
+        c_blk = torch.full((L.mr, L.pcols), 7.0, dtype=torch.float64)
+        try:
+            G.step(a_rows, b_cols, c_blk, 1.0, 0.0, sync_check=True)
+            q.put((rank, "no error", bool((c_blk == 7.0).all())))
+        except OverflowError:
+            q.put((rank, "OverflowError", bool((c_blk == 7.0).all())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,bad", [(4, 3), (8, 5), (4, -1)])
+def test_grid2d_range_error_reaches_every_rank(world, bad):
+    """sync_check: one rank's line max >= 2^921 (the reference throws
+    std::overflow_error before writing, split.cpp:124-125) makes EVERY rank of
+    the grid raise OverflowError before any GEMM, with C untouched."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_range_worker, args=(r, world, port, bad, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    want = "OverflowError" if bad >= 0 else "no error"  # bad = -1: the negative control
+    assert res == [(r, want, bad >= 0) for r in range(world)]
