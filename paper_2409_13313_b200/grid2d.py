@@ -391,7 +391,7 @@ class Grid2DGemm:
             split_b()
             wb = gather_b()  # before the A panels: the collective waits on this stream
 
-        if sync_check:
+        if sync_check and a_panels is None:
             self._check_range_across_grid()
 
         def gather_a():
@@ -415,6 +415,8 @@ class Grid2DGemm:
                     a_split.append((lo, hi, torch.cuda.Event()))
                     a_split[-1][2].record(sp)
                     mark(f"split A {lo}:{hi}")
+                if sync_check:  # after the last panel: A's lines are checked too
+                    self._check_range_across_grid()
                 wa = gather_a()
 
         def sums(a_sl, b_sl):  # line sums of the operand rows / columns a strip reads

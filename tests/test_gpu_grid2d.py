@@ -321,6 +321,18 @@ def test_grid2d_cuda_sync_check_range_error():
     with pytest.raises(OverflowError):
         G.step(a, b, c, 1.0, 0.0, sync_check=True)
     assert bool((c == 7.0).all())
+    # A in panels (the e2e upload order): the bad line sits in the last panel
+    evs = []
+    for lo, hi in ((0, 256), (256, m)):
+        e = torch.cuda.Event()
+        e.record()
+        evs.append((lo, hi, e))
+    bad2 = A.copy()
+    bad2[300, 5] = 2.0 ** 925
+    with pytest.raises(OverflowError):
+        G.step(torch.tensor(bad2, device="cuda"), b, c, 1.0, 0.0, ready={"a": evs},
+               sync_check=True)
+    assert bool((c == 7.0).all())
     want = ozmm.ozaki_gemm(1.0, torch.tensor(A, device="cuda"), b, 0.0, torch.zeros_like(c),
                            ozmm.config_for("ozIMMU_H", k)).cpu().numpy()
     G.step(torch.tensor(A, device="cuda"), b, c, 1.0, 0.0, sync_check=True)
