@@ -169,9 +169,9 @@ def test_gemm_slices_c_write_only():
                 c_write_only=True)
 
 
-def _native_case(trans):
+def _native_case(trans, k=8, n=2500):
     from paper_2409_13313_b200 import ozmm
-    m, n, p, k, alpha, beta = 1024, 2500, 768, 8, 1.25, -0.5
+    m, p, alpha, beta = 1024, 768, 1.25, -0.5
     A = ozmm.gen_phi_matrix(m, n, 1.0, 21)
     B = ozmm.gen_phi_matrix(n, p, 1.0, 22)
     C = ozmm.gen_phi_matrix(m, p, 1.0, 23)
@@ -231,8 +231,10 @@ def test_native_grid_nccl_init():
     assert ozmm.lib.ozmm_grid_destroy(g) == 0
 
 
-@pytest.mark.parametrize("world,trans", [(2, False), (4, False), (8, False), (8, True)])
-def test_native_grid_emulated_ranks(world, trans):
+@pytest.mark.parametrize("world,trans,k,n", [(2, False, 8, 2500), (4, False, 8, 2500),
+                                             (8, False, 8, 2500), (8, True, 8, 2500),
+                                             (2, True, 3, 333), (4, False, 11, 1500)])
+def test_native_grid_emulated_ranks(world, trans, k, n):
     """ozmm_dgemm_2d with W ranks as threads on the one GPU: the all-gather hook
     copies the peers' parts (cudaMemcpy) between barriers.  The native split
     into panel slots, in-place gathers and strips must tile C like the single
@@ -243,7 +245,7 @@ def test_native_grid_emulated_ranks(world, trans):
     import threading
     from paper_2409_13313_b200 import ozmm
     from paper_2409_13313_b200.grid2d import NativeGrid2D, make_layout
-    (m, n, p, k, alpha, beta), want, shard = _native_case(trans)
+    (m, n, p, k, alpha, beta), want, shard = _native_case(trans, k, n)
     cudart = ctypes.CDLL("libcudart.so.12")
     cudart.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
     barriers, pool, lock, errors = {}, {}, threading.Lock(), []
@@ -338,3 +340,29 @@ def test_grid2d_cuda_sync_check_range_error():
     G.step(torch.tensor(A, device="cuda"), b, c, 1.0, 0.0, sync_check=True)
     torch.cuda.synchronize()
     assert np.array_equal(c.cpu().numpy().view(np.uint64), want.view(np.uint64))
+
+
+def test_native_grid_rejects_bad_shapes():
+    """ozmm_dgemm_2d: m or p not divisible by Pr*Pc, and k outside 1..22, are
+    argument / config errors (no launch)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import ctypes
+    from paper_2409_13313_b200 import ozmm
+    hook = ozmm.ALLGATHER_FN(lambda *a: 0)
+    h = ozmm.Handle(0)
+    g = ctypes.c_void_p()
+    assert ozmm.lib.ozmm_grid_create(h.h, 0, 4, 1, None, ctypes.cast(hook, ctypes.c_void_p),
+                                     None, ctypes.byref(g)) == 0
+    x = torch.zeros(64, 64, dtype=torch.float64, device="cuda")
+    args = lambda m, p, k: (g, b"N", b"N", m, 64, p, 1.0, x.data_ptr(), 64, x.data_ptr(),  # noqa
+                            64, 0.0, x.data_ptr(), 64, k)
+    assert ozmm.lib.ozmm_dgemm_2d(*args(66, 64, 8)) == ozmm.OZMM_ERR_ARG
+    assert b"divisible" in ozmm.lib.ozmm_grid_last_error()
+    assert ozmm.lib.ozmm_dgemm_2d(*args(64, 62, 8)) == ozmm.OZMM_ERR_ARG
+    assert ozmm.lib.ozmm_dgemm_2d(*args(64, 64, 23)) == ozmm.OZMM_ERR_CONFIG
+    # world > 1 without an id or a hook
+    g2 = ctypes.c_void_p()
+    assert ozmm.lib.ozmm_grid_create(h.h, 0, 2, 0, None, None, None,
+                                     ctypes.byref(g2)) == ozmm.OZMM_ERR_ARG
+    assert ozmm.lib.ozmm_grid_destroy(g) == 0
