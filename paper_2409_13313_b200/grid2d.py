@@ -509,8 +509,11 @@ class Grid2DGemm:
             for lo, hi in _other_ranges(L.mr, r0, L.ms):
                 g3(lo, hi)
         else:
-            pieces = [(a, min(a + L.ms, hi)) for lo, hi in _other_ranges(L.mr, r0, L.ms)
-                      for a in range(lo, hi, L.ms)]
+            # half a peer's rows per piece: a shorter D2H tail (grid_g3_split.txt:
+            # 2x2 41 -> 38.8 ms, 2x4 21.6 -> 21.2 ms); OZMM_GRID_G3_SPLIT overrides
+            size = max(256, L.ms // int(os.environ.get("OZMM_GRID_G3_SPLIT", "2")))
+            pieces = [(a, min(a + size, hi)) for lo, hi in _other_ranges(L.mr, r0, L.ms)
+                      for a in range(lo, hi, size)]
             for i, (lo, hi) in enumerate(pieces):
                 if i % 2 and side:
                     with be.side_stream(after_current=False):
