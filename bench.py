@@ -359,8 +359,10 @@ def main():
             ev = {key: torch.cuda.Event() for key in "abc"}
             # B first, then A in row panels: B's split and gather, and the first
             # strip of each A panel, run while the rest of A is still crossing PCIe
-            a_pieces = [(lo, min(lo + max(256, L.ms // 4), L.ms))
-                        for lo in range(0, L.ms, max(256, L.ms // 4))]
+            # panels of ms/8 rows, at least 512 (tools/rank_timing.py --a-panels:
+            # profiles/r1/grid_a_panels.txt)
+            psz = max(512, L.ms // 8)
+            a_pieces = [(lo, min(lo + psz, L.ms)) for lo in range(0, L.ms, psz)]
             a_ev = [torch.cuda.Event() for _ in a_pieces]
             ev["a"] = [(lo, hi, e) for (lo, hi), e in zip(a_pieces, a_ev)]
 

@@ -47,6 +47,8 @@ def main():
     ap.add_argument("--native", action="store_true",
                     help="also time the native C-ABI grid entry (ozmm_dgemm_2d) with the same "
                          "emulated all-gather as a hook")
+    ap.add_argument("--a-panels", type=int, default=0,
+                    help="--e2e: A row panels per rank (0: bench.py's rule, ms/8 rows, >= 512)")
     ap.add_argument("--e2e", action="store_true",
                     help="also time the rank's end-to-end step (pinned H2D of its shard, step, "
                          "D2H of its C block): C rows streamed back per strip (c_host) against "
@@ -158,8 +160,8 @@ def main():
             ev = {key: torch.cuda.Event() for key in "abc"}
             # B first, then A in row panels: B's split and gather, and the first
             # strip of each A panel, run while the rest of A is still crossing PCIe
-            a_pieces = [(lo, min(lo + max(256, L.ms // 4), L.ms))
-                        for lo in range(0, L.ms, max(256, L.ms // 4))]
+            psz = max(256, L.ms // args.a_panels) if args.a_panels else max(512, L.ms // 8)
+            a_pieces = [(lo, min(lo + psz, L.ms)) for lo in range(0, L.ms, psz)]
             a_ev = [torch.cuda.Event() for _ in a_pieces]
             ev["a"] = [(lo, hi, e) for (lo, hi), e in zip(a_pieces, a_ev)]
 
