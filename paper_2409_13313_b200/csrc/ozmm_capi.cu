@@ -1153,7 +1153,14 @@ int ozmm_dgemm_ex(ozmm_handle_t handle, char transa, char transb, int64_t m, int
   }
   // B's column maxima (an HBM-bound pass) run on a side stream beside A's row
   // split (issue-bound) when A is split by rows and B by columns
-  const bool overlap_colmax = offset && !is_trans(transa) && !is_trans(transb);
+  // OZMM_SPLIT_OVERLAP: 2 (default) B's whole column split on the side stream,
+  // 1 only its column maxima, 0 none (A/B switch)
+  static const int split_overlap = [] {
+    const char* e = std::getenv("OZMM_SPLIT_OVERLAP");
+    return e ? std::atoi(e) : 2;
+  }();
+  const bool overlap_colmax = offset && !is_trans(transa) && !is_trans(transb) && split_overlap > 0;
+  const bool overlap_bsplit = overlap_colmax && split_overlap > 1;
   if (overlap_colmax) {
     if (!h->s_aux) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->s_aux, cudaStreamNonBlocking));
     if (!h->ev_fork) CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
@@ -1162,7 +1169,10 @@ int ozmm_dgemm_ex(ozmm_handle_t handle, char transa, char transb, int64_t m, int
     CUDA_TRY(h, cudaEventRecord(h->ev_fork, user));
     CUDA_TRY(h, cudaStreamWaitEvent(h->s_aux, h->ev_fork, 0));
     h->stream = h->s_aux;
-    const int rc = launch_colmax(h, p, n, B, ldb);
+    int rc = launch_colmax(h, p, n, B, ldb);
+    if (!rc && overlap_bsplit)  // split B (Right, columns) -- scheme.cpp:251
+      rc = launch_split(h, false, p, n, B, ldb, k, beta_bits, h->slices_b, lds, p * lds, out_b,
+                        h->lsb, p, 1, true);
     h->stream = user;
     if (rc) return rc;
     CUDA_TRY(h, cudaEventRecord(h->ev_join, h->s_aux));
@@ -1180,9 +1190,10 @@ int ozmm_dgemm_ex(ozmm_handle_t handle, char transa, char transb, int64_t m, int
   // split B (Right, columns of op(B)) -- scheme.cpp:251
   if (offset) {
     if (overlap_colmax) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_join, 0));
-    if (int rc = launch_split(h, is_trans(transb), p, n, B, ldb, k, beta_bits, h->slices_b, lds,
-                              p * lds, out_b, h->lsb, p, 1, overlap_colmax))
-      return rc;
+    if (!overlap_bsplit)
+      if (int rc = launch_split(h, is_trans(transb), p, n, B, ldb, k, beta_bits, h->slices_b,
+                                lds, p * lds, out_b, h->lsb, p, 1, overlap_colmax))
+        return rc;
   } else if (int rc = launch_split_m(h, mc.strategy, is_trans(transb), p, n, B, ldb, k, beta_bits,
                                      h->slices_b, lds, p * lds, out_b)) {
     return rc;
