@@ -74,7 +74,7 @@ def parse():
     ap.add_argument("--k", type=int, default=8)
     ap.add_argument("--phi", type=float, default=0.5)
     ap.add_argument("--tile-n", type=int, default=0)
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cublas", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
