@@ -1,0 +1,8 @@
+# A-operand collector reuse (OZMM_ACOLL=1: K-step-major issue within an A group, collector::a fill/use/lastuse) vs 0
+j() { python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(round(d['value'],2))"; }
+B="python bench.py --no-cpu --no-cublas --no-e2e --steps 4 --warmup 2"
+for shape in "" "--m 8192 --n 8192 --p 8192" "--k 12 --phi 4" "--m 8192 --n 65536 --p 8192"; do
+  line="shape [$shape]:"
+  for v in 0 1 0 1; do line="$line acoll$v $(OZMM_ACOLL=$v $B $shape 2>/dev/null | j)"; done
+  echo "$line"
+done
