@@ -61,6 +61,7 @@ struct GemmParams {
   int dup_mma;         // experiment hook (OZMM_DUP_MMA): repeat each product's MMAs (timing only)
   uint64_t* tile_trace;  // optional [tiles][8] globaltimer stamps of each leader CTA (OZMM_TILE_TRACE)
   int group_pairs;     // CTA-pair kernel: issue A groups two at a time (OZMM_GROUP_PAIRS)
+  int kpair;           // CTA-pair kernel: thin passes take K blocks in pairs (OZMM_KPAIR)
   // Offset-binary operands (CTA-pair kernel only; slicer.cuh): the slice planes
   // hold slice + o_s (o_1 = 2^beta - 1, o_s = 2^(beta-1)) as u8 and the MMAs run
   // u8 x u8.  For a chunk c the accumulator then holds, mod 2^32,

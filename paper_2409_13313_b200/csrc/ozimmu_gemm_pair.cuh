@@ -143,6 +143,38 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
       for (int q = 0; q < P.npass; ++q) {
         const int blo = P.p_blo[q], bhi = P.p_bhi[q], g0 = P.p_g0[q], g1 = P.p_g1[q];
         const uint32_t btx = 2u * (bhi - blo + 1) * Cfg::kBTile;
+        const int nbw = bhi - blo + 1;
+        if (kPairs == 1 && P.kpair && 2 * nbw <= Cfg::kMaxBSlots && n_kb % 2 == 0) {
+          // K-pair pass: one B buffer holds K blocks kb and kb+1; each A group loads
+          // both of its K blocks into consecutive ring slots
+          for (int kb = 0; kb < n_kb; kb += 2) {
+            ptx::mbar_wait(b_empty + bi, bph ^ 1);
+            const uint32_t fb = ptx::mapa_shared(b_full + bi, lead_rank);
+            if (leader) ptx::mbar_arrive_expect_tx(b_full + bi, 2u * btx);
+            uint8_t* dst = bbuf + bi * Cfg::kBBuf;
+            for (int h = 0; h < 2; ++h)
+              for (int t = blo; t <= bhi; ++t)
+                ptx::tma_load_3d_pair_hint(dst + (h * nbw + t - blo) * Cfg::kBTile, &map_b, fb,
+                                           (kb + h) * kKB, b_row, t - 1, pol_b);
+            if (++bi == kBBufs) {
+              bi = 0;
+              bph ^= 1;
+            }
+            for (int g = g0; g < g1; ++g)
+              for (int h = 0; h < 2; ++h) {
+                ptx::mbar_wait(a_empty + ai, aph ^ 1);
+                const uint32_t fa = ptx::mapa_shared(a_full + ai, lead_rank);
+                if (leader) ptx::mbar_arrive_expect_tx(a_full + ai, 2u * Cfg::kATile);
+                ptx::tma_load_3d_pair_hint(aring + ai * Cfg::kATile, &map_a, fa, (kb + h) * kKB,
+                                           a_row, P.ag_s[g] - 1, pol_a);
+                if (++ai == n_a) {
+                  ai = 0;
+                  aph ^= 1;
+                }
+              }
+          }
+          continue;
+        }
         for (int kb = 0; kb < n_kb; ++kb) {
           ptx::mbar_wait(b_empty + bi, bph ^ 1);
           {
@@ -187,6 +219,57 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
         ptx::tc_fence_after();
         for (int q = P.b_pass0[b]; q < P.b_pass1[b]; ++q) {
           const int blo = P.p_blo[q], g0 = P.p_g0[q], g1 = P.p_g1[q];
+          const int nbw = P.p_bhi[q] - blo + 1;
+          if (kPairs == 1 && P.kpair && 2 * nbw <= Cfg::kMaxBSlots && n_kb % 2 == 0) {
+            // K-pair pass: each product's MMAs for K blocks kb and kb+1 back to
+            // back -- runs of 8 MMAs on one accumulator instead of 4
+            for (int kb = 0; kb < n_kb; kb += 2) {
+              ptx::mbar_wait(b_full + bi, bph);
+              ptx::tc_fence_after();
+              if (trace && kb == 0 && q == P.b_pass0[b] && b < 2 && lane == 0) trace[2 + 2 * b] = ptx::globaltimer();
+              const uint64_t bdesc0 = ptx::smem_desc(ptx::smem_u32(bbuf + bi * Cfg::kBBuf), 1024, 2);
+              const uint32_t bstep = (nbw * Cfg::kBTile) >> 4;  // K block kb+1's tiles
+              for (int g = g0; g < g1; ++g) {
+                const int s1 = ai + 1 == n_a ? 0 : ai + 1;
+                const uint32_t ph1 = ai + 1 == n_a ? aph ^ 1 : aph;
+                ptx::mbar_wait(a_full + ai, aph);
+                ptx::mbar_wait(a_full + s1, ph1);
+                ptx::tc_fence_after();
+                if (ptx::elect_one()) {
+                  const uint64_t ad0 = ptx::smem_desc(ptx::smem_u32(aring + ai * Cfg::kATile), 1024, 2);
+                  const uint64_t ad1 = ptx::smem_desc(ptx::smem_u32(aring + s1 * Cfg::kATile), 1024, 2);
+                  for (int pr = P.ag_p0[g]; pr < P.ag_p1[g]; ++pr) {
+                    const uint32_t info = P.pr_info[pr];
+                    const uint64_t bdesc = bdesc0 + (info & 0xFFFFu);
+                    const uint32_t d = tmem_base + ((info >> 16) & 0x7Fu) * kBN;
+                    const bool first = kb == 0 && (info >> 24);
+#pragma unroll
+                    for (int j = 0; j < kKB / kBK; ++j)
+                      ptx::mma_i8_pair(d, ad0 + 2 * j, bdesc + 2 * j, idesc,
+                                       (first && j == 0) ? 0u : 1u);
+#pragma unroll
+                    for (int j = 0; j < kKB / kBK; ++j)
+                      ptx::mma_i8_pair(d, ad1 + 2 * j, bdesc + bstep + 2 * j, idesc, 1u);
+                  }
+                  ptx::mma_commit_pair(a_empty + ai, all_mask);
+                  ptx::mma_commit_pair(a_empty + s1, all_mask);
+                }
+                __syncwarp();
+                for (int h = 0; h < 2; ++h)
+                  if (++ai == n_a) {
+                    ai = 0;
+                    aph ^= 1;
+                  }
+              }
+              if (ptx::elect_one()) ptx::mma_commit_pair(b_empty + bi, pair_mask);
+              __syncwarp();
+              if (++bi == kBBufs) {
+                bi = 0;
+                bph ^= 1;
+              }
+            }
+            continue;
+          }
           for (int kb = 0; kb < n_kb; ++kb) {
             ptx::mbar_wait(b_full + bi, bph);
             ptx::tc_fence_after();

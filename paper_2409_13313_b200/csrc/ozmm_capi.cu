@@ -400,6 +400,11 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
   // group per round; three per round starve the producer (tools/gpairs_probe*.sh)
   P.group_pairs = 2;
   if (const char* g = std::getenv("OZMM_GROUP_PAIRS")) P.group_pairs = std::atoi(g);
+  // thin passes in K-block pairs (runs of 8 MMAs per accumulator): +4 % at C5
+  // (k = 12), +1 % at C4, but -3 % at the two-batch C3 where the power cap takes the
+  // gain back (profiles/r1/kpair_ab.txt) -- on for schedules of three or more batches
+  P.kpair = S.batches.size() >= 3 ? 1 : 0;
+  if (const char* g = std::getenv("OZMM_KPAIR")) P.kpair = std::atoi(g);
   if (const char* g = std::getenv("OZMM_IDESC_XOR")) P.idesc_xor = static_cast<uint32_t>(std::strtoul(g, nullptr, 0));
   P.nbatch = static_cast<int>(S.batches.size());
   P.npass = static_cast<int>(S.passes.size());
