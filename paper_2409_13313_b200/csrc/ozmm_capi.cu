@@ -403,7 +403,8 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
   // thin passes in K-block pairs (runs of 8 MMAs per accumulator): +4 % at C5
   // (k = 12), +1 % at C4, but -3 % at the two-batch C3 where the power cap takes the
   // gain back (profiles/r1/kpair_ab.txt) -- on for schedules of three or more batches
-  P.kpair = S.batches.size() >= 3 ? 1 : 0;
+  // and for C blocks up to 8192 x 8192 (C2 +2 %)
+  P.kpair = (S.batches.size() >= 3 || m * p <= int64_t(8192) * 8192) ? 1 : 0;
   if (const char* g = std::getenv("OZMM_KPAIR")) P.kpair = std::atoi(g);
   if (const char* g = std::getenv("OZMM_IDESC_XOR")) P.idesc_xor = static_cast<uint32_t>(std::strtoul(g, nullptr, 0));
   P.nbatch = static_cast<int>(S.batches.size());
