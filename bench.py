@@ -23,8 +23,14 @@ JSON line keys (one line, rank 0):
       launch / its CUDA-event duration vs the INT8 peak;
   cpu_baseline -- the unmodified reference (oracle/_ref) on the host cores,
       on a bounded sub-block sample of the same problem;
+  parity -- after the timed loop, a 128 x 128 sample of the TIMED output (rows
+      and columns spread over every tile row / column) against the reference
+      (oracle/_ref) on A(I,:) B(:,J), bit for bit (sub-block locality); the
+      checker runs outside every timed region;
   cublas_dgemm -- native FP64 DGEMM (torch.matmul -> cuBLAS) on the same
-      device buffers, for context (not on our path).
+      device buffers, for context (not on our path), plus cuBLASLt's INT8
+      GEMM at 16384^3, burst and sustained (>= 2 s back to back): the measured
+      INT8 denominator (roofline.peak_int8_measured).
 """
 from __future__ import annotations
 
@@ -78,6 +84,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cublas", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-pageable", action="store_true")
+    ap.add_argument("--int8-seconds", type=float, default=2.0)
     ap.add_argument("--grid", action="store_true",
                     help="use the 2-D sharded path (grid2d) even at N=1")
     ap.add_argument("--cpu-sample", type=int, default=1024,
@@ -143,25 +152,48 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ reference arm
-def cpu_reference(m_s, n, p_s, k, phi, steps, warmup, threads=None):
+def host_cpu_info():
+    """lscpu model, core count and AVX-512 VNNI presence (the reference picks its
+    VNNI INT8 kernel at run time, int_gemm.cpp:169-173)."""
+    model, flags = None, ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name") and model is None:
+                    model = line.split(":", 1)[1].strip()
+                elif line.startswith("flags") and not flags:
+                    flags = line.split(":", 1)[1]
+    except OSError:
+        pass
+    return {"model": model, "nproc": os.cpu_count(), "avx512_vnni": "avx512_vnni" in flags.split(),
+            "amx_int8": "amx_int8" in flags.split()}
+
+
+def cpu_reference(m_s, n, p_s, k, phi, steps, warmup, threads=None, full_p=None):
     """The reference CPU implementation (oracle/_ref, else the C port) on a
     bounded sub-block: rows 0..m_s of A, columns 0..p_s of B of the n=16384
-    problem (sub-block locality: identical per-entry work and results)."""
+    problem (sub-block locality: identical per-entry work and results).
+    Inputs come from the reference's own generator (gen_phi_matrix through the
+    checker library): rows 0..m_s of A directly, B's columns out of the whole
+    n x full_p matrix -- no code of the product is loaded on this arm."""
     from oracle import oracle as orc  # checker/baseline only (bench cpu leg)
     lib = orc.best()
     if threads:
         lib.set_threads(threads)
-    from paper_2409_13313_b200 import ozmm
-    A = ozmm.gen_phi_block(m_s, n, phi, ozmm.counter_hash(0, 1))
-    B = ozmm.gen_phi_block(n, p_s, phi, ozmm.counter_hash(0, 2))
+    full_p = full_p or p_s
+    t_gen = time.perf_counter()
+    A = lib.gen_phi_matrix(m_s, n, phi, lib.counter_hash(0, 1))
+    B = np.ascontiguousarray(lib.gen_phi_matrix(n, full_p, phi, lib.counter_hash(0, 2))[:, :p_s])
+    t_gen = time.perf_counter() - t_gen
     C = np.zeros((m_s, p_s))
-    times = []
+    times, phases = [], []
     for it in range(warmup + steps):
         t0 = time.perf_counter()
-        lib.gemm(1.0, A, B, 0.0, C, k=k)
+        _, info = lib.gemm(1.0, A, B, 0.0, C, k=k, with_info=True)
         dt = time.perf_counter() - t0
         if it >= warmup:
             times.append(dt)
+            phases.append(info["timings"])
     t = sum(times) / len(times)
     return {
         "value": 2.0 * m_s * n * p_s / t / 1e12,
@@ -172,6 +204,9 @@ def cpu_reference(m_s, n, p_s, k, phi, steps, warmup, threads=None):
                   f"(rows/cols of the m=n=p={n} problem, phi={phi}); {len(times)} timed call(s), "
                   f"{t:.2f} s each",
         "seconds_per_call": t,
+        "phase_timings_s": {key: sum(ph[key] for ph in phases) / len(phases) for key in phases[0]},
+        "host": host_cpu_info(),
+        "input_gen_s": t_gen,
     }
 
 
@@ -182,7 +217,7 @@ def run_reference_arm(args, rank, world):
     ms = args.cpu_sample
     # bounded: a few seconds per step on the box's host cores
     steps, warm = max(1, min(args.steps, 3)), min(args.warmup, 1)
-    cb = cpu_reference(ms, args.n, ms, k, args.phi, steps, warm)
+    cb = cpu_reference(ms, args.n, ms, k, args.phi, steps, warm, full_p=args.p)
     line = {
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
         "n_gpus": world, "steps": steps, "warmup": warm,
@@ -192,7 +227,8 @@ def run_reference_arm(args, rank, world):
         "config": {"workload": f"C3 m=n=p={args.n}, k={k}, phi={args.phi}, alpha=1, beta=0; "
                                f"CPU sample = {ms}x{args.n}x{ms} sub-block",
                    "m": args.m, "n": args.n, "p": args.p, "k": k},
-        "cpu_baseline": {kk: cb[kk] for kk in ("value", "unit", "cores", "kind", "sample")},
+        "cpu_baseline": {kk: cb[kk] for kk in ("value", "unit", "cores", "kind", "sample",
+                                                 "phase_timings_s", "host")},
         "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -200,6 +236,80 @@ def run_reference_arm(args, rank, world):
 
 
 # ----------------------------------------------------------------------- our arm
+def spread(total, count, rng):
+    """`count` distinct sorted indices, one per stratum of [0, total); first and last
+    included -- at 128 of 16384 that hits every 256-row pair tile row (twice) and
+    every 128-column tile."""
+    edges = np.linspace(0, total, count + 1).astype(np.int64)
+    idx = np.array([rng.integers(lo, hi) for lo, hi in zip(edges[:-1], edges[1:])])
+    idx[0], idx[-1] = 0, total - 1
+    return idx
+
+
+def parity_sample(ozmm, out_dev, m, n, p, k, phi, alpha, beta, row0=0, col0=0, rows_blk=None,
+                  cols_blk=None, count=128):
+    """Bit-exact check of a count x count sample of the timed output against the
+    reference (oracle/_ref; the C port where it is absent) on A(I,:) B(:,J) -- the
+    checker, outside every timed region.  out_dev is this rank's C block starting
+    at global (row0, col0).  A's rows and B's columns are regenerated on the host
+    with the same generator and seeds (generate.cpp:11-29)."""
+    from oracle import oracle as orc  # checker only (never the measured path)
+    t0 = time.perf_counter()
+    lib = orc.best()
+    rng = np.random.default_rng(20261017)
+    rows = spread(rows_blk or m, count, rng)
+    cols = spread(cols_blk or p, count, rng)
+    import torch
+    ri = torch.from_numpy(rows).to(out_dev.device)
+    ci = torch.from_numpy(cols).to(out_dev.device)
+    got = out_dev[ri][:, ci].cpu().numpy()
+    sa, sb = ozmm.counter_hash(0, 1), ozmm.counter_hash(0, 2)
+    A = np.concatenate([ozmm.gen_phi_block(m, n, phi, sa, row0 + int(r), 1, 0, n) for r in rows])
+    B = np.concatenate([ozmm.gen_phi_block(n, p, phi, sb, 0, n, col0 + int(c), 1) for c in cols],
+                       axis=1)
+    want = lib.gemm(alpha, A, B, beta, np.zeros((count, count)), k=k)
+    mism = int((got.view(np.uint64) != want.view(np.uint64)).sum())
+    return {"entries": count * count, "mismatches": mism, "oracle": lib.kind,
+            "sample": f"{count} rows x {count} columns of the timed output, one per stratum "
+                      f"(first and last included), vs ozaki_gemm_ex on A(I,:) B(:,J)",
+            "check_s": time.perf_counter() - t0}
+
+
+def int8_denominator(dev, stream, seconds=2.0):
+    """cuBLASLt's own dense INT8 GEMM (torch._int_mm, s8 x s8 -> s32) at 16384^3 on
+    uniform random int8: best single launch (burst) and back to back for >= `seconds`
+    (sustained, the power-capped figure a long kernel meets)."""
+    import torch
+    N = 16384
+    a8 = torch.randint(-128, 128, (N, N), dtype=torch.int8, device=dev)
+    b8 = torch.randint(-128, 128, (N, N), dtype=torch.int8, device=dev).t()
+    torch._int_mm(a8, b8)
+    ops = 2.0 * N ** 3
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    best = None
+    for _ in range(8):
+        ev[0].record(stream)
+        torch._int_mm(a8, b8)
+        ev[1].record(stream)
+        torch.cuda.synchronize()
+        t = ev[0].elapsed_time(ev[1])
+        best = t if best is None else min(best, t)
+    total_ms, launches = 0.0, 0
+    while total_ms < seconds * 1e3:
+        ev[0].record(stream)
+        for _ in range(50):
+            torch._int_mm(a8, b8)
+        ev[1].record(stream)
+        torch.cuda.synchronize()
+        total_ms += ev[0].elapsed_time(ev[1])
+        launches += 50
+    del a8, b8
+    return {"burst_tops": ops / (best * 1e-3) / 1e12,
+            "sustained_tops": ops * launches / (total_ms * 1e-3) / 1e12,
+            "sustained_s": total_ms * 1e-3, "shape": f"{N}^3", "data": "uniform random int8",
+            "kernel": "cuBLASLt via torch._int_mm (s8 x s8 -> s32)"}
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -219,8 +329,11 @@ def main():
         os.environ.setdefault("MASTER_PORT", "29517")
         os.environ.setdefault("RANK", str(rank))
         os.environ.setdefault("WORLD_SIZE", str(world))
-        # NCCL's version banner goes to stdout; keep stdout to the one JSON line
-        os.environ["NCCL_DEBUG"] = os.environ.get("OZMM_NCCL_DEBUG", "WARN")
+        # NCCL's communicator lines (nranks, NVLS / ring setup) go to stderr, where
+        # the driver can check the rank count; stdout stays the one JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     m, n, p, k, phi = args.m, args.n, args.p, args.k, args.phi
     dev = torch.device("cuda", local)
@@ -255,7 +368,8 @@ def main():
             if timed:
                 gemm_ms.append(res.timings.int_gemm * 1e3)
             return res
-        launches_per_step = 4  # slice_rows(A), colmax(B), slice_cols(B), fused GEMM
+        # flag fold, slice_rows(A), colmax(B), slice_cols(B), fused GEMM
+        launches_per_step = 5
     else:
         from paper_2409_13313_b200.grid2d import Backend, Grid2DGemm
         be = Backend(local)
@@ -295,6 +409,18 @@ def main():
     flops = 2.0 * m * n * p
     value = flops / (t_step * 1e-3) / 1e12
 
+    # parity of the timed output (rank 0's C block), checker outside the timed region
+    parity = None
+    if rank == 0 and not args.no_parity:
+        try:
+            if use_grid:
+                parity = parity_sample(ozmm, C, m, n, p, k, phi, 1.0, 0.0, L.c_row0, L.c_col0,
+                                       L.mr, L.pcols)
+            else:
+                parity = parity_sample(ozmm, C, m, n, p, k, phi, 1.0, 0.0)
+        except Exception as ex:  # reported, never hidden
+            parity = {"error": str(ex)[:300]}
+
     # dominant kernel time (the fused GEMM) for the roofline
     if use_grid:
         torch.cuda.synchronize()
@@ -328,7 +454,7 @@ def main():
             traffic = tj.get("dram_bytes_per_launch")
 
     # ---- e2e through the host-pointer C ABI (reference calling convention)
-    e2e = None
+    e2e = e2e_pg = None
     if not args.no_e2e:
         es = max(1, args.e2e_steps)
         if not use_grid:
@@ -349,6 +475,25 @@ def main():
             for _ in range(es):
                 e2e_call()
             t_e2e = (time.perf_counter() - t0) / es
+            # the drop-in's real callers (Eigen, numpy) pass pageable memory
+            if not args.no_pageable:
+                pA, pB, pC = np.array(npA), np.array(npB), np.array(npC)
+
+                def e2e_pageable():
+                    h.check(ozmm.lib.ozmm_dgemm_host(
+                        h.h, b"N", b"N", m, n, p, 1.0, pA.ctypes.data, n, pB.ctypes.data, p,
+                        0.0, pC.ctypes.data, p, k, ctypes.byref(opt), ctypes.byref(cnt), None))
+                e2e_pageable()
+                t0 = time.perf_counter()
+                for _ in range(2):
+                    e2e_pageable()
+                t_pg = (time.perf_counter() - t0) / 2
+                e2e_pg = {"value": 2.0 * m * n * p / t_pg / 1e12, "unit": UNIT,
+                          "ms_per_step": t_pg * 1e3,
+                          "api": "ozmm_dgemm_host (host pointers, pageable numpy arrays)",
+                          "same_output_as_pinned": bool(np.array_equal(pC.view(np.uint64),
+                                                                       npC.view(np.uint64)))}
+                del pA, pB, pC
             h.set_stream(stream.cuda_stream)
             # beta = 0 with alpha > 0: the host entry does not upload C (its
             # non-finite entries are patched on the host); A and B cross PCIe
@@ -414,28 +559,18 @@ def main():
         torch.cuda.synchronize()
         t_cb = c0.elapsed_time(c1) / 3
         cublas = {"tflops": flops / (t_cb * 1e-3) / 1e12, "ms": t_cb}
-        # INT8 tensor-core context: cuBLASLt s8xs8->s32 GEMM
+        del out
+        # the measured INT8 denominator: cuBLASLt s8 x s8 -> s32 at 16384^3
         try:
-            a8 = torch.randint(-64, 64, (8192, 8192), dtype=torch.int8, device=dev)
-            b8 = torch.randint(-64, 64, (8192, 8192), dtype=torch.int8, device=dev).t()
-            for _ in range(2):
-                torch._int_mm(a8, b8)
-            torch.cuda.synchronize()
-            c0.record(stream)
-            for _ in range(5):
-                torch._int_mm(a8, b8)
-            c1.record(stream)
-            torch.cuda.synchronize()
-            cublas["int8_cublaslt_tops_8192"] = 2 * 8192 ** 3 / (c0.elapsed_time(c1) / 5e3) / 1e12
+            cublas["int8_cublaslt"] = int8_denominator(dev, stream, args.int8_seconds)
         except Exception as ex:  # context only
             cublas["int8_cublaslt_error"] = str(ex)[:120]
-        del out
 
     # ---- CPU baseline (rank 0, N=1): the reference on the host cores
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cb = cpu_reference(args.cpu_sample, n, args.cpu_sample, k, phi, 1, 0)
+            cb = cpu_reference(args.cpu_sample, n, args.cpu_sample, k, phi, 1, 0, full_p=p)
             cpu = {kk: cb[kk] for kk in ("value", "unit", "cores", "kind", "sample")}
         except Exception as ex:
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
@@ -443,6 +578,16 @@ def main():
 
     if rank == 0:
         pr, pc = (G.L.pr, G.L.pc) if use_grid else (1, 1)
+        i8 = (cublas or {}).get("int8_cublaslt") or {}
+        roof_extra = {}
+        if i8:
+            roof_extra = {
+                "peak_int8_measured": i8["sustained_tops"],
+                "frac_of_int8_measured": achieved / i8["sustained_tops"],
+                "peak_int8_measured_burst": i8["burst_tops"],
+                "peak_int8_measured_source": "cuBLASLt dense INT8 GEMM 16384^3 on this box, "
+                                             f"sustained over {i8['sustained_s']:.1f} s (see "
+                                             "cublas_dgemm.int8_cublaslt)"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
@@ -457,6 +602,8 @@ def main():
                        "l2": "inputs larger than L2 (3 x 8*16384^2 B = 6.4 GB vs 126 MB)",
                        "tile": f"single-CTA 128x{args.tile_n}" if args.tile_n else "CTA pair 256x128"},
             "e2e": e2e,
+            "e2e_pageable": e2e_pg,
+            "parity": parity,
             "gpu_launches": launches_per_step * args.steps,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": int8_peak,
                          "unit": "TFLOP/s", "frac": achieved / int8_peak, "traffic": traffic,
@@ -467,7 +614,7 @@ def main():
                                         " dense INT8 = 2 x dense BF16 on B200; kernel timed inside"
                                         " a long power-capped loop",
                          "frac_of_burst": achieved / int8_peak_burst,
-                         "frac_of_spec_4500": achieved / SPEC_INT8_TOPS},
+                         "frac_of_spec_4500": achieved / SPEC_INT8_TOPS, **roof_extra},
             "step_roofline": {
                 "spec": step_roofline(m, n, p, k, False, t_step, SPEC_INT8_TOPS, SPEC_HBM_GBS),
                 "measured": step_roofline(m, n, p, k, False, t_step, int8_peak, pk["hbm_gbs"]),

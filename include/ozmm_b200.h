@@ -52,14 +52,18 @@ extern "C" {
  *                          split.cpp:34-36, :212-214)   -> OZMM_ERR_ARG
  *   ConfigError (scheme.hpp:20-22, scheme.cpp:162)      -> OZMM_ERR_CONFIG
  *   std::overflow_error (row max >= 2^921, split.cpp:124-125) -> OZMM_ERR_RANGE
- *   OverflowError (INT32 chunk overflow, int_gemm.hpp:15-26; unreachable with
- *                  the derived r, reachable only via force_r) -> not detected
- *                  on the GPU: the tensor core wraps like OverflowMode::Wrapping. */
+ *   OverflowError (INT32 chunk overflow in OverflowMode::Checked,
+ *                  int_gemm.hpp:13-26, int_gemm.cpp:37-59; unreachable with
+ *                  the derived beta and r, reachable through force_beta /
+ *                  force_r)                              -> OZMM_ERR_OVERFLOW
+ *                  (ozmm_options_t.overflow_wrap = 1 selects Wrapping, which
+ *                  is what the tensor core does: sums mod 2^32). */
 typedef enum {
   OZMM_OK = 0,
   OZMM_ERR_ARG = 1,
   OZMM_ERR_CONFIG = 2,
   OZMM_ERR_RANGE = 3,
+  OZMM_ERR_OVERFLOW = 4,
   OZMM_ERR_CUDA = 5,
   OZMM_ERR_NCCL = 6,
   OZMM_ERR_UNSUPPORTED = 7,
@@ -112,9 +116,25 @@ typedef struct {
                               epilogue; same results, less tensor-core power);
                               1 = keep the reference's signed int8 planes */
   int c_write_only;        /* slice-level GEMMs only: C is output only (not read).
-                              Valid only with beta == 0 and a C free of inf/NaN, where
-                              fl(beta*c) = 0 changes nothing; ozmm_gemm_slices*
-                              reject it with beta != 0 */
+                              Valid only with beta == 0, alpha > 0 and a C free of
+                              inf/NaN, where fl(alpha*d) + fl(beta*c) = fl(alpha*d)
+                              bit for bit (alpha <= 0 could need the sign of a zero
+                              from fl(beta*c)); ozmm_gemm_slices* reject it otherwise */
+  int overflow_wrap;       /* OverflowMode (int_gemm.hpp:13).  0 = Checked, the
+                              reference's default (SchemeConfig, scheme.hpp:28): when
+                              force_beta / force_r make an INT32 chunk overflow
+                              possible, the running chunk sums are verified exactly
+                              (int64, after every product, in the reference's order,
+                              int_gemm.cpp:37-59) before C is written, and a sum
+                              outside INT32 returns OZMM_ERR_OVERFLOW with C
+                              untouched.  1 = Wrapping (sums mod 2^32, the tensor
+                              core's own behaviour; no verification). */
+  int kpair;               /* tuning, same results: 0 = auto, 1 = off, 2 = on --
+                              thin passes of the CTA-pair kernel in K-block pairs */
+  int stages;              /* tuning, same results: 0 = auto, else the A-ring depth
+                              of the CTA-pair kernel (clamped to what fits, >= 2) */
+  int host_panels;         /* tuning, same results (ozmm_dgemm_host): 0 = auto (16)
+                              row panels of op(A) / column panels of op(B) */
 } ozmm_options_t;
 
 /* Scheme presets (config_for, scheme.cpp:137-159) plus the two other valid
@@ -126,7 +146,8 @@ enum {
   OZMM_METHOD_OZIMMU_RN = 2,           /* RN per slice + per-product */
   OZMM_METHOD_OZIMMU_EF = 3,           /* bitmask + group-wise */
   OZMM_METHOD_RN_CONST_PER_PRODUCT = 4,/* RN const shift + per-product */
-  OZMM_METHOD_OZIMMU_H_SIMPLE = 5      /* RN const shift + GroupwiseSimple (needs r >= k) */
+  OZMM_METHOD_OZIMMU_H_SIMPLE = 5,     /* RN const shift + GroupwiseSimple (needs r >= k) */
+  OZMM_METHOD_OZIMMU_EF_SIMPLE = 6     /* bitmask + GroupwiseSimple (needs r >= k) */
 };
 
 /* Splitting strategies of ozmm_split_ex (SliceStrategy, split.hpp:11-15). */
@@ -142,8 +163,12 @@ int ozmm_get_stream(ozmm_handle_t handle, void** stream);
 const char* ozmm_last_error(ozmm_handle_t handle);
 const char* ozmm_status_string(int status);
 /* Waits for the handle's stream; returns OZMM_ERR_RANGE if any split since the
- * last query saw a line max >= 2^921, and sets *underflow (nullable) when a
- * line scale fell below 2^-1000.  Clears both flags. */
+ * last query saw a line max >= 2^921 and that error was not already returned
+ * by the call that raised it, and sets *underflow (nullable) when a line scale
+ * fell below 2^-1000.  Clears both flags.  Every ozmm_dgemm_ex / _host call
+ * reports its own range error only (sync_check / host entry): a pending flag
+ * of an earlier stream-ordered call is kept for this query, never attributed
+ * to a later call. */
 int ozmm_sync_status(ozmm_handle_t handle, int* underflow);
 /* Bytes of device workspace the handle currently owns (grown lazily). */
 size_t ozmm_workspace_bytes(ozmm_handle_t handle);
@@ -167,7 +192,10 @@ int ozmm_dgemm_ex(ozmm_handle_t h, char transa, char transb, int64_t m, int64_t 
 
 /* Host-pointer variant (what the reference API takes): copies A, B, C to the
  * device, runs ozmm_dgemm_ex, copies C back.  Synchronous.  Range errors are
- * returned directly (sync_check is implied). */
+ * returned directly (sync_check is implied) and leave C untouched.  Host
+ * buffers may be pinned or pageable: pageable ones are registered with the
+ * driver for the duration of the call (cudaHostRegister) when that succeeds,
+ * and copied through the driver's staging otherwise. */
 int ozmm_dgemm_host(ozmm_handle_t h, char transa, char transb, int64_t m, int64_t n, int64_t p,
                     double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
                     double beta, double* C, int64_t ldc, int k, const ozmm_options_t* opt,
@@ -255,9 +283,12 @@ int ozmm_gemm_slices_offset(ozmm_handle_t h, int64_t m, int64_t n, int64_t p, in
  * ozmm_dgemm_2d splits the rank's lines, all-gathers the INT8 slice planes,
  * shifts and line sums inside the row group (A) and the column group (B) --
  * broadcasts only -- and runs the fused GEMM on the block in three strips.
- * The result is bit-identical to ozmm_dgemm on the whole matrices.  It is
- * stream-ordered on the handle's stream; range errors surface through
- * ozmm_sync_status on each rank, as for the split halves.
+ * The result is bit-identical to ozmm_dgemm on the whole matrices.  After the
+ * splits the range flags are max-reduced over the whole grid (two tiny
+ * gathers, row group then column group, and one host synchronisation): if any
+ * rank saw a line max >= 2^921, EVERY rank returns OZMM_ERR_RANGE before any
+ * strip writes C -- the reference's throw-before-write (split.cpp:124-125).
+ * The rest is stream-ordered on the handle's stream.
  * The all-gather is NCCL (every rank passes the same 128-byte id from
  * ozmm_nccl_unique_id on one rank; libnccl.so.2 is loaded on first use) or,
  * when `hook` is non-NULL, the caller's: hook(ctx, group, send, recv, bytes,

@@ -6,6 +6,12 @@ target): the kernels + C ABI (csrc/ozmm_capi.cu) and the host input generator
 intrinsics keep every FP64 operation singly rounded (the reference is built
 with -ffp-contract=off, proj/src/CMakeLists.txt:18-20).  The CUDA runtime is
 linked statically (nvcc default) so the .so needs only libcuda at run time.
+
+``--diag`` builds the diagnostic variant (-DOZMM_DIAG): the environment
+overrides used by the tuning probes under tools/ (OZMM_STAGES, OZMM_GROUP_M,
+OZMM_TILE_TRACE, ...) and the timing-only hooks that change results
+(OZMM_ONLY_BATCH, OZMM_DUP_MMA, OZMM_IDESC_XOR).  The release build reads no
+environment variable.
 """
 from __future__ import annotations
 
@@ -41,7 +47,7 @@ def _host_cxx() -> str:
     raise RuntimeError("g++ not found")
 
 
-def command(out: str = LIB, verbose_ptxas: bool = False) -> list[str]:
+def command(out: str = LIB, verbose_ptxas: bool = False, diag: bool = False) -> list[str]:
     cmd = [
         _nvcc(), "-ccbin", _host_cxx(),
         "-gencode", "arch=compute_100a,code=sm_100a",
@@ -51,11 +57,22 @@ def command(out: str = LIB, verbose_ptxas: bool = False) -> list[str]:
     ]
     if verbose_ptxas:
         cmd[1:1] = ["-Xptxas", "-v"]
+    if diag:
+        cmd[1:1] = ["-DOZMM_DIAG"]
     return cmd
+
+
+VARIANT = LIB + ".variant"  # "release" or "diag": which build the .so is
 
 
 def up_to_date(out: str = LIB) -> bool:
     if not os.path.exists(out):
+        return False
+    try:
+        with open(VARIANT) as f:
+            if f.read().strip() != "release":
+                return False
+    except OSError:
         return False
     t = os.path.getmtime(out)
     return all(os.path.getmtime(d) <= t for d in DEPS if os.path.exists(d))
@@ -71,20 +88,22 @@ def build_cli() -> str:
     return CLI
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, diag: bool = False) -> str:
+    if not force and not diag and up_to_date():
         if not os.path.exists(CLI) or os.path.getmtime(CLI) < os.path.getmtime(CLI_SRC):
             build_cli()
         return LIB
-    cmd = command(verbose_ptxas=verbose)
+    cmd = command(verbose_ptxas=verbose, diag=diag)
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc build failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
     if verbose:
         sys.stderr.write(res.stdout + res.stderr)
+    with open(VARIANT, "w") as f:
+        f.write("diag" if diag else "release")
     build_cli()
     return LIB
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, diag="--diag" in sys.argv))

@@ -6,7 +6,10 @@
 //                             double beta, const MatrixF64& c, const SchemeConfig& cfg);  :92-95
 //   OzakiResult ozaki_gemm_ex(...same...);                                                :96-98
 //   OzakiResult ozaki_mm     (const MatrixF64& a, const MatrixF64& b, const SchemeConfig&); :89-90
-// for cfg = config_for(Method::ozIMMU_H, k) (the only preset the GPU path runs).
+// for every valid SchemeConfig: the (strategy, accumulation) pair selects the
+// GPU method -- ozIMMU_H (the hot path), ozIMMU, ozIMMU_RN, ozIMMU_EF and the two
+// other valid pairs -- and overflow / force_beta / force_r are honoured
+// (scheme.hpp:24-31, scheme.cpp:137-174).
 //
 // Templated over the matrix type: anything row-major with rows(), cols(),
 // data() and a (rows, cols) constructor -- the reference's
@@ -15,7 +18,8 @@
 // semantics as the reference: inputs are const, a NEW matrix is returned
 // (scheme.cpp:281, :289), errors are thrown as the reference's exception
 // types (std::invalid_argument, a ConfigError-compatible invalid_argument,
-// std::overflow_error for rows >= 2^921).
+// std::overflow_error for rows >= 2^921, an OverflowError runtime_error for an
+// INT32 chunk overflow in OverflowMode::Checked, int_gemm.hpp:15-26).
 #pragma once
 
 #include <cstdint>
@@ -29,6 +33,10 @@ namespace gpu {
 
 struct ConfigError : std::invalid_argument {
   using std::invalid_argument::invalid_argument;
+};
+// INT32 chunk overflow in OverflowMode::Checked (int_gemm.hpp:15-26)
+struct OverflowError : std::runtime_error {
+  using std::runtime_error::runtime_error;
 };
 
 struct OpCounts {
@@ -44,17 +52,48 @@ struct OzakiResultT {
   PhaseTimings timings;
 };
 
-// Subset of the reference SchemeConfig the GPU path honours (scheme.hpp:24-31).
+// The reference SchemeConfig (scheme.hpp:24-31) as the C ABI's options.
 struct GpuConfig {
   int k = 8;
+  int method = OZMM_METHOD_OZIMMU_H;
+  int overflow_wrap = 0;  // OverflowMode::Checked (the reference's default)
   int force_beta = 0;
   std::int64_t force_r = 0;
 };
 
-// Accept the reference's SchemeConfig (or anything with k/force_beta/force_r).
+// (SliceStrategy, Accumulation) -> OZMM_METHOD_*.  Enum orders of the reference:
+// SliceStrategy {BitMask, RoundNearestPerSlice, RoundNearestConstShift}
+// (split.hpp:11-15), Accumulation {PerProduct, Groupwise, GroupwiseSimple}
+// (scheme.hpp:13-17).  The one invalid pair -- per-slice RN with group-wise
+// accumulation -- is the reference's ConfigError (validate_config, scheme.cpp:164-168).
+inline int method_code(int strategy, int accumulation) {
+  switch (strategy * 3 + accumulation) {
+    case 2 * 3 + 1: return OZMM_METHOD_OZIMMU_H;
+    case 0 * 3 + 0: return OZMM_METHOD_OZIMMU;
+    case 1 * 3 + 0: return OZMM_METHOD_OZIMMU_RN;
+    case 0 * 3 + 1: return OZMM_METHOD_OZIMMU_EF;
+    case 2 * 3 + 0: return OZMM_METHOD_RN_CONST_PER_PRODUCT;
+    case 2 * 3 + 2: return OZMM_METHOD_OZIMMU_H_SIMPLE;
+    case 0 * 3 + 2: return OZMM_METHOD_OZIMMU_EF_SIMPLE;
+    case 1 * 3 + 1:
+    case 1 * 3 + 2:
+      throw ConfigError(
+          "per-slice round-to-nearest shifts are only valid with per-product accumulation");
+    default: throw ConfigError("unknown slice strategy / accumulation");
+  }
+}
+
+// Accept the reference's SchemeConfig (k, strategy, accumulation, overflow,
+// force_beta, force_r; enum class members).
 template <class Cfg>
 GpuConfig to_gpu_config(const Cfg& cfg) {
-  return GpuConfig{cfg.k, cfg.force_beta, static_cast<std::int64_t>(cfg.force_r)};
+  GpuConfig g;
+  g.k = cfg.k;
+  g.method = method_code(static_cast<int>(cfg.strategy), static_cast<int>(cfg.accumulation));
+  g.overflow_wrap = static_cast<int>(cfg.overflow);  // OverflowMode {Checked, Wrapping}
+  g.force_beta = cfg.force_beta;
+  g.force_r = static_cast<std::int64_t>(cfg.force_r);
+  return g;
 }
 inline GpuConfig to_gpu_config(const GpuConfig& cfg) { return cfg; }
 
@@ -83,6 +122,7 @@ inline void throw_status(int rc, ozmm_handle_t h) {
     case OZMM_ERR_ARG: throw std::invalid_argument(msg);
     case OZMM_ERR_CONFIG: throw ConfigError(msg);
     case OZMM_ERR_RANGE: throw std::overflow_error(msg);
+    case OZMM_ERR_OVERFLOW: throw OverflowError(msg);
     default: throw std::runtime_error(msg + " (" + ozmm_status_string(rc) + ")");
   }
 }
@@ -99,6 +139,8 @@ OzakiResultT<Mat> ozaki_gemm_ex(double alpha, const Mat& a, const Mat& b, double
   Mat out(c.rows(), c.cols());
   std::copy(c.data(), c.data() + m * p, out.data());
   ozmm_options_t opt{};
+  opt.method = cfg.method;
+  opt.overflow_wrap = cfg.overflow_wrap;
   opt.force_beta = cfg.force_beta;
   opt.force_r = cfg.force_r;
   opt.timings = 1;

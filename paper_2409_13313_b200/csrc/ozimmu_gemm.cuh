@@ -57,8 +57,8 @@ struct GemmParams {
   int stages;          // smem pipeline depth
   int a_slots, b_slots;  // slice tiles per stage (max over passes)
   int n_chunks;
-  uint32_t idesc_xor;  // experiment hook (OZMM_IDESC_XOR): flips instruction-descriptor bits
-  int dup_mma;         // experiment hook (OZMM_DUP_MMA): repeat each product's MMAs (timing only)
+  uint32_t idesc_xor;  // diagnostic build only (OZMM_IDESC_XOR): flips instruction-descriptor bits
+  int dup_mma;         // diagnostic build only (OZMM_DUP_MMA): repeat each product's MMAs (timing only)
   uint64_t* tile_trace;  // optional [tiles][8] globaltimer stamps of each leader CTA (OZMM_TILE_TRACE)
   int group_pairs;     // CTA-pair kernel: issue A groups two at a time (OZMM_GROUP_PAIRS)
   int kpair;           // CTA-pair kernel: thin passes take K blocks in pairs (OZMM_KPAIR)

@@ -210,7 +210,11 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
   } else if (warp == 1) {
     // ------------------------------------------- MMA issuer (leader CTA)
     // u8 x u8 for offset-binary planes (instruction-descriptor bits 7 / 10)
+#ifdef OZMM_DIAG
     const uint32_t idesc = (P.bias ? (Cfg::kIdesc & ~((1u << 7) | (1u << 10))) : Cfg::kIdesc) ^ P.idesc_xor;
+#else
+    const uint32_t idesc = P.bias ? (Cfg::kIdesc & ~((1u << 7) | (1u << 10))) : Cfg::kIdesc;
+#endif
     if (leader) {
       int bi = 0, ai = 0;
       uint32_t bph = 0, aph = 0;
@@ -338,9 +342,11 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
                   for (int j = 0; j < kKB / kBK; ++j)  // K = 32 per MMA: +32 B = +2 in desc.lo
                     ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, idesc,
                                      (first && j == 0) ? 0u : 1u);
+#ifdef OZMM_DIAG
                   for (int x = 0; x < P.dup_mma; ++x)  // timing experiment only (wrong results)
                     for (int j = 0; j < kKB / kBK; ++j)
                       ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, idesc, 1u);
+#endif
                 }
                 ptx::mma_commit_pair(a_empty + ai, all_mask);  // A stage free (all sharers)
               }

@@ -31,9 +31,33 @@
 #include "slicer.cuh"
 #include "slicer_methods.cuh"
 
+// Environment overrides (tuning sweeps, timing probes, per-tile traces) exist
+// only in the diagnostic build (-DOZMM_DIAG: `python -m
+// paper_2409_13313_b200.build --diag`).  The release library reads no
+// environment variable at all -- the macro drops the names at preprocessing --
+// so no stray variable can change a launch, let alone a result.  Tuning that
+// keeps results identical is reachable in release through ozmm_options_t.
+#ifdef OZMM_DIAG
+#define OZMM_ENV(name) std::getenv(name)
+#else
+#define OZMM_ENV(name) (static_cast<const char*>(nullptr))
+#endif
+
 namespace {
 
 thread_local std::string g_thread_err;
+
+// Device flags of a handle: [0] underflow, [1] range -- raised by the splits of
+// the CURRENT call; [2] / [3] the same, pending from earlier stream-ordered
+// calls that did not report them (folded in at the start of every GEMM entry,
+// returned by ozmm_sync_status).
+constexpr int kNumFlags = 4;
+__global__ void fold_flags_kernel(int* f) {
+  f[2] |= f[0];
+  f[3] |= f[1];
+  f[0] = 0;
+  f[1] = 0;
+}
 
 // Splitting strategy (SliceStrategy, split.hpp:11-15) and FP64 flush scaling of
 // the fused GEMM (GemmParams::scale_mode).
@@ -48,6 +72,10 @@ struct FlushCfg {
   const int32_t* lsb = nullptr;
   int64_t lsa_plane = 0, lsb_plane = 0, lsa_lstride = 1, lsb_lstride = 1;
   int64_t n = 0;
+  // tuning (same results): kpair 0 auto / 1 off / 2 on, stages 0 auto; full_mp =
+  // m*p of the whole problem when this launch is one strip of it (0: this launch)
+  int kpair = 0, stages = 0;
+  int64_t full_mp = 0;
   bool biased() const { return lsa != nullptr; }
 };
 
@@ -65,6 +93,7 @@ bool method_cfg(int method, MethodCfg* out) {
     case OZMM_METHOD_OZIMMU_EF: *out = {kBitMask, false, false}; return true;
     case OZMM_METHOD_RN_CONST_PER_PRODUCT: *out = {kRNConstShift, true, false}; return true;
     case OZMM_METHOD_OZIMMU_H_SIMPLE: *out = {kRNConstShift, false, true}; return true;
+    case OZMM_METHOD_OZIMMU_EF_SIMPLE: *out = {kBitMask, false, true}; return true;
     default: return false;
   }
 }
@@ -84,7 +113,7 @@ struct Handle {
   size_t nu_n = 0;
   unsigned long long* colmax = nullptr;
   size_t colmax_n = 0;
-  int* flags = nullptr;  // [0] underflow, [1] range
+  int* flags = nullptr;  // [kNumFlags]: see fold_flags_kernel
   double* units_a = nullptr;  // per-slice units (RN per slice) [k][m] / [k][p]
   size_t units_a_n = 0;
   double* units_b = nullptr;
@@ -223,7 +252,7 @@ int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const doubl
     int csize = 0, cthreads = 128;
     {
       int t0 = 128;
-      if (const char* e = std::getenv("OZMM_ROW_CTA")) t0 = std::atoi(e);
+      if (const char* e = OZMM_ENV("OZMM_ROW_CTA")) t0 = std::atoi(e);
       for (int t : {t0, 256, 512}) {
         const int64_t c = (chunks + t - 1) / t;
         if (c <= 8) {
@@ -389,24 +418,32 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
   P.tiles_m = tiles_m;
   P.tiles_n = tiles_n;
   P.group_m = 2;  // tile-row group of the raster (measured sweep, tools/l2_sweep.sh)
-  if (const char* g = std::getenv("OZMM_GROUP_M")) P.group_m = std::max(1, std::atoi(g));
+  if (const char* g = OZMM_ENV("OZMM_GROUP_M")) P.group_m = std::max(1, std::atoi(g));
   P.hint_a = 2;  // A panels are reused by every column tile of the group: keep them in L2
   P.hint_b = 0;
-  if (const char* g = std::getenv("OZMM_HINT_A")) P.hint_a = std::atoi(g);
-  if (const char* g = std::getenv("OZMM_HINT_B")) P.hint_b = std::atoi(g);
-  if (const char* g = std::getenv("OZMM_DUP_MMA")) P.dup_mma = std::atoi(g);
+  if (const char* g = OZMM_ENV("OZMM_HINT_A")) P.hint_a = std::atoi(g);
+  if (const char* g = OZMM_ENV("OZMM_HINT_B")) P.hint_b = std::atoi(g);
+#ifdef OZMM_DIAG
+  if (const char* g = OZMM_ENV("OZMM_DUP_MMA")) P.dup_mma = std::atoi(g);  // timing probe: wrong results
+#endif
   // CTA-pair kernel: A groups issued two per barrier round (one wait burst, one
   // MMA burst, one release burst): C3 +9-12 %, C5 k=12 +7.5 %, C4 +2 % against one
   // group per round; three per round starve the producer (tools/gpairs_probe*.sh)
   P.group_pairs = 2;
-  if (const char* g = std::getenv("OZMM_GROUP_PAIRS")) P.group_pairs = std::atoi(g);
+  if (const char* g = OZMM_ENV("OZMM_GROUP_PAIRS")) P.group_pairs = std::atoi(g);
   // thin passes in K-block pairs (runs of 8 MMAs per accumulator): +4 % at C5
   // (k = 12), +1 % at C4, but -3 % at the two-batch C3 where the power cap takes the
   // gain back (profiles/r1/kpair_ab.txt) -- on for schedules of three or more batches
-  // and for C blocks up to 8192 x 8192 (C2 +2 %)
-  P.kpair = (S.batches.size() >= 3 || m * p <= int64_t(8192) * 8192) ? 1 : 0;
-  if (const char* g = std::getenv("OZMM_KPAIR")) P.kpair = std::atoi(g);
-  if (const char* g = std::getenv("OZMM_IDESC_XOR")) P.idesc_xor = static_cast<uint32_t>(std::strtoul(g, nullptr, 0));
+  // and for problems up to 8192 x 8192 (C2 +2 %).  The problem, not the launch: the
+  // host entry's strips of a C3 call are C3 work (fl.full_mp)
+  const int64_t mp = fl.full_mp ? fl.full_mp : m * p;
+  P.kpair = (S.batches.size() >= 3 || mp <= int64_t(8192) * 8192) ? 1 : 0;
+  if (fl.kpair) P.kpair = fl.kpair == 2 ? 1 : 0;
+  if (const char* g = OZMM_ENV("OZMM_KPAIR")) P.kpair = std::atoi(g);
+#ifdef OZMM_DIAG
+  // timing probe: flips instruction-descriptor bits (wrong results)
+  if (const char* g = OZMM_ENV("OZMM_IDESC_XOR")) P.idesc_xor = static_cast<uint32_t>(std::strtoul(g, nullptr, 0));
+#endif
   P.nbatch = static_cast<int>(S.batches.size());
   P.npass = static_cast<int>(S.passes.size());
   P.beta = beta_bits;
@@ -450,8 +487,9 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
     P.p_g0[q] = static_cast<uint16_t>(S.passes[q].g0);
     P.p_g1[q] = static_cast<uint16_t>(S.passes[q].g1);
   }
+#ifdef OZMM_DIAG
   // timing experiment only (results are wrong): OZMM_ONLY_BATCH=b runs batch b alone
-  if (const char* e = std::getenv("OZMM_ONLY_BATCH")) {
+  if (const char* e = OZMM_ENV("OZMM_ONLY_BATCH")) {
     const int b = std::atoi(e);
     if (b >= 0 && b < P.nbatch) {
       const int q0 = P.b_pass0[b], q1 = P.b_pass1[b];
@@ -466,6 +504,7 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
       P.nbatch = 1, P.npass = q1 - q0;
     }
   }
+#endif
   for (size_t g = 0; g < S.agroups.size(); ++g) {
     P.ag_s[g] = static_cast<uint8_t>(S.agroups[g].s);
     P.ag_p0[g] = static_cast<uint16_t>(S.agroups[g].p0);
@@ -538,19 +577,19 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   auto slot_bytes = [](int, int b) { return static_cast<int64_t>(b) * Cfg::kBTile; };
   ozb::PassCost cm;
   cm.a_tile /= kPairs;  // the 4-CTA variant multicasts A: each CTA fills half
-  if (const char* e = std::getenv("OZMM_SCHED_BATCH")) cm.batch = std::atof(e);
-  if (const char* e = std::getenv("OZMM_SCHED_FILL"))  // scale of the fill terms
+  if (const char* e = OZMM_ENV("OZMM_SCHED_BATCH")) cm.batch = std::atof(e);
+  if (const char* e = OZMM_ENV("OZMM_SCHED_FILL"))  // scale of the fill terms
     cm.a_tile *= std::atof(e), cm.b_tile *= std::atof(e);
-  if (const char* e = std::getenv("OZMM_SCHED")) cm.greedy = std::string(e) == "greedy";
+  if (const char* e = OZMM_ENV("OZMM_SCHED")) cm.greedy = std::string(e) == "greedy";
   // A groups alternate large and small when every batch is a single pass (k <= 8:
   // all B slices resident), so that the two-group issue rounds are even (8+1,
   // 7+2, ... products): C3 +3-4 % (profiles/r1/aorder_g2.txt).  Multi-window
   // schedules (k >= 9) keep the sorted order (C5 k=12: -1.7 % interleaved).
   cm.interleave = k <= Cfg::kMaxBSlots;
-  if (const char* e = std::getenv("OZMM_AORDER")) cm.interleave = std::string(e) == "interleave";
+  if (const char* e = OZMM_ENV("OZMM_AORDER")) cm.interleave = std::string(e) == "interleave";
   // ... and no two consecutive products into one accumulator (C3 +1 %)
   cm.avoid_raw = cm.interleave;
-  if (const char* e = std::getenv("OZMM_AVOID_RAW")) cm.avoid_raw = std::atoi(e) != 0;
+  if (const char* e = OZMM_ENV("OZMM_AVOID_RAW")) cm.avoid_raw = std::atoi(e) != 0;
   const ozb::Schedule S = ozb::make_schedule(k, fl.per_product ? 1 : r, Cfg::kNAcc,
                                              static_cast<int64_t>(Cfg::kMaxBSlots) * Cfg::kBTile,
                                              slot_bytes, Cfg::kMaxBSlots, cm);
@@ -572,7 +611,9 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   for (const auto& q : S.passes) a_loads += q.g1 - q.g0;
   const bool dense = a_loads > 0 && 2 * static_cast<int64_t>(S.products.size()) >= 5 * a_loads;
   int stages = static_cast<int>(std::min<size_t>(dense ? 5 : 6, (budget - fixed) / Cfg::kATile));
-  if (const char* e = std::getenv("OZMM_STAGES"))
+  if (fl.stages)
+    stages = static_cast<int>(std::min<size_t>((budget - fixed) / Cfg::kATile, std::max(2, fl.stages)));
+  if (const char* e = OZMM_ENV("OZMM_STAGES"))
     stages = static_cast<int>(std::min<size_t>((budget - fixed) / Cfg::kATile, std::max(2, std::atoi(e))));
   if (stages < 2)
     return set_err(h, OZMM_ERR_UNSUPPORTED, "A ring does not fit shared memory");
@@ -591,7 +632,7 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   // raster: tensor-bound schedules visit 4 pair-row-blocks per group (a wave of
   // 74 tiles then spans ~4 x 18 tiles and re-reads less of B from DRAM: C3 DRAM
   // 135 -> 82 GB, +3 %; tools/group_ncu.sh); L2-bound ones (C4) keep 2
-  if (!std::getenv("OZMM_GROUP_M")) P.group_m = dense ? 4 : 2;
+  if (!OZMM_ENV("OZMM_GROUP_M")) P.group_m = dense ? 4 : 2;
   CUtensorMap map_a, map_b;
   if (int rc = make_slice_map(h, &map_a, As, lds_a, m, plane_a, k, Cfg::kAPart, ozb::kKB,
                               CU_TENSOR_MAP_SWIZZLE_128B))
@@ -610,7 +651,7 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   }
   const dim3 grid(static_cast<unsigned>(Cfg::kCluster * tiles_m * tiles_n));
   // OZMM_TILE_TRACE=1 (diagnostics): per-CTA globaltimer stamps, summarised on stderr
-  const bool ttrace = std::getenv("OZMM_TILE_TRACE") != nullptr;
+  const bool ttrace = OZMM_ENV("OZMM_TILE_TRACE") != nullptr;
   uint64_t* tbuf = nullptr;
   if (ttrace) {
     CUDA_TRY(h, cudaMalloc(&tbuf, sizeof(uint64_t) * 8 * grid.x));
@@ -664,7 +705,7 @@ bool pair_kernel_selected(const ozmm_options_t* opt) {
 // the signed ones (options / OZMM_SIGNED=1) or another kernel runs.
 bool use_offset_planes(const ozmm_options_t* opt, const MethodCfg& mc) {
   if (opt && opt->signed_slices) return false;
-  if (const char* e = std::getenv("OZMM_SIGNED"))
+  if (const char* e = OZMM_ENV("OZMM_SIGNED"))
     if (std::atoi(e) != 0) return false;
   return mc.strategy == kRNConstShift && !mc.per_product && pair_kernel_selected(opt);
 }
@@ -672,13 +713,20 @@ bool use_offset_planes(const ozmm_options_t* opt, const MethodCfg& mc) {
 int launch_gemm(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_bits, int64_t r,
                 const int8_t* As, int64_t lds_a, int64_t plane_a, const double* mu, const int8_t* Bs,
                 int64_t lds_b, int64_t plane_b, const double* nu, double alpha, double beta, const double* Cin, double* Cout,
-                int64_t ldc, const ozmm_options_t* opt, const FlushCfg& fl = FlushCfg{}) {
+                int64_t ldc, const ozmm_options_t* opt, const FlushCfg& fl_in = FlushCfg{}) {
   int32_t* dump = opt ? opt->chunk_dump : nullptr;
+  FlushCfg fl = fl_in;
+  if (opt) {
+    if (opt->kpair < 0 || opt->kpair > 2 || opt->stages < 0)
+      return set_err(h, OZMM_ERR_ARG, "options: kpair must be 0..2 and stages >= 0");
+    fl.kpair = opt->kpair;
+    fl.stages = opt->stages;
+  }
   if (fl.biased() && !pair_kernel_selected(opt))
     return set_err(h, OZMM_ERR_UNSUPPORTED, "offset-binary slices need the CTA-pair kernel");
   const int tile_n = opt ? opt->tile_n : 0;
   const int pair = opt ? opt->cta_pair : 0;
-  if (pair == 3 || (pair == 0 && tile_n == 0 && std::getenv("OZMM_QUAD")))
+  if (pair == 3 || (pair == 0 && tile_n == 0 && OZMM_ENV("OZMM_QUAD")))
     return launch_gemm_pair<128, 2>(h, m, n, p, k, beta_bits, r, As, lds_a, plane_a, mu, Bs, lds_b,
                                     plane_b, nu, alpha, beta, Cin, Cout, ldc, dump, fl);
   if (pair == 2 || (pair == 0 && tile_n == 0))
@@ -699,6 +747,63 @@ int launch_gemm(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_bits
   }
 }
 
+// ---- OverflowMode::Checked ------------------------------------------------------
+// The reference checks every running INT32 chunk sum after each slice product in
+// int64 and throws OverflowError outside INT32 (gemm_wide, int_gemm.cpp:37-59; the
+// INT32 fast path runs only when no entry can leave the range, :213-219).  The
+// tensor core wraps, so the GPU verifies instead -- but only where an overflow is
+// possible at all, i.e. where a chunk's bound n * sum max|A_s| max|B_t| exceeds
+// INT32_MAX.  With the derived beta and r that never happens (r n 2^(2 beta) <=
+// 2^31 and max|slice| <= 2^beta - 1, int_gemm.cpp:24-25); force_beta / force_r can.
+//
+// max |slice s| (1-based): RN constant shift 2^beta - 1 for s = 1 (the bump rule,
+// split.cpp:126-129) and 2^(beta-1) after it (round to nearest); bitmask fields
+// and per-slice RN 2^beta - 1 (split.cpp:60, :121-130).
+int64_t slice_max(Strategy st, int beta, int s) {
+  if (st == kRNConstShift && s >= 2) return int64_t(1) << (beta - 1);
+  return (int64_t(1) << beta) - 1;
+}
+
+// 0: no overflow possible; 1: possible, verifiable per product; -1: a single
+// product may already leave INT32 (its wrapped value cannot be verified).
+int overflow_possible(Strategy st, bool per_product, int k, int64_t r, int beta, int64_t n) {
+  const int64_t lim = INT32_MAX;
+  int verdict = 0;
+  for (const ozb::Chunk& c : ozb::make_chunks(k, per_product ? 1 : r)) {
+    int64_t sum = 0;
+    for (int s0 = c.s0; s0 <= c.s1; ++s0) {
+      const int64_t one = slice_max(st, beta, s0) * slice_max(st, beta, c.g - s0);
+      if (n > lim / one) return -1;  // n * one > INT32_MAX
+      sum += one;
+    }
+    if (sum > lim / n) verdict = 1;
+  }
+  return verdict;
+}
+
+// Exact INT32 range check of the running chunk sums.  prod [P][m][p]: the exact
+// per-product sums A_s B_t in flush order (a chunk schedule with r = 1); the
+// chunks of the real r are replayed over them (scheme.cpp:81-101).  first: the
+// earliest (product, entry) that leaves INT32 as product << 40 | entry.
+__global__ void checked_overflow_kernel(const int32_t* __restrict__ prod, int64_t mp, int k,
+                                        int64_t r, unsigned long long* first) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < mp;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    int64_t q = 0;
+    for (int g = 2; g <= k + 1; ++g) {
+      int64_t acc = 0, cnt = 0;
+      for (int s = 1; s <= g - 1; ++s, ++q) {
+        acc += prod[q * mp + e];
+        if (acc < INT32_MIN || acc > INT32_MAX) {
+          atomicMin(first, (static_cast<unsigned long long>(q) << 40) | static_cast<unsigned long long>(e));
+          return;
+        }
+        if (++cnt == r || s == g - 1) acc = 0, cnt = 0;
+      }
+    }
+  }
+}
+
 int check_range_sync(Handle* h) {
   int f[2] = {0, 0};
   CUDA_TRY(h, cudaMemcpyAsync(f, h->flags, sizeof f, cudaMemcpyDeviceToHost, h->stream));
@@ -715,6 +820,67 @@ int gemm_slices_checked(Handle* h, int64_t m, int64_t n, int64_t p, int k, int b
                         const double* mu, const int8_t* Bs, int64_t lds_b, int64_t plane_b,
                         const double* nu, double alpha, double beta, double* C, int64_t ldc,
                         const ozmm_options_t* opt, const FlushCfg& fl);
+
+// OverflowMode::Checked verification of one call's split operands (see
+// overflow_possible): the per-product sums (the fused kernel's chunk dump with r
+// = 1, into scratch), then the running sums of the real chunks.  Synchronous;
+// returns OZMM_ERR_OVERFLOW with the reference's message, before C is written.
+int verify_no_overflow(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta_bits, int64_t r,
+                       const int8_t* As, int64_t lds, const double* mu, const int8_t* Bs,
+                       const double* nu, const ozmm_options_t* opt, const FlushCfg& fl) {
+  if (int rc = check_range_sync(h)) return rc;  // the split throws first (split.cpp:124)
+  const int64_t np = int64_t(k) * (k + 1) / 2, mp = m * p;
+  int32_t* prod = nullptr;
+  double* scratch = nullptr;
+  unsigned long long* first = nullptr;
+  auto release = [&] {
+    cudaFree(prod);
+    cudaFree(scratch);
+    cudaFree(first);
+  };
+  if (cudaMalloc(&prod, sizeof(int32_t) * np * mp) != cudaSuccess ||
+      cudaMalloc(&scratch, sizeof(double) * mp) != cudaSuccess ||
+      cudaMalloc(&first, sizeof(unsigned long long)) != cudaSuccess) {
+    release();
+    cudaGetLastError();
+    return set_err(h, OZMM_ERR_CUDA, "Checked overflow verification: out of device memory "
+                   "(%lld x %lld x %lld INT32 sums); use overflow_wrap", static_cast<long long>(np),
+                   static_cast<long long>(m), static_cast<long long>(p));
+  }
+  ozmm_options_t o = opt ? *opt : ozmm_options_t{};
+  o.chunk_dump = prod;
+  int rc = launch_gemm(h, m, n, p, k, beta_bits, 1, As, lds, m * lds, mu, Bs, lds, p * lds, nu,
+                       1.0, 0.0, nullptr, scratch, p, &o, fl);
+  unsigned long long hit = ~0ull;
+  if (rc == OZMM_OK) {
+    cudaMemsetAsync(first, 0xFF, sizeof hit, h->stream);
+    const int64_t blocks = std::min<int64_t>((mp + 255) / 256, int64_t(h->num_sms) * 8);
+    checked_overflow_kernel<<<static_cast<unsigned>(blocks), 256, 0, h->stream>>>(prod, mp, k, r, first);
+    cudaMemcpyAsync(&hit, first, sizeof hit, cudaMemcpyDeviceToHost, h->stream);
+    const cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) rc = set_err(h, OZMM_ERR_CUDA, "overflow check: %s", cudaGetErrorString(e));
+  }
+  if (rc == OZMM_OK && hit != ~0ull) {
+    const int64_t q = static_cast<int64_t>(hit >> 40), e = static_cast<int64_t>(hit & ((1ull << 40) - 1));
+    std::vector<int32_t> v(static_cast<size_t>(np));
+    cudaMemcpy2D(v.data(), sizeof(int32_t), prod + e, sizeof(int32_t) * mp, sizeof(int32_t), np,
+                 cudaMemcpyDeviceToHost);
+    // replay the entry's chunks up to product q for the exact value
+    int64_t qq = 0, val = 0;
+    for (int g = 2; g <= k + 1 && qq <= q; ++g) {
+      int64_t acc = 0, cnt = 0;
+      for (int s0 = 1; s0 <= g - 1 && qq <= q; ++s0, ++qq) {
+        acc += v[qq];
+        val = acc;
+        if (++cnt == r || s0 == g - 1) acc = 0, cnt = 0;
+      }
+    }
+    rc = set_err(h, OZMM_ERR_OVERFLOW, "i8_gemm: INT32 overflow at (%lld, %lld), exact value %lld",
+                 static_cast<long long>(e / p), static_cast<long long>(e % p), static_cast<long long>(val));
+  }
+  release();
+  return rc;
+}
 
 }  // namespace
 
@@ -743,8 +909,8 @@ int ozmm_create(ozmm_handle_t* out, int device) {
   }
   h->num_sms = sms;
   h->smem_optin = static_cast<size_t>(optin);
-  if (cudaMalloc(&h->flags, 2 * sizeof(int)) != cudaSuccess ||
-      cudaMemset(h->flags, 0, 2 * sizeof(int)) != cudaSuccess) {
+  if (cudaMalloc(&h->flags, kNumFlags * sizeof(int)) != cudaSuccess ||
+      cudaMemset(h->flags, 0, kNumFlags * sizeof(int)) != cudaSuccess) {
     delete h;
     return set_err(nullptr, OZMM_ERR_CUDA, "flag allocation failed");
   }
@@ -818,15 +984,29 @@ const char* ozmm_status_string(int s) {
   }
 }
 
+// Library-internal (hidden, not part of the ABI): the 2-D grid entry
+// (ozmm_grid.cpp) starts each call with clear flags and reads this call's range
+// flag on the device for its grid-wide max.
+__attribute__((visibility("hidden"))) int* ozmm_internal_range_flag(ozmm_handle_t handle) {
+  return reinterpret_cast<Handle*>(handle)->flags + 1;
+}
+__attribute__((visibility("hidden"))) int ozmm_internal_fold_flags(ozmm_handle_t handle) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  fold_flags_kernel<<<1, 1, 0, h->stream>>>(h->flags);
+  CUDA_TRY(h, cudaGetLastError());
+  return OZMM_OK;
+}
+
 int ozmm_sync_status(ozmm_handle_t handle, int* underflow) {
   Handle* h = reinterpret_cast<Handle*>(handle);
   if (!h) return set_err(nullptr, OZMM_ERR_ARG, "null handle");
-  int f[2] = {0, 0};
+  int f[kNumFlags] = {};
+  CUDA_TRY(h, cudaSetDevice(h->device));
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   CUDA_TRY(h, cudaMemcpy(f, h->flags, sizeof f, cudaMemcpyDeviceToHost));
   CUDA_TRY(h, cudaMemset(h->flags, 0, sizeof f));
-  if (underflow) *underflow = f[0];
-  if (f[1]) return set_err(h, OZMM_ERR_RANGE, "split: row magnitude too large for shift extraction");
+  if (underflow) *underflow = f[0] | f[2];
+  if (f[1] | f[3]) return set_err(h, OZMM_ERR_RANGE, "split: row magnitude too large for shift extraction");
   return OZMM_OK;
 }
 
@@ -1081,8 +1261,11 @@ int gemm_slices_checked(Handle* h, int64_t m, int64_t n, int64_t p, int k, int b
   if (r < 1) return set_err(h, OZMM_ERR_CONFIG, "force_r must be >= 1");
   CUDA_TRY(h, cudaSetDevice(h->device));
   const bool write_only = opt && opt->c_write_only;
-  if (write_only && beta != 0.0)
-    return set_err(h, OZMM_ERR_ARG, "c_write_only needs beta == 0");
+  // fl(alpha*d) + fl(beta*c) == fl(alpha*d) bit for bit needs beta == 0 AND alpha
+  // > 0: with alpha <= 0, alpha*d may be -0 and the sign of the zero would come
+  // from fl(beta*c) (-0 + +0 = +0)
+  if (write_only && !(beta == 0.0 && alpha > 0.0))
+    return set_err(h, OZMM_ERR_ARG, "c_write_only needs beta == 0 and alpha > 0");
   return launch_gemm(h, m, n, p, k, beta_bits, r, As, lds_a, plane_a, mu, Bs, lds_b, plane_b, nu,
                      alpha, beta, write_only ? nullptr : C, C, ldc, opt, fl);
 }
@@ -1122,6 +1305,15 @@ int ozmm_dgemm_ex(ozmm_handle_t handle, char transa, char transb, int64_t m, int
   const int64_t lda_need = is_trans(transa) ? m : n, ldb_need = is_trans(transb) ? n : p;
   if (lda < lda_need || ldb < ldb_need || ldc < p)
     return set_err(h, OZMM_ERR_ARG, "leading dimension too small");
+  // OverflowMode::Checked: only forced beta / r can make an INT32 overflow possible
+  const int ovf = (opt && opt->overflow_wrap) || !(fb || fr)
+                      ? 0 : overflow_possible(mc.strategy, mc.per_product, k, r, beta_bits, n);
+  if (ovf < 0)
+    return set_err(h, OZMM_ERR_UNSUPPORTED, "Checked overflow mode: a single slice product may leave "
+                   "INT32 for this forced beta and n (its wrapped sum cannot be verified); use "
+                   "overflow_wrap");
+  if (ovf > 0 && mc.per_product)  // per-product chunks are single products: in range
+    return set_err(h, OZMM_ERR_INTERNAL, "overflow bound inconsistent");
 
   CUDA_TRY(h, cudaSetDevice(h->device));
   const int64_t lds = ozmm_slice_ld(n);
@@ -1129,6 +1321,9 @@ int ozmm_dgemm_ex(ozmm_handle_t handle, char transa, char transb, int64_t m, int
   if (int rc = ensure(h, &h->slices_b, &h->slices_b_bytes, static_cast<size_t>(k) * p * lds)) return rc;
   if (int rc = ensure(h, &h->mu, &h->mu_n, static_cast<size_t>(m))) return rc;
   if (int rc = ensure(h, &h->nu, &h->nu_n, static_cast<size_t>(p))) return rc;
+  // this call's flags start clear; earlier unreported ones stay pending
+  fold_flags_kernel<<<1, 1, 0, h->stream>>>(h->flags);
+  CUDA_TRY(h, cudaGetLastError());
 
   const bool want_t = (opt && opt->timings) || timings;
   if (want_t) CUDA_TRY(h, cudaEventRecord(h->ev[0], h->stream));
@@ -1162,7 +1357,7 @@ int ozmm_dgemm_ex(ozmm_handle_t handle, char transa, char transb, int64_t m, int
   // OZMM_SPLIT_OVERLAP: 2 (default) B's whole column split on the side stream,
   // 1 only its column maxima, 0 none (A/B switch)
   static const int split_overlap = [] {
-    const char* e = std::getenv("OZMM_SPLIT_OVERLAP");
+    const char* e = OZMM_ENV("OZMM_SPLIT_OVERLAP");
     return e ? std::atoi(e) : 2;
   }();
   const bool overlap_colmax = offset && !is_trans(transa) && !is_trans(transb) && split_overlap > 0;
@@ -1207,6 +1402,10 @@ int ozmm_dgemm_ex(ozmm_handle_t handle, char transa, char transb, int64_t m, int
   if (want_t) CUDA_TRY(h, cudaEventRecord(h->ev[2], h->stream));
   if (opt && opt->sync_check)
     if (int rc = check_range_sync(h)) return rc;
+  if (ovf > 0)
+    if (int rc = verify_no_overflow(h, m, n, p, k, beta_bits, r, h->slices_a, lds, h->mu,
+                                    h->slices_b, h->nu, opt, fl))
+      return rc;
   // fused group-wise accumulation + epilogue -- scheme.cpp:261-263, :286-287
   if (int rc = launch_gemm(h, m, n, p, k, beta_bits, r, h->slices_a, lds, m * lds, h->mu,
                            h->slices_b, lds, p * lds,
@@ -1310,7 +1509,10 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   if (k > ozb::kMaxK) return set_err(h, OZMM_ERR_UNSUPPORTED, "k > %d not supported on the GPU path", ozb::kMaxK);
   if (m < 1 || n < 1 || p < 1) return set_err(h, OZMM_ERR_ARG, "split: empty matrix");
   if (m > INT32_MAX || p > INT32_MAX) return set_err(h, OZMM_ERR_ARG, "m, p must fit int32");
-  if (opt && opt->method != OZMM_METHOD_OZIMMU_H)
+  // comparison methods, and calls that need the Checked-overflow verification
+  // (forced beta / r), take the plain copy-in / ozmm_dgemm_ex / copy-out route
+  if ((opt && opt->method != OZMM_METHOD_OZIMMU_H) ||
+      (opt && !opt->overflow_wrap && (opt->force_beta || opt->force_r)))
     return dgemm_host_simple(h, transa, transb, m, n, p, alpha, A, lda, B, ldb, beta, C, ldc, k,
                              opt, counts, timings);
   const bool ta = is_trans(transa), tb = is_trans(transb);
@@ -1333,7 +1535,9 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   // panels: ~16 per operand, A panels in whole CTA-pair tile rows (256), B panels
   // in whole tile columns (128)
   int64_t npanels = 16;
-  if (const char* e = std::getenv("OZMM_HOST_PANELS")) npanels = std::max(1, std::atoi(e));
+  if (opt && opt->host_panels < 0) return set_err(h, OZMM_ERR_ARG, "options: host_panels must be >= 0");
+  if (opt && opt->host_panels) npanels = opt->host_panels;
+  if (const char* e = OZMM_ENV("OZMM_HOST_PANELS")) npanels = std::max(1, std::atoi(e));
   auto round_up = [](int64_t x, int64_t q) { return (x + q - 1) / q * q; };
   int64_t pa = round_up((m + npanels - 1) / npanels, 256), pb = round_up((p + npanels - 1) / npanels, 128);
   if (pa >= m) pa = m;
@@ -1418,7 +1622,7 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   // events: A/B copied [ra + rb], A/B split [ra + rb], C strip copied [ns], GEMM done [ns], start, splits done
   std::vector<cudaEvent_t> ev(2 * (ra + rb) + 2 * ns + 2);
   // OZMM_TRACE=1: timed events and a per-panel / per-strip timeline on stderr
-  const bool trace = std::getenv("OZMM_TRACE") != nullptr;
+  const bool trace = OZMM_ENV("OZMM_TRACE") != nullptr;
   const auto t_entry = std::chrono::steady_clock::now();
   for (auto& e : ev) CUDA_TRY(h, cudaEventCreateWithFlags(&e, trace ? 0 : cudaEventDisableTiming));
   std::vector<cudaEvent_t> evGs(trace ? ns : 0), evO(trace ? ns : 0);
@@ -1476,7 +1680,7 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   };
   if (no_c) {
     int64_t want = 8;
-    if (const char* e = std::getenv("OZMM_SCAN_THREADS")) want = std::max(1, std::atoi(e));
+    if (const char* e = OZMM_ENV("OZMM_SCAN_THREADS")) want = std::max(1, std::atoi(e));
     const int nt = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>({want, static_cast<int64_t>(std::thread::hardware_concurrency()), (m * p) >> 20})));
     bad.resize(nt);
@@ -1522,7 +1726,11 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
     fl.lsb_plane = p;
     fl.n = n;
   }
-  // every stream starts after earlier work on the handle's stream
+  fl.full_mp = m * p;  // the strips are pieces of one m x p problem (kernel tuning)
+  // this call's flags start clear (earlier unreported ones stay pending); every
+  // stream starts after earlier work on the handle's stream
+  fold_flags_kernel<<<1, 1, 0, user>>>(h->flags);
+  cu(cudaGetLastError(), "fold flags");
   cu(cudaEventRecord(evStart, user), "event");
   for (cudaStream_t s : {h->s_in, h->s_out, h->s_split, h->s_gemm[0], h->s_gemm[1]})
     cu(cudaStreamWaitEvent(s, evStart, 0), "wait");

@@ -33,6 +33,10 @@
 
 #include "../../include/ozmm_b200.h"
 
+// library-internal helpers of ozmm_capi.cu (hidden; see there)
+extern "C" int* ozmm_internal_range_flag(ozmm_handle_t h);
+extern "C" int ozmm_internal_fold_flags(ozmm_handle_t h);
+
 namespace {
 
 // ---- NCCL, resolved at run time ------------------------------------------
@@ -119,7 +123,8 @@ struct ozmm_grid {
   double* nu = nullptr;
   int32_t* lsa = nullptr;
   int32_t* lsb = nullptr;
-  size_t a_bytes = 0, b_bytes = 0, mu_n = 0, nu_n = 0, lsa_n = 0, lsb_n = 0;
+  int* gflag = nullptr;  // [pr][pc] range flags of the grid (grid-wide max)
+  size_t a_bytes = 0, b_bytes = 0, mu_n = 0, nu_n = 0, lsa_n = 0, lsb_n = 0, gflag_n = 0;
 };
 
 namespace {
@@ -259,7 +264,8 @@ int ozmm_grid_destroy(ozmm_grid_t g) {
     if (c && n.ok) n.comm_destroy(c);
   for (void* p : {static_cast<void*>(g->a_pan), static_cast<void*>(g->b_pan),
                   static_cast<void*>(g->mu), static_cast<void*>(g->nu),
-                  static_cast<void*>(g->lsa), static_cast<void*>(g->lsb)})
+                  static_cast<void*>(g->lsa), static_cast<void*>(g->lsb),
+                  static_cast<void*>(g->gflag)})
     if (p) cudaFree(p);
   for (cudaEvent_t e : {g->ev_split, g->ev_b, g->ev_a, g->ev_side})
     if (e) cudaEventDestroy(e);
@@ -302,6 +308,7 @@ int ozmm_dgemm_2d(ozmm_grid_t g, char transa, char transb, int64_t m, int64_t n,
   if (int rc = grow(&g->nu, &g->nu_n, static_cast<size_t>(pcols))) return rc;
   if (int rc = grow(&g->lsa, &g->lsa_n, static_cast<size_t>(mr * k))) return rc;
   if (int rc = grow(&g->lsb, &g->lsb_n, static_cast<size_t>(pcols * k))) return rc;
+  if (int rc = grow(&g->gflag, &g->gflag_n, static_cast<size_t>(g->pr) * g->pc)) return rc;
   GRID_CUDA(cudaSetDevice(g->device));
   cudaStream_t main_s = nullptr;
   {
@@ -311,17 +318,44 @@ int ozmm_dgemm_2d(ozmm_grid_t g, char transa, char transb, int64_t m, int64_t n,
   }
   const int64_t r0 = g->gc * ms, c0 = g->gr * ps;  // own rows / columns in the C block
 
-  // 1. split into this rank's slot of the panels (handle stream)
+  // 1. split into this rank's slot of the panels (handle stream); this call's
+  // range flag starts clear
+  GRID_OZ(ozmm_internal_fold_flags(g->h));
   GRID_OZ(ozmm_split_offset_strided(g->h, 'L', transa, ms, n, A, lda, k, beta_bits,
                                     g->a_pan + r0 * lds, lds, plane_a, g->mu + r0,
                                     g->lsa + r0 * k, 1, k));
   GRID_OZ(ozmm_split_offset_strided(g->h, 'R', transb, ps, n, B, ldb, k, beta_bits,
                                     g->b_pan + c0 * lds, lds, plane_b, g->nu + c0,
                                     g->lsb + c0 * k, 1, k));
+  // this rank's range flag into its cell of the [pr][pc] grid matrix
+  int* cell = g->gflag + g->gr * g->pc + g->gc;
+  GRID_CUDA(cudaMemcpyAsync(cell, ozmm_internal_range_flag(g->h), sizeof(int),
+                            cudaMemcpyDeviceToDevice, main_s));
   GRID_CUDA(cudaEventRecord(g->ev_split, main_s));
 
-  // 2. gathers on the comm stream: B (unblocks G2) first, then A
+  // 2. grid-wide range check before anything writes C (the reference throws
+  // from the split, split.cpp:124-125): gather the flags along the grid row,
+  // then the rows along the grid column, and read the whole matrix -- every
+  // rank sees the same flags and returns the same status
   GRID_CUDA(cudaStreamWaitEvent(g->s_comm, g->ev_split, 0));
+  if (int rc = gather_group(g, 0, {{g->gflag + g->gr * g->pc, static_cast<int64_t>(sizeof(int))}}))
+    return rc;
+  if (int rc = gather_group(g, 1, {{g->gflag, static_cast<int64_t>(sizeof(int)) * g->pc}})) return rc;
+  {
+    std::vector<int> flags(static_cast<size_t>(g->pr) * g->pc, 0);
+    GRID_CUDA(cudaMemcpyAsync(flags.data(), g->gflag, sizeof(int) * flags.size(),
+                              cudaMemcpyDeviceToHost, g->s_comm));
+    GRID_CUDA(cudaStreamSynchronize(g->s_comm));
+    for (size_t i = 0; i < flags.size(); ++i)
+      if (flags[i]) {
+        GRID_CUDA(cudaMemsetAsync(ozmm_internal_range_flag(g->h), 0, sizeof(int), main_s));
+        GRID_CUDA(cudaStreamSynchronize(main_s));
+        return fail(OZMM_ERR_RANGE, "split: row magnitude too large for shift extraction "
+                    "(grid rank %zu)", i);
+      }
+  }
+
+  // 3. gathers on the comm stream: B (unblocks G2) first, then A
   {
     std::vector<std::pair<void*, int64_t>> bb, ab;
     for (int s = 0; s < k; ++s) bb.push_back({g->b_pan + s * plane_b, ps * lds});
@@ -336,7 +370,7 @@ int ozmm_dgemm_2d(ozmm_grid_t g, char transa, char transb, int64_t m, int64_t n,
     GRID_CUDA(cudaEventRecord(g->ev_a, g->s_comm));
   }
 
-  // 3. strips
+  // 4. strips
   auto strip = [&](int64_t row0, int64_t rows, int64_t col0, int64_t cols) {
     return ozmm_gemm_slices_offset(g->h, rows, n, cols, k, beta_bits, 0, g->a_pan + row0 * lds,
                                    lds, plane_a, g->mu + row0, g->lsa + row0 * k, 1, k,

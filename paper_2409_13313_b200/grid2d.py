@@ -575,8 +575,10 @@ class NativeGrid2D:
         self.g = g
 
     def _check(self, rc):
+        # OZMM_ERR_RANGE -> OverflowError on every rank (the grid-wide check), the
+        # other codes as in ozmm
         if rc != 0:
-            raise RuntimeError(f"ozmm grid: {self.oz.lib.ozmm_grid_last_error().decode()}")
+            self.oz._raise(rc, f"ozmm grid: {self.oz.lib.ozmm_grid_last_error().decode()}")
 
     def step(self, a_rows, b_cols, c_block, alpha=1.0, beta=0.0):
         self.handle.set_stream(torch.cuda.current_stream(self.device).cuda_stream)

@@ -17,7 +17,12 @@ operator API (/root/reference/proj/include/ozmm/scheme.hpp):
 
 Exceptions follow the reference: ``ConfigError`` (a ``ValueError``, like the
 reference's ``std::invalid_argument`` subclass), ``ValueError`` for
-argument errors, ``OverflowError`` for row magnitudes >= 2^921.
+argument errors, ``OverflowError`` for row magnitudes >= 2^921
+(std::overflow_error, split.cpp:124-125) and ``Int32OverflowError`` (an
+``OverflowError``) for an INT32 chunk overflow in ``OverflowMode.Checked``
+(the reference's ``OverflowError``, int_gemm.hpp:15-26).  Both are raised
+before C is written, on the host path and -- by default (``sync_check=True``)
+-- on the device path too.
 
 Operands may be numpy arrays (host, reference semantics: a NEW result is
 returned and C is untouched) or CUDA float64 torch tensors (device path,
@@ -38,7 +43,7 @@ import numpy as np
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libozmm_b200.so")
 
-OZMM_OK, OZMM_ERR_ARG, OZMM_ERR_CONFIG, OZMM_ERR_RANGE = 0, 1, 2, 3
+OZMM_OK, OZMM_ERR_ARG, OZMM_ERR_CONFIG, OZMM_ERR_RANGE, OZMM_ERR_OVERFLOW = 0, 1, 2, 3, 4
 OZMM_ERR_CUDA, OZMM_ERR_NCCL, OZMM_ERR_UNSUPPORTED = 5, 6, 7
 
 
@@ -69,7 +74,8 @@ class Options(C.Structure):
     _fields_ = [("force_beta", C.c_int), ("force_r", C.c_int64), ("timings", C.c_int),
                 ("sync_check", C.c_int), ("chunk_dump", C.c_void_p), ("tile_n", C.c_int),
                 ("cta_pair", C.c_int), ("method", C.c_int), ("signed_slices", C.c_int),
-                ("c_write_only", C.c_int)]
+                ("c_write_only", C.c_int), ("overflow_wrap", C.c_int), ("kpair", C.c_int),
+                ("stages", C.c_int), ("host_panels", C.c_int)]
 
 
 _SIG = {
@@ -145,6 +151,11 @@ class OzmmCudaError(RuntimeError):
     """CUDA / launch failure inside the library."""
 
 
+class Int32OverflowError(OverflowError):
+    """INT32 chunk overflow in OverflowMode.Checked (the reference's
+    OverflowError, int_gemm.hpp:15-26); reachable only with force_beta / force_r."""
+
+
 def _raise(code: int, msg: str):
     if code == OZMM_ERR_CONFIG:
         raise ConfigError(msg)
@@ -152,6 +163,8 @@ def _raise(code: int, msg: str):
         raise ValueError(msg)
     if code == OZMM_ERR_RANGE:
         raise OverflowError(msg)
+    if code == OZMM_ERR_OVERFLOW:
+        raise Int32OverflowError(msg)
     if code == OZMM_ERR_UNSUPPORTED:
         raise NotImplementedError(msg)
     raise OzmmCudaError(f"[{code}] {msg}")
@@ -182,12 +195,19 @@ class Accumulation(enum.Enum):
     GroupwiseSimple = 2
 
 
+class OverflowMode(enum.Enum):
+    """int_gemm.hpp:13."""
+    Checked = 0
+    Wrapping = 1
+
+
 @dataclass
 class SchemeConfig:
     """scheme.hpp:24-31.  Defaults as the reference (k = 8)."""
     k: int = 8
     strategy: SliceStrategy = SliceStrategy.BitMask
     accumulation: Accumulation = Accumulation.PerProduct
+    overflow: OverflowMode = OverflowMode.Checked
     force_beta: int = 0
     force_r: int = 0
 
@@ -332,12 +352,15 @@ def _is_cuda_tensor(x) -> bool:
 
 
 def _options(cfg: SchemeConfig | None, timings: bool = False, dump=None, tile_n: int = 0,
-             sync_check: bool = False, cta_pair: int = 0, signed_slices: bool = False) -> Options:
+             sync_check: bool = False, cta_pair: int = 0, signed_slices: bool = False,
+             kpair: int = 0, stages: int = 0, host_panels: int = 0) -> Options:
     o = Options()
     if cfg is not None:
         o.force_beta = cfg.force_beta
         o.force_r = cfg.force_r
         o.method = _method_code(cfg)
+        o.overflow_wrap = int(cfg.overflow == OverflowMode.Wrapping)
+    o.kpair, o.stages, o.host_panels = kpair, stages, host_panels
     o.timings = int(timings)
     o.sync_check = int(sync_check)
     o.chunk_dump = dump.data_ptr() if dump is not None else None
@@ -355,6 +378,7 @@ _METHOD_CODES = {
     (SliceStrategy.BitMask, Accumulation.Groupwise): 3,                       # ozIMMU_EF
     (SliceStrategy.RoundNearestConstShift, Accumulation.PerProduct): 4,
     (SliceStrategy.RoundNearestConstShift, Accumulation.GroupwiseSimple): 5,
+    (SliceStrategy.BitMask, Accumulation.GroupwiseSimple): 6,
 }
 
 
@@ -384,7 +408,8 @@ def _to_result(counts: Counts, tim: Timings, d) -> OzakiResult:
 def ozaki_gemm_ex(alpha: float, a, b, beta: float, c, cfg: SchemeConfig | None = None, *,
                   transa: bool = False, transb: bool = False, handle: Handle | None = None,
                   out=None, timings: bool = True, chunk_dump=None,
-                  tile_n: int = 0, signed_slices: bool = False) -> OzakiResult:
+                  tile_n: int = 0, signed_slices: bool = False, sync_check: bool = True,
+                  kpair: int = 0, stages: int = 0, host_panels: int = 0) -> OzakiResult:
     """Emulated DGEMM: alpha * op(A) op(B) + beta * C (scheme.cpp:274-291).
 
     Returns OzakiResult(d=new matrix, counts, timings); C is not modified
@@ -392,6 +417,13 @@ def ozaki_gemm_ex(alpha: float, a, b, beta: float, c, cfg: SchemeConfig | None =
     C m x p, all row-major.  ``signed_slices`` keeps the reference's signed
     int8 planes inside the fused GEMM instead of the default offset-binary ones
     (same results; include/ozmm_b200.h).
+
+    Device path: ``sync_check=True`` (default) waits for the splits and raises
+    OverflowError for a line max >= 2^921 before the GEMM writes ``out``, like
+    the reference's throw.  ``sync_check=False`` keeps the call fully
+    stream-ordered (e.g. inside a CUDA graph); the range error then stays
+    pending on the handle until ``Handle.sync_status()``.  ``kpair``,
+    ``stages``, ``host_panels``: kernel tuning, same results (ozmm_options_t).
     """
     cfg = cfg or config_for(Method.ozIMMU_H, 8)
     _validate(cfg)
@@ -416,7 +448,8 @@ def ozaki_gemm_ex(alpha: float, a, b, beta: float, c, cfg: SchemeConfig | None =
             out = c.clone()
         elif out.data_ptr() != c.data_ptr():
             out.copy_(c)
-        opt = _options(cfg, timings, chunk_dump, tile_n, signed_slices=signed_slices)
+        opt = _options(cfg, timings, chunk_dump, tile_n, sync_check=sync_check,
+                       signed_slices=signed_slices, kpair=kpair, stages=stages)
         h.check(lib.ozmm_dgemm_ex(h.h, b"T" if transa else b"N", b"T" if transb else b"N", m, n,
                                   p, alpha, a.data_ptr(), a.stride(0), b.data_ptr(),
                                   b.stride(0), beta, out.data_ptr(), out.stride(0), cfg.k,
@@ -436,7 +469,8 @@ def ozaki_gemm_ex(alpha: float, a, b, beta: float, c, cfg: SchemeConfig | None =
     res = c.copy() if out is None else out
     if out is not None:
         np.copyto(res, c)
-    opt = _options(cfg, timings, None, tile_n, sync_check=True, signed_slices=signed_slices)
+    opt = _options(cfg, timings, None, tile_n, sync_check=True, signed_slices=signed_slices,
+                   kpair=kpair, stages=stages, host_panels=host_panels)
     h.set_stream(None)
     h.check(lib.ozmm_dgemm_host(h.h, b"T" if transa else b"N", b"T" if transb else b"N", m, n,
                                 p, alpha, a.ctypes.data, a.shape[1], b.ctypes.data, b.shape[1],

@@ -4,7 +4,12 @@
 // the C ABI).  Built by tests/test_dropin_cpp.py against the reference headers
 // and the Eigen shim; prints "MATCH <n>" when every entry is bitwise equal.
 //
-//   dropin_demo <m> <n> <p> <k> <phi> [--closed-forms-only]
+//   dropin_demo <m> <n> <p> <k> <phi> [method] [--closed-forms-only]
+//   method: ozIMMU_H (default) | ozIMMU | ozIMMU_RN | ozIMMU_EF -- the
+//   reference's config_for preset, passed unchanged to both calls; or
+//   "overflow <force_r>": ozIMMU_H with force_r on INT32-overflowing inputs:
+//   Wrapping bit-identical on both sides, Checked throws on the GPU side
+//   (prints "OVERFLOW-OK").
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -27,14 +32,46 @@ int main(int argc, char** argv) {
     std::printf("CLOSED-FORM MISMATCH\n");
     return 1;
   }
-  if (argc > 6 && std::strcmp(argv[6], "--closed-forms-only") == 0) {
+  if (argc > 6 && std::strcmp(argv[argc - 1], "--closed-forms-only") == 0) {
     std::printf("CLOSED-FORMS OK beta=%d r=%lld\n", beta, static_cast<long long>(r));
     return 0;
   }
   const ozmm::MatrixF64 A = ozmm::gen_phi_matrix(m, n, phi, ozmm::counter_hash(1, 1));
   const ozmm::MatrixF64 B = ozmm::gen_phi_matrix(n, p, phi, ozmm::counter_hash(1, 2));
   const ozmm::MatrixF64 C = ozmm::gen_phi_matrix(m, p, phi, ozmm::counter_hash(1, 3));
-  const ozmm::SchemeConfig cfg = ozmm::config_for(ozmm::Method::ozIMMU_H, k);
+  const char* method = argc > 6 ? argv[6] : "ozIMMU_H";
+  if (std::strcmp(method, "overflow") == 0) {
+    // constant operands whose slices are all positive (127, 63, 63, ...): every
+    // product of a group adds up, so long chunks (forced r) leave INT32 once n is
+    // large (n = 65536, k = 14, force_r = 14)
+    const double v = (127.0 + 63.0 / 127.0) / 64.0;
+    ozmm::MatrixF64 Ac(m, n), Bc(n, p), Cc(m, p);
+    for (long i = 0; i < m * n; ++i) Ac.data()[i] = v;
+    for (long i = 0; i < n * p; ++i) Bc.data()[i] = v;
+    for (long i = 0; i < m * p; ++i) Cc.data()[i] = 0.0;
+    ozmm::SchemeConfig cfg = ozmm::config_for(ozmm::Method::ozIMMU_H, k);
+    cfg.force_r = argc > 7 ? std::atol(argv[7]) : 14;
+    // Wrapping: both sides wrap mod 2^32 -- bit-identical results
+    cfg.overflow = ozmm::OverflowMode::Wrapping;
+    const ozmm::OzakiResult ref = ozmm::ozaki_gemm_ex(1.0, Ac, Bc, 0.0, Cc, cfg);
+    const auto gpu = ozmm::gpu::ozaki_gemm_ex(1.0, Ac, Bc, 0.0, Cc, cfg);
+    const bool same = std::memcmp(ref.d.data(), gpu.d.data(), sizeof(double) * m * p) == 0;
+    // Checked: the GPU adapter throws the OverflowError type.  (The reference's
+    // own Checked throw leaves an OpenMP parallel region -- gemm_wide,
+    // int_gemm.cpp:40-52 -- which terminates the process, so it is not called.)
+    cfg.overflow = ozmm::OverflowMode::Checked;
+    bool threw = false;
+    try {
+      (void)ozmm::gpu::ozaki_gemm_ex(1.0, Ac, Bc, 0.0, Cc, cfg);
+    } catch (const ozmm::gpu::OverflowError& e) {
+      threw = true;
+      std::printf("gpu Checked: %s\n", e.what());
+    }
+    std::printf("%s wrapping-match=%d checked-threw=%d\n", same && threw ? "OVERFLOW-OK" : "OVERFLOW-BAD",
+                same, threw);
+    return same && threw ? 0 : 1;
+  }
+  const ozmm::SchemeConfig cfg = ozmm::config_for(ozmm::method_from_string(method), k);
   const ozmm::OzakiResult ref = ozmm::ozaki_gemm_ex(1.5, A, B, 0.5, C, cfg);       // reference
   const auto gpu = ozmm::gpu::ozaki_gemm_ex(1.5, A, B, 0.5, C, cfg);               // B200
   long same = 0;

@@ -32,3 +32,26 @@ def test_dropin_same_call_site_bit_exact(m, n, p, k, phi):
         pytest.skip("no CUDA device")
     out = _run(m, n, p, k, phi)
     assert out.returncode == 0 and out.stdout.startswith("MATCH"), out.stdout + out.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("method", ["ozIMMU", "ozIMMU_RN", "ozIMMU_EF"])
+def test_dropin_comparison_methods_bit_exact(method):
+    """config_for(ozIMMU / ozIMMU_RN / ozIMMU_EF, k) through the same call site: the
+    adapter maps (strategy, accumulation) to the GPU method, never silently to ozIMMU_H."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    out = _run(257, 3000, 190, 9, 2.0, method)
+    assert out.returncode == 0 and out.stdout.startswith("MATCH"), out.stdout + out.stderr
+
+
+@pytest.mark.gpu
+def test_dropin_overflow_modes():
+    """force_r on INT32-overflowing inputs: Wrapping bit-identical to the reference,
+    Checked throws the adapter's OverflowError (int_gemm.hpp:15-26)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    out = _run(32, 65536, 24, 14, 0.0, "overflow", 14)
+    assert out.returncode == 0 and "OVERFLOW-OK" in out.stdout, out.stdout + out.stderr

@@ -303,6 +303,78 @@ def test_native_grid_emulated_ranks(world, trans, k, n):
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
 
 
+@pytest.mark.parametrize("world,bad", [(2, (1, "A")), (4, (2, "B")), (8, (5, "A")), (4, None)])
+def test_native_grid_range_error_reaches_every_rank(world, bad):
+    """ozmm_dgemm_2d: a line max >= 2^921 in ONE rank's shard makes EVERY rank
+    return OZMM_ERR_RANGE (OverflowError) before any strip writes its C block --
+    the grid-wide max of the range flags (row gather, then column gather).
+    bad = None is the negative control (no error anywhere, bit-exact result)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import ctypes
+    import threading
+    from paper_2409_13313_b200 import ozmm
+    from paper_2409_13313_b200.grid2d import NativeGrid2D, make_layout
+    (m, n, p, k, alpha, beta), want, shard = _native_case(False, 8, 700)
+    cudart = ctypes.CDLL("libcudart.so.12")
+    cudart.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+    barriers, pool, lock, errors, outcome = {}, {}, threading.Lock(), [], {}
+
+    def gather(ctx, group, send, recv, nbytes, stream):
+        th = threading.current_thread()
+        L = th.L
+        members = tuple(L.gr * L.pc + c for c in range(L.pc)) if group == 0 else \
+            tuple(r * L.pc + L.gc for r in range(L.pr))
+        with lock:
+            bar = barriers.setdefault(members, threading.Barrier(len(members)))
+            seq = th.seq.setdefault(members, 0)
+            th.seq[members] = seq + 1
+        torch.cuda.synchronize()
+        pool[(members, seq, th.rank)] = send
+        bar.wait(timeout=120)
+        for idx, r in enumerate(members):
+            if r != th.rank:
+                assert cudart.cudaMemcpy(recv + idx * nbytes, pool[(members, seq, r)],
+                                         nbytes, 3) == 0
+        bar.wait(timeout=120)
+        return 0
+    hook = ozmm.ALLGATHER_FN(gather)
+
+    def run(rank):
+        try:
+            th = threading.current_thread()
+            th.rank, th.seq = rank, {}
+            th.L = L = make_layout(m, n, p, world, rank)
+            G = NativeGrid2D(m, n, p, k, world=world, rank=rank, hook=hook)
+            a, b, c = shard(L)
+            if bad is not None and rank == bad[0]:
+                (a if bad[1] == "A" else b)[3, 4] = 2.0 ** 940
+            c0 = c.clone()
+            try:
+                G.step(a, b, c, alpha, beta)
+                torch.cuda.synchronize()
+                outcome[rank] = ("ok", torch.equal(c.cpu(), torch.from_numpy(
+                    want[L.c_row0:L.c_row0 + L.mr, L.c_col0:L.c_col0 + L.pcols])))
+            except OverflowError:
+                torch.cuda.synchronize()
+                outcome[rank] = ("OverflowError", torch.equal(c.view(torch.int64),
+                                                              c0.view(torch.int64)))
+            G.close()
+        except BaseException as ex:
+            errors.append(ex)
+            for b_ in list(barriers.values()):
+                b_.abort()
+
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not errors, errors
+    expect = "OverflowError" if bad is not None else "ok"
+    assert outcome == {r: (expect, True) for r in range(world)}, outcome
+
+
 def test_grid2d_cuda_sync_check_range_error():
     """Grid2DGemm.step(sync_check=True) on the CUDA backend: a line max >= 2^921
     raises OverflowError before any GEMM (C untouched), the flag is cleared, and

@@ -1,0 +1,186 @@
+"""Error semantics of the drop-in boundary on the GPU, against the reference's.
+
+* Range errors (row max >= 2^921): the reference throws std::overflow_error
+  from the split, before anything is written (split.cpp:124-125).  The device
+  path raises by default too (sync_check), the deferred mode keeps the flag
+  for Handle.sync_status(), and a pending flag is never blamed on a later call
+  on the same handle (include/ozmm_b200.h, ozmm_sync_status).
+* INT32 chunk overflow in OverflowMode::Checked: the reference's gemm_wide
+  checks every running chunk sum (int_gemm.cpp:37-59) -- reachable only with
+  force_r / force_beta.  The GPU verifies exactly and raises
+  Int32OverflowError before C is written; in Wrapping mode both sides wrap mod
+  2^32 and agree bit for bit.  (The reference's own Checked throw escapes an
+  OpenMP parallel region and terminates the process, so Checked is compared
+  with the C port, which returns the error, and Wrapping with the reference.)
+"""
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+from tests.helpers import assert_bitwise
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def oz():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2409_13313_b200 import ozmm
+    return ozmm
+
+
+@pytest.fixture(scope="module")
+def checker():
+    from oracle import oracle
+    if not os.path.exists(oracle.PORT_SO):
+        oracle.build()
+    return oracle.best()
+
+
+def dev(x):
+    return torch.tensor(np.ascontiguousarray(x), dtype=torch.float64, device="cuda")
+
+
+def inputs(oz, m, n, p, seed, phi=1.0):
+    return (oz.gen_phi_matrix(m, n, phi, seed), oz.gen_phi_matrix(n, p, phi, seed + 1),
+            oz.gen_phi_matrix(m, p, phi, seed + 2))
+
+
+def test_device_range_error_raises_and_next_host_call_is_clean(oz, checker):
+    """The ADVICE scenario: a device-path range error on the shared default handle
+    must raise there (C untouched) and must not leak into the next host call."""
+    m, n, p = 300, 700, 200
+    A, B, C = inputs(oz, m, n, p, 11)
+    bad = A.copy()
+    bad[123, 45] = 2.0 ** 950
+    cfg = oz.config_for("ozIMMU_H", 8)
+    c_dev = dev(C)
+    with pytest.raises(OverflowError):
+        oz.ozaki_gemm(1.0, dev(bad), dev(B), 0.5, c_dev, cfg, out=c_dev)
+    assert_bitwise(c_dev.cpu().numpy(), C, "C after a device range error")
+    # same (default) handle: host entry, then device entry, both bit-exact
+    want = checker.gemm(1.0, A, B, 0.5, C, k=8)
+    assert_bitwise(oz.ozaki_gemm(1.0, A, B, 0.5, C, cfg), want, "host call after the error")
+    assert_bitwise(oz.ozaki_gemm(1.0, dev(A), dev(B), 0.5, dev(C), cfg).cpu().numpy(), want,
+                   "device call after the error")
+    assert oz.default_handle(0).sync_status() in (False, True)   # nothing pending: no raise
+
+
+def test_deferred_range_error_stays_pending(oz, checker):
+    """sync_check=False: stream-ordered, no raise; later calls on the handle report
+    only their own status; Handle.sync_status() returns the pending error once."""
+    m, n, p = 256, 500, 192
+    A, B, C = inputs(oz, m, n, p, 21)
+    bad = A.copy()
+    bad[0, 0] = -(2.0 ** 921)
+    cfg = oz.config_for("ozIMMU_H", 8)
+    h = oz.Handle(0)
+    oz.ozaki_gemm(1.0, dev(bad), dev(B), 0.0, dev(C), cfg, handle=h, sync_check=False)
+    want = checker.gemm(1.0, A, B, 0.0, C, k=8)
+    got = oz.ozaki_gemm(1.0, dev(A), dev(B), 0.0, dev(C), cfg, handle=h)   # sync_check on
+    assert_bitwise(got.cpu().numpy(), want, "clean device call after a deferred error")
+    assert_bitwise(oz.ozaki_gemm(1.0, A, B, 0.0, C, cfg, handle=h), want,
+                   "clean host call after a deferred error")
+    with pytest.raises(OverflowError):
+        h.sync_status()
+    h.sync_status()   # reported once, then clear
+    h.close()
+
+
+def _overflow_inputs(m, n, p):
+    # slices 127, 63, 63, ... (all positive): the products of a group add up
+    v = (127 + 63 / 127) / 64
+    return np.full((m, n), v), np.full((n, p), v), np.zeros((m, p))
+
+
+@pytest.mark.parametrize("path", ["device", "host"])
+def test_checked_overflow_raises_like_the_reference(oz, path):
+    from oracle import oracle
+    port = oracle.PortLib()
+    m, n, p, k = 64, 65536, 48, 14
+    A, B, C = _overflow_inputs(m, n, p)
+    with pytest.raises(oracle.OracleError) as e:             # the reference semantics
+        port.gemm(1.0, A, B, 0.0, C, k=k, force_r=14)
+    assert e.value.code == oracle.ERR_OVERFLOW
+    cfg = oz.config_for("ozIMMU_H", k)
+    cfg.force_r = 14
+    if path == "device":
+        out = dev(np.full((m, p), 7.0))
+        with pytest.raises(oz.Int32OverflowError, match="INT32 overflow at"):
+            oz.ozaki_gemm(1.0, dev(A), dev(B), 0.0, dev(C), cfg, out=out)
+        assert bool((out == 7.0).all()), "C written despite the overflow"
+    else:
+        out = np.full((m, p), 7.0)
+        with pytest.raises(oz.Int32OverflowError):
+            oz.ozaki_gemm(1.0, A, B, 0.0, C, cfg, out=out)
+        assert (out == 7.0).all()
+
+
+@pytest.mark.parametrize("path", ["device", "host"])
+def test_wrapping_overflow_bit_exact(oz, checker, path):
+    """OverflowMode::Wrapping: the reference wraps each running sum mod 2^32
+    (int_gemm.cpp:50-51), so does the tensor core."""
+    m, n, p, k = 64, 65536, 48, 14
+    A, B, C = _overflow_inputs(m, n, p)
+    want = checker.gemm(1.0, A, B, 0.0, C, k=k, force_r=14, wrapping=True)
+    cfg = oz.config_for("ozIMMU_H", k)
+    cfg.force_r, cfg.overflow = 14, oz.OverflowMode.Wrapping
+    got = oz.ozaki_gemm(1.0, dev(A), dev(B), 0.0, dev(C), cfg).cpu().numpy() \
+        if path == "device" else oz.ozaki_gemm(1.0, A, B, 0.0, C, cfg)
+    assert_bitwise(got, want)
+    # and the wrapped result differs from the unforced (r = 2) one: overflow happened
+    assert not np.array_equal(got, checker.gemm(1.0, A, B, 0.0, C, k=k))
+
+
+def test_checked_no_overflow_with_forced_r_is_bit_exact(oz, checker):
+    """Forced r whose chunks could overflow but do not (random data): the verification
+    passes and the result is the reference's."""
+    m, n, p, k = 200, 40000, 150, 12
+    A, B, C = inputs(oz, m, n, p, 31, phi=0.5)
+    cfg = oz.config_for("ozIMMU_H", k)
+    cfg.force_r = 12
+    want = checker.gemm(1.25, A, B, 0.5, C, k=k, force_r=12)
+    assert_bitwise(oz.ozaki_gemm(1.25, dev(A), dev(B), 0.5, dev(C), cfg).cpu().numpy(), want)
+    assert_bitwise(oz.ozaki_gemm(1.25, A, B, 0.5, C, cfg), want)
+
+
+def test_c_write_only_needs_positive_alpha(oz):
+    """c_write_only drops fl(beta*c); with alpha <= 0 the sign of a zero would come
+    from it (-0 + +0 = +0), so the slice-level entry rejects it."""
+    m, n, p, k = 64, 64, 64, 2
+    lds = oz.slice_ld(n)
+    s = torch.zeros((k, m, lds), dtype=torch.int8, device="cuda")
+    sh = torch.ones(m, dtype=torch.float64, device="cuda")
+    c = torch.zeros((m, p), dtype=torch.float64, device="cuda")
+    h = oz.default_handle(0)
+    for alpha, ok in ((-1.0, False), (0.0, False), (-0.0, False), (2.0, True)):
+        opt = oz.Options()
+        opt.c_write_only = 1
+        rc = oz.lib.ozmm_gemm_slices(h.h, m, n, p, k, 7, 0, s.data_ptr(), lds, sh.data_ptr(),
+                                     s.data_ptr(), lds, sh.data_ptr(), alpha, 0.0, c.data_ptr(),
+                                     p, ctypes.byref(opt))
+        assert (rc == oz.OZMM_OK) == ok, (alpha, rc)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("method", ["ozIMMU", "ozIMMU_RN", "ozIMMU_EF", "ozIMMU_H"])
+def test_methods_through_host_entry(oz, checker, method):
+    m, n, p, k = 200, 1500, 170, 9
+    A, B, C = inputs(oz, m, n, p, 41, phi=2.0)
+    want = checker.gemm(1.5, A, B, 0.5, C, k=k, method=method)
+    assert_bitwise(oz.ozaki_gemm(1.5, A, B, 0.5, C, oz.config_for(method, k)), want, method)
+
+
+def test_groupwise_simple_bitmask(oz, checker):
+    """(BitMask, GroupwiseSimple): valid in the reference when r >= k."""
+    m, n, p, k = 128, 1024, 96, 8
+    A, B, C = inputs(oz, m, n, p, 51)
+    cfg = oz.config_for("ozIMMU_EF", k)
+    cfg.accumulation = oz.Accumulation.GroupwiseSimple
+    want = checker.gemm(1.0, A, B, 0.0, C, k=k, method="ozIMMU_EF")   # r = 128 >= k: same chunks
+    assert_bitwise(oz.ozaki_gemm(1.0, dev(A), dev(B), 0.0, dev(C), cfg).cpu().numpy(), want)
