@@ -409,7 +409,8 @@ def ozaki_gemm_ex(alpha: float, a, b, beta: float, c, cfg: SchemeConfig | None =
                   transa: bool = False, transb: bool = False, handle: Handle | None = None,
                   out=None, timings: bool = True, chunk_dump=None,
                   tile_n: int = 0, signed_slices: bool = False, sync_check: bool = True,
-                  kpair: int = 0, stages: int = 0, host_panels: int = 0) -> OzakiResult:
+                  kpair: int = 0, stages: int = 0, host_panels: int = 0,
+                  cta_pair: int = 0) -> OzakiResult:
     """Emulated DGEMM: alpha * op(A) op(B) + beta * C (scheme.cpp:274-291).
 
     Returns OzakiResult(d=new matrix, counts, timings); C is not modified
@@ -423,7 +424,8 @@ def ozaki_gemm_ex(alpha: float, a, b, beta: float, c, cfg: SchemeConfig | None =
     the reference's throw.  ``sync_check=False`` keeps the call fully
     stream-ordered (e.g. inside a CUDA graph); the range error then stays
     pending on the handle until ``Handle.sync_status()``.  ``kpair``,
-    ``stages``, ``host_panels``: kernel tuning, same results (ozmm_options_t).
+    ``stages``, ``host_panels``, ``cta_pair``: kernel tuning, same results
+    (ozmm_options_t).
     """
     cfg = cfg or config_for(Method.ozIMMU_H, 8)
     _validate(cfg)
@@ -444,18 +446,21 @@ def ozaki_gemm_ex(alpha: float, a, b, beta: float, c, cfg: SchemeConfig | None =
             raise ValueError("ozaki_gemm: C shape mismatch")
         h = handle or default_handle(a.device.index or 0)
         h.set_stream(torch.cuda.current_stream(a.device).cuda_stream)
-        if out is None:
-            out = c.clone()
-        elif out.data_ptr() != c.data_ptr():
-            out.copy_(c)
+        # C is read and written in place by the C ABI, which leaves it untouched on
+        # every error; a distinct ``out`` is filled only after the call succeeded
+        dst = c.clone() if out is None or out.data_ptr() != c.data_ptr() else out
         opt = _options(cfg, timings, chunk_dump, tile_n, sync_check=sync_check,
-                       signed_slices=signed_slices, kpair=kpair, stages=stages)
+                       signed_slices=signed_slices, kpair=kpair, stages=stages,
+                       cta_pair=cta_pair)
         h.check(lib.ozmm_dgemm_ex(h.h, b"T" if transa else b"N", b"T" if transb else b"N", m, n,
                                   p, alpha, a.data_ptr(), a.stride(0), b.data_ptr(),
-                                  b.stride(0), beta, out.data_ptr(), out.stride(0), cfg.k,
+                                  b.stride(0), beta, dst.data_ptr(), dst.stride(0), cfg.k,
                                   C.byref(opt), C.byref(counts),
                                   C.byref(tim) if timings else None))
-        return _to_result(counts, tim, out)
+        if out is not None and dst is not out:
+            out.copy_(dst)
+            dst = out
+        return _to_result(counts, tim, dst)
     a = np.ascontiguousarray(a, dtype=np.float64)
     b = np.ascontiguousarray(b, dtype=np.float64)
     c = np.ascontiguousarray(c, dtype=np.float64)
@@ -466,16 +471,20 @@ def ozaki_gemm_ex(alpha: float, a, b, beta: float, c, cfg: SchemeConfig | None =
     if c.shape != (m, p):
         raise ValueError("ozaki_gemm: C shape mismatch")
     h = handle or default_handle(0)
-    res = c.copy() if out is None else out
-    if out is not None:
-        np.copyto(res, c)
+    # in place only when ``out`` is C itself; otherwise ``out`` is filled after success
+    inplace = (out is not None and out.flags.c_contiguous and out.shape == c.shape
+               and out.ctypes.data == c.ctypes.data)
+    res = out if inplace else c.copy()
     opt = _options(cfg, timings, None, tile_n, sync_check=True, signed_slices=signed_slices,
-                   kpair=kpair, stages=stages, host_panels=host_panels)
+                   kpair=kpair, stages=stages, host_panels=host_panels, cta_pair=cta_pair)
     h.set_stream(None)
     h.check(lib.ozmm_dgemm_host(h.h, b"T" if transa else b"N", b"T" if transb else b"N", m, n,
                                 p, alpha, a.ctypes.data, a.shape[1], b.ctypes.data, b.shape[1],
                                 beta, res.ctypes.data, p, cfg.k, C.byref(opt), C.byref(counts),
                                 C.byref(tim) if timings else None))
+    if out is not None and res is not out:
+        np.copyto(out, res)
+        res = out
     return _to_result(counts, tim, res)
 
 
