@@ -110,6 +110,7 @@ struct GemmParams {
   uint16_t p_g0[kMaxPasses], p_g1[kMaxPasses];
   uint8_t ag_s[kMaxAGroups];
   uint16_t ag_p0[kMaxAGroups], ag_p1[kMaxAGroups];
+  int b_buf_slots;     // CTA-pair kernel: B slice tiles per B buffer (sized per launch)
 };
 
 template <int kBN>

@@ -37,7 +37,27 @@ constexpr int kPairThreads = 384;
 constexpr int kPairEpiWarps = 8;  // per CTA
 constexpr int kKB = 128;          // bytes of K per block (= one 128B swizzle row)
 constexpr int kBBufs = 2;
-
+// Shared-memory header in front of the operand pools (byte offsets): barriers,
+// TMEM slot, the tile's column shifts nu, their exponents for the fast flush, and
+// the per-column offset corrections of a batch.
+constexpr int kHdrTmem = 512, kHdrNu = 1024, kHdrEc = 2048, kHdrCcol = 3072;
+constexpr int kPairHdr = 5120;
+// diagnostics (OZMM_TILE_TRACE, -DOZMM_DIAG builds): per-CTA stamps 0..7 (globaltimer,
+// see below) and wait accounting in SM clocks: 8 MMA thread on A tiles, 9 on B
+// tiles, 10 on TMEM (epilogue drain), 11 MMA thread total; 12/13 globaltimer when
+// the epilogue sees batch 0 / the last batch complete; 14/15 producer on free A / B
+// slots
+constexpr int kTraceSlots = 16;
+#ifdef OZMM_DIAG
+#define OZMM_TWAIT(slot, call)                    \
+  do {                                            \
+    const long long tw0_ = trace ? clock64() : 0; \
+    call;                                         \
+    if (trace) tw_[slot] += clock64() - tw0_;     \
+  } while (0)
+#else
+#define OZMM_TWAIT(slot, call) call
+#endif
 template <int kBN, int kPairs = 1>
 struct PairCfg {
   static constexpr int kNAcc = 512 / kBN;
@@ -47,8 +67,14 @@ struct PairCfg {
   static constexpr uint32_t kATile = kBM * kKB;           // 16 KB
   static constexpr uint32_t kBTile = kBHalf * kKB;        // bytes per CTA per B slice
   static constexpr int kMaxBSlots = 8;                    // B slices resident per K block
-  static constexpr uint32_t kBBuf = kMaxBSlots * kBTile;  // one B buffer
   static constexpr uint32_t kIdesc = ptx::idesc_i8(2 * kBM, kBN);
+  static constexpr int kMaxStages = (512 - 16 - 8 * 2 * kBBufs) / 16;  // barrier header room
+  // host: dynamic shared memory for B buffers of b_slots tiles and `stages` A stages
+  static constexpr size_t smem_bytes(int b_slots, int stages) {
+    return 1024 + kPairHdr + size_t(kBBufs) * b_slots * kBTile + size_t(stages) * kATile;
+  }
+  // the C pass stages the 128 x kBN FP64 tile (rows padded by one double) in the pools
+  static constexpr size_t kStageBytes = size_t(kBM) * (kBN + 1) * 8;
 };
 
 // kPairs = 2: a 4-CTA cluster of two CTA pairs side by side along N that share
@@ -65,27 +91,30 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
                             const __grid_constant__ GemmParams P) {
   using Cfg = PairCfg<kBN, kPairs>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned (128-byte swizzle atoms); pointer arithmetic on smem_raw keeps
+  // the shared state space visible to the compiler (LDS/STS, not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int n_a = P.stages;  // A ring depth
-  uint8_t* bbuf = smem;
-  uint8_t* aring = smem + kBBufs * Cfg::kBBuf;
-  // offset mode: the batch's per-column corrections [kNAcc][kBN] (int32)
-  uint32_t* ccol = reinterpret_cast<uint32_t*>(aring + n_a * Cfg::kATile);
-  uint64_t* b_full = reinterpret_cast<uint64_t*>(ccol + (P.bias ? Cfg::kNAcc * kBN : 0));
+  const uint32_t b_buf = static_cast<uint32_t>(P.b_buf_slots) * Cfg::kBTile;  // one B buffer
+  uint64_t* b_full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* b_empty = b_full + kBBufs;
   uint64_t* a_full = b_empty + kBBufs;
   uint64_t* a_empty = a_full + n_a;
   uint64_t* tmem_full = a_empty + n_a;
   uint64_t* tmem_empty = tmem_full + 1;
-  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tmem_empty + 1);
-  double* nu_s = reinterpret_cast<double*>(tmem_base_smem + 4);
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(smem + kHdrTmem);
+  double* nu_s = reinterpret_cast<double*>(smem + kHdrNu);
+  int32_t* ec20 = reinterpret_cast<int32_t*>(smem + kHdrEc);  // exponent of nu_j << 20
+  // offset mode: the batch's per-column corrections [kNAcc][kBN] (int32)
+  uint32_t* ccol = reinterpret_cast<uint32_t*>(smem + kHdrCcol);
+  uint8_t* bbuf = smem + kPairHdr;
+  uint8_t* aring = bbuf + kBBufs * b_buf;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   // diagnostics: stamps 0 start, 1 prologue done, 2 first MMA issued, 3 batch 0
   // drained, 4 second batch's first MMA, 5 last batch drained, 6 C written, 7 end
-  uint64_t* trace = P.tile_trace ? P.tile_trace + static_cast<int64_t>(blockIdx.x) * 8 : nullptr;
+  uint64_t* trace = P.tile_trace ? P.tile_trace + static_cast<int64_t>(blockIdx.x) * kTraceSlots : nullptr;
   if (trace && threadIdx.x == 0) trace[0] = ptx::globaltimer();
   const uint32_t rank = ptx::cluster_ctarank();
   const uint32_t lead_rank = rank & ~1u;      // leader of this CTA's pair
@@ -123,7 +152,10 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
   if (warp == 1) ptx::tmem_alloc_pair<512>(tmem_base_smem);
   for (int j = threadIdx.x; j < kBN; j += blockDim.x) {
     const int col = col_tile * kBN + j;
-    nu_s[j] = col < P.p ? P.nu[col] : 0.0;
+    const double nu = col < P.p ? P.nu[col] : 0.0;
+    nu_s[j] = nu;
+    // unbiased exponent << 20 (the high word's exponent field) for the fast flush
+    ec20[j] = static_cast<int32_t>(((__double2hiint(nu) >> 20) & 0x7FF) - 1023) * (1 << 20);
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();  // barrier inits + TMEM address visible cluster-wide
@@ -134,6 +166,8 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
     if (ptx::elect_one()) {
+      long long tw_[16] = {};
+      (void)tw_;
       int bi = 0, ai = 0;
       uint32_t bph = 0, aph = 0;
       const int b_row = col_tile * kBN + static_cast<int>(rank & 1u) * Cfg::kBHalf;
@@ -144,14 +178,14 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
         const int blo = P.p_blo[q], bhi = P.p_bhi[q], g0 = P.p_g0[q], g1 = P.p_g1[q];
         const uint32_t btx = 2u * (bhi - blo + 1) * Cfg::kBTile;
         const int nbw = bhi - blo + 1;
-        if (kPairs == 1 && P.kpair && 2 * nbw <= Cfg::kMaxBSlots && n_kb % 2 == 0) {
+        if (kPairs == 1 && P.kpair && 2 * nbw <= P.b_buf_slots && n_kb % 2 == 0) {
           // K-pair pass: one B buffer holds K blocks kb and kb+1; each A group loads
           // both of its K blocks into consecutive ring slots
           for (int kb = 0; kb < n_kb; kb += 2) {
-            ptx::mbar_wait(b_empty + bi, bph ^ 1);
+            OZMM_TWAIT(15, ptx::mbar_wait(b_empty + bi, bph ^ 1));
             const uint32_t fb = ptx::mapa_shared(b_full + bi, lead_rank);
             if (leader) ptx::mbar_arrive_expect_tx(b_full + bi, 2u * btx);
-            uint8_t* dst = bbuf + bi * Cfg::kBBuf;
+            uint8_t* dst = bbuf + bi * b_buf;
             for (int h = 0; h < 2; ++h)
               for (int t = blo; t <= bhi; ++t)
                 ptx::tma_load_3d_pair_hint(dst + (h * nbw + t - blo) * Cfg::kBTile, &map_b, fb,
@@ -162,7 +196,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
             }
             for (int g = g0; g < g1; ++g)
               for (int h = 0; h < 2; ++h) {
-                ptx::mbar_wait(a_empty + ai, aph ^ 1);
+                OZMM_TWAIT(14, ptx::mbar_wait(a_empty + ai, aph ^ 1));
                 const uint32_t fa = ptx::mapa_shared(a_full + ai, lead_rank);
                 if (leader) ptx::mbar_arrive_expect_tx(a_full + ai, 2u * Cfg::kATile);
                 ptx::tma_load_3d_pair_hint(aring + ai * Cfg::kATile, &map_a, fa, (kb + h) * kKB,
@@ -176,11 +210,11 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
           continue;
         }
         for (int kb = 0; kb < n_kb; ++kb) {
-          ptx::mbar_wait(b_empty + bi, bph ^ 1);
+          OZMM_TWAIT(15, ptx::mbar_wait(b_empty + bi, bph ^ 1));
           {
             const uint32_t fb = ptx::mapa_shared(b_full + bi, lead_rank);
             if (leader) ptx::mbar_arrive_expect_tx(b_full + bi, btx);
-            uint8_t* dst = bbuf + bi * Cfg::kBBuf;
+            uint8_t* dst = bbuf + bi * b_buf;
             for (int t = blo; t <= bhi; ++t)
               ptx::tma_load_3d_pair_hint(dst + (t - blo) * Cfg::kBTile, &map_b, fb, kb * kKB,
                                          b_row, t - 1, pol_b);
@@ -190,7 +224,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
             bph ^= 1;
           }
           for (int g = g0; g < g1; ++g) {
-            ptx::mbar_wait(a_empty + ai, aph ^ 1);
+            OZMM_TWAIT(14, ptx::mbar_wait(a_empty + ai, aph ^ 1));
             const uint32_t fa = ptx::mapa_shared(a_full + ai, lead_rank);
             if (leader) ptx::mbar_arrive_expect_tx(a_full + ai, 2u * Cfg::kATile);
             if constexpr (kPairs == 1)
@@ -206,6 +240,9 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
           }
         }
       }
+#ifdef OZMM_DIAG
+      if (trace && leader) trace[14] = tw_[14], trace[15] = tw_[15];
+#endif
     }
   } else if (warp == 1) {
     // ------------------------------------------- MMA issuer (leader CTA)
@@ -216,28 +253,33 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
     const uint32_t idesc = P.bias ? (Cfg::kIdesc & ~((1u << 7) | (1u << 10))) : Cfg::kIdesc;
 #endif
     if (leader) {
+      long long tw_[16] = {};
+      (void)tw_;
+#ifdef OZMM_DIAG
+      const long long t_mma0 = clock64();
+#endif
       int bi = 0, ai = 0;
       uint32_t bph = 0, aph = 0;
       for (int b = 0; b < P.nbatch; ++b) {
-        ptx::mbar_wait(tmem_empty, (b & 1) ^ 1);
+        OZMM_TWAIT(10, ptx::mbar_wait(tmem_empty, (b & 1) ^ 1));
         ptx::tc_fence_after();
         for (int q = P.b_pass0[b]; q < P.b_pass1[b]; ++q) {
           const int blo = P.p_blo[q], g0 = P.p_g0[q], g1 = P.p_g1[q];
           const int nbw = P.p_bhi[q] - blo + 1;
-          if (kPairs == 1 && P.kpair && 2 * nbw <= Cfg::kMaxBSlots && n_kb % 2 == 0) {
+          if (kPairs == 1 && P.kpair && 2 * nbw <= P.b_buf_slots && n_kb % 2 == 0) {
             // K-pair pass: each product's MMAs for K blocks kb and kb+1 back to
             // back -- runs of 8 MMAs on one accumulator instead of 4
             for (int kb = 0; kb < n_kb; kb += 2) {
-              ptx::mbar_wait(b_full + bi, bph);
+              OZMM_TWAIT(9, ptx::mbar_wait(b_full + bi, bph));
               ptx::tc_fence_after();
               if (trace && kb == 0 && q == P.b_pass0[b] && b < 2 && lane == 0) trace[2 + 2 * b] = ptx::globaltimer();
-              const uint64_t bdesc0 = ptx::smem_desc(ptx::smem_u32(bbuf + bi * Cfg::kBBuf), 1024, 2);
+              const uint64_t bdesc0 = ptx::smem_desc(ptx::smem_u32(bbuf + bi * b_buf), 1024, 2);
               const uint32_t bstep = (nbw * Cfg::kBTile) >> 4;  // K block kb+1's tiles
               for (int g = g0; g < g1; ++g) {
                 const int s1 = ai + 1 == n_a ? 0 : ai + 1;
                 const uint32_t ph1 = ai + 1 == n_a ? aph ^ 1 : aph;
-                ptx::mbar_wait(a_full + ai, aph);
-                ptx::mbar_wait(a_full + s1, ph1);
+                OZMM_TWAIT(8, ptx::mbar_wait(a_full + ai, aph));
+                OZMM_TWAIT(8, ptx::mbar_wait(a_full + s1, ph1));
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
                   const uint64_t ad0 = ptx::smem_desc(ptx::smem_u32(aring + ai * Cfg::kATile), 1024, 2);
@@ -275,10 +317,10 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
             continue;
           }
           for (int kb = 0; kb < n_kb; ++kb) {
-            ptx::mbar_wait(b_full + bi, bph);
+            OZMM_TWAIT(9, ptx::mbar_wait(b_full + bi, bph));
             ptx::tc_fence_after();
             if (trace && kb == 0 && q == P.b_pass0[b] && b < 2 && lane == 0) trace[2 + 2 * b] = ptx::globaltimer();
-            const uint32_t sb = ptx::smem_u32(bbuf + bi * Cfg::kBBuf);
+            const uint32_t sb = ptx::smem_u32(bbuf + bi * b_buf);
             const uint64_t bdesc0 = ptx::smem_desc(sb, 1024, 2);
             for (int g = g0; g < g1; ++g) {
               if (P.group_pairs > 1 && g + 1 < g1) {
@@ -289,7 +331,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
                   int sl = ai;
                   uint32_t ph = aph;
                   for (int h2 = 0; h2 < ng; ++h2) {
-                    ptx::mbar_wait(a_full + sl, ph);
+                    OZMM_TWAIT(8, ptx::mbar_wait(a_full + sl, ph));
                     if (++sl == n_a) sl = 0, ph ^= 1;
                   }
                 }
@@ -329,7 +371,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
                   }
                 continue;
               }
-              ptx::mbar_wait(a_full + ai, aph);
+              OZMM_TWAIT(8, ptx::mbar_wait(a_full + ai, aph));
               ptx::tc_fence_after();
               if (ptx::elect_one()) {
                 const uint64_t adesc = ptx::smem_desc(ptx::smem_u32(aring + ai * Cfg::kATile), 1024, 2);
@@ -367,6 +409,12 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
         if (ptx::elect_one()) ptx::mma_commit_pair(tmem_full, pair_mask);
         __syncwarp();
       }
+#ifdef OZMM_DIAG
+      if (trace && lane == 0) {
+        trace[8] = tw_[8], trace[9] = tw_[9], trace[10] = tw_[10];
+        trace[11] = clock64() - t_mma0;
+      }
+#endif
     }
   } else if (warp >= 4) {
     // --------------------------------------------------------- epilogue
@@ -382,6 +430,23 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
     double d[kCols];
 #pragma unroll
     for (int j = 0; j < kCols; ++j) d[j] = 0.0;
+    // fast-flush preconditions (see the chunk loop): group-wise scaling, mu a normal
+    // power of two (or 0: a zero row), and this warp's column shifts normal powers of
+    // two (or 0), with their exponent range [ec_lo, ec_hi] -- warp-uniform
+    const uint32_t mu_hi = static_cast<uint32_t>(__double2hiint(mu));
+    const int mu_e = static_cast<int>((mu_hi >> 20) & 0x7FF) - 1023;
+    bool fast_ok = P.scale_mode == 0 &&
+                   (mu == 0.0 || (mu_e > -1023 && (mu_hi & 0xFFFFF) == 0 && __double2loint(mu) == 0));
+    int ec_lo = 4096, ec_hi = -4096;
+    for (int j = 0; j < kCols; ++j) {
+      const double nu = nu_s[cslice * kCols + j];
+      if (nu == 0.0) continue;
+      const uint32_t hi = static_cast<uint32_t>(__double2hiint(nu));
+      const int e = static_cast<int>((hi >> 20) & 0x7FF) - 1023;
+      if (e == -1023 || (hi & 0xFFFFF) != 0 || __double2loint(nu) != 0) fast_ok = false;
+      ec_lo = min(ec_lo, e);
+      ec_hi = max(ec_hi, e);
+    }
 
     const uint32_t o1 = (1u << P.beta) - 1u, os = 1u << (P.beta - 1);  // slice offsets
     // C is read once, after the last MMA: pull this CTA's 128 rows x kBN columns
@@ -415,40 +480,94 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
         }
         asm volatile("bar.sync 1, %0;" ::"r"(kPairEpiWarps * 32) : "memory");
       }
-      ptx::mbar_wait(tmem_full, b & 1);
-      ptx::tc_fence_after();
-      for (int ci = 0; ci < nc; ++ci) {
-        const int c = c0 + ci;
-        const double ru = flush_row_scale(P, c, row, mu);
-        uint32_t rrow = 0;  // per-row part: sum_{(s,t)} o_t lsa[s][row]
-        if (P.bias && row_ok)
+      // per-row part of the offset corrections, sum_{(s,t) in chunk} o_t lsa[s][row],
+      // loaded before the wait so the drain does not start with global loads
+      uint32_t rrow[Cfg::kNAcc];
+#pragma unroll
+      for (int ci = 0; ci < Cfg::kNAcc; ++ci) {
+        rrow[ci] = 0;
+        if (P.bias && row_ok && ci < nc) {
+          const int c = c0 + ci;
           for (int s = P.c_s[c]; s <= P.c_e[c]; ++s) {
             const int t = P.c_g[c] - s;
-            rrow += (t == 1 ? o1 : os) * static_cast<uint32_t>(P.lsa[(s - 1) * P.lsa_plane + row * P.lsa_lstride]);
+            rrow[ci] += (t == 1 ? o1 : os) * static_cast<uint32_t>(P.lsa[(s - 1) * P.lsa_plane + row * P.lsa_lstride]);
           }
+        }
+      }
+      ptx::mbar_wait(tmem_full, b & 1);
+      ptx::tc_fence_after();
+      if (trace && warp == 4 && lane == 0 && (b == 0 || b == P.nbatch - 1))
+        trace[b == 0 ? 12 : 13] = ptx::globaltimer();
+#pragma unroll 1
+      for (int ci = 0; ci < nc; ++ci) {
+        const int c = c0 + ci;
+        uint32_t rr = rrow[0];
 #pragma unroll
-        for (int cc = 0; cc < kCols; cc += kLd) {
-          uint32_t v[kLd];
-          ptx::tmem_ld_32x32b<kLd>(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
-                                       ci * kBN + cslice * kCols + cc,
-                                   v);
-          ptx::tmem_ld_wait();
-          if (P.bias) {
+        for (int x = 1; x < Cfg::kNAcc; ++x)
+          if (ci == x) rr = rrow[x];
+        const uint32_t* cc_s = ccol + ci * kBN + cslice * kCols;
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + ci * kBN + cslice * kCols;
+        // Fast flush (group-wise scaling): ru = mu 2^(2 - beta g) and cv = nu_j are
+        // powers of two, so t = fl(fl(ru acc) cv) = acc 2^(Er + Ec) exactly whenever
+        // both products stay normal -- the reference's two rounded multiplies are
+        // then exact.  acc -> double by the 2^52 + 2^31 bias (one exact subtract),
+        // the scale by an add to the exponent field; acc = 0 (also every entry of a
+        // zero row or column) contributes +0, which leaves D unchanged (D is never -0).
+        const int er = mu_e + 2 - P.beta * P.c_g[c];
+        // warp-uniform: tcgen05.ld is .sync.aligned (a row outside the range sends
+        // its whole warp down the exact path)
+        const bool fast = __all_sync(0xffffffffu, fast_ok && P.dump == nullptr &&
+                                                      (mu == 0.0 || (er >= -1022 && er <= 992 && er + ec_lo >= -1022 &&
+                                                                     er + ec_hi <= 992)));
+        if (fast) {
+          const int er20 = er * (1 << 20);
+          const uint32_t cc_addr = ptx::smem_u32(cc_s), ec_addr = ptx::smem_u32(ec20 + cslice * kCols);
 #pragma unroll
-            for (int j = 0; j < kLd; ++j) v[j] -= rrow + ccol[ci * kBN + cslice * kCols + cc + j];
+          for (int cc = 0; cc < kCols; cc += kLd) {
+            uint32_t v[kLd];
+            ptx::tmem_ld_32x32b<kLd>(taddr + cc, v);
+            uint32_t corr[kLd], esh[kLd];
+#pragma unroll
+            for (int q = 0; q < kLd; q += 4) {
+              const uint4 e4 = ptx::lds_u32x4(ec_addr + 4 * (cc + q));
+              esh[q] = e4.x + er20, esh[q + 1] = e4.y + er20, esh[q + 2] = e4.z + er20, esh[q + 3] = e4.w + er20;
+              const uint4 c4 = P.bias ? ptx::lds_u32x4(cc_addr + 4 * (cc + q)) : make_uint4(0, 0, 0, 0);
+              corr[q] = c4.x + rr, corr[q + 1] = c4.y + rr, corr[q + 2] = c4.z + rr, corr[q + 3] = c4.w + rr;
+            }
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < kLd; ++j) {
+              const uint32_t a = v[j] - corr[j];  // the exact INT32 chunk sum (wrapping)
+              const double ad = __dsub_rn(__hiloint2double(0x43300000, static_cast<int>(a ^ 0x80000000u)),
+                                          4503601774854144.0);  // == (double)(int32)a, exactly
+              const int hi = a != 0u ? __double2hiint(ad) + static_cast<int>(esh[j]) : 0;
+              d[cc + j] = __dadd_rn(d[cc + j], __hiloint2double(hi, __double2loint(ad)));
+            }
           }
-          if (P.dump != nullptr && row_ok) {
-            int32_t* dst = P.dump + (static_cast<int64_t>(c) * P.m + row) * P.p;
+        } else {
+          const double ru = flush_row_scale(P, c, row, mu);
 #pragma unroll
-            for (int j = 0; j < kLd; ++j)
-              if (col0 + cc + j < P.p) dst[col0 + cc + j] = static_cast<int32_t>(v[j]);
-          }
+          for (int cc = 0; cc < kCols; cc += kLd) {
+            uint32_t v[kLd];
+            ptx::tmem_ld_32x32b<kLd>(taddr + cc, v);
+            ptx::tmem_ld_wait();
+            if (P.bias) {
 #pragma unroll
-          for (int j = 0; j < kLd; ++j) {
-            const double cv = flush_col_scale(P, c, col0 + cc + j, nu_s[cslice * kCols + cc + j]);
-            const double t =
-                __dmul_rn(__dmul_rn(ru, static_cast<double>(static_cast<int32_t>(v[j]))), cv);
-            d[cc + j] = __dadd_rn(d[cc + j], t);
+              for (int j = 0; j < kLd; ++j) v[j] -= rr + cc_s[cc + j];
+            }
+            if (P.dump != nullptr && row_ok) {
+              int32_t* dst = P.dump + (static_cast<int64_t>(c) * P.m + row) * P.p;
+#pragma unroll
+              for (int j = 0; j < kLd; ++j)
+                if (col0 + cc + j < P.p) dst[col0 + cc + j] = static_cast<int32_t>(v[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < kLd; ++j) {
+              const double cv = flush_col_scale(P, c, col0 + cc + j, nu_s[cslice * kCols + cc + j]);
+              const double t =
+                  __dmul_rn(__dmul_rn(ru, static_cast<double>(static_cast<int32_t>(v[j]))), cv);
+              d[cc + j] = __dadd_rn(d[cc + j], t);
+            }
           }
         }
       }
@@ -467,7 +586,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
     // -- and C is read and written row by row with consecutive lanes on
     // consecutive columns.
     constexpr int kStageLd = kBN + 1;  // doubles; the pad spreads a row-per-lane write over banks
-    double* stage = reinterpret_cast<double*>(smem);
+    double* stage = reinterpret_cast<double*>(bbuf);  // host sizes the pools >= Cfg::kStageBytes
     const int lrow = quarter * 32 + lane;
 #pragma unroll
     for (int j = 0; j < kCols; ++j) stage[lrow * kStageLd + cslice * kCols + j] = d[j];

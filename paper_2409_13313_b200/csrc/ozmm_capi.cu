@@ -431,15 +431,6 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
   // group per round; three per round starve the producer (tools/gpairs_probe*.sh)
   P.group_pairs = 2;
   if (const char* g = OZMM_ENV("OZMM_GROUP_PAIRS")) P.group_pairs = std::atoi(g);
-  // thin passes in K-block pairs (runs of 8 MMAs per accumulator): +4 % at C5
-  // (k = 12), +1 % at C4, but -3 % at the two-batch C3 where the power cap takes the
-  // gain back (profiles/r1/kpair_ab.txt) -- on for schedules of three or more batches
-  // and for problems up to 8192 x 8192 (C2 +2 %).  The problem, not the launch: the
-  // host entry's strips of a C3 call are C3 work (fl.full_mp)
-  const int64_t mp = fl.full_mp ? fl.full_mp : m * p;
-  P.kpair = (S.batches.size() >= 3 || mp <= int64_t(8192) * 8192) ? 1 : 0;
-  if (fl.kpair) P.kpair = fl.kpair == 2 ? 1 : 0;
-  if (const char* g = OZMM_ENV("OZMM_KPAIR")) P.kpair = std::atoi(g);
 #ifdef OZMM_DIAG
   // timing probe: flips instruction-descriptor bits (wrong results)
   if (const char* g = OZMM_ENV("OZMM_IDESC_XOR")) P.idesc_xor = static_cast<uint32_t>(std::strtoul(g, nullptr, 0));
@@ -572,7 +563,6 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
                      const double* Cin, double* Cout, int64_t ldc, int32_t* dump,
                      const FlushCfg& fl) {
   using Cfg = ozb::PairCfg<kBN, kPairs>;
-  const size_t budget = h->smem_optin - kSmemReserve - kBN * sizeof(double);
   // passes are limited by the resident B slices per K block (A slices stream)
   auto slot_bytes = [](int, int b) { return static_cast<int64_t>(b) * Cfg::kBTile; };
   ozb::PassCost cm;
@@ -596,8 +586,25 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   if (!schedule_fits(S))
     return set_err(h, OZMM_ERR_UNSUPPORTED, "schedule too large (k=%d, r=%lld)", k,
                    static_cast<long long>(r));
-  const size_t ccol_bytes = fl.biased() ? sizeof(uint32_t) * Cfg::kNAcc * kBN : 0;
-  const size_t fixed = ozb::kBBufs * Cfg::kBBuf + ccol_bytes;
+  // K-pair decision (the kernel re-derives it per pass from P.kpair and the B
+  // buffer size): thin passes in K-block pairs (runs of 8 MMAs per accumulator):
+  // +4 % at C5 (k = 12), +1 % at C4, but -3 % at the two-batch C3 where the power
+  // cap takes the gain back (profiles/r1/kpair_ab.txt) -- on for schedules of three
+  // or more batches and for problems up to 8192 x 8192 (C2 +2 %).  The problem, not
+  // the launch: the host entry's strips of a C3 call are C3 work (fl.full_mp)
+  const int64_t full_mp = fl.full_mp ? fl.full_mp : m * p;
+  int kpair = (S.batches.size() >= 3 || full_mp <= int64_t(8192) * 8192) ? 1 : 0;
+  if (fl.kpair) kpair = fl.kpair == 2 ? 1 : 0;
+  if (const char* g = OZMM_ENV("OZMM_KPAIR")) kpair = std::atoi(g);
+  const int n_kb = static_cast<int>((std::max(lds_a, lds_b) + ozb::kKB - 1) / ozb::kKB);
+  // B buffers sized for the widest pass (two K blocks of a K-pair pass)
+  int b_slots = 1;
+  for (const auto& q : S.passes) {
+    const int nbw = q.bhi - q.blo + 1;
+    const bool pair_kb = kPairs == 1 && kpair && 2 * nbw <= Cfg::kMaxBSlots && n_kb % 2 == 0;
+    b_slots = std::max(b_slots, pair_kb ? 2 * nbw : nbw);
+  }
+  const size_t fixed = Cfg::smem_bytes(b_slots, 0);
   // A-ring depth.  When each A tile feeds >= 2.5 products on average (tensor-bound
   // schedules, e.g. C3), 5 stages, not the 6 that fit.  With one A group per
   // barrier round, a deeper ring let each CTA pair run further ahead along K:
@@ -610,19 +617,26 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   int64_t a_loads = 0;
   for (const auto& q : S.passes) a_loads += q.g1 - q.g0;
   const bool dense = a_loads > 0 && 2 * static_cast<int64_t>(S.products.size()) >= 5 * a_loads;
-  int stages = static_cast<int>(std::min<size_t>(dense ? 5 : 6, (budget - fixed) / Cfg::kATile));
-  if (fl.stages)
-    stages = static_cast<int>(std::min<size_t>((budget - fixed) / Cfg::kATile, std::max(2, fl.stages)));
+  const size_t fit = std::min<size_t>(Cfg::kMaxStages, (h->smem_optin - fixed) / Cfg::kATile);
+  int stages = static_cast<int>(std::min<size_t>(dense ? 5 : 6, fit));
+  if (fl.stages) stages = static_cast<int>(std::min<size_t>(fit, std::max(2, fl.stages)));
   if (const char* e = OZMM_ENV("OZMM_STAGES"))
-    stages = static_cast<int>(std::min<size_t>((budget - fixed) / Cfg::kATile, std::max(2, std::atoi(e))));
+    stages = static_cast<int>(std::min<size_t>(fit, std::max(2, std::atoi(e))));
   if (stages < 2)
     return set_err(h, OZMM_ERR_UNSUPPORTED, "A ring does not fit shared memory");
+  // the C pass stages the FP64 tile in the operand pools: grow the B buffers if
+  // a small schedule leaves the pools short of it
+  while (Cfg::smem_bytes(b_slots, stages) - Cfg::smem_bytes(0, 0) < Cfg::kStageBytes) ++b_slots;
+  if (Cfg::smem_bytes(b_slots, stages) > h->smem_optin)
+    return set_err(h, OZMM_ERR_UNSUPPORTED, "operand pools do not fit shared memory");
   ozb::GemmParams P;
   const int tiles_m = static_cast<int>((m + 2 * ozb::kBM - 1) / (2 * ozb::kBM));
   const int tiles_n = static_cast<int>((p + kPairs * kBN - 1) / (kPairs * kBN));
   fill_params(P, S, m, p, lds_a, lds_b, tiles_m, tiles_n, beta_bits, stages, alpha, beta, mu, nu,
               Cin, Cout, ldc, dump, fl);
-  P.n_kb = static_cast<int>((std::max(lds_a, lds_b) + ozb::kKB - 1) / ozb::kKB);
+  P.n_kb = n_kb;
+  P.kpair = kpair;
+  P.b_buf_slots = b_slots;
   for (const auto& ps : S.passes)
     for (int i = ps.p0; i < ps.p1; ++i) {
       const auto& pr = S.products[i];
@@ -642,7 +656,7 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
     return rc;
   if (fl.biased() && (fl.per_product || fl.scale_mode != 0))
     return set_err(h, OZMM_ERR_UNSUPPORTED, "offset-binary slices need the CTA-pair ozIMMU_H kernel");
-  const size_t smem = fixed + stages * Cfg::kATile + kSmemReserve + kBN * sizeof(double);
+  const size_t smem = Cfg::smem_bytes(b_slots, stages);
   if (!h->pair_attr_set[kPairs - 1]) {
     CUDA_TRY(h, cudaFuncSetAttribute(ozb::ozimmu_gemm_pair_kernel<kBN, kPairs>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -653,25 +667,27 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   // OZMM_TILE_TRACE=1 (diagnostics): per-CTA globaltimer stamps, summarised on stderr
   const bool ttrace = OZMM_ENV("OZMM_TILE_TRACE") != nullptr;
   uint64_t* tbuf = nullptr;
+  constexpr int kTS = ozb::kTraceSlots;
   if (ttrace) {
-    CUDA_TRY(h, cudaMalloc(&tbuf, sizeof(uint64_t) * 8 * grid.x));
-    CUDA_TRY(h, cudaMemsetAsync(tbuf, 0, sizeof(uint64_t) * 8 * grid.x, h->stream));
+    CUDA_TRY(h, cudaMalloc(&tbuf, sizeof(uint64_t) * kTS * grid.x));
+    CUDA_TRY(h, cudaMemsetAsync(tbuf, 0, sizeof(uint64_t) * kTS * grid.x, h->stream));
     P.tile_trace = tbuf;
   }
   ozb::ozimmu_gemm_pair_kernel<kBN, kPairs>
       <<<grid, ozb::kPairThreads, smem, h->stream>>>(map_a, map_b, P);
   CUDA_TRY(h, cudaGetLastError());
   if (ttrace) {
-    std::vector<uint64_t> t(8 * static_cast<size_t>(grid.x));
+    std::vector<uint64_t> t(kTS * static_cast<size_t>(grid.x));
     CUDA_TRY(h, cudaMemcpyAsync(t.data(), tbuf, t.size() * 8, cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     cudaFree(tbuf);
-    // mean interval between consecutive stamps over leader CTAs (us)
-    double sum[8] = {}, tot = 0;
+    // mean interval between consecutive stamps over leader CTAs (us), plus the
+    // MMA thread's / producer's wait shares and the epilogue drain times
+    double sum[8] = {}, tot = 0, w[16] = {}, drain0 = 0, drainl = 0, mma0 = 0;
     int cnt = 0;
     uint64_t t_min = ~0ull, t_max = 0;
     for (unsigned c = 0; c < grid.x; c += Cfg::kCluster) {
-      const uint64_t* r = t.data() + 8 * c;
+      const uint64_t* r = t.data() + kTS * c;
       if (!r[0] || !r[7]) continue;
       ++cnt;
       t_min = std::min(t_min, r[0]);
@@ -683,12 +699,21 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
           prev = r[i];
         }
       tot += static_cast<double>(r[7] - r[0]) * 1e-3;
+      for (int i = 8; i < 16; ++i) w[i] += static_cast<double>(r[i]);
+      if (r[12] && r[2]) mma0 += static_cast<double>(r[12] - r[2]) * 1e-3;
+      const uint64_t d0 = P.nbatch > 1 ? r[3] : r[5];
+      if (r[12] && d0 > r[12]) drain0 += static_cast<double>(d0 - r[12]) * 1e-3;
+      if (r[13] && r[5] > r[13]) drainl += static_cast<double>(r[5] - r[13]) * 1e-3;
     }
+    const double n = cnt ? cnt : 1, mt = w[11] > 0 ? w[11] : 1;
     std::fprintf(stderr,
                  "[ozmm tile trace] %d tiles, launch span %.2f ms, mean tile %.1f us: prologue %.1f | to 1st MMA %.1f |"
-                 " batch0 %.1f | to next MMA %.1f | rest %.1f | C write %.1f | teardown %.1f\n",
-                 cnt, (t_max - t_min) * 1e-6, cnt ? tot / cnt : 0.0, sum[1] / cnt, sum[2] / cnt,
-                 sum[3] / cnt, sum[4] / cnt, sum[5] / cnt, sum[6] / cnt, sum[7] / cnt);
+                 " batch0 %.1f | to next MMA %.1f | rest %.1f | C write %.1f | teardown %.1f\n"
+                 "[ozmm tile trace] batch0 MMAs %.1f us, drain %.1f us; last drain %.1f us | MMA thread "
+                 "%.0f clk/tile: waits A %.1f%% B %.1f%% TMEM %.1f%% | producer waits A-slot %.1f%% B-slot %.1f%%\n",
+                 cnt, (t_max - t_min) * 1e-6, tot / n, sum[1] / n, sum[2] / n, sum[3] / n, sum[4] / n,
+                 sum[5] / n, sum[6] / n, sum[7] / n, mma0 / n, drain0 / n, drainl / n, w[11] / n,
+                 100 * w[8] / mt, 100 * w[9] / mt, 100 * w[10] / mt, 100 * w[14] / mt, 100 * w[15] / mt);
   }
   return OZMM_OK;
 }
@@ -1092,7 +1117,7 @@ int ozmm_debug_schedule(int k, int64_t r, int cta_pair, int tile_n, int* rows, i
   }
   const size_t stage_bytes =
       pair_kernel ? static_cast<size_t>(a_tile) : static_cast<size_t>(slot_bytes(S.a_slots, S.b_slots));
-  const size_t fixed = pair_kernel ? ozb::kBBufs * ozb::PairCfg<128, 1>::kBBuf : 0;
+  const size_t fixed = pair_kernel ? ozb::kBBufs * ozb::PairCfg<128, 1>::kMaxBSlots * b_tile : 0;
   info[0] = np;
   info[1] = static_cast<int>(S.chunks.size());
   info[2] = static_cast<int>(S.batches.size());
