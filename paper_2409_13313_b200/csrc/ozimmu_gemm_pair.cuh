@@ -163,149 +163,244 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
   const uint32_t tmem_base = *tmem_base_smem;
   if (trace && threadIdx.x == 0) trace[1] = ptx::globaltimer();
 
-  if (warp == 0) {
-    // ------------------------------------------------------ TMA producer
-    if (ptx::elect_one()) {
-      long long tw_[16] = {};
-      (void)tw_;
-      int bi = 0, ai = 0;
-      uint32_t bph = 0, aph = 0;
-      const int b_row = col_tile * kBN + static_cast<int>(rank & 1u) * Cfg::kBHalf;
-      const int a_row = row_base + static_cast<int>(pp) * Cfg::kAPart;
-      const uint16_t a_mask = static_cast<uint16_t>(kPairs == 1 ? 0 : (0x5u << (rank & 1u)));
-      const uint64_t pol_a = ptx::l2_policy(P.hint_a), pol_b = ptx::l2_policy(P.hint_b);
-      for (int q = 0; q < P.npass; ++q) {
-        const int blo = P.p_blo[q], bhi = P.p_bhi[q], g0 = P.p_g0[q], g1 = P.p_g1[q];
-        const uint32_t btx = 2u * (bhi - blo + 1) * Cfg::kBTile;
-        const int nbw = bhi - blo + 1;
-        if (kPairs == 1 && P.kpair && 2 * nbw <= P.b_buf_slots && n_kb % 2 == 0) {
-          // K-pair pass: one B buffer holds K blocks kb and kb+1; each A group loads
-          // both of its K blocks into consecutive ring slots
-          for (int kb = 0; kb < n_kb; kb += 2) {
+  // registers: the producer / MMA warpgroup needs few, the epilogue holds a 64-column
+  // FP64 row of D plus 32 of a chunk's INT32 sums per thread (no spills at 216)
+  if (warp < 4) {
+    ptx::setmaxnreg_dec<72>();
+    if (warp == 0) {
+      // ------------------------------------------------------ TMA producer
+      if (ptx::elect_one()) {
+        long long tw_[16] = {};
+        (void)tw_;
+        int bi = 0, ai = 0;
+        uint32_t bph = 0, aph = 0;
+        const int b_row = col_tile * kBN + static_cast<int>(rank & 1u) * Cfg::kBHalf;
+        const int a_row = row_base + static_cast<int>(pp) * Cfg::kAPart;
+        const uint16_t a_mask = static_cast<uint16_t>(kPairs == 1 ? 0 : (0x5u << (rank & 1u)));
+        const uint64_t pol_a = ptx::l2_policy(P.hint_a), pol_b = ptx::l2_policy(P.hint_b);
+        for (int q = 0; q < P.npass; ++q) {
+          const int blo = P.p_blo[q], bhi = P.p_bhi[q], g0 = P.p_g0[q], g1 = P.p_g1[q];
+          const uint32_t btx = 2u * (bhi - blo + 1) * Cfg::kBTile;
+          const int nbw = bhi - blo + 1;
+          if (kPairs == 1 && P.kpair && 2 * nbw <= P.b_buf_slots && n_kb % 2 == 0) {
+            // K-pair pass: one B buffer holds K blocks kb and kb+1; each A group loads
+            // both of its K blocks into consecutive ring slots
+            for (int kb = 0; kb < n_kb; kb += 2) {
+              OZMM_TWAIT(15, ptx::mbar_wait(b_empty + bi, bph ^ 1));
+              const uint32_t fb = ptx::mapa_shared(b_full + bi, lead_rank);
+              if (leader) ptx::mbar_arrive_expect_tx(b_full + bi, 2u * btx);
+              uint8_t* dst = bbuf + bi * b_buf;
+              for (int h = 0; h < 2; ++h)
+                for (int t = blo; t <= bhi; ++t)
+                  ptx::tma_load_3d_pair_hint(dst + (h * nbw + t - blo) * Cfg::kBTile, &map_b, fb,
+                                             (kb + h) * kKB, b_row, t - 1, pol_b);
+              if (++bi == kBBufs) {
+                bi = 0;
+                bph ^= 1;
+              }
+              for (int g = g0; g < g1; ++g)
+                for (int h = 0; h < 2; ++h) {
+                  OZMM_TWAIT(14, ptx::mbar_wait(a_empty + ai, aph ^ 1));
+                  const uint32_t fa = ptx::mapa_shared(a_full + ai, lead_rank);
+                  if (leader) ptx::mbar_arrive_expect_tx(a_full + ai, 2u * Cfg::kATile);
+                  ptx::tma_load_3d_pair_hint(aring + ai * Cfg::kATile, &map_a, fa, (kb + h) * kKB,
+                                             a_row, P.ag_s[g] - 1, pol_a);
+                  if (++ai == n_a) {
+                    ai = 0;
+                    aph ^= 1;
+                  }
+                }
+            }
+            continue;
+          }
+          for (int kb = 0; kb < n_kb; ++kb) {
             OZMM_TWAIT(15, ptx::mbar_wait(b_empty + bi, bph ^ 1));
-            const uint32_t fb = ptx::mapa_shared(b_full + bi, lead_rank);
-            if (leader) ptx::mbar_arrive_expect_tx(b_full + bi, 2u * btx);
-            uint8_t* dst = bbuf + bi * b_buf;
-            for (int h = 0; h < 2; ++h)
+            {
+              const uint32_t fb = ptx::mapa_shared(b_full + bi, lead_rank);
+              if (leader) ptx::mbar_arrive_expect_tx(b_full + bi, btx);
+              uint8_t* dst = bbuf + bi * b_buf;
               for (int t = blo; t <= bhi; ++t)
-                ptx::tma_load_3d_pair_hint(dst + (h * nbw + t - blo) * Cfg::kBTile, &map_b, fb,
-                                           (kb + h) * kKB, b_row, t - 1, pol_b);
+                ptx::tma_load_3d_pair_hint(dst + (t - blo) * Cfg::kBTile, &map_b, fb, kb * kKB,
+                                           b_row, t - 1, pol_b);
+            }
             if (++bi == kBBufs) {
               bi = 0;
               bph ^= 1;
             }
-            for (int g = g0; g < g1; ++g)
-              for (int h = 0; h < 2; ++h) {
-                OZMM_TWAIT(14, ptx::mbar_wait(a_empty + ai, aph ^ 1));
-                const uint32_t fa = ptx::mapa_shared(a_full + ai, lead_rank);
-                if (leader) ptx::mbar_arrive_expect_tx(a_full + ai, 2u * Cfg::kATile);
-                ptx::tma_load_3d_pair_hint(aring + ai * Cfg::kATile, &map_a, fa, (kb + h) * kKB,
-                                           a_row, P.ag_s[g] - 1, pol_a);
-                if (++ai == n_a) {
-                  ai = 0;
-                  aph ^= 1;
-                }
+            for (int g = g0; g < g1; ++g) {
+              OZMM_TWAIT(14, ptx::mbar_wait(a_empty + ai, aph ^ 1));
+              const uint32_t fa = ptx::mapa_shared(a_full + ai, lead_rank);
+              if (leader) ptx::mbar_arrive_expect_tx(a_full + ai, 2u * Cfg::kATile);
+              if constexpr (kPairs == 1)
+                ptx::tma_load_3d_pair_hint(aring + ai * Cfg::kATile, &map_a, fa, kb * kKB, a_row,
+                                           P.ag_s[g] - 1, pol_a);
+              else
+                ptx::tma_load_3d_pair_mc(aring + ai * Cfg::kATile + pp * Cfg::kAPart * kKB, &map_a,
+                                         a_full + ai, kb * kKB, a_row, P.ag_s[g] - 1, a_mask, pol_a);
+              if (++ai == n_a) {
+                ai = 0;
+                aph ^= 1;
               }
-          }
-          continue;
-        }
-        for (int kb = 0; kb < n_kb; ++kb) {
-          OZMM_TWAIT(15, ptx::mbar_wait(b_empty + bi, bph ^ 1));
-          {
-            const uint32_t fb = ptx::mapa_shared(b_full + bi, lead_rank);
-            if (leader) ptx::mbar_arrive_expect_tx(b_full + bi, btx);
-            uint8_t* dst = bbuf + bi * b_buf;
-            for (int t = blo; t <= bhi; ++t)
-              ptx::tma_load_3d_pair_hint(dst + (t - blo) * Cfg::kBTile, &map_b, fb, kb * kKB,
-                                         b_row, t - 1, pol_b);
-          }
-          if (++bi == kBBufs) {
-            bi = 0;
-            bph ^= 1;
-          }
-          for (int g = g0; g < g1; ++g) {
-            OZMM_TWAIT(14, ptx::mbar_wait(a_empty + ai, aph ^ 1));
-            const uint32_t fa = ptx::mapa_shared(a_full + ai, lead_rank);
-            if (leader) ptx::mbar_arrive_expect_tx(a_full + ai, 2u * Cfg::kATile);
-            if constexpr (kPairs == 1)
-              ptx::tma_load_3d_pair_hint(aring + ai * Cfg::kATile, &map_a, fa, kb * kKB, a_row,
-                                         P.ag_s[g] - 1, pol_a);
-            else
-              ptx::tma_load_3d_pair_mc(aring + ai * Cfg::kATile + pp * Cfg::kAPart * kKB, &map_a,
-                                       a_full + ai, kb * kKB, a_row, P.ag_s[g] - 1, a_mask, pol_a);
-            if (++ai == n_a) {
-              ai = 0;
-              aph ^= 1;
             }
           }
         }
+#ifdef OZMM_DIAG
+        if (trace && leader) trace[14] = tw_[14], trace[15] = tw_[15];
+#endif
       }
+    } else if (warp == 1) {
+      // ------------------------------------------- MMA issuer (leader CTA)
+      // u8 x u8 for offset-binary planes (instruction-descriptor bits 7 / 10)
 #ifdef OZMM_DIAG
-      if (trace && leader) trace[14] = tw_[14], trace[15] = tw_[15];
-#endif
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------- MMA issuer (leader CTA)
-    // u8 x u8 for offset-binary planes (instruction-descriptor bits 7 / 10)
-#ifdef OZMM_DIAG
-    const uint32_t idesc = (P.bias ? (Cfg::kIdesc & ~((1u << 7) | (1u << 10))) : Cfg::kIdesc) ^ P.idesc_xor;
+      const uint32_t idesc = (P.bias ? (Cfg::kIdesc & ~((1u << 7) | (1u << 10))) : Cfg::kIdesc) ^ P.idesc_xor;
 #else
-    const uint32_t idesc = P.bias ? (Cfg::kIdesc & ~((1u << 7) | (1u << 10))) : Cfg::kIdesc;
+      const uint32_t idesc = P.bias ? (Cfg::kIdesc & ~((1u << 7) | (1u << 10))) : Cfg::kIdesc;
 #endif
-    if (leader) {
-      long long tw_[16] = {};
-      (void)tw_;
+      if (leader) {
+        long long tw_[16] = {};
+        (void)tw_;
 #ifdef OZMM_DIAG
-      const long long t_mma0 = clock64();
+        const long long t_mma0 = clock64();
 #endif
-      int bi = 0, ai = 0;
-      uint32_t bph = 0, aph = 0;
-      for (int b = 0; b < P.nbatch; ++b) {
-        OZMM_TWAIT(10, ptx::mbar_wait(tmem_empty, (b & 1) ^ 1));
-        ptx::tc_fence_after();
-        for (int q = P.b_pass0[b]; q < P.b_pass1[b]; ++q) {
-          const int blo = P.p_blo[q], g0 = P.p_g0[q], g1 = P.p_g1[q];
-          const int nbw = P.p_bhi[q] - blo + 1;
-          if (kPairs == 1 && P.kpair && 2 * nbw <= P.b_buf_slots && n_kb % 2 == 0) {
-            // K-pair pass: each product's MMAs for K blocks kb and kb+1 back to
-            // back -- runs of 8 MMAs on one accumulator instead of 4
-            for (int kb = 0; kb < n_kb; kb += 2) {
+        int bi = 0, ai = 0;
+        uint32_t bph = 0, aph = 0;
+        for (int b = 0; b < P.nbatch; ++b) {
+          OZMM_TWAIT(10, ptx::mbar_wait(tmem_empty, (b & 1) ^ 1));
+          ptx::tc_fence_after();
+          for (int q = P.b_pass0[b]; q < P.b_pass1[b]; ++q) {
+            const int blo = P.p_blo[q], g0 = P.p_g0[q], g1 = P.p_g1[q];
+            const int nbw = P.p_bhi[q] - blo + 1;
+            if (kPairs == 1 && P.kpair && 2 * nbw <= P.b_buf_slots && n_kb % 2 == 0) {
+              // K-pair pass: each product's MMAs for K blocks kb and kb+1 back to
+              // back -- runs of 8 MMAs on one accumulator instead of 4
+              for (int kb = 0; kb < n_kb; kb += 2) {
+                OZMM_TWAIT(9, ptx::mbar_wait(b_full + bi, bph));
+                ptx::tc_fence_after();
+                if (trace && kb == 0 && q == P.b_pass0[b] && b < 2 && lane == 0) trace[2 + 2 * b] = ptx::globaltimer();
+                const uint64_t bdesc0 = ptx::smem_desc(ptx::smem_u32(bbuf + bi * b_buf), 1024, 2);
+                const uint32_t bstep = (nbw * Cfg::kBTile) >> 4;  // K block kb+1's tiles
+                for (int g = g0; g < g1; ++g) {
+                  const int s1 = ai + 1 == n_a ? 0 : ai + 1;
+                  const uint32_t ph1 = ai + 1 == n_a ? aph ^ 1 : aph;
+                  OZMM_TWAIT(8, ptx::mbar_wait(a_full + ai, aph));
+                  OZMM_TWAIT(8, ptx::mbar_wait(a_full + s1, ph1));
+                  ptx::tc_fence_after();
+                  if (ptx::elect_one()) {
+                    const uint64_t ad0 = ptx::smem_desc(ptx::smem_u32(aring + ai * Cfg::kATile), 1024, 2);
+                    const uint64_t ad1 = ptx::smem_desc(ptx::smem_u32(aring + s1 * Cfg::kATile), 1024, 2);
+                    for (int pr = P.ag_p0[g]; pr < P.ag_p1[g]; ++pr) {
+                      const uint32_t info = P.pr_info[pr];
+                      const uint64_t bdesc = bdesc0 + (info & 0xFFFFu);
+                      const uint32_t d = tmem_base + ((info >> 16) & 0x7Fu) * kBN;
+                      const bool first = kb == 0 && (info >> 24);
+#pragma unroll
+                      for (int j = 0; j < kKB / kBK; ++j)
+                        ptx::mma_i8_pair(d, ad0 + 2 * j, bdesc + 2 * j, idesc,
+                                         (first && j == 0) ? 0u : 1u);
+#pragma unroll
+                      for (int j = 0; j < kKB / kBK; ++j)
+                        ptx::mma_i8_pair(d, ad1 + 2 * j, bdesc + bstep + 2 * j, idesc, 1u);
+                    }
+                    ptx::mma_commit_pair(a_empty + ai, all_mask);
+                    ptx::mma_commit_pair(a_empty + s1, all_mask);
+                  }
+                  __syncwarp();
+                  for (int h = 0; h < 2; ++h)
+                    if (++ai == n_a) {
+                      ai = 0;
+                      aph ^= 1;
+                    }
+                }
+                if (ptx::elect_one()) ptx::mma_commit_pair(b_empty + bi, pair_mask);
+                __syncwarp();
+                if (++bi == kBBufs) {
+                  bi = 0;
+                  bph ^= 1;
+                }
+              }
+              continue;
+            }
+            for (int kb = 0; kb < n_kb; ++kb) {
               OZMM_TWAIT(9, ptx::mbar_wait(b_full + bi, bph));
               ptx::tc_fence_after();
               if (trace && kb == 0 && q == P.b_pass0[b] && b < 2 && lane == 0) trace[2 + 2 * b] = ptx::globaltimer();
-              const uint64_t bdesc0 = ptx::smem_desc(ptx::smem_u32(bbuf + bi * b_buf), 1024, 2);
-              const uint32_t bstep = (nbw * Cfg::kBTile) >> 4;  // K block kb+1's tiles
+              const uint32_t sb = ptx::smem_u32(bbuf + bi * b_buf);
+              const uint64_t bdesc0 = ptx::smem_desc(sb, 1024, 2);
               for (int g = g0; g < g1; ++g) {
-                const int s1 = ai + 1 == n_a ? 0 : ai + 1;
-                const uint32_t ph1 = ai + 1 == n_a ? aph ^ 1 : aph;
+                if (P.group_pairs > 1 && g + 1 < g1) {
+                  // up to group_pairs A stages per barrier round: wait for all, issue
+                  // their MMAs in one burst, release all (fewer issue-stream breaks)
+                  const int ng = min(P.group_pairs, g1 - g);
+                  {
+                    int sl = ai;
+                    uint32_t ph = aph;
+                    for (int h2 = 0; h2 < ng; ++h2) {
+                      OZMM_TWAIT(8, ptx::mbar_wait(a_full + sl, ph));
+                      if (++sl == n_a) sl = 0, ph ^= 1;
+                    }
+                  }
+                  ptx::tc_fence_after();
+                  if (ptx::elect_one()) {
+                    int sl = ai;
+                    for (int h2 = 0; h2 < ng; ++h2) {
+                      const int gg = g + h2;
+                      const uint64_t adesc = ptx::smem_desc(ptx::smem_u32(aring + sl * Cfg::kATile), 1024, 2);
+                      for (int pr = P.ag_p0[gg]; pr < P.ag_p1[gg]; ++pr) {
+                        // one 32-bit word per product (host-packed): B tile offset in
+                        // descriptor units | accumulator << 16 | first << 24 -- the
+                        // issuing thread was the bottleneck of thin batches
+                        const uint32_t info = P.pr_info[pr];
+                        const uint64_t bdesc = bdesc0 + (info & 0xFFFFu);
+                        const uint32_t d = tmem_base + ((info >> 16) & 0x7Fu) * kBN;
+                        const bool first = kb == 0 && (info >> 24);
+#pragma unroll
+                        for (int j = 0; j < kKB / kBK; ++j)
+                          ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, idesc,
+                                           (first && j == 0) ? 0u : 1u);
+                      }
+                      if (++sl == n_a) sl = 0;
+                    }
+                    sl = ai;
+                    for (int h2 = 0; h2 < ng; ++h2) {
+                      ptx::mma_commit_pair(a_empty + sl, all_mask);
+                      if (++sl == n_a) sl = 0;
+                    }
+                  }
+                  __syncwarp();
+                  g += ng - 1;
+                  for (int h2 = 0; h2 < ng; ++h2)
+                    if (++ai == n_a) {
+                      ai = 0;
+                      aph ^= 1;
+                    }
+                  continue;
+                }
                 OZMM_TWAIT(8, ptx::mbar_wait(a_full + ai, aph));
-                OZMM_TWAIT(8, ptx::mbar_wait(a_full + s1, ph1));
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
-                  const uint64_t ad0 = ptx::smem_desc(ptx::smem_u32(aring + ai * Cfg::kATile), 1024, 2);
-                  const uint64_t ad1 = ptx::smem_desc(ptx::smem_u32(aring + s1 * Cfg::kATile), 1024, 2);
+                  const uint64_t adesc = ptx::smem_desc(ptx::smem_u32(aring + ai * Cfg::kATile), 1024, 2);
                   for (int pr = P.ag_p0[g]; pr < P.ag_p1[g]; ++pr) {
                     const uint32_t info = P.pr_info[pr];
                     const uint64_t bdesc = bdesc0 + (info & 0xFFFFu);
                     const uint32_t d = tmem_base + ((info >> 16) & 0x7Fu) * kBN;
                     const bool first = kb == 0 && (info >> 24);
 #pragma unroll
-                    for (int j = 0; j < kKB / kBK; ++j)
-                      ptx::mma_i8_pair(d, ad0 + 2 * j, bdesc + 2 * j, idesc,
+                    for (int j = 0; j < kKB / kBK; ++j)  // K = 32 per MMA: +32 B = +2 in desc.lo
+                      ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, idesc,
                                        (first && j == 0) ? 0u : 1u);
-#pragma unroll
-                    for (int j = 0; j < kKB / kBK; ++j)
-                      ptx::mma_i8_pair(d, ad1 + 2 * j, bdesc + bstep + 2 * j, idesc, 1u);
+#ifdef OZMM_DIAG
+                    for (int x = 0; x < P.dup_mma; ++x)  // timing experiment only (wrong results)
+                      for (int j = 0; j < kKB / kBK; ++j)
+                        ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, idesc, 1u);
+#endif
                   }
-                  ptx::mma_commit_pair(a_empty + ai, all_mask);
-                  ptx::mma_commit_pair(a_empty + s1, all_mask);
+                  ptx::mma_commit_pair(a_empty + ai, all_mask);  // A stage free (all sharers)
                 }
                 __syncwarp();
-                for (int h = 0; h < 2; ++h)
-                  if (++ai == n_a) {
-                    ai = 0;
-                    aph ^= 1;
-                  }
+                if (++ai == n_a) {
+                  ai = 0;
+                  aph ^= 1;
+                }
               }
               if (ptx::elect_one()) ptx::mma_commit_pair(b_empty + bi, pair_mask);
               __syncwarp();
@@ -314,109 +409,20 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
                 bph ^= 1;
               }
             }
-            continue;
           }
-          for (int kb = 0; kb < n_kb; ++kb) {
-            OZMM_TWAIT(9, ptx::mbar_wait(b_full + bi, bph));
-            ptx::tc_fence_after();
-            if (trace && kb == 0 && q == P.b_pass0[b] && b < 2 && lane == 0) trace[2 + 2 * b] = ptx::globaltimer();
-            const uint32_t sb = ptx::smem_u32(bbuf + bi * b_buf);
-            const uint64_t bdesc0 = ptx::smem_desc(sb, 1024, 2);
-            for (int g = g0; g < g1; ++g) {
-              if (P.group_pairs > 1 && g + 1 < g1) {
-                // up to group_pairs A stages per barrier round: wait for all, issue
-                // their MMAs in one burst, release all (fewer issue-stream breaks)
-                const int ng = min(P.group_pairs, g1 - g);
-                {
-                  int sl = ai;
-                  uint32_t ph = aph;
-                  for (int h2 = 0; h2 < ng; ++h2) {
-                    OZMM_TWAIT(8, ptx::mbar_wait(a_full + sl, ph));
-                    if (++sl == n_a) sl = 0, ph ^= 1;
-                  }
-                }
-                ptx::tc_fence_after();
-                if (ptx::elect_one()) {
-                  int sl = ai;
-                  for (int h2 = 0; h2 < ng; ++h2) {
-                    const int gg = g + h2;
-                    const uint64_t adesc = ptx::smem_desc(ptx::smem_u32(aring + sl * Cfg::kATile), 1024, 2);
-                    for (int pr = P.ag_p0[gg]; pr < P.ag_p1[gg]; ++pr) {
-                      // one 32-bit word per product (host-packed): B tile offset in
-                      // descriptor units | accumulator << 16 | first << 24 -- the
-                      // issuing thread was the bottleneck of thin batches
-                      const uint32_t info = P.pr_info[pr];
-                      const uint64_t bdesc = bdesc0 + (info & 0xFFFFu);
-                      const uint32_t d = tmem_base + ((info >> 16) & 0x7Fu) * kBN;
-                      const bool first = kb == 0 && (info >> 24);
-#pragma unroll
-                      for (int j = 0; j < kKB / kBK; ++j)
-                        ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, idesc,
-                                         (first && j == 0) ? 0u : 1u);
-                    }
-                    if (++sl == n_a) sl = 0;
-                  }
-                  sl = ai;
-                  for (int h2 = 0; h2 < ng; ++h2) {
-                    ptx::mma_commit_pair(a_empty + sl, all_mask);
-                    if (++sl == n_a) sl = 0;
-                  }
-                }
-                __syncwarp();
-                g += ng - 1;
-                for (int h2 = 0; h2 < ng; ++h2)
-                  if (++ai == n_a) {
-                    ai = 0;
-                    aph ^= 1;
-                  }
-                continue;
-              }
-              OZMM_TWAIT(8, ptx::mbar_wait(a_full + ai, aph));
-              ptx::tc_fence_after();
-              if (ptx::elect_one()) {
-                const uint64_t adesc = ptx::smem_desc(ptx::smem_u32(aring + ai * Cfg::kATile), 1024, 2);
-                for (int pr = P.ag_p0[g]; pr < P.ag_p1[g]; ++pr) {
-                  const uint32_t info = P.pr_info[pr];
-                  const uint64_t bdesc = bdesc0 + (info & 0xFFFFu);
-                  const uint32_t d = tmem_base + ((info >> 16) & 0x7Fu) * kBN;
-                  const bool first = kb == 0 && (info >> 24);
-#pragma unroll
-                  for (int j = 0; j < kKB / kBK; ++j)  // K = 32 per MMA: +32 B = +2 in desc.lo
-                    ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, idesc,
-                                     (first && j == 0) ? 0u : 1u);
-#ifdef OZMM_DIAG
-                  for (int x = 0; x < P.dup_mma; ++x)  // timing experiment only (wrong results)
-                    for (int j = 0; j < kKB / kBK; ++j)
-                      ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, idesc, 1u);
-#endif
-                }
-                ptx::mma_commit_pair(a_empty + ai, all_mask);  // A stage free (all sharers)
-              }
-              __syncwarp();
-              if (++ai == n_a) {
-                ai = 0;
-                aph ^= 1;
-              }
-            }
-            if (ptx::elect_one()) ptx::mma_commit_pair(b_empty + bi, pair_mask);
-            __syncwarp();
-            if (++bi == kBBufs) {
-              bi = 0;
-              bph ^= 1;
-            }
-          }
+          if (ptx::elect_one()) ptx::mma_commit_pair(tmem_full, pair_mask);
+          __syncwarp();
         }
-        if (ptx::elect_one()) ptx::mma_commit_pair(tmem_full, pair_mask);
-        __syncwarp();
-      }
 #ifdef OZMM_DIAG
-      if (trace && lane == 0) {
-        trace[8] = tw_[8], trace[9] = tw_[9], trace[10] = tw_[10];
-        trace[11] = clock64() - t_mma0;
-      }
+        if (trace && lane == 0) {
+          trace[8] = tw_[8], trace[9] = tw_[9], trace[10] = tw_[10];
+          trace[11] = clock64() - t_mma0;
+        }
 #endif
+      }
     }
-  } else if (warp >= 4) {
+  } else {
+    ptx::setmaxnreg_inc<216>();
     // --------------------------------------------------------- epilogue
     const int quarter = warp & 3;          // TMEM lane quarter
     const int cslice = (warp - 4) >> 2;    // 0/1: which column half
@@ -522,26 +528,27 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
         if (fast) {
           const int er20 = er * (1 << 20);
           const uint32_t cc_addr = ptx::smem_u32(cc_s), ec_addr = ptx::smem_u32(ec20 + cslice * kCols);
+          // 32 columns per TMEM round trip (two x16 loads, one wait)
 #pragma unroll
-          for (int cc = 0; cc < kCols; cc += kLd) {
-            uint32_t v[kLd];
-            ptx::tmem_ld_32x32b<kLd>(taddr + cc, v);
-            uint32_t corr[kLd], esh[kLd];
-#pragma unroll
-            for (int q = 0; q < kLd; q += 4) {
-              const uint4 e4 = ptx::lds_u32x4(ec_addr + 4 * (cc + q));
-              esh[q] = e4.x + er20, esh[q + 1] = e4.y + er20, esh[q + 2] = e4.z + er20, esh[q + 3] = e4.w + er20;
-              const uint4 c4 = P.bias ? ptx::lds_u32x4(cc_addr + 4 * (cc + q)) : make_uint4(0, 0, 0, 0);
-              corr[q] = c4.x + rr, corr[q + 1] = c4.y + rr, corr[q + 2] = c4.z + rr, corr[q + 3] = c4.w + rr;
-            }
+          for (int cc = 0; cc < kCols; cc += 2 * kLd) {
+            uint32_t v0[kLd], v1[kLd];
+            ptx::tmem_ld_32x32b<kLd>(taddr + cc, v0);
+            ptx::tmem_ld_32x32b<kLd>(taddr + cc + kLd, v1);
             ptx::tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < kLd; ++j) {
-              const uint32_t a = v[j] - corr[j];  // the exact INT32 chunk sum (wrapping)
-              const double ad = __dsub_rn(__hiloint2double(0x43300000, static_cast<int>(a ^ 0x80000000u)),
-                                          4503601774854144.0);  // == (double)(int32)a, exactly
-              const int hi = a != 0u ? __double2hiint(ad) + static_cast<int>(esh[j]) : 0;
-              d[cc + j] = __dadd_rn(d[cc + j], __hiloint2double(hi, __double2loint(ad)));
+            for (int q = 0; q < 2 * kLd; q += 4) {
+              const uint4 e4 = ptx::lds_u32x4(ec_addr + 4 * (cc + q));
+              const uint4 c4 = P.bias ? ptx::lds_u32x4(cc_addr + 4 * (cc + q)) : make_uint4(0, 0, 0, 0);
+              const uint32_t esh[4] = {e4.x, e4.y, e4.z, e4.w}, cor[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int j = q + u;
+                const uint32_t a = (j < kLd ? v0[j] : v1[j - kLd]) - rr - cor[u];  // exact INT32 chunk sum
+                const double ad = __dsub_rn(__hiloint2double(0x43300000, static_cast<int>(a ^ 0x80000000u)),
+                                            4503601774854144.0);  // == (double)(int32)a, exactly
+                const int hi = a != 0u ? __double2hiint(ad) + er20 + static_cast<int>(esh[u]) : 0;
+                d[cc + j] = __dadd_rn(d[cc + j], __hiloint2double(hi, __double2loint(ad)));
+              }
             }
           }
         } else {
