@@ -58,6 +58,12 @@ constexpr int kTraceSlots = 16;
 #else
 #define OZMM_TWAIT(slot, call) call
 #endif
+// timing probe (diag builds, OZMM_DUP_MMA=-1): skip the MMAs, keep loads and commits
+#ifdef OZMM_DIAG
+#define OZMM_MMA_ON (P.dup_mma >= 0)
+#else
+#define OZMM_MMA_ON true
+#endif
 template <int kBN, int kPairs = 1>
 struct PairCfg {
   static constexpr int kNAcc = 512 / kBN;
@@ -295,11 +301,11 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
                       const bool first = kb == 0 && (info >> 24);
 #pragma unroll
                       for (int j = 0; j < kKB / kBK; ++j)
-                        ptx::mma_i8_pair(d, ad0 + 2 * j, bdesc + 2 * j, idesc,
+                        if (OZMM_MMA_ON) ptx::mma_i8_pair(d, ad0 + 2 * j, bdesc + 2 * j, idesc,
                                          (first && j == 0) ? 0u : 1u);
 #pragma unroll
                       for (int j = 0; j < kKB / kBK; ++j)
-                        ptx::mma_i8_pair(d, ad1 + 2 * j, bdesc + bstep + 2 * j, idesc, 1u);
+                        if (OZMM_MMA_ON) ptx::mma_i8_pair(d, ad1 + 2 * j, bdesc + bstep + 2 * j, idesc, 1u);
                     }
                     ptx::mma_commit_pair(a_empty + ai, all_mask);
                     ptx::mma_commit_pair(a_empty + s1, all_mask);
@@ -355,7 +361,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
                         const bool first = kb == 0 && (info >> 24);
 #pragma unroll
                         for (int j = 0; j < kKB / kBK; ++j)
-                          ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, idesc,
+                          if (OZMM_MMA_ON) ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, idesc,
                                            (first && j == 0) ? 0u : 1u);
                       }
                       if (++sl == n_a) sl = 0;
@@ -386,12 +392,12 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
                     const bool first = kb == 0 && (info >> 24);
 #pragma unroll
                     for (int j = 0; j < kKB / kBK; ++j)  // K = 32 per MMA: +32 B = +2 in desc.lo
-                      ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, idesc,
+                      if (OZMM_MMA_ON) ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, idesc,
                                        (first && j == 0) ? 0u : 1u);
 #ifdef OZMM_DIAG
                     for (int x = 0; x < P.dup_mma; ++x)  // timing experiment only (wrong results)
                       for (int j = 0; j < kKB / kBK; ++j)
-                        ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, idesc, 1u);
+                        if (OZMM_MMA_ON) ptx::mma_i8_pair(d, adesc + 2 * j, bdesc + 2 * j, idesc, 1u);
 #endif
                   }
                   ptx::mma_commit_pair(a_empty + ai, all_mask);  // A stage free (all sharers)

@@ -21,6 +21,9 @@ using namespace ozb;
 
 struct BP {
   int rounds, prods, commit, wait, nacc, run, fill, nbars, bn, mode;
+  int copy_kb;        // > 0: warp 2 streams bulk copies of copy_kb KB global -> smem meanwhile
+  int copy_sleep_ns;  // pause between copies (rate control)
+  const uint8_t* src; // copy source (L2-resident buffer)
   uint32_t info[64];  // per product: B tile offset (desc units) | acc << 16 (mode 1, like pr_info)
 };
 
@@ -33,7 +36,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* aring = smem;                 // 5 A tiles
   uint8_t* bbuf = smem + 5 * kATile;     // 8 B tiles
-  uint64_t* bars = reinterpret_cast<uint64_t*>(bbuf + 8 * kBTile);  // [0..15] commit ring, 16 ready, 17 final
+  uint8_t* cbuf = bbuf + 8 * kBTile;    // 2 x 16 KB copy targets
+  uint64_t* bars = reinterpret_cast<uint64_t*>(cbuf + 2 * 16384);  // [0..15] commit ring, 16 ready, 17 final, 18/19 copy
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 20);
   const int warp = threadIdx.x >> 5;
   const uint32_t rank = ptx::cluster_ctarank();
@@ -49,7 +53,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
     reinterpret_cast<uint32_t*>(smem)[i] = v;
   }
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 18; ++i) ptx::mbar_init(bars + i, 1);
+    for (int i = 0; i < 20; ++i) ptx::mbar_init(bars + i, 1);
     ptx::fence_barrier_init();
   }
   if (warp == 1) ptx::tmem_alloc_pair<512>(tslot);
@@ -112,6 +116,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
     if (threadIdx.x == 32) out[blockIdx.x / 2] = t1 - t0;
   } else if (warp == 1) {
     ptx::mbar_wait(bars + 17, 0);  // the peer's copy of the final commit
+  } else if (warp == 2 && P.copy_kb > 0 && ptx::elect_one()) {
+    // concurrent smem fill traffic: bulk copies until the MMA side is done
+    const uint32_t bytes = P.copy_kb * 1024u;
+    unsigned long long t0 = clock64(), moved = 0;
+    for (int i = 0; !ptx::mbar_try_wait(bars + 17, 0); ++i) {
+      uint64_t* bar = bars + 18 + (i & 1);
+      if (i >= 2) ptx::mbar_wait(bar, ((i >> 1) - 1) & 1);
+      ptx::mbar_arrive_expect_tx(bar, bytes);
+      const uint8_t* src = P.src + (static_cast<uint64_t>(blockIdx.x * 7 + i) % 64) * 65536;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(ptx::smem_u32(cbuf + (i & 1) * 16384)), "l"(src), "r"(bytes), "r"(ptx::smem_u32(bar)) : "memory");
+      moved += bytes;
+      if (P.copy_sleep_ns) __nanosleep(P.copy_sleep_ns);
+    }
+    unsigned long long t1 = clock64();
+    out[1024 + blockIdx.x] = (moved << 20) / (t1 - t0 + 1);  // bytes/clk << 20
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();
@@ -122,7 +142,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
 }
 
 int main(int argc, char** argv) {
-  BP P{2000, 4, 1, 1, 4, 4, 1, 5, 128, 0, {}};
+  BP P{2000, 4, 1, 1, 4, 4, 1, 5, 128, 0, 0, 0, nullptr, {}};
   if (argc > 1) P.rounds = atoi(argv[1]);
   if (argc > 2) P.prods = atoi(argv[2]);
   if (argc > 3) P.commit = atoi(argv[3]);
@@ -134,13 +154,19 @@ int main(int argc, char** argv) {
   if (argc > 9) P.bn = atoi(argv[9]);
   int grid = argc > 10 ? atoi(argv[10]) : 148;
   if (argc > 11) P.mode = atoi(argv[11]);
+  if (argc > 12) P.copy_kb = atoi(argv[12]);
+  if (argc > 13) P.copy_sleep_ns = atoi(argv[13]);
+  uint8_t* src;
+  cudaMalloc(&src, 64 << 20);
+  cudaMemset(src, 0x5a, 64 << 20);
+  P.src = src;
   if (P.mode >= 2) P.prods = 8, P.run = 4, P.nacc = 4;
   for (int p = 0; p < 64; ++p) P.info[p] = ((p % 8) * kBTile >> 4) | ((p % P.nacc) << 16);
-  const size_t smem = 5 * kATile + 8 * kBTile + 1024 + 256;
+  const size_t smem = 5 * kATile + 8 * kBTile + 2 * 16384 + 1024 + 256;
   cudaFuncSetAttribute(mma_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   unsigned long long* d;
-  cudaMalloc(&d, sizeof(unsigned long long) * grid / 2);
-  cudaMemset(d, 0, sizeof(unsigned long long) * grid / 2);
+  cudaMalloc(&d, sizeof(unsigned long long) * 2048);
+  cudaMemset(d, 0, sizeof(unsigned long long) * 2048);
   mma_bench<<<grid, 128, smem>>>(P, d);  // warm-up
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -158,13 +184,18 @@ int main(int argc, char** argv) {
   std::vector<unsigned long long> h(grid / 2);
   cudaMemcpy(h.data(), d, sizeof(unsigned long long) * grid / 2, cudaMemcpyDeviceToHost);
   std::sort(h.begin(), h.end());
+  std::vector<unsigned long long> hc(grid);
+  cudaMemcpy(hc.data(), d + 1024, sizeof(unsigned long long) * grid, cudaMemcpyDeviceToHost);
+  double cbw = 0;
+  for (auto x : hc) cbw += x / double(1 << 20);
+  cbw /= grid;
   const double mmas = double(P.rounds) * P.prods * P.run;
   const double floor_cyc = 256.0 * P.bn / 512.0;  // max(M,128)*N/(256*2)
   printf("mode=%d rounds=%d prods=%d commit=%d wait=%d nacc=%d run=%d fill=%d nbars=%d N=%d grid=%d: "
-         "cyc/MMA med %.1f (min %.1f max %.1f) floor %.0f -> eff %.3f | %.3f ms, %.0f TOPS\n",
+         "cyc/MMA med %.1f (min %.1f max %.1f) floor %.0f -> eff %.3f | %.3f ms, %.0f TOPS | copy %dKB: %.1f B/clk/SM\n",
          P.mode, P.rounds, P.prods, P.commit, P.wait, P.nacc, P.run, P.fill, P.nbars, P.bn, grid,
          h[h.size() / 2] / mmas, h[0] / mmas, h.back() / mmas, floor_cyc,
          floor_cyc / (h[h.size() / 2] / mmas), ms,
-         mmas * (grid / 2) * 256.0 * P.bn * 32 * 2 / (ms * 1e-3) / 1e12);
+         mmas * (grid / 2) * 256.0 * P.bn * 32 * 2 / (ms * 1e-3) / 1e12, P.copy_kb, cbw);
   return 0;
 }
