@@ -135,6 +135,14 @@ typedef struct {
                               of the CTA-pair kernel (clamped to what fits, >= 2) */
   int host_panels;         /* tuning, same results (ozmm_dgemm_host): 0 = auto (16)
                               row panels of op(A) / column panels of op(B) */
+  int host_staging;        /* ozmm_dgemm_host, same results: 0 = auto -- pageable
+                              (unregistered) A / B / C go through rings of pinned
+                              slots filled by a team of host threads, pinned ones
+                              are copied directly; 1 = off (the driver copies
+                              pageable memory itself, single-threaded);
+                              2 = stage every buffer (tests) */
+  int host_threads;        /* ozmm_dgemm_host staging team size; 0 = auto
+                              (min(8, hardware threads)) */
 } ozmm_options_t;
 
 /* Scheme presets (config_for, scheme.cpp:137-159) plus the two other valid
@@ -245,7 +253,8 @@ int ozmm_gemm_slices_strided(ozmm_handle_t h, int64_t m, int64_t n, int64_t p, i
 
 /* Offset-binary halves (the fused GEMM's fast operand format, see
  * ozmm_options_t.signed_slices).  ozmm_split_offset writes byte = slice + o_s
- * (o_1 = 2^beta - 1, o_s = 2^(beta-1) for s >= 2; padding bytes 0) and the
+ * (even offsets o_1 = 2^beta, o_s = max(2, 2^(beta-1)) for s >= 2; padding
+ * bytes 0) and the
  * line sums of the SIGNED slices (mod 2^32) at
  *   lsum[s * lsum_plane + line * lsum_lstride],  s = 0..k-1
  * -- [k][lines] (lsum_lstride = 1, lsum_plane >= lines) or [lines][k]

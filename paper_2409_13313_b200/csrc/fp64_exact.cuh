@@ -13,6 +13,15 @@ namespace ozb {
 // 2^e as a double, exactly as std::ldexp(1.0, e) rounds it: normal for
 // e >= -1022, subnormal down to 2^-1074, 0 below (2^-1075 is a tie that rounds
 // to even = 0), +inf above 1023.
+// Slice offsets of the offset-binary planes: o_1 = 2^beta, o_s = max(2, 2^(beta-1))
+// for s >= 2 -- both EVEN, see emit16 -- so every byte slice + o_s lies in
+// [0, 255]: slice 1 + o_1 in [1, 2^(beta+1) - 1] (|slice_1| <= 2^beta - 1 by
+// rn_unit's bump rule), slice s + o_s in [0, 2^beta] (|slice_s| <= 2^(beta-1)
+// after round-to-nearest).
+__host__ __device__ __forceinline__ uint32_t slice_offset(int s, int beta) {
+  return s == 1 ? (1u << beta) : (beta >= 2 ? 1u << (beta - 1) : 2u);
+}
+
 __host__ __device__ __forceinline__ double pow2(int e) {
   uint64_t bits;
   if (e >= -1022) {

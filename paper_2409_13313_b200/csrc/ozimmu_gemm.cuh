@@ -63,7 +63,7 @@ struct GemmParams {
   int group_pairs;     // CTA-pair kernel: issue A groups two at a time (OZMM_GROUP_PAIRS)
   int kpair;           // CTA-pair kernel: thin passes take K blocks in pairs (OZMM_KPAIR)
   // Offset-binary operands (CTA-pair kernel only; slicer.cuh): the slice planes
-  // hold slice + o_s (o_1 = 2^beta - 1, o_s = 2^(beta-1)) as u8 and the MMAs run
+  // hold slice + o_s (o_1 = 2^beta, o_s = max(2, 2^(beta-1)), slice_offset) as u8 and the MMAs run
   // u8 x u8.  For a chunk c the accumulator then holds, mod 2^32,
   //   acc_c + sum_{(s,t) in c} [ o_t lsa[s][i] + o_s lsb[t][j] + o_s o_t n ]
   // and the epilogue subtracts that exactly (lsa / lsb = signed line sums).

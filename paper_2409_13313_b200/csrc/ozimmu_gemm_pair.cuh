@@ -460,7 +460,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
       ec_hi = max(ec_hi, e);
     }
 
-    const uint32_t o1 = (1u << P.beta) - 1u, os = 1u << (P.beta - 1);  // slice offsets
+    const uint32_t o1 = slice_offset(1, P.beta), os = slice_offset(2, P.beta);  // slice offsets
     // C is read once, after the last MMA: pull this CTA's 128 rows x kBN columns
     // into L2 now, while the MMAs run, so that the final pass waits on L2 rather
     // than HBM (it was 31 us per tile, profiles/r1/tile_trace.txt)

@@ -27,6 +27,7 @@
 #include "../../include/ozmm_b200.h"
 #include "ozimmu_gemm.cuh"
 #include "ozimmu_gemm_pair.cuh"
+#include "host_stage.hpp"
 #include "schedule.hpp"
 #include "slicer.cuh"
 #include "slicer_methods.cuh"
@@ -113,6 +114,8 @@ struct Handle {
   size_t nu_n = 0;
   unsigned long long* colmax = nullptr;
   size_t colmax_n = 0;
+  int* psync = nullptr;  // one-pass column split: work counter + per-panel counters
+  size_t psync_n = 0;
   int* flags = nullptr;  // [kNumFlags]: see fold_flags_kernel
   double* units_a = nullptr;  // per-slice units (RN per slice) [k][m] / [k][p]
   size_t units_a_n = 0;
@@ -139,6 +142,9 @@ struct Handle {
   cudaStream_t s_aux = nullptr;                   // device entry: B's column maxima
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int* hflags = nullptr;                          // pinned copy of flags (host entry gate)
+  // host entry, pageable caller buffers: pinned slot rings + the copy team (host_stage.hpp)
+  std::unique_ptr<ozb::WorkerPool> pool;
+  ozb::HostStager stage_in, stage_out;
   cudaEvent_t ev[5] = {};
   bool gemm_attr_set[3] = {false, false, false};
   bool pair_attr_set[2] = {false, false};
@@ -238,6 +244,45 @@ int launch_colmax(Handle* h, int64_t lines, int64_t n, const double* X, int64_t 
   return OZMM_OK;
 }
 
+// One-pass column split (slice_cols_panel_kernel: op(B) read from HBM once, the
+// slicing pass re-reads each column panel from L2).  Panels of ~32 MB; the
+// maxima of panel q + 1 are taken while panel q is sliced.
+int launch_cols_onepass(Handle* h, int64_t lines, int64_t n, const double* X, int64_t ldx, int k, int beta,
+                        int8_t* S, int64_t lds, int64_t plane, double* shift, int* lsum, int64_t lsum_plane,
+                        int64_t lsum_lstride) {
+  int64_t panel_mb = 32;
+  if (const char* e = OZMM_ENV("OZMM_PANEL_MB")) panel_mb = std::max(1, std::atoi(e));
+  const int64_t col_tiles = (lines + 31) / 32;
+  const int panel_tiles = static_cast<int>(
+      std::min<int64_t>(col_tiles, std::max<int64_t>(1, (panel_mb << 20) / (32 * 8 * std::max<int64_t>(1, n)))));
+  const int npanels = static_cast<int>((col_tiles + panel_tiles - 1) / panel_tiles);
+  if (int rc = ensure(h, &h->colmax, &h->colmax_n, static_cast<size_t>(lines))) return rc;
+  if (int rc = ensure(h, &h->psync, &h->psync_n, static_cast<size_t>(npanels) + 1)) return rc;
+  CUDA_TRY(h, cudaMemsetAsync(h->colmax, 0, sizeof(unsigned long long) * lines, h->stream));
+  CUDA_TRY(h, cudaMemsetAsync(h->psync, 0, sizeof(int) * (npanels + 1), h->stream));
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    CUDA_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ozb::slice_cols_panel_kernel, 256, 0));
+    per_sm = std::max(1, per_sm);
+  }
+  const int tpc = lsum ? 8 : 1;
+  int lag = 1;
+  if (const char* e = OZMM_ENV("OZMM_PANEL_LAG")) lag = std::max(1, std::atoi(e));
+  ozb::slice_cols_panel_kernel<<<h->num_sms * per_sm, 256, 0, h->stream>>>(
+      X, ldx, n, lines, lds, k, beta, h->colmax, S, plane, shift, h->flags, lsum, lsum_plane, lsum_lstride, tpc,
+      h->psync, panel_tiles, lag, 512);
+  CUDA_TRY(h, cudaGetLastError());
+  return OZMM_OK;
+}
+
+// Column split path: the two-pass colmax_kernel + slice_cols_kernel (default:
+// 1.16 ms at C3 against 2.1 ms for the panel walk, tools/cols_probe.py) or the
+// one-pass panel walk (OZMM_COLS_TWO_PASS=0, diag builds).
+bool cols_two_pass() {
+  const char* e = OZMM_ENV("OZMM_COLS_TWO_PASS");
+  return e == nullptr || std::atoi(e) != 0;
+}
+
 // colmax_ready: column mode only, h->colmax already holds this X's maxima.
 int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const double* X, int64_t ldx,
                  int k, int beta, int8_t* S, int64_t lds, int64_t plane, double* shift,
@@ -294,6 +339,10 @@ int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const doubl
                                                                        beta, S, plane, shift,
                                                                        h->flags, lsum, lsum_plane, lsum_lstride);
     }
+  } else if (!colmax_ready && !cols_two_pass()) {
+    if (int rc = launch_cols_onepass(h, lines, n, X, ldx, k, beta, S, lds, plane, shift, lsum, lsum_plane,
+                                     lsum_lstride))
+      return rc;
   } else {
     if (!colmax_ready)
       if (int rc = launch_colmax(h, lines, n, X, ldx)) return rc;
@@ -575,14 +624,17 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   // all B slices resident), so that the two-group issue rounds are even (8+1,
   // 7+2, ... products): C3 +3-4 % (profiles/r1/aorder_g2.txt).  Multi-window
   // schedules (k >= 9) keep the sorted order (C5 k=12: -1.7 % interleaved).
-  cm.interleave = k <= Cfg::kMaxBSlots;
+  // B slices resident per K block (the window of a pass); OZMM_BWIN (diag) probes
+  // wider windows at the cost of A-ring depth
+  int bwin = Cfg::kMaxBSlots;
+  if (const char* e = OZMM_ENV("OZMM_BWIN")) bwin = std::max(1, std::min(12, std::atoi(e)));
+  cm.interleave = k <= bwin;
   if (const char* e = OZMM_ENV("OZMM_AORDER")) cm.interleave = std::string(e) == "interleave";
   // ... and no two consecutive products into one accumulator (C3 +1 %)
   cm.avoid_raw = cm.interleave;
   if (const char* e = OZMM_ENV("OZMM_AVOID_RAW")) cm.avoid_raw = std::atoi(e) != 0;
   const ozb::Schedule S = ozb::make_schedule(k, fl.per_product ? 1 : r, Cfg::kNAcc,
-                                             static_cast<int64_t>(Cfg::kMaxBSlots) * Cfg::kBTile,
-                                             slot_bytes, Cfg::kMaxBSlots, cm);
+                                             static_cast<int64_t>(bwin) * Cfg::kBTile, slot_bytes, bwin, cm);
   if (!schedule_fits(S))
     return set_err(h, OZMM_ERR_UNSUPPORTED, "schedule too large (k=%d, r=%lld)", k,
                    static_cast<long long>(r));
@@ -601,7 +653,7 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   int b_slots = 1;
   for (const auto& q : S.passes) {
     const int nbw = q.bhi - q.blo + 1;
-    const bool pair_kb = kPairs == 1 && kpair && 2 * nbw <= Cfg::kMaxBSlots && n_kb % 2 == 0;
+    const bool pair_kb = kPairs == 1 && kpair && 2 * nbw <= bwin && n_kb % 2 == 0;
     b_slots = std::max(b_slots, pair_kb ? 2 * nbw : nbw);
   }
   const size_t fixed = Cfg::smem_bytes(b_slots, 0);
@@ -953,6 +1005,7 @@ int ozmm_destroy(ozmm_handle_t handle) {
   cudaFree(h->mu);
   cudaFree(h->nu);
   cudaFree(h->colmax);
+  cudaFree(h->psync);
   cudaFree(h->flags);
   cudaFree(h->units_a);
   cudaFree(h->units_b);
@@ -973,6 +1026,8 @@ int ozmm_destroy(ozmm_handle_t handle) {
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->hflags) cudaFreeHost(h->hflags);
   for (auto& ev : h->ev) cudaEventDestroy(ev);
+  h->stage_in.release();
+  h->stage_out.release();
   delete h;
   return OZMM_OK;
 }
@@ -1395,10 +1450,12 @@ int ozmm_dgemm_ex(ozmm_handle_t handle, char transa, char transb, int64_t m, int
     CUDA_TRY(h, cudaEventRecord(h->ev_fork, user));
     CUDA_TRY(h, cudaStreamWaitEvent(h->s_aux, h->ev_fork, 0));
     h->stream = h->s_aux;
-    int rc = launch_colmax(h, p, n, B, ldb);
+    // one-pass column split: no separate maxima pass
+    const bool one_pass = overlap_bsplit && !cols_two_pass();
+    int rc = one_pass ? OZMM_OK : launch_colmax(h, p, n, B, ldb);
     if (!rc && overlap_bsplit)  // split B (Right, columns) -- scheme.cpp:251
       rc = launch_split(h, false, p, n, B, ldb, k, beta_bits, h->slices_b, lds, p * lds, out_b,
-                        h->lsb, p, 1, true);
+                        h->lsb, p, 1, !one_pass);
     h->stream = user;
     if (rc) return rc;
     CUDA_TRY(h, cudaEventRecord(h->ev_join, h->s_aux));
@@ -1583,6 +1640,7 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   if (int rc = ensure(h, &h->nu, &h->nu_n, static_cast<size_t>(p))) return rc;
   // column-line splits reuse h->colmax: size it once so no launch reallocates it
   if (int rc = ensure(h, &h->colmax, &h->colmax_n, static_cast<size_t>(std::max(pa, pb)))) return rc;
+  if (int rc = ensure(h, &h->psync, &h->psync_n, static_cast<size_t>((std::max(pa, pb) + 31) / 32 + 1))) return rc;
   if (!h->s_in) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
   if (!h->s_out) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
   if (!h->s_split) {
@@ -1595,6 +1653,26 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   if (!h->hflags) CUDA_TRY(h, cudaMallocHost(reinterpret_cast<void**>(&h->hflags), 2 * sizeof(int)));
   double *dA = h->host_a, *dB = h->host_b, *dC = h->host_c, *dO = h->host_o;
   const size_t D = sizeof(double);
+  // Pageable caller buffers (numpy, Eigen, std::vector) cross PCIe through rings
+  // of pinned slots filled by a team of host threads (host_stage.hpp); pinned
+  // ones are copied directly by the DMA engines.
+  const int hs_mode = opt ? opt->host_staging : 0;
+  if (hs_mode < 0 || hs_mode > 2 || (opt && opt->host_threads < 0))
+    return set_err(h, OZMM_ERR_ARG, "options: host_staging must be 0..2 and host_threads >= 0");
+  auto staged = [&](const void* ptr) { return hs_mode == 2 || (hs_mode == 0 && ozb::host_pageable(ptr)); };
+  const bool pg_a = staged(A), pg_b = staged(B), pg_c = staged(C);
+  if (pg_a || pg_b || pg_c) {
+    int nt = opt && opt->host_threads ? opt->host_threads
+                                      : static_cast<int>(std::min(8u, std::max(1u, std::thread::hardware_concurrency())));
+    if (const char* e = OZMM_ENV("OZMM_STAGE_THREADS")) nt = std::max(1, std::atoi(e));
+    if (!h->pool || h->pool->size() != nt) h->pool.reset(new ozb::WorkerPool(nt));
+    size_t slot = size_t(32) << 20;
+    int nslots = 4;
+    if (const char* e = OZMM_ENV("OZMM_STAGE_SLOT_MB")) slot = size_t(std::max(1, std::atoi(e))) << 20;
+    if (const char* e = OZMM_ENV("OZMM_STAGE_SLOTS")) nslots = std::max(2, std::atoi(e));
+    CUDA_TRY(h, h->stage_in.init(slot, nslots, h->pool.get()));
+    CUDA_TRY(h, h->stage_out.init(slot, nslots, h->pool.get()));
+  }
 
   // Panel arrival order over PCIe: A_s then B_s per step, except that the last
   // step sends B first, so the final strip is a row strip -- full-width host
@@ -1667,6 +1745,24 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
       rc = set_err(h, OZMM_ERR_CUDA, "%s failed: %s", what, cudaGetErrorString(e));
     return e == cudaSuccess;
   };
+  // 2-D copies between the caller's buffers and the device: direct for pinned
+  // memory, through the slot rings for pageable memory (the staged calls return
+  // once the host side is done: they pace the issue loop below)
+  // With A and B both staged (no_c mode), the staging copy also screens every
+  // element for the range error (host_stage.hpp copy_screen), so no scanner has
+  // to re-read them; with C staged too, the old C entries are checked for inf /
+  // NaN as the result overwrites them (copy_patch) instead of by a separate scan.
+  const bool screen_ab = no_c && pg_a && pg_b, patch_c = no_c && pg_c;
+  std::atomic<uint64_t> big_ab{0};
+  auto h2d = [&](bool pg, void* dst, size_t dp, const void* src, size_t sp, size_t w, size_t rows,
+                 const char* what, bool screen = false) {
+    return cu(pg ? h->stage_in.h2d(dst, dp, src, sp, w, rows, h->s_in, screen ? &big_ab : nullptr)
+                 : cudaMemcpy2DAsync(dst, dp, src, sp, w, rows, cudaMemcpyHostToDevice, h->s_in), what);
+  };
+  auto d2h = [&](void* dst, size_t dp, const void* src, size_t sp, size_t w, size_t rows, const char* what) {
+    return cu(pg_c ? h->stage_out.d2h(dst, dp, src, sp, w, rows, h->s_out, patch_c ? &beta : nullptr)
+                   : cudaMemcpy2DAsync(dst, dp, src, sp, w, rows, cudaMemcpyDeviceToHost, h->s_out), what);
+  };
 
   // Host scans (no-C mode), concurrent with the GPU:
   //  1. C for non-finite entries (patched on the host afterwards, see below);
@@ -1703,16 +1799,16 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
     }
     return big;
   };
-  if (no_c) {
+  if (no_c && (!patch_c || !screen_ab)) {
     int64_t want = 8;
     if (const char* e = OZMM_ENV("OZMM_SCAN_THREADS")) want = std::max(1, std::atoi(e));
     const int nt = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>({want, static_cast<int64_t>(std::thread::hardware_concurrency()), (m * p) >> 20})));
     bad.resize(nt);
-    c_scans_left = nt;
+    c_scans_left = patch_c ? 0 : nt;
     for (int t = 0; t < nt; ++t)
       scanners.emplace_back([&, t, nt] {
-        const int64_t i0 = m * t / nt, i1 = m * (t + 1) / nt;
+        const int64_t i0 = patch_c ? 0 : m * t / nt, i1 = patch_c ? 0 : m * (t + 1) / nt;
         constexpr uint64_t kExp = 0x7FF0000000000000ull, kOne = 0x0010000000000000ull;
         for (int64_t i = i0; i < i1; ++i) {
           const uint64_t* row = reinterpret_cast<const uint64_t*>(C + i * ldc);
@@ -1725,7 +1821,8 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
               if ((row[j] & 0x7FF0000000000000ull) == 0x7FF0000000000000ull)
                 bad[t].push_back({i * ldc + j, C[i * ldc + j]});
         }
-        --c_scans_left;
+        if (!patch_c) --c_scans_left;
+        if (screen_ab) return;  // the staging copies screen A and B
         // tail scan: claim steps from the last one backwards until the gate opens
         while (!stop_tail.load() && !tail_hit.load()) {
           const int st = next_tail.fetch_sub(1);
@@ -1760,11 +1857,15 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   for (cudaStream_t s : {h->s_in, h->s_out, h->s_split, h->s_gemm[0], h->s_gemm[1]})
     cu(cudaStreamWaitEvent(s, evStart, 0), "wait");
 
-  // H2D stream: the panels in arrival order, each followed by the C block its strip reads
+  // One issue loop over the panel arrivals: the panel's H2D copy (each followed by
+  // the C block its strip reads), its split on the high-priority split stream,
+  // then the strip of C it completes on one of the two GEMM streams (the split
+  // stream is in order, so the strip's split event covers every panel it reads).
+  // Staged copies block here while the host team fills the slots; everything
+  // else is asynchronous.
   auto copy_c = [&](int q) {
     const Strip& t = strips[q];
-    cu(cudaMemcpy2DAsync(dC + t.r0 * p + t.c0, D * p, C + t.r0 * ldc + t.c0, D * ldc, D * t.cols, t.rows,
-                         cudaMemcpyHostToDevice, h->s_in), "H2D C");
+    h2d(pg_c, dC + t.r0 * p + t.c0, D * p, C + t.r0 * ldc + t.c0, D * ldc, D * t.cols, t.rows, "H2D C");
     cu(cudaEventRecord(evC[q], h->s_in), "event");
   };
   for (size_t o = 0; o < order.size() && rc == OZMM_OK; ++o) {
@@ -1772,28 +1873,22 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
     if (order[o].is_a) {
       const int64_t r0 = s0 * pa, rows = std::min(pa, m - r0);
       if (ta)  // op(A) rows r0.. = columns r0.. of the stored n x m A
-        cu(cudaMemcpy2DAsync(dA + r0, D * m, A + r0, D * lda, D * rows, n, cudaMemcpyHostToDevice,
-                             h->s_in), "H2D A");
+        h2d(pg_a, dA + r0, D * m, A + r0, D * lda, D * rows, n, "H2D A", screen_ab);
       else
-        cu(cudaMemcpy2DAsync(dA + r0 * n, D * n, A + r0 * lda, D * lda, D * n, rows,
-                             cudaMemcpyHostToDevice, h->s_in), "H2D A");
+        h2d(pg_a, dA + r0 * n, D * n, A + r0 * lda, D * lda, D * n, rows, "H2D A", screen_ab);
       cu(cudaEventRecord(evA[s0], h->s_in), "event");
     } else {
       const int64_t c0 = s0 * pb, cols = std::min(pb, p - c0);
       if (tb)  // op(B) columns c0.. = rows c0.. of the stored p x n B
-        cu(cudaMemcpy2DAsync(dB + c0 * n, D * n, B + c0 * ldb, D * ldb, D * n, cols,
-                             cudaMemcpyHostToDevice, h->s_in), "H2D B");
+        h2d(pg_b, dB + c0 * n, D * n, B + c0 * ldb, D * ldb, D * n, cols, "H2D B", screen_ab);
       else
-        cu(cudaMemcpy2DAsync(dB + c0, D * p, B + c0, D * ldb, D * cols, n, cudaMemcpyHostToDevice,
-                             h->s_in), "H2D B");
+        h2d(pg_b, dB + c0, D * p, B + c0, D * ldb, D * cols, n, "H2D B", screen_ab);
       cu(cudaEventRecord(evB[s0], h->s_in), "event");
     }
-    if (!no_c && strip_of[o] >= 0) copy_c(strip_of[o]);
-  }
-  // split stream (high priority): each panel as soon as it lands
-  h->stream = h->s_split;
-  for (size_t o = 0; o < order.size() && rc == OZMM_OK; ++o) {
-    const int s0 = order[o].idx;
+    const int q = strip_of[o];
+    if (!no_c && q >= 0) copy_c(q);
+    // split (high-priority stream), as soon as the panel lands
+    h->stream = h->s_split;
     if (order[o].is_a) {
       const int64_t r0 = s0 * pa, rows = std::min(pa, m - r0);
       cu(cudaStreamWaitEvent(h->s_split, evA[s0], 0), "wait");
@@ -1811,11 +1906,8 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
                           offset ? h->lsb + c0 : nullptr, p);
       cu(cudaEventRecord(evSB[s0], h->s_split), "event");
     }
-  }
-  cu(cudaEventRecord(evSplit, h->s_split), "event");
-  // GEMM streams: one fused launch per strip (the split stream is in order, so the
-  // strip's last split event covers every panel it reads)
-  for (int q = 0; q < ns && rc == OZMM_OK; ++q) {
+    if (q < 0 || rc != OZMM_OK) continue;
+    // the strip of C this arrival completes
     const Strip& t = strips[q];
     cudaStream_t sg = h->s_gemm[q & 1];
     cu(cudaStreamWaitEvent(sg, t.trig_a ? evSA[t.trig] : evSB[t.trig], 0), "wait");
@@ -1832,12 +1924,12 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
                        no_c ? nullptr : dC + t.r0 * p + t.c0, dO + t.r0 * p + t.c0, p, opt, fl);
     cu(cudaEventRecord(evG[q], sg), "event");
   }
+  cu(cudaEventRecord(evSplit, h->s_split), "event");
   h->stream = user;
   auto copy_out = [&](int q) {
     const Strip& t = strips[q];
     cu(cudaStreamWaitEvent(h->s_out, evG[q], 0), "wait");
-    cu(cudaMemcpy2DAsync(C + t.r0 * ldc + t.c0, D * ldc, dO + t.r0 * p + t.c0, D * p, D * t.cols, t.rows,
-                         cudaMemcpyDeviceToHost, h->s_out), "D2H C");
+    d2h(C + t.r0 * ldc + t.c0, D * ldc, dO + t.r0 * p + t.c0, D * p, D * t.cols, t.rows, "D2H C");
     if (trace) cu(cudaEventRecord(evO[q], h->s_out), "event");
   };
   bool range_err = false;
@@ -1854,7 +1946,13 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
     // steps [s, steps) clean; otherwise (a big element on the host side, or a
     // device error) after every split, as before
     bool early = false;
-    for (;;) {
+    // staged A and B: every panel has been screened on its way in (the issue loop
+    // above returned), so a clean screen opens the gate at once
+    if (screen_ab && rc == OZMM_OK) {
+      early = (big_ab.load() >> 63) == 0;
+      if (!early) tail_hit = 1;  // the device flags decide, after every split
+    }
+    for (; !screen_ab;) {
       if (tail_hit.load() || rc != OZMM_OK) break;
       int gd = 0;
       while (gd < steps && (gd >= ra || cudaEventQuery(evSA[gd]) == cudaSuccess) &&
@@ -1896,8 +1994,7 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
         }
         if (area == R * Cc) {
           for (int q = 0; q < qd; ++q) cu(cudaStreamWaitEvent(h->s_out, evG[q], 0), "wait");
-          cu(cudaMemcpy2DAsync(C, D * ldc, dO, D * p, D * Cc, R, cudaMemcpyDeviceToHost, h->s_out),
-             "D2H C");
+          d2h(C, D * ldc, dO, D * p, D * Cc, R, "D2H C");
           if (trace)
             for (int q = 0; q < qd; ++q) cu(cudaEventRecord(evO[q], h->s_out), "event");
           q0 = qd;

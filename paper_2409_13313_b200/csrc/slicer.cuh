@@ -14,10 +14,10 @@
 // zeros.  The shift vector is written as doubles (const_shift, split.hpp:37).
 //
 // Offset-binary planes (`lsum != nullptr`, the fused GEMM's operand format):
-// byte = slice + o_s with o_1 = 2^beta - 1 and o_s = 2^(beta-1) for s >= 2, so
-// every byte is an unsigned value in [0, 2^(beta+1) - 2] (|slice_1| <= 2^beta - 1
-// by rn_unit's bump rule, |slice_s| <= 2^(beta-1) after round-to-nearest);
-// padding bytes stay 0.  lsum[s * lsum_plane + line * lsum_lstride] (zeroed by
+// byte = slice + o_s with the even offsets o_1 = 2^beta and o_s = max(2,
+// 2^(beta-1)) for s >= 2 (slice_offset), so every byte is an unsigned value in
+// [0, 255] (|slice_1| <= 2^beta - 1 by rn_unit's bump rule, |slice_s| <=
+// 2^(beta-1) after round-to-nearest); padding bytes stay 0.  lsum[s * lsum_plane + line * lsum_lstride] (zeroed by
 // the caller) receives the line's sum of the SIGNED slice values (mod 2^32), from which the GEMM removes
 // the offsets' contribution exactly (ozimmu_gemm_pair.cuh).  The signed planes
 // (lsum == nullptr) are the reference's SplitMatrix slices, bit for bit.
@@ -54,72 +54,79 @@ __device__ __forceinline__ void report_flags(int* flags, bool under, bool range)
 // store the k 16-byte runs.  PE == INT32_MIN marks a zero line.
 //
 // Per element and slice: t = w + sigma, x = t - sigma, w -= x (three RN adds,
-// exactly extract_row's (w+sigma)-sigma and w -= x).  The slice integer
-// x / unit is read off the bit pattern: sigma = 1.5 * 2^52 * unit and
-// |x| < 2^51 * unit put t in sigma's binade [2^52 unit, 2^53 unit), whose ulp
-// is unit, so bits(t) - bits(sigma) == x / unit exactly (no division, no
-// float->int conversion).  Valid for every unit >= 2^-1074 (sigma is then
-// normal); unit == 0 (underflowed grid) is handled separately.
+// exactly extract_row's (w+sigma)-sigma and w -= x).  sigma = 1.5 * 2^52 *
+// unit is built from its bits (its low word is 0) and |x| < 2^51 * unit puts
+// t in sigma's binade [2^52 unit, 2^53 unit), whose ulp is unit, so the low
+// word of bits(t) is the slice integer x / unit in two's complement -- no
+// subtract, division or float->int conversion.  Valid for every unit >=
+// 2^-1074 (sigma is then normal); unit == 0 (underflowed grid) is handled
+// separately.
 //
-// Offset mode (lsum != nullptr): the `nvalid` leading elements get the slice
-// offset; the per-slice sums of the signed values are reduced over the lanes
-// that share the line (kLaneGroup: 32 = the whole warp is one line, 8 = lanes
-// l, l^4, l^8, .. of slice_cols_kernel) and added into lsum[s-1][0] by the
-// group's first lane.  Every lane of the warp must call it (nvalid = 0 and
-// store = false for lanes without data).
+// Offset mode (lsum != nullptr): sigma is replaced by sigma' = sigma + o_s unit
+// (bits(sigma) + o_s: same binade).  Adding an exact multiple of the ulp
+// commutes with round-to-nearest inside a binade, and because o_s is EVEN the
+// ties-to-even choice is the same too, so t' = RN(w + sigma') = t + o_s unit
+// and x = t' - sigma' = t - sigma bit for bit; the low byte of bits(t') is the
+// offset-binary byte slice + o_s with no further instruction.  Padding elements
+// (the `nvalid`.. 15 tail of a line) are masked to byte 0.  The per-slice sums
+// of the SIGNED values (sum of the bytes minus o_s per valid element) are
+// reduced over the lanes that share the line (kLaneGroup: 32 = the whole warp
+// is one line, 8 = lanes l, l^4, l^8, .. of slice_cols_kernel) and added into
+// lsum[s-1][0] by the group's first lane.  Every lane of the warp must call it
+// (nvalid = 0 and store = false for lanes without data).
 template <int kLaneGroup = 32>
 __device__ __forceinline__ void emit16(double (&w)[16], int PE, int beta, int k,
                                        int8_t* dst, int64_t plane, int nvalid = 16,
                                        bool store = true, int* lsum = nullptr,
                                        int64_t lsum_plane = 0) {
   for (int s = 1; s <= k; ++s) {
-    // offset of this slice (0 for the signed planes); the byte (q + off) & 0xFF
-    // is slice + off because slice + off lies in [0, 254]
-    const uint32_t off = lsum == nullptr ? 0u : (s == 1 ? (1u << beta) - 1u : 1u << (beta - 1));
+    const uint32_t off = lsum == nullptr ? 0u : slice_offset(s, beta);  // 0: signed planes
     const uint32_t off4 = off * 0x01010101u;
     uint32_t packed[4] = {off4, off4, off4, off4};  // zero line / underflowed grid: slice 0
-    int qsum = 0;
-    if (PE != INT32_MIN) {
-      const int ue = PE + 1 - beta * s;
-      const double unit = pow2(ue);
-      if (unit != 0.0) {
-        const double sigma = __dmul_rn(kSigmaScale, unit);  // exact
-        // only the low byte of bits(t) - bits(sigma) is kept: the low words suffice
-        const uint32_t slo = static_cast<uint32_t>(__double2loint(sigma));
-        uint32_t q[16];
+    int qsum = 0;  // signed slice sum of this lane's elements (offset mode)
+    const int ue = PE + 1 - beta * s;  // exponent of unit_s
+    if (PE != INT32_MIN && ue >= -1074) {
+      // sigma' = (1.5 * 2^52 + off) * 2^ue: exponent field ue + 1075, mantissa 0x8000000000000 + off
+      const double sig = __hiloint2double(((ue + 1075) << 20) | 0x00080000, static_cast<int>(off));
+      uint32_t q[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const double t = __dadd_rn(w[e], sigma);
-          const double x = __dadd_rn(t, -sigma);
-          q[e] = static_cast<uint32_t>(__double2loint(t)) - slo;
-          w[e] = __dadd_rn(w[e], -x);
-        }
-        // byte-pack 4 slices with two PRMTs + one; the line sum of the signed
-        // bytes with one dp4a per 4; the offset with one per-byte add (the slicer
-        // is issue-bound, ncu: 79 % issue slots busy)
+      for (int e = 0; e < 16; ++e) {
+        const double t = __dadd_rn(w[e], sig);
+        const double x = __dadd_rn(t, -sig);
+        q[e] = static_cast<uint32_t>(__double2loint(t));
+        w[e] = __dadd_rn(w[e], -x);
+      }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint32_t lo = __byte_perm(q[4 * i], q[4 * i + 1], 0x0040);
-          const uint32_t hi = __byte_perm(q[4 * i + 2], q[4 * i + 3], 0x0040);
-          packed[i] = __byte_perm(lo, hi, 0x5410);
-          if (lsum != nullptr) {
-            qsum = __dp4a(static_cast<int>(packed[i]), 0x01010101, qsum);  // padding bytes are 0
-            packed[i] = __vadd4(packed[i], off4);  // no carries: slice + off in [0, 254]
-          }
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t lo = __byte_perm(q[4 * i], q[4 * i + 1], 0x0040);
+        const uint32_t hi = __byte_perm(q[4 * i + 2], q[4 * i + 3], 0x0040);
+        packed[i] = __byte_perm(lo, hi, 0x5410);
+      }
+      if (lsum != nullptr) {
+        if (nvalid < 16) {  // padding bytes stay 0
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (e >= nvalid) packed[e >> 2] &= ~(0xFFu << (8 * (e & 3)));
         }
-      } else {
+        uint32_t bsum = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) bsum = __dp4a(packed[i], 0x01010101u, bsum);
+        qsum = static_cast<int>(bsum - off * static_cast<uint32_t>(nvalid));
+      }
+    } else {
+      if (PE != INT32_MIN) {
         // unit underflowed to 0: the reference computes x = w, int8(w/0) = 0
         // (cvttsd2si of +-inf/NaN), w -= x -> 0.
 #pragma unroll
         for (int e = 0; e < 16; ++e) w[e] = __dadd_rn(w[e], -w[e]);
       }
-    }
-    if (lsum != nullptr) {
-      if (nvalid < 16) {  // padding bytes stay 0
+      if (lsum != nullptr && nvalid < 16) {
 #pragma unroll
         for (int e = 0; e < 16; ++e)
           if (e >= nvalid) packed[e >> 2] &= ~(0xFFu << (8 * (e & 3)));
       }
+    }
+    if (lsum != nullptr) {
       if constexpr (kLaneGroup == 32) {
         qsum = __reduce_add_sync(0xffffffffu, qsum);
         if ((threadIdx.x & 31) == 0 && qsum != 0)
@@ -299,8 +306,17 @@ __global__ void __launch_bounds__(256) colmax_kernel(const double* __restrict__ 
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_block;
   const int64_t r1 = min(len, r0 + rows_per_block);
   double m = 0.0;
-  if (col < cols)
-    for (int64_t r = r0 + ty; r < r1; r += 8) m = fmax(m, fabs(__ldg(X + r * ld + col)));
+  if (col < cols) {
+    int64_t r = r0 + ty;
+    for (; r + 56 < r1; r += 64) {  // 8 independent loads in flight per thread
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(X + (r + 8 * u) * ld + col);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) m = fmax(m, fabs(v[u]));
+    }
+    for (; r < r1; r += 8) m = fmax(m, fabs(__ldg(X + r * ld + col)));
+  }
   red[ty][tx] = m;
   __syncthreads();
   if (ty == 0) {
@@ -317,24 +333,29 @@ __global__ void __launch_bounds__(256) colmax_kernel(const double* __restrict__ 
 // rows 16*(l >> 2) .. +16.  Each warp load then touches 8 fully used 32-byte
 // sectors (4 adjacent columns x 8 rows) and, per slice, each column's 8
 // chunks form one contiguous 128-byte line of the output plane.
-__global__ void __launch_bounds__(256) slice_cols_kernel(const double* __restrict__ X, int64_t ld,
-                                                         int64_t len, int64_t cols, int64_t lds,
-                                                         int k, int beta,
-                                                         const unsigned long long* __restrict__ colmax,
-                                                         int8_t* __restrict__ S, int64_t plane,
-                                                         double* __restrict__ shift,
-                                                         int* __restrict__ flags,
-                                                         int* __restrict__ lsum, int64_t lsum_plane,
-                                                         int64_t lsum_lstride, int tiles_per_cta) {
+//
+// slice_cols_tile: the work of one CTA (tile bx of 32 columns, tile by of
+// tiles_per_cta x 128 rows); `kCoherent` reads the maxima with ld.global.cg
+// (they were written in the same launch, see slice_cols_panel_kernel).
+template <bool kCoherent>
+__device__ __forceinline__ void slice_cols_tile(const double* __restrict__ X, int64_t ld, int64_t len,
+                                                int64_t cols, int64_t lds, int k, int beta,
+                                                const unsigned long long* colmax, int8_t* __restrict__ S,
+                                                int64_t plane, double* __restrict__ shift, int* __restrict__ flags,
+                                                int* __restrict__ lsum, int64_t lsum_plane, int64_t lsum_lstride,
+                                                int tiles_per_cta, int64_t bx, int64_t by, int (*lsum_s)[32]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t col = static_cast<int64_t>(blockIdx.x) * 32 + warp * 4 + (lane & 3);
+  const int64_t col = bx * 32 + warp * 4 + (lane & 3);
+  auto cmax = [&](int64_t c) {
+    return __longlong_as_double(static_cast<long long>(kCoherent ? __ldcg(colmax + c) : colmax[c]));
+  };
   if (lsum == nullptr) {  // signed planes: one 128-row tile per CTA
-    const int64_t base = static_cast<int64_t>(blockIdx.y) * 128 + 16 * (lane >> 2);
+    const int64_t base = by * 128 + 16 * (lane >> 2);
     if (col >= cols || base >= lds) return;
-    const double rm = __longlong_as_double(static_cast<long long>(colmax[col]));
+    const double rm = cmax(col);
     bool under = false, range = false;
     const int PE = line_pe(rm, beta, &under, &range);
-    if (blockIdx.y == 0 && (lane >> 2) == 0) {
+    if (by == 0 && (lane >> 2) == 0) {
       shift[col] = PE == INT32_MIN ? 0.0 : pow2(PE);
       report_flags(flags, under, range);
     }
@@ -346,19 +367,17 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(const double* __restric
   }
   // offset planes: `tiles_per_cta` 128-row tiles per CTA; the column sums
   // collect in shared memory and leave with one atomic per column and slice
-  __shared__ int lsum_s[kMaxSlices][32];
   for (int i = threadIdx.x; i < kMaxSlices * 32; i += blockDim.x) lsum_s[i / 32][i % 32] = 0;
   __syncthreads();
-  const double rm = col < cols ? __longlong_as_double(static_cast<long long>(colmax[col])) : 0.0;
+  const double rm = col < cols ? cmax(col) : 0.0;
   bool under = false, range = false;
   const int PE = line_pe(rm, beta, &under, &range);
-  if (col < cols && blockIdx.y == 0 && (lane >> 2) == 0) {
+  if (col < cols && by == 0 && (lane >> 2) == 0) {
     shift[col] = PE == INT32_MIN ? 0.0 : pow2(PE);
     report_flags(flags, under, range);
   }
   for (int it = 0; it < tiles_per_cta; ++it) {  // uniform trip count: every lane reduces
-    const int64_t base =
-        (static_cast<int64_t>(blockIdx.y) * tiles_per_cta + it) * 128 + 16 * (lane >> 2);
+    const int64_t base = (by * tiles_per_cta + it) * 128 + 16 * (lane >> 2);
     const bool valid = col < cols && base < lds;
     double w[16];
 #pragma unroll
@@ -369,9 +388,124 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(const double* __restric
   }
   __syncthreads();
   for (int i = threadIdx.x; i < k * 32; i += blockDim.x) {
-    const int64_t c = static_cast<int64_t>(blockIdx.x) * 32 + (i % 32);
+    const int64_t c = bx * 32 + (i % 32);
     if (c < cols && lsum_s[i / 32][i % 32] != 0)
       atomicAdd(lsum + (i / 32) * lsum_plane + c * lsum_lstride, lsum_s[i / 32][i % 32]);
+  }
+}
+
+__global__ void __launch_bounds__(256) slice_cols_kernel(const double* __restrict__ X, int64_t ld,
+                                                         int64_t len, int64_t cols, int64_t lds,
+                                                         int k, int beta,
+                                                         const unsigned long long* __restrict__ colmax,
+                                                         int8_t* __restrict__ S, int64_t plane,
+                                                         double* __restrict__ shift,
+                                                         int* __restrict__ flags,
+                                                         int* __restrict__ lsum, int64_t lsum_plane,
+                                                         int64_t lsum_lstride, int tiles_per_cta) {
+  __shared__ int lsum_s[kMaxSlices][32];
+  slice_cols_tile<false>(X, ld, len, cols, lds, k, beta, colmax, S, plane, shift, flags, lsum, lsum_plane,
+                         lsum_lstride, tiles_per_cta, blockIdx.x, blockIdx.y, lsum_s);
+}
+
+// Column maxima of one 32-column x rows_per_tile tile (block 32 x 8 threads),
+// folded into colmax with one atomicMax per column.
+__device__ __forceinline__ void colmax_tile(const double* __restrict__ X, int64_t ld, int64_t len, int64_t cols,
+                                            int64_t rows_per_tile, int64_t bx, int64_t by,
+                                            unsigned long long* colmax, double (*red)[33]) {
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t col = bx * 32 + tx;
+  const int64_t r0 = by * rows_per_tile;
+  const int64_t r1 = min(len, r0 + rows_per_tile);
+  double m = 0.0;
+  if (col < cols) {
+    int64_t r = r0 + ty;
+    for (; r + 56 < r1; r += 64) {  // 8 independent loads in flight per thread
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(X + (r + 8 * u) * ld + col);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) m = fmax(m, fabs(v[u]));
+    }
+    for (; r < r1; r += 8) m = fmax(m, fabs(__ldg(X + r * ld + col)));
+  }
+  red[ty][tx] = m;
+  __syncthreads();
+  if (ty == 0) {
+#pragma unroll
+    for (int q = 1; q < 8; ++q) m = fmax(m, red[q][tx]);
+    if (col < cols && m != 0.0)
+      atomicMax(colmax + col, static_cast<unsigned long long>(__double_as_longlong(m)));
+  }
+}
+
+// One-pass column split (K1 for op(B) columns, HBM reads op(B) ONCE): a
+// persistent grid walks a work list over column panels of `panel_tiles` x 32
+// columns -- the maxima tiles of panel q + lag come before the slicing tiles of
+// panel q -- so a panel is sliced while the maxima pass has just pulled it into
+// L2 (panel_tiles x 32 columns x len doubles, sized by the host to stay
+// L2-resident for `lag` + 1 panels).  Work items are claimed in order with one
+// atomic counter; a slicing tile waits until its panel's maxima tiles are done
+// (per-panel completion counters, release/acquire through __threadfence and
+// L2-coherent loads).  Every item it waits for was claimed earlier by a
+// running CTA that never waits itself, so the walk cannot deadlock.
+// sync[0] = work counter, sync[1 + q] = finished maxima tiles of panel q
+// (zeroed by the host, as is colmax).
+__global__ void __launch_bounds__(256) slice_cols_panel_kernel(
+    const double* __restrict__ X, int64_t ld, int64_t len, int64_t cols, int64_t lds, int k, int beta,
+    unsigned long long* colmax, int8_t* __restrict__ S, int64_t plane, double* __restrict__ shift,
+    int* __restrict__ flags, int* __restrict__ lsum, int64_t lsum_plane, int64_t lsum_lstride,
+    int tiles_per_cta, int* sync, int panel_tiles, int lag, int64_t max_rows_per_tile) {
+  __shared__ int lsum_s[kMaxSlices][32];
+  __shared__ double red[8][33];
+  __shared__ int item_s;
+  const int64_t col_tiles = (cols + 31) / 32;
+  const int npanels = static_cast<int>((col_tiles + panel_tiles - 1) / panel_tiles);
+  const int64_t mt = (len + max_rows_per_tile - 1) / max_rows_per_tile;         // maxima tiles per column tile
+  const int64_t st = (lds + 128 * tiles_per_cta - 1) / (128 * tiles_per_cta);  // slicing tiles per column tile
+  // work list: step q = [maxima of panel q (q < npanels)] [slicing of panel q - lag (q >= lag)]
+  for (;;) {
+    if (threadIdx.x == 0) item_s = atomicAdd(sync, 1);
+    __syncthreads();
+    int64_t item = item_s;
+    __syncthreads();
+    int q = 0;
+    bool found = false, is_max = false;
+    int panel = 0;
+    for (q = 0; q < npanels + lag && !found; ++q) {
+      const int64_t ct0 = static_cast<int64_t>(q) * panel_tiles;
+      if (q < npanels) {
+        const int64_t nmax = min(static_cast<int64_t>(panel_tiles), col_tiles - ct0) * mt;
+        if (item < nmax) { found = true, is_max = true, panel = q; break; }
+        item -= nmax;
+      }
+      if (q >= lag) {
+        const int pq = q - lag;
+        const int64_t nsl = min(static_cast<int64_t>(panel_tiles), col_tiles - static_cast<int64_t>(pq) * panel_tiles) * st;
+        if (item < nsl) { found = true, is_max = false, panel = pq; break; }
+        item -= nsl;
+      }
+    }
+    if (!found) return;
+    const int64_t ct0 = static_cast<int64_t>(panel) * panel_tiles;
+    if (is_max) {
+      colmax_tile(X, ld, len, cols, max_rows_per_tile, ct0 + item / mt, item % mt, colmax, red);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();  // the atomicMax results before the completion count
+        atomicAdd(sync + 1 + panel, 1);
+      }
+    } else {
+      if (threadIdx.x == 0) {
+        const int want = static_cast<int>(min(static_cast<int64_t>(panel_tiles), col_tiles - ct0) * mt);
+        while (atomicAdd(sync + 1 + panel, 0) < want) __nanosleep(256);
+        __threadfence();
+      }
+      __syncthreads();
+      slice_cols_tile<true>(X, ld, len, cols, lds, k, beta, colmax, S, plane, shift, flags, lsum, lsum_plane,
+                            lsum_lstride, tiles_per_cta, ct0 + item / st, item % st, lsum_s);
+      __syncthreads();
+    }
   }
 }
 

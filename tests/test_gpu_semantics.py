@@ -184,3 +184,100 @@ def test_groupwise_simple_bitmask(oz, checker):
     cfg.accumulation = oz.Accumulation.GroupwiseSimple
     want = checker.gemm(1.0, A, B, 0.0, C, k=k, method="ozIMMU_EF")   # r = 128 >= k: same chunks
     assert_bitwise(oz.ozaki_gemm(1.0, dev(A), dev(B), 0.0, dev(C), cfg).cpu().numpy(), want)
+
+
+def _host_call(oz, ta, tb, m, n, p, alpha, A, B, beta, C, k, **opt_kw):
+    """ozmm_dgemm_host straight through the C ABI on the caller's own buffers
+    (lda / ldb / ldc from the arrays' row strides)."""
+    h = oz.default_handle(0)
+    h.set_stream(None)
+    opt = oz.Options()
+    for key, v in opt_kw.items():
+        setattr(opt, key, v)
+    return oz.lib.ozmm_dgemm_host(h.h, b"T" if ta else b"N", b"T" if tb else b"N", m, n, p, alpha,
+                                  A.ctypes.data, A.strides[0] // 8, B.ctypes.data,
+                                  B.strides[0] // 8, beta, C.ctypes.data, C.strides[0] // 8, k,
+                                  ctypes.byref(opt), None, None)
+
+
+def _pinned_like(x):
+    t = torch.empty(x.shape, dtype=torch.float64).pin_memory()
+    a = t.numpy()
+    a[...] = x
+    return a, t
+
+
+@pytest.mark.parametrize("staging", [0, 1, 2])
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("case", [
+    # (transa, transb, m, n, p, alpha, beta, pad)
+    (False, False, 700, 1100, 530, 1.0, 0.0, 0),
+    (True, False, 512, 900, 384, 1.5, 0.5, 3),
+    (False, True, 333, 640, 257, -2.0, 0.0, 5),
+])
+def test_host_entry_staging_bit_exact(oz, checker, staging, pinned, case):
+    """Pageable caller buffers go through the pinned slot rings (host_stage.hpp);
+    pinned ones are copied directly; the driver-copy mode stays available.
+    Every combination must give the reference's bits, with strided leading
+    dimensions, transposes, beta != 0 (C read) and beta = 0 (C write-only)."""
+    ta, tb, m, n, p, alpha, beta, pad = case
+    k = 8
+    A0, B0, C0 = inputs(oz, m, n, p, 61, phi=1.0)
+    # non-finite C entries: beta = 0 still forms fl(beta*c) (scheme.cpp:287)
+    C0[3, 5], C0[m - 1, p - 2], C0[m // 2, 0] = np.inf, np.nan, -np.inf
+    want = checker.gemm(alpha, A0, B0, beta, C0, k=k)
+    sa = np.ascontiguousarray(A0.T) if ta else A0
+    sb = np.ascontiguousarray(B0.T) if tb else B0
+
+    def padded(x):  # leading dimension cols + pad, pad columns poisoned
+        y = np.full((x.shape[0], x.shape[1] + pad), np.nan)
+        y[:, :x.shape[1]] = x
+        return y
+
+    keep = []
+    bufs = []
+    for x in (padded(sa), padded(sb), padded(C0)):
+        if pinned:
+            a, t = _pinned_like(x)
+            keep.append(t)
+            bufs.append(a)
+        else:
+            bufs.append(x.copy())
+    A, B, C = bufs
+    rc = _host_call(oz, ta, tb, m, n, p, alpha, A[:, :sa.shape[1]], B[:, :sb.shape[1]], beta,
+                    C[:, :p], k, host_staging=staging, host_panels=3, sync_check=1)
+    assert rc == oz.OZMM_OK, oz.lib.ozmm_last_error(oz.default_handle(0).h)
+    assert_bitwise(C[:, :p], want, f"staging={staging} pinned={pinned}")
+    if pad:
+        assert np.isnan(C[:, p:]).all(), "padding columns of C were written"
+
+
+@pytest.mark.parametrize("staging", [0, 2])
+def test_host_entry_staged_range_error_leaves_c(oz, staging):
+    """Range error with staged (pageable) buffers: OZMM_ERR_RANGE, C untouched,
+    then a clean call on the same handle."""
+    m, n, p, k = 600, 800, 300, 8
+    A, B, C = inputs(oz, m, n, p, 71)
+    bad = A.copy()
+    bad[m - 5, 17] = 2.0 ** 950
+    for beta in (0.0, 0.5):
+        c = C.copy()
+        rc = _host_call(oz, False, False, m, n, p, 1.0, bad, B, beta, c, k, host_staging=staging,
+                        host_panels=4)
+        assert rc == oz.OZMM_ERR_RANGE
+        assert_bitwise(c, C, "C must be untouched on a range error")
+    c = C.copy()
+    assert _host_call(oz, False, False, m, n, p, 1.0, A, B, 0.0, c, k,
+                      host_staging=staging) == oz.OZMM_OK
+
+
+def test_host_entry_staging_options_checked(oz):
+    A, B, C = inputs(oz, 64, 64, 64, 81)
+    assert _host_call(oz, False, False, 64, 64, 64, 1.0, A, B, 0.0, C.copy(), 8,
+                      host_staging=3) == oz.OZMM_ERR_ARG
+    assert _host_call(oz, False, False, 64, 64, 64, 1.0, A, B, 0.0, C.copy(), 8,
+                      host_threads=-1) == oz.OZMM_ERR_ARG
+    for nt in (1, 3):
+        c = C.copy()
+        assert _host_call(oz, False, False, 64, 64, 64, 1.0, A, B, 0.0, c, 8, host_staging=2,
+                          host_threads=nt) == oz.OZMM_OK

@@ -75,7 +75,7 @@ class OracleBackend:
 
 class OffsetOracleBackend(OracleBackend):
     """Test stand-in with the CUDA backend's offset-binary contract: split()
-    emits byte = slice + o_s (o_1 = 2^beta - 1, o_s = 2^(beta-1); padding 0) and
+    emits byte = slice + o_s (o_1 = 2^beta, o_s = max(2, 2^(beta-1)); padding 0) and
     the signed line sums into lsum ([lines][k]); gemm() recovers the signed
     planes from the bytes, checks the line sums that travelled through the
     gathers against them, then accumulates like OracleBackend."""
@@ -84,7 +84,7 @@ class OffsetOracleBackend(OracleBackend):
 
     @staticmethod
     def _offsets(k, beta):
-        return np.array([(1 << beta) - 1] + [1 << (beta - 1)] * (k - 1), np.int64)
+        return np.array([1 << beta] + [max(2, 1 << (beta - 1))] * (k - 1), np.int64)
 
     def split(self, x, k, side, trans, beta, out_slices, out_shift, lsum=None):
         super().split(x, k, side, trans, beta, out_slices, out_shift)

@@ -18,6 +18,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--calls", type=int, default=12)
     ap.add_argument("--n", type=int, default=16384)
+    ap.add_argument("--pageable", action="store_true", help="plain numpy (pageable) buffers")
+    ap.add_argument("--staging", type=int, default=0, help="ozmm_options_t.host_staging")
     args = ap.parse_args()
     from paper_2409_13313_b200 import ozmm
     n = args.n
@@ -26,7 +28,12 @@ def main():
     hC = torch.zeros((n, n), dtype=torch.float64).pin_memory()
     h = ozmm.Handle(0)
     opt, cnt = ozmm.Options(), ozmm.Counts()
+    if hasattr(opt, "host_staging"):
+        opt.host_staging = args.staging
     a, b, c = hA.numpy(), hB.numpy(), hC.numpy()
+    if args.pageable:
+        import numpy as np
+        a, b, c = np.array(a), np.array(b), np.array(c)
     ts = []
     for _ in range(args.calls):
         t0 = time.perf_counter()

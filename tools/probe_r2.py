@@ -44,12 +44,19 @@ class Clock:
 
 
 def parse_opt(s):
+    """name:key=v,... -- ozaki_gemm_ex kwargs; env.NAME=v sets a (diag-build)
+    environment variable for that option's calls only."""
     name, _, rest = s.partition(":")
     kw = {}
     for item in filter(None, rest.split(",")):
         k, v = item.split("=")
-        kw[k] = int(v)
+        kw[k] = v if k.startswith("env.") else int(v)
     return name, kw
+
+
+def split_env(kw):
+    env = {k[4:]: v for k, v in kw.items() if k.startswith("env.")}
+    return env, {k: v for k, v in kw.items() if not k.startswith("env.")}
 
 
 def main():
@@ -81,7 +88,12 @@ def main():
         res = {o[0]: [] for o in opts}
         clk = {o[0]: [] for o in opts}
         for _ in range(args.rounds):
-            for oname, kw in opts:
+            for oname, kw_all in opts:
+                env, kw = split_env(kw_all)
+                for key in list(os.environ):
+                    if key.startswith("OZMM_") and key not in env:
+                        os.environ.pop(key)
+                os.environ.update(env)
                 call = lambda: oz.ozaki_gemm_ex(alpha, A, B, beta, C, cfg, transa=ta, transb=tb,  # noqa: E731
                                                 out=C, timings=False, **kw)
                 call()
