@@ -142,7 +142,8 @@ typedef struct {
                               pageable memory itself, single-threaded);
                               2 = stage every buffer (tests) */
   int host_threads;        /* ozmm_dgemm_host staging team size; 0 = auto
-                              (min(8, hardware threads)) */
+                              (the hardware threads, at most 16; each
+                              holds two 8 MB pinned slots per direction) */
 } ozmm_options_t;
 
 /* Scheme presets (config_for, scheme.cpp:137-159) plus the two other valid

@@ -8,14 +8,13 @@
 // (cudaHostRegister) costs more than the copy itself.  Instead the host entry
 // streams each panel through a ring of pinned slots:
 //
-//   H2D  slot j:  wait until slot j's previous DMA has drained (its event),
-//                 copy the block's rows into it with the worker pool (host
-//                 memcpy at DRAM speed, several threads), enqueue the DMA
-//                 slot -> device on the copy stream, record the slot's event.
-//                 The DMA of block j overlaps the host copy of block j+1.
-//   D2H  the DMAs of up to `nslots` blocks are enqueued ahead; block j is
-//                 copied out of its slot by the pool as soon as its event
-//                 fires, then the slot takes block j + nslots.
+//   H2D  each team thread takes every T-th block: it waits until its slot's
+//        previous DMA has drained (the slot's event), copies the block's rows
+//        into the slot (host memcpy at DRAM speed), enqueues the DMA slot ->
+//        device on the copy stream and records the slot's event.  With two
+//        slots per thread, a thread's DMA overlaps its next copy.
+//   D2H  each thread DMAs its next blocks into its slots ahead and copies each
+//        out as soon as its event fires.
 //
 // Pure plumbing: bytes are copied, never interpreted, so results are the
 // same as with direct copies (tests/test_gpu_semantics.py checks pinned,
@@ -83,7 +82,7 @@ inline uint64_t copy_screen(double* dst, const double* src, size_t n) {
 // reference's fl(fl(alpha d) + fl(beta c)) (scheme.cpp:287), so it is applied
 // here, reading each old entry just before it is overwritten.
 inline void copy_patch(double* c, const double* res, size_t n, double beta) {
-  for (size_t i = 0; i < n; ++i) {
+  auto one = [&](size_t i) {
     double v = res[i];
     uint64_t b;
     std::memcpy(&b, c + i, 8);
@@ -92,7 +91,27 @@ inline void copy_patch(double* c, const double* res, size_t n, double beta) {
       v = v + z;
     }
     c[i] = v;
+  };
+  size_t i = 0;
+#if defined(__SSE2__)
+  // 4 entries per step: the exponent test on the high dwords (one compare + one
+  // movemask); a group with an inf / NaN entry takes the scalar path
+  const __m128i ke = _mm_set1_epi32(0x7FF00000);
+  for (; i + 4 <= n; i += 4) {
+    const __m128i c0 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(c + i));
+    const __m128i c1 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(c + i + 2));
+    const __m128i e0 = _mm_cmpeq_epi32(_mm_and_si128(c0, ke), ke);
+    const __m128i e1 = _mm_cmpeq_epi32(_mm_and_si128(c1, ke), ke);
+    if ((_mm_movemask_epi8(_mm_or_si128(e0, e1)) & 0xF0F0) != 0) {
+      for (size_t j = i; j < i + 4; ++j) one(j);
+      continue;
+    }
+    _mm_storeu_si128(reinterpret_cast<__m128i*>(c + i), _mm_loadu_si128(reinterpret_cast<const __m128i*>(res + i)));
+    _mm_storeu_si128(reinterpret_cast<__m128i*>(c + i + 2),
+                     _mm_loadu_si128(reinterpret_cast<const __m128i*>(res + i + 2)));
   }
+#endif
+  for (; i < n; ++i) one(i);
 }
 
 // Fixed team of worker threads; run(n, fn) executes fn(0..n-1) on the team
@@ -166,16 +185,25 @@ class WorkerPool {
   std::atomic<int> next_{0}, left_{0};
 };
 
-// A ring of pinned slots for one copy direction.
+// Pinned slots for one copy direction, two per team thread.  A region is cut
+// into blocks that fit one slot, dealt round-robin to the team; each thread
+// streams ITS blocks through ITS two slots (double buffering), so threads never
+// wait for each other per block -- a shared ring with a team barrier per block
+// ran at 35-45 GB/s (profiles/r2/stage_bench.txt), the barrier and wake-up cost
+// rivalling a block's copy.  All DMAs go to one stream, enqueued from several
+// threads (the CUDA runtime serialises the calls); each slot's event guards its
+// reuse.
 class HostStager {
  public:
   ~HostStager() { release(); }
 
-  cudaError_t init(size_t slot_bytes, int nslots, WorkerPool* pool) {
+  cudaError_t init(size_t slot_bytes, int nslots_per_thread, WorkerPool* pool) {
     if (!slot_.empty()) return cudaSuccess;
     pool_ = pool;
     slot_bytes_ = slot_bytes;
-    for (int i = 0; i < nslots; ++i) {
+    per_thread_ = std::max(2, nslots_per_thread);
+    const int n = per_thread_ * pool->size();
+    for (int i = 0; i < n; ++i) {
       void* p = nullptr;
       cudaError_t e = cudaHostAlloc(&p, slot_bytes, cudaHostAllocDefault);
       if (e != cudaSuccess) {
@@ -207,25 +235,37 @@ class HostStager {
   // range error on its way through (copy_screen), bit 63 of *screen = found.
   cudaError_t h2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
                   cudaStream_t s, std::atomic<uint64_t>* screen = nullptr) {
-    return for_blocks(width, height, [&](size_t r0, size_t nr, size_t c0, size_t nc) -> cudaError_t {
-      const int j = next_;
-      next_ = (next_ + 1) % static_cast<int>(slot_.size());
-      cudaError_t e = cudaEventSynchronize(ev_[j]);  // the slot's previous DMA has drained
-      if (e != cudaSuccess) return e;
-      uint8_t* sl = slot_[j];
-      const uint8_t* sp = static_cast<const uint8_t*>(src) + r0 * spitch + c0;
-      if (screen)
-        copy_rows(sl, nc, sp, spitch, nc, nr, [&](uint8_t* d, const uint8_t* x, size_t bytes) {
-          const uint64_t a = copy_screen(reinterpret_cast<double*>(d), reinterpret_cast<const double*>(x), bytes / 8);
-          if (a >> 63) screen->fetch_or(a);
-        });
-      else
-        copy_rows(sl, nc, sp, spitch, nc, nr);
-      e = cudaMemcpy2DAsync(static_cast<uint8_t*>(dst) + r0 * dpitch + c0, dpitch, sl, nc, nc, nr,
-                            cudaMemcpyHostToDevice, s);
-      if (e != cudaSuccess) return e;
-      return cudaEventRecord(ev_[j], s);
+    const std::vector<Blk> blks = blocks(width, height);
+    const int nt = std::min<int>(pool_->size(), static_cast<int>(blks.size()));
+    std::atomic<int> err{0};
+    pool_->run(nt, [&](int t) {
+      int use = 0;
+      for (size_t b = t; b < blks.size() && err.load() == 0; b += nt) {
+        const Blk& k = blks[b];
+        const int j = t * per_thread_ + use;
+        use = (use + 1) % per_thread_;
+        cudaError_t e = cudaEventSynchronize(ev_[j]);  // the slot's previous DMA has drained
+        uint8_t* sl = slot_[j];
+        const uint8_t* sp = static_cast<const uint8_t*>(src) + k.r0 * spitch + k.c0;
+        if (e == cudaSuccess) {
+          uint64_t acc = 0;
+          for (size_t r = 0; r < k.nr; ++r) {
+            if (screen)
+              acc |= copy_screen(reinterpret_cast<double*>(sl + r * k.nc),
+                                 reinterpret_cast<const double*>(sp + r * spitch), k.nc / 8);
+            else
+              std::memcpy(sl + r * k.nc, sp + r * spitch, k.nc);
+          }
+          fence();
+          if (screen && (acc >> 63)) screen->fetch_or(acc);
+          e = cudaMemcpy2DAsync(static_cast<uint8_t*>(dst) + k.r0 * dpitch + k.c0, dpitch, sl, k.nc, k.nc, k.nr,
+                                cudaMemcpyHostToDevice, s);
+        }
+        if (e == cudaSuccess) e = cudaEventRecord(ev_[j], s);
+        if (e != cudaSuccess) err = static_cast<int>(e);
+      }
     });
+    return static_cast<cudaError_t>(err.load());
   }
 
   // dst (pageable host, dpitch) <- src (device, spitch), after the work already
@@ -234,91 +274,61 @@ class HostStager {
   // uploaded): copy_patch instead of a plain copy.
   cudaError_t d2h(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
                   cudaStream_t s, const double* patch_beta = nullptr) {
-    struct Blk {
-      size_t r0, nr, c0, nc;
-    };
-    std::vector<Blk> blks;
-    for_blocks(width, height, [&](size_t r0, size_t nr, size_t c0, size_t nc) -> cudaError_t {
-      blks.push_back({r0, nr, c0, nc});
-      return cudaSuccess;
-    });
-    const int ns = static_cast<int>(slot_.size());
-    auto issue = [&](size_t b) -> cudaError_t {
-      const Blk& k = blks[b];
-      const int j = static_cast<int>(b % ns);
-      cudaError_t e = cudaMemcpy2DAsync(slot_[j], k.nc, static_cast<const uint8_t*>(src) + k.r0 * spitch + k.c0,
-                                        spitch, k.nc, k.nr, cudaMemcpyDeviceToHost, s);
-      if (e != cudaSuccess) return e;
-      return cudaEventRecord(ev_[j], s);
-    };
-    for (size_t b = 0; b < blks.size() && b < static_cast<size_t>(ns); ++b)
-      if (cudaError_t e = issue(b)) return e;
-    for (size_t b = 0; b < blks.size(); ++b) {
-      const int j = static_cast<int>(b % ns);
-      if (cudaError_t e = cudaEventSynchronize(ev_[j])) return e;
-      const Blk& k = blks[b];
-      uint8_t* d = static_cast<uint8_t*>(dst) + k.r0 * dpitch + k.c0;
-      if (patch_beta) {
-        const double pb = *patch_beta;
-        copy_rows(d, dpitch, slot_[j], k.nc, k.nc, k.nr, [pb](uint8_t* o, const uint8_t* x, size_t bytes) {
-          copy_patch(reinterpret_cast<double*>(o), reinterpret_cast<const double*>(x), bytes / 8, pb);
-        });
-      } else {
-        copy_rows(d, dpitch, slot_[j], k.nc, k.nc, k.nr);
+    const std::vector<Blk> blks = blocks(width, height);
+    const int nt = std::min<int>(pool_->size(), static_cast<int>(blks.size()));
+    std::atomic<int> err{0};
+    pool_->run(nt, [&](int t) {
+      // this thread's blocks b = t, t + nt, ...: DMA up to per_thread_ of them
+      // ahead into its own slots, copy each out as its event fires
+      std::vector<size_t> mine;
+      for (size_t b = t; b < blks.size(); b += nt) mine.push_back(b);
+      auto issue = [&](size_t i) -> cudaError_t {
+        const Blk& k = blks[mine[i]];
+        const int j = t * per_thread_ + static_cast<int>(i % per_thread_);
+        cudaError_t e = cudaMemcpy2DAsync(slot_[j], k.nc, static_cast<const uint8_t*>(src) + k.r0 * spitch + k.c0,
+                                          spitch, k.nc, k.nr, cudaMemcpyDeviceToHost, s);
+        return e == cudaSuccess ? cudaEventRecord(ev_[j], s) : e;
+      };
+      cudaError_t e = cudaSuccess;
+      for (size_t i = 0; i < mine.size() && i < static_cast<size_t>(per_thread_) && e == cudaSuccess; ++i) e = issue(i);
+      for (size_t i = 0; i < mine.size() && e == cudaSuccess; ++i) {
+        const int j = t * per_thread_ + static_cast<int>(i % per_thread_);
+        e = cudaEventSynchronize(ev_[j]);
+        if (e != cudaSuccess) break;
+        const Blk& k = blks[mine[i]];
+        uint8_t* d = static_cast<uint8_t*>(dst) + k.r0 * dpitch + k.c0;
+        for (size_t r = 0; r < k.nr; ++r) {
+          if (patch_beta)
+            copy_patch(reinterpret_cast<double*>(d + r * dpitch),
+                       reinterpret_cast<const double*>(slot_[j] + r * k.nc), k.nc / 8, *patch_beta);
+          else
+            std::memcpy(d + r * dpitch, slot_[j] + r * k.nc, k.nc);
+        }
+        if (i + per_thread_ < mine.size()) e = issue(i + per_thread_);
       }
-      if (b + ns < blks.size())
-        if (cudaError_t e = issue(b + ns)) return e;
-    }
-    next_ = 0;
-    return cudaSuccess;
+      if (e != cudaSuccess) err = static_cast<int>(e);
+    });
+    return static_cast<cudaError_t>(err.load());
   }
 
  private:
+  struct Blk {
+    size_t r0, nr, c0, nc;
+  };
   // Cuts a height x width-byte region into blocks that fit one slot: whole rows
-  // when a row fits, else one row in slot-sized pieces.
-  template <class F>
-  cudaError_t for_blocks(size_t width, size_t height, F&& f) {
-    if (width == 0 || height == 0) return cudaSuccess;
+  // when a row fits, else one row in slot-sized pieces (multiples of 64 bytes).
+  std::vector<Blk> blocks(size_t width, size_t height) const {
+    std::vector<Blk> out;
+    if (width == 0 || height == 0) return out;
     if (width <= slot_bytes_) {
       const size_t rows = std::max<size_t>(1, slot_bytes_ / width);
-      for (size_t r0 = 0; r0 < height; r0 += rows)
-        if (cudaError_t e = f(r0, std::min(rows, height - r0), size_t(0), width)) return e;
+      for (size_t r0 = 0; r0 < height; r0 += rows) out.push_back({r0, std::min(rows, height - r0), 0, width});
     } else {
+      const size_t piece = slot_bytes_ & ~size_t(63);
       for (size_t r0 = 0; r0 < height; ++r0)
-        for (size_t c0 = 0; c0 < width; c0 += slot_bytes_)
-          if (cudaError_t e = f(r0, size_t(1), c0, std::min(slot_bytes_, width - c0))) return e;
+        for (size_t c0 = 0; c0 < width; c0 += piece) out.push_back({r0, 1, c0, std::min(piece, width - c0)});
     }
-    return cudaSuccess;
-  }
-  // rows x width bytes, split over the pool in pieces of >= 1 MB; `op(dst, src,
-  // bytes)` copies one contiguous run (memcpy by default)
-  template <class Op>
-  void copy_rows(uint8_t* dst, size_t dpitch, const uint8_t* src, size_t spitch, size_t width, size_t rows,
-                 Op op) {
-    const size_t total = width * rows;
-    const int parts = static_cast<int>(std::max<size_t>(
-        1, std::min<size_t>(static_cast<size_t>(2 * pool_->size()), total >> 20)));
-    if (rows >= static_cast<size_t>(parts)) {
-      pool_->run(parts, [&](int t) {
-        const size_t i0 = rows * t / parts, i1 = rows * (t + 1) / parts;
-        if (dpitch == width && spitch == width) {
-          op(dst + i0 * width, src + i0 * width, (i1 - i0) * width);
-        } else {
-          for (size_t i = i0; i < i1; ++i) op(dst + i * dpitch, src + i * spitch, width);
-        }
-        fence();
-      });
-    } else {  // few wide rows: split each row's bytes (8-byte aligned pieces)
-      pool_->run(parts, [&](int t) {
-        const size_t b0 = (width * t / parts) & ~size_t(63), b1 = t + 1 == parts ? width : (width * (t + 1) / parts) & ~size_t(63);
-        for (size_t i = 0; i < rows; ++i) op(dst + i * dpitch + b0, src + i * spitch + b0, b1 - b0);
-        fence();
-      });
-    }
-  }
-  void copy_rows(uint8_t* dst, size_t dpitch, const uint8_t* src, size_t spitch, size_t width, size_t rows) {
-    copy_rows(dst, dpitch, src, spitch, width, rows,
-              [](uint8_t* d, const uint8_t* x, size_t bytes) { std::memcpy(d, x, bytes); });
+    return out;
   }
   // streaming stores are weakly ordered: drain them before the DMA may read the slot
   static void fence() {
@@ -329,9 +339,9 @@ class HostStager {
 
   WorkerPool* pool_ = nullptr;
   size_t slot_bytes_ = 0;
+  int per_thread_ = 2;
   std::vector<uint8_t*> slot_;
   std::vector<cudaEvent_t> ev_;
-  int next_ = 0;
 };
 
 // true when p is ordinary (pageable) host memory; pinned / registered / managed

@@ -114,8 +114,6 @@ struct Handle {
   size_t nu_n = 0;
   unsigned long long* colmax = nullptr;
   size_t colmax_n = 0;
-  int* psync = nullptr;  // one-pass column split: work counter + per-panel counters
-  size_t psync_n = 0;
   int* flags = nullptr;  // [kNumFlags]: see fold_flags_kernel
   double* units_a = nullptr;  // per-slice units (RN per slice) [k][m] / [k][p]
   size_t units_a_n = 0;
@@ -244,45 +242,6 @@ int launch_colmax(Handle* h, int64_t lines, int64_t n, const double* X, int64_t 
   return OZMM_OK;
 }
 
-// One-pass column split (slice_cols_panel_kernel: op(B) read from HBM once, the
-// slicing pass re-reads each column panel from L2).  Panels of ~32 MB; the
-// maxima of panel q + 1 are taken while panel q is sliced.
-int launch_cols_onepass(Handle* h, int64_t lines, int64_t n, const double* X, int64_t ldx, int k, int beta,
-                        int8_t* S, int64_t lds, int64_t plane, double* shift, int* lsum, int64_t lsum_plane,
-                        int64_t lsum_lstride) {
-  int64_t panel_mb = 32;
-  if (const char* e = OZMM_ENV("OZMM_PANEL_MB")) panel_mb = std::max(1, std::atoi(e));
-  const int64_t col_tiles = (lines + 31) / 32;
-  const int panel_tiles = static_cast<int>(
-      std::min<int64_t>(col_tiles, std::max<int64_t>(1, (panel_mb << 20) / (32 * 8 * std::max<int64_t>(1, n)))));
-  const int npanels = static_cast<int>((col_tiles + panel_tiles - 1) / panel_tiles);
-  if (int rc = ensure(h, &h->colmax, &h->colmax_n, static_cast<size_t>(lines))) return rc;
-  if (int rc = ensure(h, &h->psync, &h->psync_n, static_cast<size_t>(npanels) + 1)) return rc;
-  CUDA_TRY(h, cudaMemsetAsync(h->colmax, 0, sizeof(unsigned long long) * lines, h->stream));
-  CUDA_TRY(h, cudaMemsetAsync(h->psync, 0, sizeof(int) * (npanels + 1), h->stream));
-  static int per_sm = 0;
-  if (per_sm == 0) {
-    CUDA_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ozb::slice_cols_panel_kernel, 256, 0));
-    per_sm = std::max(1, per_sm);
-  }
-  const int tpc = lsum ? 8 : 1;
-  int lag = 1;
-  if (const char* e = OZMM_ENV("OZMM_PANEL_LAG")) lag = std::max(1, std::atoi(e));
-  ozb::slice_cols_panel_kernel<<<h->num_sms * per_sm, 256, 0, h->stream>>>(
-      X, ldx, n, lines, lds, k, beta, h->colmax, S, plane, shift, h->flags, lsum, lsum_plane, lsum_lstride, tpc,
-      h->psync, panel_tiles, lag, 512);
-  CUDA_TRY(h, cudaGetLastError());
-  return OZMM_OK;
-}
-
-// Column split path: the two-pass colmax_kernel + slice_cols_kernel (default:
-// 1.16 ms at C3 against 2.1 ms for the panel walk, tools/cols_probe.py) or the
-// one-pass panel walk (OZMM_COLS_TWO_PASS=0, diag builds).
-bool cols_two_pass() {
-  const char* e = OZMM_ENV("OZMM_COLS_TWO_PASS");
-  return e == nullptr || std::atoi(e) != 0;
-}
-
 // colmax_ready: column mode only, h->colmax already holds this X's maxima.
 int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const double* X, int64_t ldx,
                  int k, int beta, int8_t* S, int64_t lds, int64_t plane, double* shift,
@@ -339,10 +298,6 @@ int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const doubl
                                                                        beta, S, plane, shift,
                                                                        h->flags, lsum, lsum_plane, lsum_lstride);
     }
-  } else if (!colmax_ready && !cols_two_pass()) {
-    if (int rc = launch_cols_onepass(h, lines, n, X, ldx, k, beta, S, lds, plane, shift, lsum, lsum_plane,
-                                     lsum_lstride))
-      return rc;
   } else {
     if (!colmax_ready)
       if (int rc = launch_colmax(h, lines, n, X, ldx)) return rc;
@@ -1005,7 +960,6 @@ int ozmm_destroy(ozmm_handle_t handle) {
   cudaFree(h->mu);
   cudaFree(h->nu);
   cudaFree(h->colmax);
-  cudaFree(h->psync);
   cudaFree(h->flags);
   cudaFree(h->units_a);
   cudaFree(h->units_b);
@@ -1450,12 +1404,10 @@ int ozmm_dgemm_ex(ozmm_handle_t handle, char transa, char transb, int64_t m, int
     CUDA_TRY(h, cudaEventRecord(h->ev_fork, user));
     CUDA_TRY(h, cudaStreamWaitEvent(h->s_aux, h->ev_fork, 0));
     h->stream = h->s_aux;
-    // one-pass column split: no separate maxima pass
-    const bool one_pass = overlap_bsplit && !cols_two_pass();
-    int rc = one_pass ? OZMM_OK : launch_colmax(h, p, n, B, ldb);
+    int rc = launch_colmax(h, p, n, B, ldb);
     if (!rc && overlap_bsplit)  // split B (Right, columns) -- scheme.cpp:251
       rc = launch_split(h, false, p, n, B, ldb, k, beta_bits, h->slices_b, lds, p * lds, out_b,
-                        h->lsb, p, 1, !one_pass);
+                        h->lsb, p, 1, true);
     h->stream = user;
     if (rc) return rc;
     CUDA_TRY(h, cudaEventRecord(h->ev_join, h->s_aux));
@@ -1640,7 +1592,6 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   if (int rc = ensure(h, &h->nu, &h->nu_n, static_cast<size_t>(p))) return rc;
   // column-line splits reuse h->colmax: size it once so no launch reallocates it
   if (int rc = ensure(h, &h->colmax, &h->colmax_n, static_cast<size_t>(std::max(pa, pb)))) return rc;
-  if (int rc = ensure(h, &h->psync, &h->psync_n, static_cast<size_t>((std::max(pa, pb) + 31) / 32 + 1))) return rc;
   if (!h->s_in) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
   if (!h->s_out) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
   if (!h->s_split) {
@@ -1662,12 +1613,20 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   auto staged = [&](const void* ptr) { return hs_mode == 2 || (hs_mode == 0 && ozb::host_pageable(ptr)); };
   const bool pg_a = staged(A), pg_b = staged(B), pg_c = staged(C);
   if (pg_a || pg_b || pg_c) {
-    int nt = opt && opt->host_threads ? opt->host_threads
-                                      : static_cast<int>(std::min(8u, std::max(1u, std::thread::hardware_concurrency())));
+    // default team: every hardware thread, at most 16 (16-core box, C3 call: 8 threads
+    // 157-162 ms, 12 155-159 ms, 16 147-150 ms; profiles/r2/stage_sweep3.txt)
+    int nt = opt && opt->host_threads
+                 ? opt->host_threads
+                 : static_cast<int>(std::min(16u, std::max(1u, std::thread::hardware_concurrency())));
     if (const char* e = OZMM_ENV("OZMM_STAGE_THREADS")) nt = std::max(1, std::atoi(e));
-    if (!h->pool || h->pool->size() != nt) h->pool.reset(new ozb::WorkerPool(nt));
-    size_t slot = size_t(32) << 20;
-    int nslots = 4;
+    if (!h->pool || h->pool->size() != nt) {
+      h->stage_in.release();  // slots are per team thread
+      h->stage_out.release();
+      h->pool.reset(new ozb::WorkerPool(nt));
+    }
+    // two 8 MB slots per team thread and direction (16 threads: 512 MB pinned in all)
+    size_t slot = size_t(8) << 20;
+    int nslots = 2;
     if (const char* e = OZMM_ENV("OZMM_STAGE_SLOT_MB")) slot = size_t(std::max(1, std::atoi(e))) << 20;
     if (const char* e = OZMM_ENV("OZMM_STAGE_SLOTS")) nslots = std::max(2, std::atoi(e));
     CUDA_TRY(h, h->stage_in.init(slot, nslots, h->pool.get()));

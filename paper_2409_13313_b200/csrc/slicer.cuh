@@ -335,9 +335,7 @@ __global__ void __launch_bounds__(256) colmax_kernel(const double* __restrict__ 
 // chunks form one contiguous 128-byte line of the output plane.
 //
 // slice_cols_tile: the work of one CTA (tile bx of 32 columns, tile by of
-// tiles_per_cta x 128 rows); `kCoherent` reads the maxima with ld.global.cg
-// (they were written in the same launch, see slice_cols_panel_kernel).
-template <bool kCoherent>
+// tiles_per_cta x 128 rows).
 __device__ __forceinline__ void slice_cols_tile(const double* __restrict__ X, int64_t ld, int64_t len,
                                                 int64_t cols, int64_t lds, int k, int beta,
                                                 const unsigned long long* colmax, int8_t* __restrict__ S,
@@ -346,9 +344,7 @@ __device__ __forceinline__ void slice_cols_tile(const double* __restrict__ X, in
                                                 int tiles_per_cta, int64_t bx, int64_t by, int (*lsum_s)[32]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t col = bx * 32 + warp * 4 + (lane & 3);
-  auto cmax = [&](int64_t c) {
-    return __longlong_as_double(static_cast<long long>(kCoherent ? __ldcg(colmax + c) : colmax[c]));
-  };
+  auto cmax = [&](int64_t c) { return __longlong_as_double(static_cast<long long>(colmax[c])); };
   if (lsum == nullptr) {  // signed planes: one 128-row tile per CTA
     const int64_t base = by * 128 + 16 * (lane >> 2);
     if (col >= cols || base >= lds) return;
@@ -404,109 +400,8 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(const double* __restric
                                                          int* __restrict__ lsum, int64_t lsum_plane,
                                                          int64_t lsum_lstride, int tiles_per_cta) {
   __shared__ int lsum_s[kMaxSlices][32];
-  slice_cols_tile<false>(X, ld, len, cols, lds, k, beta, colmax, S, plane, shift, flags, lsum, lsum_plane,
+  slice_cols_tile(X, ld, len, cols, lds, k, beta, colmax, S, plane, shift, flags, lsum, lsum_plane,
                          lsum_lstride, tiles_per_cta, blockIdx.x, blockIdx.y, lsum_s);
-}
-
-// Column maxima of one 32-column x rows_per_tile tile (block 32 x 8 threads),
-// folded into colmax with one atomicMax per column.
-__device__ __forceinline__ void colmax_tile(const double* __restrict__ X, int64_t ld, int64_t len, int64_t cols,
-                                            int64_t rows_per_tile, int64_t bx, int64_t by,
-                                            unsigned long long* colmax, double (*red)[33]) {
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int64_t col = bx * 32 + tx;
-  const int64_t r0 = by * rows_per_tile;
-  const int64_t r1 = min(len, r0 + rows_per_tile);
-  double m = 0.0;
-  if (col < cols) {
-    int64_t r = r0 + ty;
-    for (; r + 56 < r1; r += 64) {  // 8 independent loads in flight per thread
-      double v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldg(X + (r + 8 * u) * ld + col);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) m = fmax(m, fabs(v[u]));
-    }
-    for (; r < r1; r += 8) m = fmax(m, fabs(__ldg(X + r * ld + col)));
-  }
-  red[ty][tx] = m;
-  __syncthreads();
-  if (ty == 0) {
-#pragma unroll
-    for (int q = 1; q < 8; ++q) m = fmax(m, red[q][tx]);
-    if (col < cols && m != 0.0)
-      atomicMax(colmax + col, static_cast<unsigned long long>(__double_as_longlong(m)));
-  }
-}
-
-// One-pass column split (K1 for op(B) columns, HBM reads op(B) ONCE): a
-// persistent grid walks a work list over column panels of `panel_tiles` x 32
-// columns -- the maxima tiles of panel q + lag come before the slicing tiles of
-// panel q -- so a panel is sliced while the maxima pass has just pulled it into
-// L2 (panel_tiles x 32 columns x len doubles, sized by the host to stay
-// L2-resident for `lag` + 1 panels).  Work items are claimed in order with one
-// atomic counter; a slicing tile waits until its panel's maxima tiles are done
-// (per-panel completion counters, release/acquire through __threadfence and
-// L2-coherent loads).  Every item it waits for was claimed earlier by a
-// running CTA that never waits itself, so the walk cannot deadlock.
-// sync[0] = work counter, sync[1 + q] = finished maxima tiles of panel q
-// (zeroed by the host, as is colmax).
-__global__ void __launch_bounds__(256) slice_cols_panel_kernel(
-    const double* __restrict__ X, int64_t ld, int64_t len, int64_t cols, int64_t lds, int k, int beta,
-    unsigned long long* colmax, int8_t* __restrict__ S, int64_t plane, double* __restrict__ shift,
-    int* __restrict__ flags, int* __restrict__ lsum, int64_t lsum_plane, int64_t lsum_lstride,
-    int tiles_per_cta, int* sync, int panel_tiles, int lag, int64_t max_rows_per_tile) {
-  __shared__ int lsum_s[kMaxSlices][32];
-  __shared__ double red[8][33];
-  __shared__ int item_s;
-  const int64_t col_tiles = (cols + 31) / 32;
-  const int npanels = static_cast<int>((col_tiles + panel_tiles - 1) / panel_tiles);
-  const int64_t mt = (len + max_rows_per_tile - 1) / max_rows_per_tile;         // maxima tiles per column tile
-  const int64_t st = (lds + 128 * tiles_per_cta - 1) / (128 * tiles_per_cta);  // slicing tiles per column tile
-  // work list: step q = [maxima of panel q (q < npanels)] [slicing of panel q - lag (q >= lag)]
-  for (;;) {
-    if (threadIdx.x == 0) item_s = atomicAdd(sync, 1);
-    __syncthreads();
-    int64_t item = item_s;
-    __syncthreads();
-    int q = 0;
-    bool found = false, is_max = false;
-    int panel = 0;
-    for (q = 0; q < npanels + lag && !found; ++q) {
-      const int64_t ct0 = static_cast<int64_t>(q) * panel_tiles;
-      if (q < npanels) {
-        const int64_t nmax = min(static_cast<int64_t>(panel_tiles), col_tiles - ct0) * mt;
-        if (item < nmax) { found = true, is_max = true, panel = q; break; }
-        item -= nmax;
-      }
-      if (q >= lag) {
-        const int pq = q - lag;
-        const int64_t nsl = min(static_cast<int64_t>(panel_tiles), col_tiles - static_cast<int64_t>(pq) * panel_tiles) * st;
-        if (item < nsl) { found = true, is_max = false, panel = pq; break; }
-        item -= nsl;
-      }
-    }
-    if (!found) return;
-    const int64_t ct0 = static_cast<int64_t>(panel) * panel_tiles;
-    if (is_max) {
-      colmax_tile(X, ld, len, cols, max_rows_per_tile, ct0 + item / mt, item % mt, colmax, red);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence();  // the atomicMax results before the completion count
-        atomicAdd(sync + 1 + panel, 1);
-      }
-    } else {
-      if (threadIdx.x == 0) {
-        const int want = static_cast<int>(min(static_cast<int64_t>(panel_tiles), col_tiles - ct0) * mt);
-        while (atomicAdd(sync + 1 + panel, 0) < want) __nanosleep(256);
-        __threadfence();
-      }
-      __syncthreads();
-      slice_cols_tile<true>(X, ld, len, cols, lds, k, beta, colmax, S, plane, shift, flags, lsum, lsum_plane,
-                            lsum_lstride, tiles_per_cta, ct0 + item / st, item % st, lsum_s);
-      __syncthreads();
-    }
-  }
 }
 
 }  // namespace ozb

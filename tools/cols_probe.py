@@ -19,9 +19,7 @@ def main():
     ap.add_argument("--p", type=int, default=16384)
     ap.add_argument("--k", type=int, default=8)
     ap.add_argument("--reps", type=int, default=10)
-    ap.add_argument("--variants", default="two:OZMM_COLS_TWO_PASS=1,one32:OZMM_COLS_TWO_PASS=0+OZMM_PANEL_MB=32,"
-                    "one64:OZMM_COLS_TWO_PASS=0+OZMM_PANEL_MB=64,"
-                    "lag2:OZMM_COLS_TWO_PASS=0+OZMM_PANEL_LAG=2")
+    ap.add_argument("--variants", default="default:OZMM_NONE=0")
     a = ap.parse_args()
     from paper_2409_13313_b200 import ozmm
     n, p, k = a.n, a.p, a.k
