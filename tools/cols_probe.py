@@ -20,6 +20,8 @@ def main():
     ap.add_argument("--k", type=int, default=8)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--variants", default="default:OZMM_NONE=0")
+    ap.add_argument("--row-variants", default="default:OZMM_NONE=0",
+                    help="env settings for the row split timing, e.g. cta256:OZMM_ROW_CTA=256")
     a = ap.parse_args()
     from paper_2409_13313_b200 import ozmm
     n, p, k = a.n, a.p, a.k
@@ -68,24 +70,31 @@ def main():
               f"{gbs:.0f} GB/s algorithmic{same}", flush=True)
     for key in ("OZMM_COLS_TWO_PASS", "OZMM_PANEL_MB", "OZMM_PANEL_LAG"):
         os.environ.pop(key, None)
-    # row split of A (same shape) for reference
+    # row split of A (same shape), per row variant
     if p < n:
         return
-    S = torch.zeros((k, n, lds), dtype=torch.int8, device="cuda")
-    sh = torch.zeros(n, dtype=torch.float64, device="cuda")
-    ls = torch.zeros((k, n), dtype=torch.int32, device="cuda")
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ts = []
-    for _ in range(a.reps):
-        e0.record(st)
-        ls.zero_()
-        h.check(ozmm.lib.ozmm_split_offset(h.h, b"L", b"N", min(n, p), n, B.data_ptr(), p, k, 0,
-                                           S.data_ptr(), lds, sh.data_ptr(), ls.data_ptr(), n, 1))
-        e1.record(st)
-        torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1))
-    t = sorted(ts)[len(ts) // 2]
-    print(f"row split (A): {t:.3f} ms {(8.0 * n * p + k * n * lds) / (t * 1e-3) / 1e9:.0f} GB/s")
+    for spec in a.row_variants.split(","):
+        v, kv = spec.split(":")
+        for assign in kv.split("+"):
+            key, val = assign.split("=")
+            os.environ[key] = val
+        S = torch.zeros((k, n, lds), dtype=torch.int8, device="cuda")
+        sh = torch.zeros(n, dtype=torch.float64, device="cuda")
+        ls = torch.zeros((k, n), dtype=torch.int32, device="cuda")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ts = []
+        for _ in range(a.reps):
+            e0.record(st)
+            ls.zero_()
+            h.check(ozmm.lib.ozmm_split_offset(h.h, b"L", b"N", min(n, p), n, B.data_ptr(), p, k, 0,
+                                               S.data_ptr(), lds, sh.data_ptr(), ls.data_ptr(), n, 1))
+            e1.record(st)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        t = sorted(ts)[len(ts) // 2]
+        print(f"row split (A) {v}: {t:.3f} ms {(8.0 * n * p + k * n * lds) / (t * 1e-3) / 1e9:.0f} GB/s")
+        for assign in kv.split("+"):
+            os.environ.pop(assign.split("=")[0], None)
 
 
 if __name__ == "__main__":
