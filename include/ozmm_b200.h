@@ -135,6 +135,13 @@ typedef struct {
                               of the CTA-pair kernel (clamped to what fits, >= 2) */
   int host_panels;         /* tuning, same results (ozmm_dgemm_host): 0 = auto (16)
                               row panels of op(A) / column panels of op(B) */
+  int col_split;           /* tuning, same results: column splits of op(B) (op(A)
+                              when transa).  0 = auto: the one-pass kernel
+                              (slice_cols_onepass_kernel, op(B) read from HBM once)
+                              in ozmm_dgemm_host, whose panel splits hide under
+                              PCIe; the faster two-pass colmax + slice_cols path
+                              in ozmm_dgemm[_ex].  1 = two-pass, 2 = one-pass
+                              (columns up to 24576 long; longer ones two-pass) */
   int host_staging;        /* ozmm_dgemm_host, same results: 0 = auto -- pageable
                               (unregistered) A / B / C go through rings of pinned
                               slots filled by a team of host threads, pinned ones
@@ -143,7 +150,8 @@ typedef struct {
                               2 = stage every buffer (tests) */
   int host_threads;        /* ozmm_dgemm_host staging team size; 0 = auto
                               (the hardware threads, at most 16; each
-                              holds two 8 MB pinned slots per direction) */
+                              holds two pinned slots of up to 8 MB per
+                              direction, sized by the operands) */
 } ozmm_options_t;
 
 /* Scheme presets (config_for, scheme.cpp:137-159) plus the two other valid

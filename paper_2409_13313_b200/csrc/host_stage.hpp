@@ -222,6 +222,7 @@ class HostStager {
     return cudaSuccess;
   }
   bool ready() const { return !slot_.empty(); }
+  size_t slot_bytes() const { return slot_bytes_; }
   void release() {
     for (auto e : ev_) cudaEventDestroy(e);
     for (auto p : slot_) cudaFreeHost(p);

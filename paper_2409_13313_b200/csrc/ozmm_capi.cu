@@ -140,6 +140,7 @@ struct Handle {
   cudaStream_t s_aux = nullptr;                   // device entry: B's column maxima
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int* hflags = nullptr;                          // pinned copy of flags (host entry gate)
+  bool one_pass_cols = false;  // this call's column splits: one-pass kernel (ozmm_options_t.col_split)
   // host entry, pageable caller buffers: pinned slot rings + the copy team (host_stage.hpp)
   std::unique_ptr<ozb::WorkerPool> pool;
   ozb::HostStager stage_in, stage_out;
@@ -148,6 +149,14 @@ struct Handle {
   bool pair_attr_set[2] = {false, false};
   int num_sms = 148;
   size_t smem_optin = 232448;
+};
+
+// Scoped choice of the column-split kernel for one call (restored on return).
+struct ColSplitScope {
+  Handle* h;
+  bool saved;
+  ColSplitScope(Handle* hh, bool one_pass);
+  ~ColSplitScope();
 };
 
 int set_err(Handle* h, int code, const char* fmt, ...) {
@@ -181,6 +190,11 @@ int ensure(Handle* h, T** ptr, size_t* have, size_t want) {
   *have = std::max<size_t>(want, 256);
   return OZMM_OK;
 }
+
+ColSplitScope::ColSplitScope(Handle* hh, bool one_pass) : h(hh), saved(hh->one_pass_cols) {
+  hh->one_pass_cols = one_pass;
+}
+ColSplitScope::~ColSplitScope() { h->one_pass_cols = saved; }
 
 // ---- TMA descriptor encoding through the driver entry point (no -lcuda) ----
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -242,6 +256,68 @@ int launch_colmax(Handle* h, int64_t lines, int64_t n, const double* X, int64_t 
   return OZMM_OK;
 }
 
+// One-pass column split (slice_cols_onepass_kernel): columns of up to
+// 16 x 1536 rows, X 16-byte aligned with an even ld (TMA).  cols_onepass_units
+// returns the kernel's rows-per-CTA factor kU, or 0 when the shape does not
+// qualify and the two-pass path runs.
+int cols_onepass_units(const Handle* h, int64_t n, const double* X, int64_t ldx) {
+  bool on = h->one_pass_cols;
+  if (const char* e = OZMM_ENV("OZMM_COLS_TWO_PASS")) on = std::atoi(e) == 0;
+  if (!on) return 0;
+  if (reinterpret_cast<uintptr_t>(X) % 16 != 0 || ldx % 2 != 0 || ldx > (int64_t(1) << 36) / 8) return 0;
+  int kU = n <= 512 ? 1 : (n <= 16 * 1024 ? 2 : (n <= 16 * 1536 ? 3 : 0));
+  if (const char* e = OZMM_ENV("OZMM_COLS_UNITS")) kU = std::max(1, std::min(3, std::atoi(e)));
+  if (kU == 0 || (n + 512 * kU - 1) / (512 * kU) > 16) return 0;
+  return kU;
+}
+
+int launch_cols_onepass(Handle* h, int kU, int64_t lines, int64_t n, const double* X, int64_t ldx, int k,
+                        int beta, int8_t* S, int64_t lds, int64_t plane, double* shift, int* lsum,
+                        int64_t lsum_plane, int64_t lsum_lstride) {
+  const int cs = static_cast<int>((n + 512 * kU - 1) / (512 * kU));
+  EncodeFn fn = encode_fn();
+  if (!fn) return set_err(h, OZMM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(lines), static_cast<cuuint64_t>(n)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldx) * 8};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(ozb::kOPCols), static_cast<cuuint32_t>(ozb::kOPBox)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(h, OZMM_ERR_CUDA, "cuTensorMapEncodeTiled (columns) failed (%d)", r);
+  const size_t smem = size_t(512) * kU * ozb::kOPCols * 8 + 16 + (2 * 16 + 8) * ozb::kOPCols * 8 +
+                      ozb::kMaxSlices * ozb::kOPCols * 4;
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(ozb::kOPThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = h->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  auto go = [&](auto kern) -> int {
+    CUDA_TRY(h, cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CUDA_TRY(h, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    // as many clusters as fit at once (strips are dealt round-robin), at most one per strip
+    cfg.gridDim = dim3(static_cast<unsigned>(cs));
+    int nclusters = 0;
+    CUDA_TRY(h, cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg));
+    const int64_t nstrips = (lines + ozb::kOPCols - 1) / ozb::kOPCols;
+    nclusters = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nstrips, std::max(1, nclusters))));
+    cfg.gridDim = dim3(static_cast<unsigned>(nclusters * cs));
+    CUDA_TRY(h, cudaLaunchKernelEx(&cfg, kern, map, n, lines, lds, k, beta, S, plane, shift, h->flags, lsum,
+                                   lsum_plane, lsum_lstride));
+    return OZMM_OK;
+  };
+  if (kU == 1) return go(ozb::slice_cols_onepass_kernel<1>);
+  if (kU == 2) return go(ozb::slice_cols_onepass_kernel<2>);
+  return go(ozb::slice_cols_onepass_kernel<3>);
+}
+
 // colmax_ready: column mode only, h->colmax already holds this X's maxima.
 int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const double* X, int64_t ldx,
                  int k, int beta, int8_t* S, int64_t lds, int64_t plane, double* shift,
@@ -299,8 +375,12 @@ int launch_split(Handle* h, bool row_mode, int64_t lines, int64_t n, const doubl
                                                                        h->flags, lsum, lsum_plane, lsum_lstride);
     }
   } else {
-    if (!colmax_ready)
+    if (!colmax_ready) {
+      if (const int kU = cols_onepass_units(h, n, X, ldx))
+        return launch_cols_onepass(h, kU, lines, n, X, ldx, k, beta, S, lds, plane, shift, lsum, lsum_plane,
+                                   lsum_lstride);
       if (int rc = launch_colmax(h, lines, n, X, ldx)) return rc;
+    }
     // offset planes: 8 row tiles per CTA (column sums leave with one atomic per
     // column, slice and CTA); signed planes: one tile per CTA
     const int tpc = lsum ? 8 : 1;
@@ -1320,6 +1400,9 @@ int ozmm_dgemm_ex(ozmm_handle_t handle, char transa, char transb, int64_t m, int
   if (k > ozb::kMaxK) return set_err(h, OZMM_ERR_UNSUPPORTED, "k > %d not supported on the GPU path", ozb::kMaxK);
   if (m < 1 || n < 1 || p < 1) return set_err(h, OZMM_ERR_ARG, "split: empty matrix");
   if (m > INT32_MAX || p > INT32_MAX) return set_err(h, OZMM_ERR_ARG, "m, p must fit int32");
+  if (opt && (opt->col_split < 0 || opt->col_split > 2)) return set_err(h, OZMM_ERR_ARG, "options: col_split must be 0..2");
+  // device entry: the two-pass column split unless asked (it is on the critical path)
+  ColSplitScope col_scope(h, opt && opt->col_split == 2);
   const int fb = opt ? opt->force_beta : 0;
   int beta_bits;
   if (fb) {
@@ -1404,10 +1487,12 @@ int ozmm_dgemm_ex(ozmm_handle_t handle, char transa, char transb, int64_t m, int
     CUDA_TRY(h, cudaEventRecord(h->ev_fork, user));
     CUDA_TRY(h, cudaStreamWaitEvent(h->s_aux, h->ev_fork, 0));
     h->stream = h->s_aux;
-    int rc = launch_colmax(h, p, n, B, ldb);
+    // one-pass column split: no separate maxima pass
+    const bool one_pass = overlap_bsplit && cols_onepass_units(h, n, B, ldb) != 0;
+    int rc = one_pass ? OZMM_OK : launch_colmax(h, p, n, B, ldb);
     if (!rc && overlap_bsplit)  // split B (Right, columns) -- scheme.cpp:251
       rc = launch_split(h, false, p, n, B, ldb, k, beta_bits, h->slices_b, lds, p * lds, out_b,
-                        h->lsb, p, 1, true);
+                        h->lsb, p, 1, !one_pass);
     h->stream = user;
     if (rc) return rc;
     CUDA_TRY(h, cudaEventRecord(h->ev_join, h->s_aux));
@@ -1552,6 +1637,10 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   const bool ta = is_trans(transa), tb = is_trans(transb);
   const int64_t acols = ta ? m : n, bcols = tb ? n : p;
   if (lda < acols || ldb < bcols || ldc < p) return set_err(h, OZMM_ERR_ARG, "leading dimension too small");
+  if (opt && (opt->col_split < 0 || opt->col_split > 2)) return set_err(h, OZMM_ERR_ARG, "options: col_split must be 0..2");
+  // host entry: the one-pass column split by default -- the panel splits run under the
+  // PCIe transfers, so the kernel's extra time is hidden and B crosses HBM once
+  ColSplitScope col_scope(h, !(opt && opt->col_split == 1));
   const int fb = opt ? opt->force_beta : 0;
   int beta_bits;
   if (fb) {
@@ -1624,13 +1713,20 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
       h->stage_out.release();
       h->pool.reset(new ozb::WorkerPool(nt));
     }
-    // two 8 MB slots per team thread and direction (16 threads: 512 MB pinned in all)
-    size_t slot = size_t(8) << 20;
+    // two slots per team thread and direction: 8 MB for large operands (16 threads:
+    // 512 MB pinned in all), smaller for small ones (a power of two >= 256 KB, about a
+    // quarter of a thread's share of the largest staged matrix); grown when a later
+    // call is larger
+    const size_t big = D * static_cast<size_t>(std::max({pg_a ? m * n : 0, pg_b ? n * p : 0, pg_c ? m * p : 0}));
+    size_t slot = size_t(256) << 10;
+    while (slot < (size_t(8) << 20) && slot * 4 * nt < big) slot <<= 1;
     int nslots = 2;
     if (const char* e = OZMM_ENV("OZMM_STAGE_SLOT_MB")) slot = size_t(std::max(1, std::atoi(e))) << 20;
     if (const char* e = OZMM_ENV("OZMM_STAGE_SLOTS")) nslots = std::max(2, std::atoi(e));
-    CUDA_TRY(h, h->stage_in.init(slot, nslots, h->pool.get()));
-    CUDA_TRY(h, h->stage_out.init(slot, nslots, h->pool.get()));
+    for (ozb::HostStager* st : {&h->stage_in, &h->stage_out}) {
+      if (st->ready() && st->slot_bytes() < slot) st->release();
+      CUDA_TRY(h, st->init(slot, nslots, h->pool.get()));
+    }
   }
 
   // Panel arrival order over PCIe: A_s then B_s per step, except that the last

@@ -38,6 +38,7 @@
 #include <cstdint>
 
 #include "fp64_exact.cuh"
+#include "ptx.cuh"
 
 namespace ozb {
 
@@ -402,6 +403,123 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(const double* __restric
   __shared__ int lsum_s[kMaxSlices][32];
   slice_cols_tile(X, ld, len, cols, lds, k, beta, colmax, S, plane, shift, flags, lsum, lsum_plane,
                          lsum_lstride, tiles_per_cta, blockIdx.x, blockIdx.y, lsum_s);
+}
+
+// One-pass column split (K1 for columns of op(B), op(B) read from HBM ONCE).
+// A thread-block cluster of up to 16 CTAs owns a strip of 8 columns over the
+// whole column length: CTA r holds rows [r R, (r+1) R) of the strip in shared
+// memory (R = 512 kU), brought in by 2-D TMA boxes of 256 rows x 8 columns
+// (64 B per row, zero-filled past the matrix).  Pass 1 over shared memory takes
+// the column maxima (lane shuffles, the 8 warps through shared memory, then the
+// cluster's CTAs through distributed shared memory: every CTA stores its 8
+// maxima into slot r of every CTA, double-buffered by strip parity, one cluster
+// barrier per strip).  Pass 2 slices each thread's kU units of 16 rows x 1
+// column straight out of shared memory with emit16.  Nothing is held in
+// registers across the cluster barrier, so several CTAs share an SM and one's
+// barrier and TMA latency hide behind another's slicing.  Columns longer than
+// 16 x 1536 rows take the two-pass path (colmax_kernel + slice_cols_kernel).
+constexpr int kOPCols = 8, kOPThreads = 256, kOPBox = 256;
+template <int kU>
+__global__ void __launch_bounds__(kOPThreads, 3) slice_cols_onepass_kernel(
+    const __grid_constant__ CUtensorMap map_x, int64_t len, int64_t cols, int64_t lds, int k, int beta,
+    int8_t* __restrict__ S, int64_t plane, double* __restrict__ shift, int* __restrict__ flags,
+    int* __restrict__ lsum, int64_t lsum_plane, int64_t lsum_lstride) {
+  constexpr int kR = 512 * kU;                            // rows per CTA
+  constexpr uint32_t kBufBytes = kR * kOPCols * 8;        // this CTA's part of a strip
+  extern __shared__ __align__(1024) uint8_t op_smem[];
+  double* buf = reinterpret_cast<double*>(op_smem);       // [kR][8]
+  uint64_t* full = reinterpret_cast<uint64_t*>(op_smem + kBufBytes);
+  double* cmax = reinterpret_cast<double*>(full + 2);     // [2][16][8]: per parity, source CTA, column
+  double* red = cmax + 2 * 16 * kOPCols;                  // [8 warps][8]
+  int* lsum_s = reinterpret_cast<int*>(red + 8 * kOPCols);  // [kMaxSlices][8]
+  const uint32_t crank = ptx::cluster_ctarank();
+  uint32_t csize;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
+  const int64_t ncl = gridDim.x / csize, cl = blockIdx.x / csize;
+  const int64_t nstrips = (cols + kOPCols - 1) / kOPCols;
+  const int64_t row0 = static_cast<int64_t>(crank) * kR;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = threadIdx.x & (kOPCols - 1);  // this thread's column in the strip
+  if (threadIdx.x == 0) {
+    ptx::tma_prefetch_desc(&map_x);
+    ptx::mbar_init(full, 1);
+    ptx::fence_barrier_init();
+  }
+  for (int i = threadIdx.x; i < kMaxSlices * kOPCols; i += kOPThreads) lsum_s[i] = 0;
+  ptx::cluster_sync();  // barrier init visible; every CTA of the cluster is running (DSMEM)
+  auto issue = [&](int64_t q) {
+    ptx::mbar_arrive_expect_tx(full, kBufBytes);
+    for (int j = 0; j < kR / kOPBox; ++j)
+      ptx::tma_load_2d(buf + j * kOPBox * kOPCols, &map_x, full, static_cast<int32_t>(q * kOPCols),
+                       static_cast<int32_t>(row0 + j * kOPBox));
+  };
+  if (threadIdx.x == 0 && cl < nstrips) issue(cl);
+  int it = 0;
+  for (int64_t q = cl; q < nstrips; q += ncl, ++it) {
+    const int par = it & 1;
+    const int64_t col = q * kOPCols + c;
+    ptx::mbar_wait(full, it & 1);
+    // pass 1: column maxima
+    double m = 0.0;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int chunk = (threadIdx.x + kOPThreads * u) >> 3;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) m = fmax(m, fabs(buf[(chunk * 16 + e) * kOPCols + c]));
+    }
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 8));
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 16));
+    if (lane < kOPCols) red[warp * kOPCols + lane] = m;
+    __syncthreads();
+    if (threadIdx.x < kOPCols) {
+      double v = 0.0;
+#pragma unroll
+      for (int r = 0; r < kOPThreads / 32; ++r) v = fmax(v, red[r * kOPCols + threadIdx.x]);
+      red[threadIdx.x] = v;  // row 0 of red: this CTA's maxima
+    }
+    __syncthreads();
+    if (threadIdx.x < kOPCols * csize) {  // this CTA's maxima into slot crank of every CTA
+      const int cc = threadIdx.x % kOPCols, dst = threadIdx.x / kOPCols;
+      const uint32_t remote = ptx::mapa_shared(&cmax[(par * 16 + crank) * kOPCols + cc], dst);
+      asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(red[cc]) : "memory");
+    }
+    ptx::cluster_sync();
+    double rm = 0.0;
+    for (uint32_t r = 0; r < csize; ++r) rm = fmax(rm, cmax[(par * 16 + r) * kOPCols + c]);
+    bool under = false, range = false;
+    const int PE = line_pe(rm, beta, &under, &range);
+    if (crank == 0 && threadIdx.x < kOPCols && col < cols) {
+      shift[col] = PE == INT32_MIN ? 0.0 : pow2(PE);
+      report_flags(flags, under, range);
+    }
+    // pass 2: slices
+#pragma unroll 1
+    for (int u = 0; u < kU; ++u) {
+      const int chunk = (threadIdx.x + kOPThreads * u) >> 3;
+      const int64_t base = row0 + chunk * 16;
+      const bool valid = col < cols && base < lds;
+      double w[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) w[e] = buf[(chunk * 16 + e) * kOPCols + c];
+      if (lsum)  // every lane takes part in the column-sum reduction (4 lanes per column)
+        emit16<4>(w, PE, beta, k, S + col * lds + base, plane, valid ? valid16(len - base) : 0, valid,
+                  lsum_s + c, kOPCols);
+      else if (valid)
+        emit16<4>(w, PE, beta, k, S + col * lds + base, plane);
+    }
+    __syncthreads();  // the strip buffer is free: fetch the next one while the sums leave
+    if (threadIdx.x == 0 && q + ncl < nstrips) issue(q + ncl);
+    if (lsum) {
+      for (int i = threadIdx.x; i < k * kOPCols; i += kOPThreads) {
+        const int64_t cg = q * kOPCols + (i % kOPCols);
+        const int v = lsum_s[i];
+        if (cg < cols && v != 0) atomicAdd(lsum + (i / kOPCols) * lsum_plane + cg * lsum_lstride, v);
+        lsum_s[i] = 0;
+      }
+      __syncthreads();
+    }
+  }
+  ptx::cluster_sync();  // no CTA leaves while a peer may still address its shared memory
 }
 
 }  // namespace ozb

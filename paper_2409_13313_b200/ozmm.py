@@ -75,8 +75,8 @@ class Options(C.Structure):
                 ("sync_check", C.c_int), ("chunk_dump", C.c_void_p), ("tile_n", C.c_int),
                 ("cta_pair", C.c_int), ("method", C.c_int), ("signed_slices", C.c_int),
                 ("c_write_only", C.c_int), ("overflow_wrap", C.c_int), ("kpair", C.c_int),
-                ("stages", C.c_int), ("host_panels", C.c_int), ("host_staging", C.c_int),
-                ("host_threads", C.c_int)]
+                ("stages", C.c_int), ("host_panels", C.c_int), ("col_split", C.c_int),
+                ("host_staging", C.c_int), ("host_threads", C.c_int)]
 
 
 _SIG = {
@@ -355,7 +355,7 @@ def _is_cuda_tensor(x) -> bool:
 def _options(cfg: SchemeConfig | None, timings: bool = False, dump=None, tile_n: int = 0,
              sync_check: bool = False, cta_pair: int = 0, signed_slices: bool = False,
              kpair: int = 0, stages: int = 0, host_panels: int = 0,
-             host_staging: int = 0) -> Options:
+             host_staging: int = 0, col_split: int = 0) -> Options:
     o = Options()
     if cfg is not None:
         o.force_beta = cfg.force_beta
@@ -364,6 +364,7 @@ def _options(cfg: SchemeConfig | None, timings: bool = False, dump=None, tile_n:
         o.overflow_wrap = int(cfg.overflow == OverflowMode.Wrapping)
     o.kpair, o.stages, o.host_panels = kpair, stages, host_panels
     o.host_staging = host_staging
+    o.col_split = col_split
     o.timings = int(timings)
     o.sync_check = int(sync_check)
     o.chunk_dump = dump.data_ptr() if dump is not None else None
@@ -413,7 +414,7 @@ def ozaki_gemm_ex(alpha: float, a, b, beta: float, c, cfg: SchemeConfig | None =
                   out=None, timings: bool = True, chunk_dump=None,
                   tile_n: int = 0, signed_slices: bool = False, sync_check: bool = True,
                   kpair: int = 0, stages: int = 0, host_panels: int = 0,
-                  cta_pair: int = 0, host_staging: int = 0) -> OzakiResult:
+                  cta_pair: int = 0, host_staging: int = 0, col_split: int = 0) -> OzakiResult:
     """Emulated DGEMM: alpha * op(A) op(B) + beta * C (scheme.cpp:274-291).
 
     Returns OzakiResult(d=new matrix, counts, timings); C is not modified
@@ -427,8 +428,8 @@ def ozaki_gemm_ex(alpha: float, a, b, beta: float, c, cfg: SchemeConfig | None =
     the reference's throw.  ``sync_check=False`` keeps the call fully
     stream-ordered (e.g. inside a CUDA graph); the range error then stays
     pending on the handle until ``Handle.sync_status()``.  ``kpair``,
-    ``stages``, ``host_panels``, ``cta_pair``: kernel tuning, same results
-    (ozmm_options_t).  ``host_staging`` (host path): 0 = pageable arrays go
+    ``stages``, ``host_panels``, ``cta_pair``, ``col_split``: kernel tuning,
+    same results (ozmm_options_t).  ``host_staging`` (host path): 0 = pageable arrays go
     through pinned slots (default), 1 = driver copies, 2 = stage everything.
     """
     cfg = cfg or config_for(Method.ozIMMU_H, 8)
@@ -455,7 +456,7 @@ def ozaki_gemm_ex(alpha: float, a, b, beta: float, c, cfg: SchemeConfig | None =
         dst = c.clone() if out is None or out.data_ptr() != c.data_ptr() else out
         opt = _options(cfg, timings, chunk_dump, tile_n, sync_check=sync_check,
                        signed_slices=signed_slices, kpair=kpair, stages=stages,
-                       cta_pair=cta_pair)
+                       cta_pair=cta_pair, col_split=col_split)
         h.check(lib.ozmm_dgemm_ex(h.h, b"T" if transa else b"N", b"T" if transb else b"N", m, n,
                                   p, alpha, a.data_ptr(), a.stride(0), b.data_ptr(),
                                   b.stride(0), beta, dst.data_ptr(), dst.stride(0), cfg.k,
@@ -481,7 +482,7 @@ def ozaki_gemm_ex(alpha: float, a, b, beta: float, c, cfg: SchemeConfig | None =
     res = out if inplace else c.copy()
     opt = _options(cfg, timings, None, tile_n, sync_check=True, signed_slices=signed_slices,
                    kpair=kpair, stages=stages, host_panels=host_panels, cta_pair=cta_pair,
-                   host_staging=host_staging)
+                   host_staging=host_staging, col_split=col_split)
     h.set_stream(None)
     h.check(lib.ozmm_dgemm_host(h.h, b"T" if transa else b"N", b"T" if transb else b"N", m, n,
                                 p, alpha, a.ctypes.data, a.shape[1], b.ctypes.data, b.shape[1],

@@ -194,3 +194,32 @@ def test_tuning_knobs_bit_exact(oz, checker, m, n, p, k, phi, kpair, stages):
     got_h = oz.ozaki_gemm(1.5, A, B, 0.5, C, oz.config_for("ozIMMU_H", k), kpair=kpair,
                           stages=stages, host_panels=3)
     assert_bitwise(got_h, want, f"host kpair={kpair} stages={stages}")
+
+
+@pytest.mark.parametrize("m,n,p,k,phi,ta,tb", [
+    (200, 400, 77, 8, 0.5, False, False),     # columns <= 512: one CTA per strip
+    (256, 1000, 130, 9, 1.0, False, False),   # one 1024-row CTA, ragged strip of 2 columns
+    (300, 4111, 261, 12, 4.0, False, False),  # a 5-CTA cluster, rows past n zero-filled
+    (130, 17000, 96, 8, 2.0, False, False),   # 1536 rows per CTA, 12-CTA cluster
+    (97, 30000, 64, 7, 0.5, False, False),    # too long for one pass: the two-pass path
+    (160, 2500, 200, 10, 1.0, True, True),    # op(A) columns (transa), op(B) rows (transb)
+])
+@pytest.mark.parametrize("col_split", [1, 2])
+def test_one_pass_column_split_bit_exact(oz, checker, m, n, p, k, phi, ta, tb, col_split):
+    """The one-pass column split (TMA-fed cluster kernel, op(B) read from HBM once)
+    against the two-pass colmax + slice_cols path: both must give the reference's
+    bits, through the device entry (offset and signed planes) and the host entry."""
+    A = oz.gen_phi_matrix(n if ta else m, m if ta else n, phi, 111)
+    B = oz.gen_phi_matrix(p if tb else n, n if tb else p, phi, 112)
+    C = oz.gen_phi_matrix(m, p, phi, 113)
+    Ar = np.ascontiguousarray(A.T) if ta else A
+    Br = np.ascontiguousarray(B.T) if tb else B
+    want = checker.gemm(1.5, Ar, Br, 0.5, C, k=k)
+    cfg = oz.config_for("ozIMMU_H", k)
+    for signed in (False, True):
+        got = oz.ozaki_gemm(1.5, dev(A), dev(B), 0.5, dev(C), cfg, transa=ta, transb=tb,
+                            col_split=col_split, signed_slices=signed).cpu().numpy()
+        assert_bitwise(got, want, f"device col_split={col_split} signed={signed}")
+    got_h = oz.ozaki_gemm(1.5, A, B, 0.5, C, cfg, transa=ta, transb=tb, col_split=col_split,
+                          host_panels=3)
+    assert_bitwise(got_h, want, f"host col_split={col_split}")

@@ -281,3 +281,23 @@ def test_host_entry_staging_options_checked(oz):
         c = C.copy()
         assert _host_call(oz, False, False, 64, 64, 64, 1.0, A, B, 0.0, c, 8, host_staging=2,
                           host_threads=nt) == oz.OZMM_OK
+
+
+def test_host_entry_staging_slots_grow_with_the_operands(oz, checker):
+    """Slots are sized by the operands and re-allocated when a later pageable call
+    on the same handle is larger: small, large, small again -- all bit-exact."""
+    h = oz.Handle(0)
+    try:
+        for (m, n, p) in [(64, 96, 80), (1536, 2048, 1280), (100, 130, 70)]:
+            A, B, C = inputs(oz, m, n, p, 101)
+            want = checker.gemm(1.0, A, B, 0.0, C, k=8)
+            c = C.copy()
+            opt = oz.Options()
+            h.set_stream(None)
+            rc = oz.lib.ozmm_dgemm_host(h.h, b"N", b"N", m, n, p, 1.0, A.ctypes.data, n,
+                                        B.ctypes.data, p, 0.0, c.ctypes.data, p, 8,
+                                        ctypes.byref(opt), None, None)
+            assert rc == oz.OZMM_OK
+            assert_bitwise(c, want, f"{m}x{n}x{p}")
+    finally:
+        h.close()

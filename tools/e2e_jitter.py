@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--n", type=int, default=16384)
     ap.add_argument("--pageable", action="store_true", help="plain numpy (pageable) buffers")
     ap.add_argument("--staging", type=int, default=0, help="ozmm_options_t.host_staging")
+    ap.add_argument("--col-split", type=int, default=0, help="ozmm_options_t.col_split")
     args = ap.parse_args()
     from paper_2409_13313_b200 import ozmm
     n = args.n
@@ -30,6 +31,8 @@ def main():
     opt, cnt = ozmm.Options(), ozmm.Counts()
     if hasattr(opt, "host_staging"):
         opt.host_staging = args.staging
+    if hasattr(opt, "col_split"):
+        opt.col_split = args.col_split
     a, b, c = hA.numpy(), hB.numpy(), hC.numpy()
     if args.pageable:
         import numpy as np
