@@ -257,7 +257,7 @@ int launch_colmax(Handle* h, int64_t lines, int64_t n, const double* X, int64_t 
 }
 
 // One-pass column split (slice_cols_onepass_kernel): columns of up to
-// 16 x 1536 rows, X 16-byte aligned with an even ld (TMA).  cols_onepass_units
+// 16 x 2048 rows, X 16-byte aligned with an even ld (TMA).  cols_onepass_units
 // returns the kernel's rows-per-CTA factor kU, or 0 when the shape does not
 // qualify and the two-pass path runs.
 int cols_onepass_units(const Handle* h, int64_t n, const double* X, int64_t ldx) {
@@ -265,8 +265,10 @@ int cols_onepass_units(const Handle* h, int64_t n, const double* X, int64_t ldx)
   if (const char* e = OZMM_ENV("OZMM_COLS_TWO_PASS")) on = std::atoi(e) == 0;
   if (!on) return 0;
   if (reinterpret_cast<uintptr_t>(X) % 16 != 0 || ldx % 2 != 0 || ldx > (int64_t(1) << 36) / 8) return 0;
-  int kU = n <= 512 ? 1 : (n <= 16 * 1024 ? 2 : (n <= 16 * 1536 ? 3 : 0));
-  if (const char* e = OZMM_ENV("OZMM_COLS_UNITS")) kU = std::max(1, std::min(3, std::atoi(e)));
+  // the fewest rows per CTA the 16-CTA limit allows: 1024 rows (kU = 2) beat 1536 and
+  // 2048 at C3 (1.53 / 1.66 / 2.16 ms) and C2 (profiles/r2/cols_onepass_v4.txt)
+  int kU = n <= 512 ? 1 : (n <= 16 * 1024 ? 2 : (n <= 16 * 1536 ? 3 : (n <= 16 * 2048 ? 4 : 0)));
+  if (const char* e = OZMM_ENV("OZMM_COLS_UNITS")) kU = std::max(1, std::min(4, std::atoi(e)));
   if (kU == 0 || (n + 512 * kU - 1) / (512 * kU) > 16) return 0;
   return kU;
 }
@@ -315,7 +317,8 @@ int launch_cols_onepass(Handle* h, int kU, int64_t lines, int64_t n, const doubl
   };
   if (kU == 1) return go(ozb::slice_cols_onepass_kernel<1>);
   if (kU == 2) return go(ozb::slice_cols_onepass_kernel<2>);
-  return go(ozb::slice_cols_onepass_kernel<3>);
+  if (kU == 3) return go(ozb::slice_cols_onepass_kernel<3>);
+  return go(ozb::slice_cols_onepass_kernel<4>);
 }
 
 // colmax_ready: column mode only, h->colmax already holds this X's maxima.

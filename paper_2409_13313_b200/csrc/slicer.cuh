@@ -80,13 +80,37 @@ __device__ __forceinline__ void emit16(double (&w)[16], int PE, int beta, int k,
                                        int8_t* dst, int64_t plane, int nvalid = 16,
                                        bool store = true, int* lsum = nullptr,
                                        int64_t lsum_plane = 0) {
-  for (int s = 1; s <= k; ++s) {
-    const uint32_t off = lsum == nullptr ? 0u : slice_offset(s, beta);  // 0: signed planes
+  // Loop invariants (the slicer is issue-bound: ncu 73 % of issue slots, with the
+  // FP64 pipe the next limit): the padding mask, both offsets and their share of
+  // the line sums, the unit exponent (stepped by -beta), the store pointer (stepped
+  // by plane) and the shared-memory address of the line sums (lsum always points
+  // into shared memory; red.shared avoids the generic atomic's warp aggregation).
+  const bool partial = lsum != nullptr && nvalid < 16;
+  uint32_t keep[4] = {~0u, ~0u, ~0u, ~0u};
+  if (partial) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+      if (e >= nvalid) keep[e >> 2] &= ~(0xFFu << (8 * (e & 3)));
+  }
+  uint32_t o1 = lsum == nullptr ? 0u : slice_offset(1, beta);  // 0: signed planes
+  uint32_t os = lsum == nullptr ? 0u : slice_offset(2, beta);
+  uint32_t nv = static_cast<uint32_t>(nvalid);
+  uint32_t part = partial ? 1u : 0u, st = store ? 1u : 0u;
+  uint32_t lead = kLaneGroup == 32 ? ((threadIdx.x & 31) == 0 ? 1u : 0u)
+                                   : ((threadIdx.x & 31) < 32 / kLaneGroup ? 1u : 0u);
+  // opaque to the optimiser: kept in registers, not re-derived inside the slice loop
+  asm volatile("" : "+r"(o1), "+r"(os), "+r"(nv), "+r"(part), "+r"(st), "+r"(lead));
+  const bool zero_line = PE == INT32_MIN;
+  uint32_t ls_addr = lsum == nullptr ? 0u : static_cast<uint32_t>(__cvta_generic_to_shared(lsum));
+  const uint32_t ls_step = static_cast<uint32_t>(lsum_plane) * 4u;
+  int ue = PE + 1 - beta;  // exponent of unit_s
+  int8_t* out = dst;
+  for (int s = 1; s <= k; ++s, ue -= beta, out += plane, ls_addr += ls_step) {
+    const uint32_t off = s == 1 ? o1 : os;
     const uint32_t off4 = off * 0x01010101u;
     uint32_t packed[4] = {off4, off4, off4, off4};  // zero line / underflowed grid: slice 0
     int qsum = 0;  // signed slice sum of this lane's elements (offset mode)
-    const int ue = PE + 1 - beta * s;  // exponent of unit_s
-    if (PE != INT32_MIN && ue >= -1074) {
+    if (!zero_line && ue >= -1074) {
       // sigma' = (1.5 * 2^52 + off) * 2^ue: exponent field ue + 1075, mantissa 0x8000000000000 + off
       const double sig = __hiloint2double(((ue + 1075) << 20) | 0x00080000, static_cast<int>(off));
       uint32_t q[16];
@@ -104,44 +128,41 @@ __device__ __forceinline__ void emit16(double (&w)[16], int PE, int beta, int k,
         packed[i] = __byte_perm(lo, hi, 0x5410);
       }
       if (lsum != nullptr) {
-        if (nvalid < 16) {  // padding bytes stay 0
+        if (part) {  // padding bytes stay 0
 #pragma unroll
-          for (int e = 0; e < 16; ++e)
-            if (e >= nvalid) packed[e >> 2] &= ~(0xFFu << (8 * (e & 3)));
+          for (int i = 0; i < 4; ++i) packed[i] &= keep[i];
         }
         uint32_t bsum = 0;
 #pragma unroll
         for (int i = 0; i < 4; ++i) bsum = __dp4a(packed[i], 0x01010101u, bsum);
-        qsum = static_cast<int>(bsum - off * static_cast<uint32_t>(nvalid));
+        qsum = static_cast<int>(bsum - off * nv);
       }
     } else {
-      if (PE != INT32_MIN) {
+      if (!zero_line) {
         // unit underflowed to 0: the reference computes x = w, int8(w/0) = 0
         // (cvttsd2si of +-inf/NaN), w -= x -> 0.
 #pragma unroll
         for (int e = 0; e < 16; ++e) w[e] = __dadd_rn(w[e], -w[e]);
       }
-      if (lsum != nullptr && nvalid < 16) {
+      if (part) {
 #pragma unroll
-        for (int e = 0; e < 16; ++e)
-          if (e >= nvalid) packed[e >> 2] &= ~(0xFFu << (8 * (e & 3)));
+        for (int i = 0; i < 4; ++i) packed[i] &= keep[i];
       }
     }
     if (lsum != nullptr) {
+      bool add;
       if constexpr (kLaneGroup == 32) {
         qsum = __reduce_add_sync(0xffffffffu, qsum);
-        if ((threadIdx.x & 31) == 0 && qsum != 0)
-          atomicAdd(lsum + static_cast<int64_t>(s - 1) * lsum_plane, qsum);
+        add = lead && qsum != 0;
       } else {
 #pragma unroll
         for (int o = 32 / kLaneGroup; o < 32; o <<= 1) qsum += __shfl_xor_sync(0xffffffffu, qsum, o);
-        if ((threadIdx.x & 31) < 32 / kLaneGroup && store && qsum != 0)
-          atomicAdd(lsum + static_cast<int64_t>(s - 1) * lsum_plane, qsum);
+        add = lead && st && qsum != 0;
       }
+      if (add) asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(ls_addr), "r"(qsum) : "memory");
     }
-    if (store)
-      *reinterpret_cast<uint4*>(dst + static_cast<int64_t>(s - 1) * plane) =
-          make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    if (st)
+      *reinterpret_cast<uint4*>(out) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
   }
 }
 
