@@ -240,6 +240,18 @@ int ozmm_split_ex(ozmm_handle_t h, char side, char trans, int64_t lines, int64_t
                   const double* X, int64_t ldx, int k, int beta, int strategy, int8_t* slices,
                   int64_t lds, double* out);
 
+/* Host-memory split with its residual: the reference's SplitMatrix as
+ * dump_split / `ozmm gemm --dump-splits` write it (split.cpp:254-270,
+ * tools/ozmm_cli.cpp:73-86).  X (host) is split by side/trans/strategy as in
+ * ozmm_split_ex on the GPU; results (host), line-major (transpose them for the
+ * reference's Right-side layout): slices [k][lines][n] int8, out = the const
+ * shift [lines] or per-slice units [k][lines], residual [lines][n] (nullable) --
+ * what is left of each element after the k slices.  Range errors return
+ * OZMM_ERR_RANGE like the reference's throw. */
+int ozmm_split_host(ozmm_handle_t h, char side, char trans, int64_t lines, int64_t n,
+                    const double* X, int64_t ldx, int k, int beta, int strategy, int8_t* slices,
+                    double* out, double* residual);
+
 /* K2+K3 over already-split operands: C <- alpha * D + beta * C with D the
  * group-wise ozIMMU_H accumulation of A slices [k][m][lds_a] / mu [m] and
  * B slices [k][p][lds_b] / nu [p] (B stored transposed: row j = column j of

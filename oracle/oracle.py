@@ -226,7 +226,7 @@ class RefLib(_Base):
     def __init__(self, path: str = REF_SO):
         super().__init__(path)
         self.lib.ozref_split_any.argtypes = [C.c_int, _dp, _i64, _i64, C.c_int, C.c_int, C.c_int,
-                                             _i8p, _dp]
+                                             _i8p, _dp, _dp]
         self.lib.ozref_total_bound.argtypes = [C.c_int, C.c_int, C.c_int, _i64, _dp, _i64, _i64,
                                                _dp, _i64, _dp]
 
@@ -239,18 +239,21 @@ class RefLib(_Base):
                                                _ptr(b, _dp), b.shape[1], _ptr(out, _dp)))
         return out
 
-    def split_any(self, a, k, strategy, side="left", force_beta=0):
-        """strategy: "rn_const" | "bitmask" | "rn_per_slice".  Returns (slices, shift or units)."""
+    def split_any(self, a, k, strategy, side="left", force_beta=0, residual=False):
+        """strategy: "rn_const" | "bitmask" | "rn_per_slice".  Returns (slices, shift or
+        units), plus the residual matrix when ``residual``."""
         code = {"rn_const": 0, "bitmask": 1, "rn_per_slice": 2}[strategy]
         a = _f64(a)
         rows, cols = a.shape
         lines = rows if side == "left" else cols
         sl = np.zeros((k, rows, cols), np.int8)
         out = np.zeros((k, lines) if code == 2 else (lines,), np.float64)
+        res = np.zeros((rows, cols), np.float64) if residual else None
         self._check(self.lib.ozref_split_any(code, _ptr(a, _dp), rows, cols, k,
                                              0 if side == "left" else 1, force_beta,
-                                             _ptr(sl, _i8p), _ptr(out, _dp)))
-        return sl, out
+                                             _ptr(sl, _i8p), _ptr(out, _dp),
+                                             _ptr(res, _dp) if residual else None))
+        return (sl, out, res) if residual else (sl, out)
 
 
 class PortLib(_Base):

@@ -172,9 +172,9 @@ int ozref_split_rn_const_shift(const double* a, std::int64_t rows, std::int64_t 
 
 // Any splitting strategy: 0 = RN const shift, 1 = bitmask, 2 = RN per slice
 // (split.cpp:223-237).  out: const shift [rows or cols] (0, 1) or per-slice
-// units [k][rows or cols] (2).
+// units [k][rows or cols] (2); residual (nullable): rows x cols.
 int ozref_split_any(int strategy, const double* a, std::int64_t rows, std::int64_t cols, int k,
-                    int side, int force_beta, std::int8_t* slices, double* out) {
+                    int side, int force_beta, std::int8_t* slices, double* out, double* residual) {
   return guard([&] {
     const MatrixF64 A = load(a, rows, cols);
     const Side sd = side ? Side::Right : Side::Left;
@@ -191,6 +191,8 @@ int ozref_split_any(int strategy, const double* a, std::int64_t rows, std::int64
     } else {
       std::memcpy(out, s.const_shift.data(), sizeof(double) * s.const_shift.size());
     }
+    // SplitMatrix::residual in the matrix's own layout (dump_split, split.cpp:269)
+    if (residual) std::memcpy(residual, s.residual.data(), sizeof(double) * rows * cols);
   });
 }
 

@@ -3,7 +3,8 @@
 // writing the reference's OZMM matrix files (proj/src/io.cpp:16-89).
 //
 //   ozmm_b200_cli gemm A.ozmm B.ozmm [C.ozmm] --out D.ozmm [--alpha a] [--beta b]
-//                 [--k 8] [--method ozIMMU_H] [--force-beta b] [--force-r r]
+//                 [--k 8] [--method ozIMMU_H] [--overflow-mode checked|wrapping]
+//                 [--force-beta b] [--force-r r] [--dump-splits PREFIX]
 //                 [--transa] [--transb] [--device d]
 //   ozmm_b200_cli counts --n N --k K --method M [--force-beta b] [--force-r r]
 //
@@ -11,8 +12,13 @@
 // errors, 1 anything else (ozmm_cli.cpp:279-304).  `gemm` prints one JSON
 // line with the reference's keys (:92-106); timings are CUDA-event phases.
 // --transa/--transb are the DGEMM-style extension: op(X) = X^T of the stored
-// matrix.  Overflow mode and --dump-splits are not offered (the GPU path
-// accumulates in wrapping INT32, which the derived r makes overflow-free).
+// matrix.  --overflow-mode as the reference (checked: an INT32 chunk overflow,
+// reachable only with --force-r / --force-beta, is an error and D is not
+// written; wrapping: sums mod 2^32).  --dump-splits writes the split of op(A)
+// (Left) and op(B) (Right) with the method's strategy as the reference's
+// dump_split does (split.cpp:254-270): PREFIX.{a,b}.slice<s>.ozmm (int8),
+// PREFIX.{a,b}.shift.ozmm (1 x lines) or .shift<s>.ozmm (per-slice units) and
+// PREFIX.{a,b}.residual.ozmm, computed on the GPU (ozmm_split_host).
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -81,22 +87,26 @@ Matrix load_f64(const std::string& path) {
   return m;
 }
 
-void save_f64(const std::string& path, const Matrix& m) {
+// element kind 0 = F64, 1 = I8 (io.hpp:17)
+void save_raw(const std::string& path, uint64_t rows, uint64_t cols, int kind, const void* data, size_t bytes) {
   std::ofstream out(path, std::ios::binary | std::ios::trunc);
   if (!out) throw FormatError(path + ": cannot open for writing");
-  unsigned char h[28] = {'O', 'Z', 'M', 'M', 1, 0};
-  put_u64(h + 12, m.rows);
-  put_u64(h + 20, m.cols);
+  unsigned char h[28] = {'O', 'Z', 'M', 'M', 1, static_cast<unsigned char>(kind)};
+  put_u64(h + 12, rows);
+  put_u64(h + 20, cols);
   out.write(reinterpret_cast<const char*>(h), sizeof h);
-  out.write(reinterpret_cast<const char*>(m.data.data()),
-            static_cast<std::streamsize>(sizeof(double) * m.data.size()));
+  out.write(static_cast<const char*>(data), static_cast<std::streamsize>(bytes));
   if (!out) throw FormatError(path + ": write failed");
+}
+
+void save_f64(const std::string& path, const Matrix& m) {
+  save_raw(path, m.rows, m.cols, 0, m.data.data(), sizeof(double) * m.data.size());
 }
 
 // ---------------------------------------------------------------- args
 struct Args {
   std::vector<std::string> pos;
-  std::string out, method = "ozIMMU_H";
+  std::string out, method = "ozIMMU_H", overflow = "checked", dump_prefix;
   double alpha = 1.0, beta = 0.0;
   int k = 8, force_beta = 0, device = 0;
   int64_t force_r = 0, n = -1;
@@ -122,6 +132,8 @@ Args parse(int argc, char** argv, int first) {
     else if (s == "--beta") a.beta = num(val());
     else if (s == "--k") a.k = static_cast<int>(num(val())), a.have_k = true;
     else if (s == "--method") a.method = val(), a.have_method = true;
+    else if (s == "--overflow-mode") a.overflow = val();
+    else if (s == "--dump-splits") a.dump_prefix = val();
     else if (s == "--force-beta") a.force_beta = static_cast<int>(num(val()));
     else if (s == "--force-r") a.force_r = static_cast<int64_t>(num(val()));
     else if (s == "--device") a.device = static_cast<int>(num(val()));
@@ -156,6 +168,49 @@ void check(int rc, ozmm_handle_t h) {
   throw std::runtime_error(msg + " (" + ozmm_status_string(rc) + ")");
 }
 
+// ---------------------------------------------------------------- dump
+// split strategy of a method (config_for, scheme.cpp:137-159): 0 RN const shift,
+// 1 bitmask, 2 RN per slice
+int method_strategy(int code) {
+  if (code == OZMM_METHOD_OZIMMU || code == OZMM_METHOD_OZIMMU_EF) return OZMM_SPLIT_BITMASK;
+  if (code == OZMM_METHOD_OZIMMU_RN) return OZMM_SPLIT_RN_PER_SLICE;
+  return OZMM_SPLIT_RN_CONST_SHIFT;
+}
+
+// dump_split (split.cpp:254-270) of op(X) split on `side`: lines x n line-major
+// results from the GPU, written in op(X)'s own layout (Right: transposed back).
+void dump_split(ozmm_handle_t h, const std::string& prefix, char side, bool trans, const Matrix& X, int64_t lines,
+                int64_t n, int k, int force_beta, int strategy) {
+  std::vector<int8_t> sl(static_cast<size_t>(k) * lines * n);
+  std::vector<double> out(static_cast<size_t>(strategy == OZMM_SPLIT_RN_PER_SLICE ? k * lines : lines));
+  std::vector<double> res(static_cast<size_t>(lines * n));
+  // op(X) lines: Left = rows of op(X), Right = columns of op(X)
+  const char tr = trans ? 'T' : 'N';
+  check(ozmm_split_host(h, side, tr, lines, n, X.data.data(), static_cast<int64_t>(X.cols), k, force_beta, strategy,
+                        sl.data(), out.data(), res.data()),
+        h);
+  const bool right = side == 'R';
+  const uint64_t R = right ? n : lines, Cc = right ? lines : n;  // op(X) shape
+  std::vector<int8_t> tile(R * Cc);
+  for (int s = 0; s < k; ++s) {
+    const int8_t* p = sl.data() + static_cast<size_t>(s) * lines * n;
+    for (int64_t i = 0; i < lines; ++i)
+      for (int64_t j = 0; j < n; ++j) tile[right ? j * lines + i : i * n + j] = p[i * n + j];
+    save_raw(prefix + ".slice" + std::to_string(s + 1) + ".ozmm", R, Cc, 1, tile.data(), tile.size());
+  }
+  if (strategy == OZMM_SPLIT_RN_PER_SLICE) {
+    for (int s = 0; s < k; ++s)
+      save_raw(prefix + ".shift" + std::to_string(s + 1) + ".ozmm", 1, lines, 0, out.data() + s * lines,
+               sizeof(double) * lines);
+  } else {
+    save_raw(prefix + ".shift.ozmm", 1, lines, 0, out.data(), sizeof(double) * lines);
+  }
+  std::vector<double> rt(R * Cc);
+  for (int64_t i = 0; i < lines; ++i)
+    for (int64_t j = 0; j < n; ++j) rt[right ? j * lines + i : i * n + j] = res[i * n + j];
+  save_raw(prefix + ".residual.ozmm", R, Cc, 0, rt.data(), sizeof(double) * rt.size());
+}
+
 // ---------------------------------------------------------------- gemm
 int run_gemm(const Args& a) {
   if (a.pos.size() < 2 || a.pos.size() > 3) throw UsageError("gemm: expected A B [C]");
@@ -180,9 +235,23 @@ int run_gemm(const Args& a) {
     throw std::runtime_error(std::string("ozmm_create: ") + ozmm_last_error(nullptr) + " (" +
                              ozmm_status_string(rc) + ")");
   }
+  if (a.overflow != "checked" && a.overflow != "wrapping") {
+    ozmm_destroy(h);
+    throw ConfigError("--overflow-mode must be 'checked' or 'wrapping'");
+  }
+  if (!a.dump_prefix.empty()) {  // before the GEMM, as the reference CLI does (ozmm_cli.cpp:73-86)
+    try {
+      dump_split(h, a.dump_prefix + ".a", 'L', a.transa, A, m, n, a.k, a.force_beta, method_strategy(code));
+      dump_split(h, a.dump_prefix + ".b", 'R', a.transb, B, p, n, a.k, a.force_beta, method_strategy(code));
+    } catch (...) {
+      ozmm_destroy(h);
+      throw;
+    }
+  }
   ozmm_options_t opt{};
   opt.force_beta = a.force_beta;
   opt.force_r = a.force_r;
+  opt.overflow_wrap = a.overflow == "wrapping" ? 1 : 0;
   opt.timings = 1;
   opt.method = code;
   ozmm_counts_t cnt{};

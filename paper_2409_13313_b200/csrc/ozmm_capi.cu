@@ -1337,6 +1337,64 @@ int ozmm_split_ex(ozmm_handle_t handle, char side, char trans, int64_t lines, in
                         row_mode, lines, n, X, ldx, k, beta, slices, lds, lines * lds, out);
 }
 
+int ozmm_split_host(ozmm_handle_t handle, char side, char trans, int64_t lines, int64_t n, const double* X,
+                    int64_t ldx, int k, int beta, int strategy, int8_t* slices, double* out, double* residual) {
+  // Host-memory split with its residual (the reference's SplitMatrix as
+  // dump_split writes it, split.cpp:254-270): X is uploaded, split on the GPU by
+  // ozmm_split_ex, the residual recurrence runs on the GPU
+  // (split_residual_kernel), and the results come back line-major.
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return set_err(nullptr, OZMM_ERR_ARG, "null handle");
+  if (!X || !slices || !out) return set_err(h, OZMM_ERR_ARG, "null pointer");
+  if (side != 'L' && side != 'R') return set_err(h, OZMM_ERR_ARG, "side must be 'L' or 'R'");
+  if (!valid_trans(trans)) return set_err(h, OZMM_ERR_ARG, "trans must be 'N' or 'T'");
+  if (lines < 1 || n < 1) return set_err(h, OZMM_ERR_ARG, "split: empty matrix");
+  const bool row_mode = (side == 'L') != is_trans(trans);
+  const int64_t rows = row_mode ? lines : n, cols = row_mode ? n : lines;  // X as stored
+  if (ldx < cols) return set_err(h, OZMM_ERR_ARG, "split: leading dimension too small");
+  if (beta == 0) {
+    beta = ozb::compute_beta_host(n);
+    if (beta < 0) return set_err(h, OZMM_ERR_ARG, "compute_beta: n out of range");
+  }
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  const int64_t lds = ozmm_slice_ld(n);
+  const size_t nout = static_cast<size_t>(strategy == 2 ? k * lines : lines);
+  double *dX = nullptr, *dOut = nullptr, *dR = nullptr;
+  int8_t* dS = nullptr;
+  int rc = OZMM_OK;
+  auto cu = [&](cudaError_t e, const char* what) {
+    if (e != cudaSuccess && rc == OZMM_OK) rc = set_err(h, OZMM_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return rc == OZMM_OK;
+  };
+  if (cu(cudaMalloc(&dX, sizeof(double) * rows * cols), "cudaMalloc") &&
+      cu(cudaMalloc(&dS, static_cast<size_t>(k) * lines * lds), "cudaMalloc") &&
+      cu(cudaMalloc(&dOut, sizeof(double) * nout), "cudaMalloc") &&
+      cu(cudaMalloc(&dR, sizeof(double) * lines * n), "cudaMalloc") &&
+      cu(cudaMemcpy2DAsync(dX, sizeof(double) * cols, X, sizeof(double) * ldx, sizeof(double) * cols, rows,
+                           cudaMemcpyHostToDevice, h->stream), "H2D")) {
+    fold_flags_kernel<<<1, 1, 0, h->stream>>>(h->flags);  // this call's range flag starts clear
+    rc = ozmm_split_ex(handle, side, trans, lines, n, dX, cols, k, beta, strategy, dS, lds, dOut);
+    if (rc == OZMM_OK) rc = check_range_sync(h);  // the reference throws from the split
+    if (rc == OZMM_OK) {
+      const int64_t total = lines * n;
+      ozb::split_residual_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, h->stream>>>(
+          dX, cols, row_mode ? 1 : 0, lines, n, k, beta, strategy, dS, lds, lines * lds, dOut, dR);
+      cu(cudaGetLastError(), "residual kernel") &&
+          cu(cudaMemcpy2DAsync(slices, n, dS, lds, n, static_cast<size_t>(k) * lines, cudaMemcpyDeviceToHost,
+                               h->stream), "D2H") &&
+          cu(cudaMemcpyAsync(out, dOut, sizeof(double) * nout, cudaMemcpyDeviceToHost, h->stream), "D2H") &&
+          (!residual || cu(cudaMemcpyAsync(residual, dR, sizeof(double) * lines * n, cudaMemcpyDeviceToHost,
+                                           h->stream), "D2H")) &&
+          cu(cudaStreamSynchronize(h->stream), "sync");
+    }
+  }
+  cudaFree(dX);
+  cudaFree(dS);
+  cudaFree(dOut);
+  cudaFree(dR);
+  return rc;
+}
+
 int ozmm_gemm_slices(ozmm_handle_t handle, int64_t m, int64_t n, int64_t p, int k, int beta_bits,
                      int64_t r, const int8_t* As, int64_t lds_a, const double* mu, const int8_t* Bs,
                      int64_t lds_b, const double* nu, double alpha, double beta, double* C,

@@ -213,4 +213,47 @@ __global__ void __launch_bounds__(256) transpose_f64_kernel(const double* __rest
     if (c0 + j < cols && r0 + tx < rows) Y[(c0 + j) * rows + r0 + tx] = tile[tx][j];
 }
 
+// Residual of a split, the reference's SplitMatrix::residual (split.cpp:49,
+// dumped by dump_split, :269): w = x, then for s = 1..k the exact w -= slice_s
+// unit_s of the strategy's extraction.  Every step is exact in all three
+// splitters (the slice is w's rounded or truncated digit on the unit grid), so
+// the FP64 recurrence reproduces the reference bit for bit; the sign-of-zero
+// cases follow the reference's control flow:
+//   * RN (const shift, per slice): a unit that underflowed to 0 extracts x = w,
+//     so w becomes +0 unless it already was a zero;
+//   * bitmask: a zero element, or a unit below 2^-1074 (no bits there), leaves
+//     the skeleton's +0 / w unchanged;
+//   * a zero line (shift 0) keeps the skeleton's +0 for the const-shift
+//     splitters, while the per-slice splitter stores w (x itself) there.
+// X: the op(X) lines as in the splitters (row_mode: line i = X[i][0..n), else
+// X[0..n)[i]); sh: const shift [lines] (strategy 0, 1) or units [k][lines] (2).
+// R: [lines][n].
+__global__ void split_residual_kernel(const double* __restrict__ X, int64_t ldx, int row_mode, int64_t lines,
+                                      int64_t n, int k, int beta, int strategy, const int8_t* __restrict__ S,
+                                      int64_t lds, int64_t plane, const double* __restrict__ sh,
+                                      double* __restrict__ R) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= lines * n) return;
+  const int64_t line = idx / n, j = idx % n;
+  const double x = row_mode ? X[line * ldx + j] : X[j * ldx + line];
+  double w = x;
+  if (strategy != 2 && sh[line] == 0.0) {
+    w = 0.0;  // zero line: the const-shift splitters skip it (residual stays +0)
+  } else if (strategy == 1 && x == 0.0) {
+    w = 0.0;  // bitmask: zero elements are skipped
+  } else {
+    for (int s = 1; s <= k; ++s) {
+      const double unit = strategy == 2 ? sh[static_cast<int64_t>(s - 1) * lines + line]
+                                        : __dmul_rn(sh[line], pow2(1 - beta * s));
+      if (unit == 0.0) {
+        if (strategy != 1 && w != 0.0) w = 0.0;
+        continue;
+      }
+      const int8_t v = S[static_cast<int64_t>(s - 1) * plane + line * lds + j];
+      w = __dsub_rn(w, __dmul_rn(static_cast<double>(v), unit));
+    }
+  }
+  R[line * n + j] = w;
+}
+
 }  // namespace ozb

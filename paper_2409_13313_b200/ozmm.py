@@ -103,6 +103,8 @@ _SIG = {
                     _vp], C.c_int),
     "ozmm_split_ex": ([_vp, C.c_char, C.c_char, _i64, _i64, _vp, _i64, C.c_int, C.c_int, C.c_int,
                        _vp, _i64, _vp], C.c_int),
+    "ozmm_split_host": ([_vp, C.c_char, C.c_char, _i64, _i64, _vp, _i64, C.c_int, C.c_int, C.c_int,
+                         _vp, _vp, _vp], C.c_int),
     "ozmm_gemm_slices": ([_vp, _i64, _i64, _i64, C.c_int, C.c_int, _i64, _vp, _i64, _vp, _vp,
                           _i64, _vp, C.c_double, C.c_double, _vp, _i64, C.POINTER(Options)],
                          C.c_int),
@@ -557,6 +559,33 @@ def split_rn_const_shift(x, k: int, side: str = "L", *, trans: bool = False, for
     h.check(lib.ozmm_split(h.h, side.encode(), b"T" if trans else b"N", lines, n, x.data_ptr(),
                            x.stride(0), k, beta, sl.data_ptr(), lds, sh.data_ptr()))
     return SplitMatrix(side, k, beta, sl, sh, n)
+
+
+def split_dump(a, k: int, side: str = "L", strategy: SliceStrategy = SliceStrategy.RoundNearestConstShift,
+               *, force_beta: int = 0, handle: Handle | None = None):
+    """The reference's SplitMatrix of a host matrix, as dump_split writes it
+    (split.cpp:254-270): ``(slices [k][rows][cols] int8, shift or units,
+    residual [rows][cols])`` in the matrix's own layout, computed on the GPU
+    (ozmm_split_host).  side 'L' splits rows, 'R' columns; ``shift`` is [lines]
+    (const-shift strategies) or the per-slice units [k][lines]."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    rows, cols = a.shape
+    side = side.upper()
+    lines, n = (rows, cols) if side == "L" else (cols, rows)
+    code = {SliceStrategy.RoundNearestConstShift: 0, SliceStrategy.BitMask: 1,
+            SliceStrategy.RoundNearestPerSlice: 2}[SliceStrategy(strategy)]
+    sl = np.empty((k, lines, n), np.int8)
+    out = np.empty((k, lines) if code == 2 else (lines,), np.float64)
+    res = np.empty((lines, n), np.float64)
+    h = handle or default_handle(0)
+    h.set_stream(None)
+    h.check(lib.ozmm_split_host(h.h, side.encode(), b"N", lines, n, a.ctypes.data, cols, k,
+                                force_beta, code, sl.ctypes.data, out.ctypes.data,
+                                res.ctypes.data))
+    if side == "R":  # line-major (columns) back to the matrix's layout (transpose_back, :175-180)
+        sl = np.ascontiguousarray(sl.transpose(0, 2, 1))
+        res = np.ascontiguousarray(res.T)
+    return sl, out, res
 
 
 def split(x, k: int, side: str = "L", strategy: SliceStrategy = SliceStrategy.RoundNearestConstShift,

@@ -51,9 +51,10 @@ def save_ozmm(path, m, kind=0):
         f.write(m.tobytes())
 
 
-def load_ozmm(path):
+def load_ozmm(path, kind=0):
+    """kind 0 = F64, 1 = I8 (io.hpp:17)."""
     import struct
     raw = open(path, "rb").read()
-    assert raw[:4] == b"OZMM" and raw[4] == 1 and raw[5] == 0
+    assert raw[:4] == b"OZMM" and raw[4] == 1 and raw[5] == kind
     rows, cols = struct.unpack("<QQ", raw[12:28])
-    return np.frombuffer(raw[28:], dtype="<f8").reshape(rows, cols)
+    return np.frombuffer(raw[28:], dtype="<f8" if kind == 0 else "i1").reshape(rows, cols)

@@ -90,3 +90,80 @@ def test_gemm_over_ozmm_files(tmp_path, method, trans):
     assert (line["m"], line["n"], line["p"], line["k"]) == (m, n, p, k)
     assert_bitwise(load_ozmm(tmp_path / "D.ozmm"),
                    ref.gemm(1.5, A, B, 0.5, C, k=k, method=method))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("method,strategy,trans", [("ozIMMU_H", "rn_const", False),
+                                                   ("ozIMMU_H", "rn_const", True),
+                                                   ("ozIMMU_EF", "bitmask", False),
+                                                   ("ozIMMU_RN", "rn_per_slice", False)])
+def test_dump_splits_match_reference(tmp_path, method, strategy, trans):
+    """--dump-splits writes dump_split's files (split.cpp:254-270) for op(A) (Left)
+    and op(B) (Right): slices, shift / per-slice units and residual bit-identical
+    to the reference's SplitMatrix, including zero lines and signed zeros."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from oracle import oracle
+    from paper_2409_13313_b200 import ozmm
+    if not oracle.have_ref():
+        pytest.skip("reference build absent")
+    ref = oracle.RefLib()
+    m, n, p, k = 70, 500, 45, 9
+    A = ozmm.gen_phi_matrix(m, n, 2.0, 5)
+    B = ozmm.gen_phi_matrix(n, p, 2.0, 6)
+    A[3, :] = 0.0
+    A[3, 7] = -0.0       # zero row holding a -0
+    A[10, 11] = -0.0     # -0 in a live row
+    B[:, 4] = -0.0       # zero column of -0
+    A[20, 5] = 2.0 ** -1070   # bits below the slice grid / underflowing units
+    save_ozmm(tmp_path / "A.ozmm", A.T.copy() if trans else A)
+    save_ozmm(tmp_path / "B.ozmm", B.T.copy() if trans else B)
+    args = ["gemm", tmp_path / "A.ozmm", tmp_path / "B.ozmm", "--out", tmp_path / "D.ozmm",
+            "--k", k, "--method", method, "--dump-splits", tmp_path / "d"]
+    if trans:
+        args += ["--transa", "--transb"]
+    out = run(*args)
+    assert out.returncode == 0, out.stderr
+    for name, X, side in (("a", A, "left"), ("b", B, "right")):
+        sl, sh, res = ref.split_any(X, k, strategy, side, residual=True)
+        for s in range(k):
+            np.testing.assert_array_equal(load_ozmm(tmp_path / f"d.{name}.slice{s + 1}.ozmm", 1), sl[s])
+        if strategy == "rn_per_slice":
+            for s in range(k):
+                assert_bitwise(load_ozmm(tmp_path / f"d.{name}.shift{s + 1}.ozmm")[0], sh[s])
+        else:
+            assert_bitwise(load_ozmm(tmp_path / f"d.{name}.shift.ozmm")[0], sh)
+        assert_bitwise(load_ozmm(tmp_path / f"d.{name}.residual.ozmm"), res, f"{name} residual")
+
+
+@pytest.mark.gpu
+def test_overflow_mode_option(tmp_path):
+    """--overflow-mode checked|wrapping (ozmm_cli.cpp:27-31): wrapping matches the
+    reference's Wrapping result on inputs whose forced-r chunks overflow INT32;
+    checked reports the overflow (exit 1) and writes no D; other values exit 2."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from oracle import oracle
+    if not oracle.have_ref():
+        pytest.skip("reference build absent")
+    ref = oracle.RefLib()
+    # the drop-in demo's overflowing case (tests/cpp/dropin_demo.cpp): constant operands
+    # whose slices are all positive, so forced long chunks leave INT32
+    m, n, p, k = 32, 65536, 24, 14
+    v = (127.0 + 63.0 / 127.0) / 64.0
+    A = np.full((m, n), v)
+    B = np.full((n, p), v)
+    save_ozmm(tmp_path / "A.ozmm", A)
+    save_ozmm(tmp_path / "B.ozmm", B)
+    base = ["gemm", tmp_path / "A.ozmm", tmp_path / "B.ozmm", "--k", k, "--force-r", 14]
+    out = run(*base, "--out", tmp_path / "W.ozmm", "--overflow-mode", "wrapping")
+    assert out.returncode == 0, out.stderr
+    want = ref.gemm(1.0, A, B, 0.0, np.zeros((m, p)), k=k, force_r=14, wrapping=True)
+    assert_bitwise(load_ozmm(tmp_path / "W.ozmm"), want)
+    out = run(*base, "--out", tmp_path / "K.ozmm", "--overflow-mode", "checked")
+    assert out.returncode == 1 and "overflow" in out.stderr.lower(), (out.stdout, out.stderr)
+    assert not (tmp_path / "K.ozmm").exists()
+    out = run(*base, "--out", tmp_path / "X.ozmm", "--overflow-mode", "saturating")
+    assert out.returncode == 2
