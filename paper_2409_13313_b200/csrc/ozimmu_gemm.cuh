@@ -38,12 +38,15 @@ namespace ozb {
 
 constexpr int kBM = 128;         // UMMA M (cta_group::1), TMEM lanes
 constexpr int kBK = 32;          // bytes of K per pipeline stage = one MMA (kind::i8, K=32)
-constexpr int kMaxK = 22;
-constexpr int kMaxChunks = 256;    // >= k(k+1)/2 for k <= kMaxK
-constexpr int kMaxProducts = 256;  // k(k+1)/2 for k <= kMaxK
-constexpr int kMaxBatches = 128;
-constexpr int kMaxPasses = 192;
-constexpr int kMaxAGroups = 256;
+// Slice counts up to 32 (the FP64 floor is reached by k ~ 13-14; the reference
+// only requires k >= 1).  The schedule tables below travel as kernel parameters
+// (about 16 KB of the 32 KB parameter space).
+constexpr int kMaxK = 32;
+constexpr int kMaxChunks = 528;    // >= k(k+1)/2 for k <= kMaxK (r = 1)
+constexpr int kMaxProducts = 528;  // k(k+1)/2 for k <= kMaxK
+constexpr int kMaxBatches = 192;
+constexpr int kMaxPasses = 384;
+constexpr int kMaxAGroups = 528;
 constexpr int kGemmThreads = 320;
 constexpr int kEpiWarps = 8;
 
@@ -92,7 +95,7 @@ struct GemmParams {
   int64_t ldc;
   int32_t* dump;       // optional [n_chunks][m][p] INT32 chunk sums (parity/debug)
   // per batch: first chunk, chunk count, pass range [pass0, pass1)
-  uint8_t b_c0[kMaxBatches], b_nc[kMaxBatches], b_pass0[kMaxBatches], b_pass1[kMaxBatches];
+  uint16_t b_c0[kMaxBatches], b_nc[kMaxBatches], b_pass0[kMaxBatches], b_pass1[kMaxBatches];
   // per pass: A slice range, B slice range (1-based, inclusive), product range
   uint8_t p_alo[kMaxPasses], p_ahi[kMaxPasses], p_blo[kMaxPasses], p_bhi[kMaxPasses];
   uint16_t p_p0[kMaxPasses], p_p1[kMaxPasses];

@@ -538,10 +538,10 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
   P.ldc = ldc;
   P.dump = dump;
   for (size_t b = 0; b < S.batches.size(); ++b) {
-    P.b_c0[b] = static_cast<uint8_t>(S.batches[b].c0);
-    P.b_nc[b] = static_cast<uint8_t>(S.batches[b].nc);
-    P.b_pass0[b] = static_cast<uint8_t>(S.batches[b].pass0);
-    P.b_pass1[b] = static_cast<uint8_t>(S.batches[b].pass1);
+    P.b_c0[b] = static_cast<uint16_t>(S.batches[b].c0);
+    P.b_nc[b] = static_cast<uint16_t>(S.batches[b].nc);
+    P.b_pass0[b] = static_cast<uint16_t>(S.batches[b].pass0);
+    P.b_pass1[b] = static_cast<uint16_t>(S.batches[b].pass1);
   }
   for (size_t q = 0; q < S.passes.size(); ++q) {
     P.p_alo[q] = static_cast<uint8_t>(S.passes[q].alo);
@@ -578,7 +578,7 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
         P.p_g0[q - q0] = P.p_g0[q], P.p_g1[q - q0] = P.p_g1[q];
       }
       P.b_c0[0] = P.b_c0[b], P.b_nc[0] = P.b_nc[b];
-      P.b_pass0[0] = 0, P.b_pass1[0] = static_cast<uint8_t>(q1 - q0);
+      P.b_pass0[0] = 0, P.b_pass1[0] = static_cast<uint16_t>(q1 - q0);
       P.nbatch = 1, P.npass = q1 - q0;
     }
   }

@@ -293,7 +293,7 @@ int ozmm_dgemm_2d(ozmm_grid_t g, char transa, char transb, int64_t m, int64_t n,
   if (m % cells || p % cells)
     return fail(OZMM_ERR_ARG, "m=%lld and p=%lld must be divisible by Pr*Pc=%lld",
                 static_cast<long long>(m), static_cast<long long>(p), static_cast<long long>(cells));
-  if (k < 1 || k > 22) return fail(OZMM_ERR_CONFIG, "k must be in 1..22");
+  if (k < 1 || k > 32) return fail(OZMM_ERR_CONFIG, "k must be in 1..32");
   const int64_t mr = m / g->pr, pcols = p / g->pc;  // C block
   const int64_t ms = mr / g->pc, ps = pcols / g->pr;  // lines this rank slices
   if (ldc < pcols) return fail(OZMM_ERR_ARG, "ldc below the C block's %lld columns",

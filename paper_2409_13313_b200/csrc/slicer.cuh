@@ -43,7 +43,7 @@
 namespace ozb {
 
 constexpr double kSigmaScale = 6755399441055744.0;  // 0.75 * 2^53 (split.cpp:16)
-constexpr int kMaxSlices = 22;  // = kMaxK of the GEMM (line-sum scratch in shared memory)
+constexpr int kMaxSlices = 32;  // = kMaxK of the GEMM (line-sum scratch in shared memory)
 
 // flags[0] |= underflow (pe < -1000), flags[1] |= range (pe > 920).
 __device__ __forceinline__ void report_flags(int* flags, bool under, bool range) {

@@ -223,3 +223,22 @@ def test_one_pass_column_split_bit_exact(oz, checker, m, n, p, k, phi, ta, tb, c
     got_h = oz.ozaki_gemm(1.5, A, B, 0.5, C, cfg, transa=ta, transb=tb, col_split=col_split,
                           host_panels=3)
     assert_bitwise(got_h, want, f"host col_split={col_split}")
+
+
+@pytest.mark.parametrize("k,phi,r,method", [(23, 4.0, 0, "ozIMMU_H"), (28, 2.0, 0, "ozIMMU_H"),
+                                            (32, 4.0, 0, "ozIMMU_H"), (26, 1.0, 1, "ozIMMU_H"),
+                                            (24, 2.0, 0, "ozIMMU_EF"), (25, 2.0, 0, "ozIMMU")])
+def test_large_k_bit_exact(oz, checker, k, phi, r, method):
+    """k beyond 22 (up to 32): 253..528 slice products, chunk counts up to 528 with
+    r = 1; the device and host entries match the reference bit for bit."""
+    m, n, p = 150, 700, 130
+    A = oz.gen_phi_matrix(m, n, phi, 121)
+    B = oz.gen_phi_matrix(n, p, phi, 122)
+    C = oz.gen_phi_matrix(m, p, phi, 123)
+    cfg = oz.config_for(method, k)
+    if r:
+        cfg.force_r = r
+    want = checker.gemm(1.5, A, B, 0.5, C, k=k, method=method, force_r=r)
+    got = oz.ozaki_gemm(1.5, dev(A), dev(B), 0.5, dev(C), cfg).cpu().numpy()
+    assert_bitwise(got, want, f"device k={k}")
+    assert_bitwise(oz.ozaki_gemm(1.5, A, B, 0.5, C, cfg), want, f"host k={k}")

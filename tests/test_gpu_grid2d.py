@@ -415,7 +415,7 @@ def test_grid2d_cuda_sync_check_range_error():
 
 
 def test_native_grid_rejects_bad_shapes():
-    """ozmm_dgemm_2d: m or p not divisible by Pr*Pc, and k outside 1..22, are
+    """ozmm_dgemm_2d: m or p not divisible by Pr*Pc, and k outside 1..32, are
     argument / config errors (no launch)."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -432,7 +432,7 @@ def test_native_grid_rejects_bad_shapes():
     assert ozmm.lib.ozmm_dgemm_2d(*args(66, 64, 8)) == ozmm.OZMM_ERR_ARG
     assert b"divisible" in ozmm.lib.ozmm_grid_last_error()
     assert ozmm.lib.ozmm_dgemm_2d(*args(64, 62, 8)) == ozmm.OZMM_ERR_ARG
-    assert ozmm.lib.ozmm_dgemm_2d(*args(64, 64, 23)) == ozmm.OZMM_ERR_CONFIG
+    assert ozmm.lib.ozmm_dgemm_2d(*args(64, 64, 33)) == ozmm.OZMM_ERR_CONFIG
     # world > 1 without an id or a hook
     g2 = ctypes.c_void_p()
     assert ozmm.lib.ozmm_grid_create(h.h, 0, 2, 0, None, None, None,

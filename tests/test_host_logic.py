@@ -96,7 +96,7 @@ def test_schedule_matches_reference_flushes(golden, name, mode):
 
 
 def test_schedule_k_sweep():
-    for k in range(1, 23):
+    for k in range(1, 33):
         for r in (1, 2, 3, 8, 16, 128):
             rows, info = oz.debug_schedule(k, r)
             assert info["products"] == k * (k + 1) // 2
