@@ -147,32 +147,43 @@ class WorkerPool {
       ++gen_;
     }
     cv_.notify_all();
-    work();
+    work(&fn, n);
     while (left_.load(std::memory_order_acquire) > 0) std::this_thread::yield();
-    std::lock_guard<std::mutex> lk(mu_);
-    fn_ = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = nullptr;  // no worker joins this job from here on
+    }
+    // workers that joined may still be leaving work(): the next job may not reset
+    // the shared counters under them
+    while (active_.load(std::memory_order_acquire) > 0) std::this_thread::yield();
   }
 
  private:
-  void work() {
+  void work(const std::function<void(int)>* fn, int n) {
     for (;;) {
       const int i = next_.fetch_add(1);
-      if (i >= n_) return;
-      (*fn_)(i);
+      if (i >= n) return;
+      (*fn)(i);
       left_.fetch_sub(1, std::memory_order_release);
     }
   }
   void loop() {
     uint64_t seen = 0;
     for (;;) {
+      const std::function<void(int)>* fn = nullptr;
+      int n = 0;
       {
         std::unique_lock<std::mutex> lk(mu_);
         cv_.wait(lk, [&] { return gen_ != seen; });
         seen = gen_;
         if (quit_) return;
-        if (fn_ == nullptr) continue;
+        if (fn_ == nullptr) continue;  // that job is already over
+        fn = fn_;
+        n = n_;
+        active_.fetch_add(1, std::memory_order_relaxed);
       }
-      work();
+      work(fn, n);
+      active_.fetch_sub(1, std::memory_order_release);
     }
   }
   std::vector<std::thread> workers_;
@@ -182,7 +193,7 @@ class WorkerPool {
   bool quit_ = false;
   const std::function<void(int)>* fn_ = nullptr;
   int n_ = 0;
-  std::atomic<int> next_{0}, left_{0};
+  std::atomic<int> next_{0}, left_{0}, active_{0};
 };
 
 // Pinned slots for one copy direction, two per team thread.  A region is cut
