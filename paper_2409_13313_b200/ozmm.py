@@ -354,6 +354,18 @@ def _is_cuda_tensor(x) -> bool:
     return isinstance(x, torch.Tensor) and x.is_cuda
 
 
+def _row_major(t) -> bool:
+    """Row-major with unit column stride; a dimension of size 1 may carry any
+    stride (numpy and torch leave such strides arbitrary)."""
+    return t.dim() == 2 and (t.shape[1] == 1 or t.stride(1) == 1)
+
+
+def _ld(t) -> int:
+    """Leading dimension of a row-major 2-D tensor: its row stride, or the row
+    length when there is a single row (the stride is then meaningless)."""
+    return int(t.stride(0)) if t.shape[0] > 1 else max(1, int(t.shape[1]))
+
+
 def _options(cfg: SchemeConfig | None, timings: bool = False, dump=None, tile_n: int = 0,
              sync_check: bool = False, cta_pair: int = 0, signed_slices: bool = False,
              kpair: int = 0, stages: int = 0, host_panels: int = 0,
@@ -443,7 +455,7 @@ def ozaki_gemm_ex(alpha: float, a, b, beta: float, c, cfg: SchemeConfig | None =
         for t in (a, b, c):
             if not (_is_cuda_tensor(t) and t.dtype == torch.float64):
                 raise ValueError("device path needs float64 CUDA tensors for A, B and C")
-            if t.stride(-1) != 1:
+            if not _row_major(t):
                 raise ValueError("operands must be row-major (unit column stride)")
         m, n = (a.shape[1], a.shape[0]) if transa else (a.shape[0], a.shape[1])
         nb, p = (b.shape[1], b.shape[0]) if transb else (b.shape[0], b.shape[1])
@@ -460,8 +472,8 @@ def ozaki_gemm_ex(alpha: float, a, b, beta: float, c, cfg: SchemeConfig | None =
                        signed_slices=signed_slices, kpair=kpair, stages=stages,
                        cta_pair=cta_pair, col_split=col_split)
         h.check(lib.ozmm_dgemm_ex(h.h, b"T" if transa else b"N", b"T" if transb else b"N", m, n,
-                                  p, alpha, a.data_ptr(), a.stride(0), b.data_ptr(),
-                                  b.stride(0), beta, dst.data_ptr(), dst.stride(0), cfg.k,
+                                  p, alpha, a.data_ptr(), _ld(a), b.data_ptr(),
+                                  _ld(b), beta, dst.data_ptr(), _ld(dst), cfg.k,
                                   C.byref(opt), C.byref(counts),
                                   C.byref(tim) if timings else None))
         if out is not None and dst is not out:
@@ -542,7 +554,7 @@ def split_rn_const_shift(x, k: int, side: str = "L", *, trans: bool = False, for
     side 'L': rows of op(X) (op(X) = lines x n); 'R': columns of op(X)
     (op(X) = n x lines).  x: float64 CUDA tensor, row-major."""
     torch = _torch()
-    if not (_is_cuda_tensor(x) and x.dtype == torch.float64 and x.stride(-1) == 1):
+    if not (_is_cuda_tensor(x) and x.dtype == torch.float64 and _row_major(x)):
         raise ValueError("split_rn_const_shift needs a row-major float64 CUDA tensor")
     side = side.upper()
     rows, cols = x.shape
@@ -557,7 +569,7 @@ def split_rn_const_shift(x, k: int, side: str = "L", *, trans: bool = False, for
     sl = torch.empty((k, lines, lds), dtype=torch.int8, device=x.device)
     sh = torch.empty((lines,), dtype=torch.float64, device=x.device)
     h.check(lib.ozmm_split(h.h, side.encode(), b"T" if trans else b"N", lines, n, x.data_ptr(),
-                           x.stride(0), k, beta, sl.data_ptr(), lds, sh.data_ptr()))
+                           _ld(x), k, beta, sl.data_ptr(), lds, sh.data_ptr()))
     return SplitMatrix(side, k, beta, sl, sh, n)
 
 
@@ -594,7 +606,7 @@ def split(x, k: int, side: str = "L", strategy: SliceStrategy = SliceStrategy.Ro
     split.cpp:223-237).  Returns SplitMatrix; for RoundNearestPerSlice its
     ``shift`` holds the per-slice units [k][lines] (slice_units, split.hpp:38)."""
     torch = _torch()
-    if not (_is_cuda_tensor(x) and x.dtype == torch.float64 and x.stride(-1) == 1):
+    if not (_is_cuda_tensor(x) and x.dtype == torch.float64 and _row_major(x)):
         raise ValueError("split needs a row-major float64 CUDA tensor")
     side = side.upper()
     rows, cols = x.shape
@@ -612,7 +624,7 @@ def split(x, k: int, side: str = "L", strategy: SliceStrategy = SliceStrategy.Ro
     out = torch.empty((k, lines) if code == 2 else (lines,), dtype=torch.float64,
                       device=x.device)
     h.check(lib.ozmm_split_ex(h.h, side.encode(), b"T" if trans else b"N", lines, n,
-                              x.data_ptr(), x.stride(0), k, beta, code, sl.data_ptr(), lds,
+                              x.data_ptr(), _ld(x), k, beta, code, sl.data_ptr(), lds,
                               out.data_ptr()))
     return SplitMatrix(side, k, beta, sl, out, n)
 
@@ -630,7 +642,7 @@ def gemm_slices(sa: SplitMatrix, sb: SplitMatrix, alpha: float, beta: float, c, 
     h.check(lib.ozmm_gemm_slices(h.h, m, sa.n, p, sa.k, sa.beta, r, sa.slices.data_ptr(),
                                  sa.slices.shape[2], sa.shift.data_ptr(), sb.slices.data_ptr(),
                                  sb.slices.shape[2], sb.shift.data_ptr(), alpha, beta,
-                                 c.data_ptr(), c.stride(0), C.byref(opt)))
+                                 c.data_ptr(), _ld(c), C.byref(opt)))
     return c
 
 
