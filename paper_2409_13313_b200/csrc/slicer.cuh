@@ -480,17 +480,28 @@ __global__ void __launch_bounds__(kOPThreads, 3) slice_cols_onepass_kernel(
     const int par = it & 1;
     const int64_t col = q * kOPCols + c;
     ptx::mbar_wait(full, it & 1);
-    // pass 1: column maxima
-    double m = 0.0;
+    // pass 1: column maxima, read as 16-byte column pairs -- a warp reads 512
+    // contiguous bytes per instruction (8 rows x 4 pairs), conflict-free
+    {
+      const int pr = lane & 3;  // column pair 2pr, 2pr + 1
+      double m0 = 0.0, m1 = 0.0;
+      const double2* b2 = reinterpret_cast<const double2*>(buf);
+#pragma unroll 8
+      for (int row = warp * 8 + (lane >> 2); row < kR; row += kOPThreads / 4) {
+        const double2 v = b2[row * (kOPCols / 2) + pr];
+        m0 = fmax(m0, fabs(v.x));
+        m1 = fmax(m1, fabs(v.y));
+      }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int chunk = (threadIdx.x + kOPThreads * u) >> 3;
-#pragma unroll
-      for (int e = 0; e < 16; ++e) m = fmax(m, fabs(buf[(chunk * 16 + e) * kOPCols + c]));
+      for (int o = 4; o < 32; o <<= 1) {
+        m0 = fmax(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+        m1 = fmax(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+      }
+      if (lane < 4) {
+        red[warp * kOPCols + 2 * pr] = m0;
+        red[warp * kOPCols + 2 * pr + 1] = m1;
+      }
     }
-    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 8));
-    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 16));
-    if (lane < kOPCols) red[warp * kOPCols + lane] = m;
     __syncthreads();
     if (threadIdx.x < kOPCols) {
       double v = 0.0;
@@ -519,9 +530,17 @@ __global__ void __launch_bounds__(kOPThreads, 3) slice_cols_onepass_kernel(
       const int chunk = (threadIdx.x + kOPThreads * u) >> 3;
       const int64_t base = row0 + chunk * 16;
       const bool valid = col < cols && base < lds;
+      // the 4 lanes of a column sit on rows 16 apart (same banks): odd chunks read
+      // their row pairs swapped so a warp load spans all 32 banks (2 wavefronts)
       double w[16];
+      const bool odd = chunk & 1;
 #pragma unroll
-      for (int e = 0; e < 16; ++e) w[e] = buf[(chunk * 16 + e) * kOPCols + c];
+      for (int e = 0; e < 16; e += 2) {
+        const double x0 = buf[(chunk * 16 + e + (odd ? 1 : 0)) * kOPCols + c];
+        const double x1 = buf[(chunk * 16 + e + (odd ? 0 : 1)) * kOPCols + c];
+        w[e] = odd ? x1 : x0;
+        w[e + 1] = odd ? x0 : x1;
+      }
       if (lsum)  // every lane takes part in the column-sum reduction (4 lanes per column)
         emit16<4>(w, PE, beta, k, S + col * lds + base, plane, valid ? valid16(len - base) : 0, valid,
                   lsum_s + c, kOPCols);

@@ -2,7 +2,7 @@
 L=paper_2409_13313_b200/libozmm_b200.so
 cp $L /tmp/rel.so
 cp tools/_alt/new_diag.so $L
-V="two:OZMM_COLS_TWO_PASS=1,u2:OZMM_COLS_TWO_PASS=0+OZMM_COLS_UNITS=2,u3:OZMM_COLS_TWO_PASS=0+OZMM_COLS_UNITS=3,u4:OZMM_COLS_TWO_PASS=0+OZMM_COLS_UNITS=4"
+V="two:OZMM_COLS_TWO_PASS=1,u2:OZMM_COLS_TWO_PASS=0+OZMM_COLS_UNITS=2,db:OZMM_COLS_TWO_PASS=0+OZMM_COLS_UNITS=2+OZMM_COLS_DB=1"
 timeout 300 python tools/cols_probe.py --variants "$V"
 timeout 300 python tools/cols_probe.py --n 8192 --p 8192 --variants "$V"
 timeout 300 python tools/cols_probe.py --n 1000 --p 777 --k 12 --variants "two:OZMM_COLS_TWO_PASS=1,one:OZMM_COLS_TWO_PASS=0"
