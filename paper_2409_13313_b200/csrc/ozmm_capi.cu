@@ -526,6 +526,8 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
   P.npass = static_cast<int>(S.passes.size());
   P.beta = beta_bits;
   P.stages = stages;
+  // a round waits for group_pairs A stages at once: never more than the ring holds
+  P.group_pairs = std::max(1, std::min(P.group_pairs, stages));
   P.a_slots = S.a_slots;
   P.b_slots = S.b_slots;
   P.n_chunks = static_cast<int>(S.chunks.size());

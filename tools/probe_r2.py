@@ -48,7 +48,7 @@ def parse_opt(s):
     environment variable for that option's calls only."""
     name, _, rest = s.partition(":")
     kw = {}
-    for item in filter(None, rest.split(",")):
+    for item in filter(None, rest.replace("+", ",").split(",")):
         k, v = item.split("=")
         kw[k] = v if k.startswith("env.") else int(v)
     return name, kw
