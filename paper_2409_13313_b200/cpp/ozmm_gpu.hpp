@@ -6,6 +6,11 @@
 //                             double beta, const MatrixF64& c, const SchemeConfig& cfg);  :92-95
 //   OzakiResult ozaki_gemm_ex(...same...);                                                :96-98
 //   OzakiResult ozaki_mm     (const MatrixF64& a, const MatrixF64& b, const SchemeConfig&); :89-90
+// and for the splitters (proj/include/ozmm/split.hpp:61-74), filling the
+// reference's SplitMatrix (or any type with its members):
+//   split<SplitMatrix>(a, k, side, strategy [, forced_beta])  -- split_bitmask /
+//   split_round_nearest / split_rn_const_shift, slices + shifts (or per-slice
+//   units) + residual + underflow flag, computed on the GPU (ozmm_split_host)
 // for every valid SchemeConfig: the (strategy, accumulation) pair selects the
 // GPU method -- ozIMMU_H (the hot path), ozIMMU, ozIMMU_RN, ozIMMU_EF and the two
 // other valid pairs -- and overflow / force_beta / force_r are honoured
@@ -25,6 +30,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "../../include/ozmm_b200.h"
 
@@ -167,6 +173,67 @@ OzakiResultT<Mat> ozaki_mm(const Mat& a, const Mat& b, const Cfg& cfg) {
   Mat zero(a.rows(), b.cols());
   std::fill(zero.data(), zero.data() + a.rows() * b.cols(), 0.0);
   return ozaki_gemm_ex(1.0, a, b, 0.0, zero, cfg);
+}
+
+// The reference's splitters on the GPU (split.hpp:61-74): Split is the caller's
+// SplitMatrix type (split.hpp:31-50); side / strategy are its Side {Left, Right}
+// and SliceStrategy {BitMask, RoundNearestPerSlice, RoundNearestConstShift}.
+// Fills side, k, beta, strategy, slices (the matrix's own layout), const_shift
+// (const-shift strategies) or slice_units (per-slice RN), residual and
+// underflow_flagged exactly as the reference's split_any does (split.cpp:182-198).
+template <class Split, class Mat, class SideT, class StrategyT>
+Split split(const Mat& a, int k, SideT side, StrategyT strategy, int forced_beta = 0) {
+  if (k < 1) throw std::invalid_argument("split: k must be >= 1");
+  const int sd = static_cast<int>(side), st = static_cast<int>(strategy);
+  const int code = st == 0 ? OZMM_SPLIT_BITMASK : (st == 1 ? OZMM_SPLIT_RN_PER_SLICE : OZMM_SPLIT_RN_CONST_SHIFT);
+  const std::int64_t rows = a.rows(), cols = a.cols();
+  const std::int64_t lines = sd == 0 ? rows : cols, n = sd == 0 ? cols : rows;
+  std::vector<std::int8_t> sl(static_cast<size_t>(k * lines * n));
+  std::vector<double> out(static_cast<size_t>(st == 1 ? k * lines : lines));
+  std::vector<double> res(static_cast<size_t>(lines * n));
+  ozmm_handle_t h = thread_handle();
+  int pending_under = 0;
+  ozmm_sync_status(h, &pending_under);  // start from clear flags (this call's underflow only)
+  throw_status(ozmm_split_host(h, sd == 0 ? 'L' : 'R', 'N', lines, n, a.data(), cols, k, forced_beta, code,
+                               sl.data(), out.data(), res.data()),
+               h);
+  int under = 0;
+  throw_status(ozmm_sync_status(h, &under), h);
+  int beta = forced_beta;
+  if (!beta) throw_status(ozmm_compute_beta(n, &beta), nullptr);
+  Split s;
+  s.side = side;
+  s.k = k;
+  s.beta = beta;
+  s.strategy = strategy;
+  using MatI8 = typename decltype(s.slices)::value_type;
+  using Vec = decltype(s.const_shift);
+  // line-major [lines][n] -> the matrix's own rows x cols (Right: transposed back)
+  auto at = [&](std::int64_t i, std::int64_t j) { return sd == 0 ? i * n + j : j * n + i; };
+  for (int t = 0; t < k; ++t) {
+    MatI8 m(rows, cols);
+    const std::int8_t* src = sl.data() + static_cast<size_t>(t) * lines * n;
+    for (std::int64_t i = 0; i < rows; ++i)
+      for (std::int64_t j = 0; j < cols; ++j) m.data()[i * cols + j] = src[at(i, j)];
+    s.slices.push_back(std::move(m));
+  }
+  if (st == 1) {
+    for (int t = 0; t < k; ++t) {
+      Vec v(lines);
+      for (std::int64_t i = 0; i < lines; ++i) v.data()[i] = out[t * lines + i];
+      s.slice_units.push_back(std::move(v));
+    }
+  } else {
+    Vec v(lines);
+    for (std::int64_t i = 0; i < lines; ++i) v.data()[i] = out[i];
+    s.const_shift = std::move(v);
+  }
+  decltype(s.residual) r(rows, cols);
+  for (std::int64_t i = 0; i < rows; ++i)
+    for (std::int64_t j = 0; j < cols; ++j) r.data()[i * cols + j] = res[at(i, j)];
+  s.residual = std::move(r);
+  s.underflow_flagged = under != 0;
+  return s;
 }
 
 }  // namespace gpu

@@ -9,14 +9,35 @@
 //   reference's config_for preset, passed unchanged to both calls; or
 //   "overflow <force_r>": ozIMMU_H with force_r on INT32-overflowing inputs:
 //   Wrapping bit-identical on both sides, Checked throws on the GPU side
-//   (prints "OVERFLOW-OK").
+//   (prints "OVERFLOW-OK");
+//   "split": the reference's split_bitmask / split_round_nearest /
+//   split_rn_const_shift of A (Left) and B (Right) against ozmm::gpu::split
+//   into the reference's own SplitMatrix type (prints "SPLIT-OK").
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
 #include "ozmm/generate.hpp"
 #include "ozmm/scheme.hpp"
+#include "ozmm/split.hpp"
 #include "ozmm_gpu.hpp"
+
+// bitwise equality of two reference SplitMatrix objects
+static bool same_split(const ozmm::SplitMatrix& x, const ozmm::SplitMatrix& y) {
+  auto eq = [](const void* a, const void* b, size_t bytes) { return std::memcmp(a, b, bytes) == 0; };
+  if (x.side != y.side || x.k != y.k || x.beta != y.beta || x.strategy != y.strategy ||
+      x.underflow_flagged != y.underflow_flagged || x.slices.size() != y.slices.size() ||
+      x.slice_units.size() != y.slice_units.size() || x.const_shift.size() != y.const_shift.size())
+    return false;
+  const size_t cells = static_cast<size_t>(x.residual.rows() * x.residual.cols());
+  for (size_t t = 0; t < x.slices.size(); ++t)
+    if (!eq(x.slices[t].data(), y.slices[t].data(), cells)) return false;
+  for (size_t t = 0; t < x.slice_units.size(); ++t)
+    if (!eq(x.slice_units[t].data(), y.slice_units[t].data(), sizeof(double) * x.slice_units[t].size()))
+      return false;
+  return eq(x.const_shift.data(), y.const_shift.data(), sizeof(double) * x.const_shift.size()) &&
+         eq(x.residual.data(), y.residual.data(), sizeof(double) * cells);
+}
 
 int main(int argc, char** argv) {
   if (argc < 6) return 2;
@@ -70,6 +91,25 @@ int main(int argc, char** argv) {
     std::printf("%s wrapping-match=%d checked-threw=%d\n", same && threw ? "OVERFLOW-OK" : "OVERFLOW-BAD",
                 same, threw);
     return same && threw ? 0 : 1;
+  }
+  if (std::strcmp(method, "split") == 0) {
+    bool ok = true;
+    for (auto st : {ozmm::SliceStrategy::BitMask, ozmm::SliceStrategy::RoundNearestPerSlice,
+                    ozmm::SliceStrategy::RoundNearestConstShift}) {
+      auto ref_split = [&](const ozmm::MatrixF64& x, ozmm::Side sd) {
+        return st == ozmm::SliceStrategy::BitMask ? ozmm::split_bitmask(x, k, sd)
+               : st == ozmm::SliceStrategy::RoundNearestPerSlice ? ozmm::split_round_nearest(x, k, sd)
+                                                                  : ozmm::split_rn_const_shift(x, k, sd);
+      };
+      const bool a_ok = same_split(ref_split(A, ozmm::Side::Left),
+                                   ozmm::gpu::split<ozmm::SplitMatrix>(A, k, ozmm::Side::Left, st));
+      const bool b_ok = same_split(ref_split(B, ozmm::Side::Right),
+                                   ozmm::gpu::split<ozmm::SplitMatrix>(B, k, ozmm::Side::Right, st));
+      std::printf("strategy %s: A %s B %s\n", ozmm::to_string(st), a_ok ? "same" : "DIFFERS", b_ok ? "same" : "DIFFERS");
+      ok = ok && a_ok && b_ok;
+    }
+    std::printf("%s\n", ok ? "SPLIT-OK" : "SPLIT-BAD");
+    return ok ? 0 : 1;
   }
   const ozmm::SchemeConfig cfg = ozmm::config_for(ozmm::method_from_string(method), k);
   const ozmm::OzakiResult ref = ozmm::ozaki_gemm_ex(1.5, A, B, 0.5, C, cfg);       // reference

@@ -55,3 +55,17 @@ def test_dropin_overflow_modes():
         pytest.skip("no CUDA device")
     out = _run(32, 65536, 24, 14, 0.0, "overflow", 14)
     assert out.returncode == 0 and "OVERFLOW-OK" in out.stdout, out.stdout + out.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,p,k,phi", [(90, 700, 70, 9, 2.0), (33, 4111, 20, 14, 4.0)])
+def test_dropin_split_api_bit_exact(m, n, p, k, phi):
+    """ozmm::gpu::split<ozmm::SplitMatrix> at the reference's split_bitmask /
+    split_round_nearest / split_rn_const_shift call sites (split.hpp:61-74):
+    slices, shifts or per-slice units, residual, underflow flag and metadata
+    identical, for A split by rows and B by columns."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    out = _run(m, n, p, k, phi, "split")
+    assert out.returncode == 0 and "SPLIT-OK" in out.stdout, out.stdout + out.stderr
