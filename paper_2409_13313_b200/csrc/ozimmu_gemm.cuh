@@ -114,6 +114,10 @@ struct GemmParams {
   uint8_t ag_s[kMaxAGroups];
   uint16_t ag_p0[kMaxAGroups], ag_p1[kMaxAGroups];
   int b_buf_slots;     // CTA-pair kernel: B slice tiles per B buffer (sized per launch)
+  // CTA-pair kernel: odd passes sweep the K blocks in reverse, so each pass starts on
+  // the K blocks the previous one loaded last (still in L2); the INT32 sums are
+  // order-free, so results are unchanged
+  int ksnake;
 };
 
 template <int kBN>

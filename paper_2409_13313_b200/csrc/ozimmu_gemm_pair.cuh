@@ -188,10 +188,13 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
           const int blo = P.p_blo[q], bhi = P.p_bhi[q], g0 = P.p_g0[q], g1 = P.p_g1[q];
           const uint32_t btx = 2u * (bhi - blo + 1) * Cfg::kBTile;
           const int nbw = bhi - blo + 1;
+          // K block of loop step kb (the MMA side only needs the step: integer sums)
+          const bool rev = P.ksnake && (q & 1);
           if (kPairs == 1 && P.kpair && 2 * nbw <= P.b_buf_slots && n_kb % 2 == 0) {
             // K-pair pass: one B buffer holds K blocks kb and kb+1; each A group loads
             // both of its K blocks into consecutive ring slots
             for (int kb = 0; kb < n_kb; kb += 2) {
+              const int kc = rev ? n_kb - 2 - kb : kb;  // first K block of the pair
               OZMM_TWAIT(15, ptx::mbar_wait(b_empty + bi, bph ^ 1));
               const uint32_t fb = ptx::mapa_shared(b_full + bi, lead_rank);
               if (leader) ptx::mbar_arrive_expect_tx(b_full + bi, 2u * btx);
@@ -199,7 +202,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
               for (int h = 0; h < 2; ++h)
                 for (int t = blo; t <= bhi; ++t)
                   ptx::tma_load_3d_pair_hint(dst + (h * nbw + t - blo) * Cfg::kBTile, &map_b, fb,
-                                             (kb + h) * kKB, b_row, t - 1, pol_b);
+                                             (kc + h) * kKB, b_row, t - 1, pol_b);
               if (++bi == kBBufs) {
                 bi = 0;
                 bph ^= 1;
@@ -209,7 +212,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
                   OZMM_TWAIT(14, ptx::mbar_wait(a_empty + ai, aph ^ 1));
                   const uint32_t fa = ptx::mapa_shared(a_full + ai, lead_rank);
                   if (leader) ptx::mbar_arrive_expect_tx(a_full + ai, 2u * Cfg::kATile);
-                  ptx::tma_load_3d_pair_hint(aring + ai * Cfg::kATile, &map_a, fa, (kb + h) * kKB,
+                  ptx::tma_load_3d_pair_hint(aring + ai * Cfg::kATile, &map_a, fa, (kc + h) * kKB,
                                              a_row, P.ag_s[g] - 1, pol_a);
                   if (++ai == n_a) {
                     ai = 0;
@@ -220,13 +223,14 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
             continue;
           }
           for (int kb = 0; kb < n_kb; ++kb) {
+            const int kc = rev ? n_kb - 1 - kb : kb;
             OZMM_TWAIT(15, ptx::mbar_wait(b_empty + bi, bph ^ 1));
             {
               const uint32_t fb = ptx::mapa_shared(b_full + bi, lead_rank);
               if (leader) ptx::mbar_arrive_expect_tx(b_full + bi, btx);
               uint8_t* dst = bbuf + bi * b_buf;
               for (int t = blo; t <= bhi; ++t)
-                ptx::tma_load_3d_pair_hint(dst + (t - blo) * Cfg::kBTile, &map_b, fb, kb * kKB,
+                ptx::tma_load_3d_pair_hint(dst + (t - blo) * Cfg::kBTile, &map_b, fb, kc * kKB,
                                            b_row, t - 1, pol_b);
             }
             if (++bi == kBBufs) {
@@ -238,11 +242,11 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
               const uint32_t fa = ptx::mapa_shared(a_full + ai, lead_rank);
               if (leader) ptx::mbar_arrive_expect_tx(a_full + ai, 2u * Cfg::kATile);
               if constexpr (kPairs == 1)
-                ptx::tma_load_3d_pair_hint(aring + ai * Cfg::kATile, &map_a, fa, kb * kKB, a_row,
+                ptx::tma_load_3d_pair_hint(aring + ai * Cfg::kATile, &map_a, fa, kc * kKB, a_row,
                                            P.ag_s[g] - 1, pol_a);
               else
                 ptx::tma_load_3d_pair_mc(aring + ai * Cfg::kATile + pp * Cfg::kAPart * kKB, &map_a,
-                                         a_full + ai, kb * kKB, a_row, P.ag_s[g] - 1, a_mask, pol_a);
+                                         a_full + ai, kc * kKB, a_row, P.ag_s[g] - 1, a_mask, pol_a);
               if (++ai == n_a) {
                 ai = 0;
                 aph ^= 1;

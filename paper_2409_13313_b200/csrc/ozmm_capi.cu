@@ -522,6 +522,8 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
   // timing probe: flips instruction-descriptor bits (wrong results)
   if (const char* g = OZMM_ENV("OZMM_IDESC_XOR")) P.idesc_xor = static_cast<uint32_t>(std::strtoul(g, nullptr, 0));
 #endif
+  P.ksnake = 1;
+  if (const char* g = OZMM_ENV("OZMM_KSNAKE")) P.ksnake = std::atoi(g);
   P.nbatch = static_cast<int>(S.batches.size());
   P.npass = static_cast<int>(S.passes.size());
   P.beta = beta_bits;
