@@ -1353,6 +1353,9 @@ int ozmm_split_host(ozmm_handle_t handle, char side, char trans, int64_t lines, 
   if (side != 'L' && side != 'R') return set_err(h, OZMM_ERR_ARG, "side must be 'L' or 'R'");
   if (!valid_trans(trans)) return set_err(h, OZMM_ERR_ARG, "trans must be 'N' or 'T'");
   if (lines < 1 || n < 1) return set_err(h, OZMM_ERR_ARG, "split: empty matrix");
+  // checked before the workspace is sized from them (ozmm_split_ex repeats it)
+  if (strategy < 0 || strategy > 2) return set_err(h, OZMM_ERR_ARG, "unknown split strategy");
+  if (k < 1 || k > ozb::kMaxK) return set_err(h, OZMM_ERR_ARG, "split: k must be in 1..%d", ozb::kMaxK);
   const bool row_mode = (side == 'L') != is_trans(trans);
   const int64_t rows = row_mode ? lines : n, cols = row_mode ? n : lines;  // X as stored
   if (ldx < cols) return set_err(h, OZMM_ERR_ARG, "split: leading dimension too small");

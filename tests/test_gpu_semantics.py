@@ -301,3 +301,49 @@ def test_host_entry_staging_slots_grow_with_the_operands(oz, checker):
             assert_bitwise(c, want, f"{m}x{n}x{p}")
     finally:
         h.close()
+
+
+@pytest.fixture(scope="module")
+def ref():
+    from oracle import oracle
+    if not os.path.exists(oracle.REF_SO):
+        pytest.skip("oracle/_ref not built")
+    return oracle.RefLib()
+
+
+@pytest.mark.parametrize("strategy", ["rn_const", "bitmask", "rn_per_slice"])
+@pytest.mark.parametrize("side", ["L", "R"])
+def test_split_dump_matches_reference_split(oz, ref, strategy, side):
+    """split_dump (ozmm_split_host) against the reference's split_any on the same
+    matrix: slices, shift or per-slice units and the residual, bit for bit
+    (split.cpp:182-198, dump_split :254-270), with zero, -0, power-of-two,
+    tiny (underflowing grid) and ragged-magnitude lines."""
+    rng = np.random.default_rng(11)
+    a = (rng.random((37, 301)) - 0.5) * np.exp(2.0 * rng.standard_normal((37, 301)))
+    a[3] = 0.0
+    a[4] = -0.0
+    a[5] = 2.0 ** rng.integers(-20, 20, 301)
+    a[6] *= 2.0 ** -1060
+    a[:, 7] = 0.0
+    a[:, 8] = 2.0 ** 40
+    if side == "R":
+        a = np.ascontiguousarray(a.T)
+    k = 9
+    strat = {"rn_const": oz.SliceStrategy.RoundNearestConstShift, "bitmask": oz.SliceStrategy.BitMask,
+             "rn_per_slice": oz.SliceStrategy.RoundNearestPerSlice}[strategy]
+    sl, out, res = oz.split_dump(a, k, side, strat)
+    want_sl, want_out, want_res = ref.split_any(a, k, strategy, "left" if side == "L" else "right",
+                                                residual=True)
+    np.testing.assert_array_equal(sl, want_sl)
+    assert_bitwise(out, want_out, "shift / units")
+    assert_bitwise(res, want_res, "residual")
+
+
+def test_split_dump_argument_errors(oz):
+    a = np.ones((4, 8))
+    with pytest.raises(ValueError):
+        oz.split_dump(a, 0)
+    with pytest.raises(ValueError):
+        oz.split_dump(a, 33)  # kMaxK = 32 (csrc/ozimmu_gemm.cuh)
+    with pytest.raises(OverflowError):
+        oz.split_dump(np.full((4, 8), 2.0 ** 950), 4)
