@@ -150,7 +150,7 @@ typedef struct {
                               2 = stage every buffer (tests) */
   int host_threads;        /* ozmm_dgemm_host staging team size; 0 = auto
                               (the hardware threads, at most 16; each
-                              holds two pinned slots of up to 8 MB per
+                              holds four pinned slots of up to 2 MB per
                               direction, sized by the operands) */
 } ozmm_options_t;
 

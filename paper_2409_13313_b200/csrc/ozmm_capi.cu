@@ -1781,14 +1781,15 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
       h->stage_out.release();
       h->pool.reset(new ozb::WorkerPool(nt));
     }
-    // two slots per team thread and direction: 8 MB for large operands (16 threads:
-    // 512 MB pinned in all), smaller for small ones (a power of two >= 256 KB, about a
+    // four slots per team thread and direction: 2 MB for large operands (16 threads:
+    // 256 MB pinned in all), smaller for small ones (a power of two >= 256 KB, about a
     // quarter of a thread's share of the largest staged matrix); grown when a later
-    // call is larger
+    // call is larger.  C3 pageable call, 16 threads: 2 MB x 4 146-148 ms, 4 MB x 2
+    // 143-157, 8 MB x 2 153-170, 1 MB x 8 151-152 (profiles/r2/stage_sweep4.txt)
     const size_t big = D * static_cast<size_t>(std::max({pg_a ? m * n : 0, pg_b ? n * p : 0, pg_c ? m * p : 0}));
     size_t slot = size_t(256) << 10;
-    while (slot < (size_t(8) << 20) && slot * 4 * nt < big) slot <<= 1;
-    int nslots = 2;
+    while (slot < (size_t(2) << 20) && slot * 4 * nt < big) slot <<= 1;
+    int nslots = 4;
     if (const char* e = OZMM_ENV("OZMM_STAGE_SLOT_MB")) slot = size_t(std::max(1, std::atoi(e))) << 20;
     if (const char* e = OZMM_ENV("OZMM_STAGE_SLOTS")) nslots = std::max(2, std::atoi(e));
     for (ozb::HostStager* st : {&h->stage_in, &h->stage_out}) {
