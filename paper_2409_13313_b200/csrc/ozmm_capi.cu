@@ -73,10 +73,8 @@ struct FlushCfg {
   const int32_t* lsb = nullptr;
   int64_t lsa_plane = 0, lsb_plane = 0, lsa_lstride = 1, lsb_lstride = 1;
   int64_t n = 0;
-  // tuning (same results): kpair 0 auto / 1 off / 2 on, stages 0 auto; full_mp =
-  // m*p of the whole problem when this launch is one strip of it (0: this launch)
+  // tuning (same results): kpair 0 auto (on) / 1 off / 2 on, stages 0 auto
   int kpair = 0, stages = 0;
-  int64_t full_mp = 0;
   bool biased() const { return lsa != nullptr; }
 };
 
@@ -682,12 +680,11 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
                    static_cast<long long>(r));
   // K-pair decision (the kernel re-derives it per pass from P.kpair and the B
   // buffer size): thin passes in K-block pairs (runs of 8 MMAs per accumulator):
-  // +4 % at C5 (k = 12), +1 % at C4, but -3 % at the two-batch C3 where the power
-  // cap takes the gain back (profiles/r1/kpair_ab.txt) -- on for schedules of three
-  // or more batches and for problems up to 8192 x 8192 (C2 +2 %).  The problem, not
-  // the launch: the host entry's strips of a C3 call are C3 work (fl.full_mp)
-  const int64_t full_mp = fl.full_mp ? fl.full_mp : m * p;
-  int kpair = (S.batches.size() >= 3 || full_mp <= int64_t(8192) * 8192) ? 1 : 0;
+  // +4 % at C5 (k = 12), +1 % at C4, C2 +2 %.  Round 1 measured -3 % at the
+  // two-batch C3 (profiles/r1/kpair_ab.txt) and kept it off there; after the
+  // round-2 epilogue and the K-snake pass order it is +0.4..+3.5 % at C3 (two boxes,
+  // profiles/r2/kpair_c3.txt), so it is on everywhere.
+  int kpair = 1;
   if (fl.kpair) kpair = fl.kpair == 2 ? 1 : 0;
   if (const char* g = OZMM_ENV("OZMM_KPAIR")) kpair = std::atoi(g);
   const int n_kb = static_cast<int>((std::max(lds_a, lds_b) + ozb::kKB - 1) / ozb::kKB);
@@ -1972,7 +1969,6 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
     fl.lsb_plane = p;
     fl.n = n;
   }
-  fl.full_mp = m * p;  // the strips are pieces of one m x p problem (kernel tuning)
   // this call's flags start clear (earlier unreported ones stay pending); every
   // stream starts after earlier work on the handle's stream
   fold_flags_kernel<<<1, 1, 0, user>>>(h->flags);
