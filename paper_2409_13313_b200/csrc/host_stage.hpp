@@ -57,7 +57,7 @@ inline uint64_t copy_screen(double* dst, const double* src, size_t n) {
     dst[j] = src[j];
   };
 #if defined(__SSE2__)
-  if (reinterpret_cast<uintptr_t>(dst) & 15) one(i++);
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) && n > 0) one(i++);
   __m128i va = _mm_setzero_si128();
   const __m128i ke = _mm_set1_epi64x(static_cast<long long>(kExpMask)),
                 kb = _mm_set1_epi64x(static_cast<long long>(kBigBias));
@@ -112,6 +112,26 @@ inline void copy_patch(double* c, const double* res, size_t n, double beta) {
   }
 #endif
   for (; i < n; ++i) one(i);
+}
+
+// dst <- src (n doubles) with streaming stores: the destination (the caller's C)
+// is not read back here, so its lines need not be fetched or kept in cache.
+inline void copy_stream(double* dst, const double* src, size_t n) {
+  size_t i = 0;
+#if defined(__SSE2__)
+  if (reinterpret_cast<uintptr_t>(dst) & 15) {
+    if (n == 0) return;
+    dst[0] = src[0];
+    i = 1;
+  }
+  for (; i + 4 <= n; i += 4) {
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i)));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 2),
+                     _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 2)));
+  }
+  _mm_sfence();
+#endif
+  for (; i < n; ++i) dst[i] = src[i];
 }
 
 // Fixed team of worker threads; run(n, fn) executes fn(0..n-1) on the team
@@ -313,6 +333,9 @@ class HostStager {
           if (patch_beta)
             copy_patch(reinterpret_cast<double*>(d + r * dpitch),
                        reinterpret_cast<const double*>(slot_[j] + r * k.nc), k.nc / 8, *patch_beta);
+          else if (k.nc % 8 == 0)  // streaming stores: 150-157 vs 159-180 ms with plain ones
+            copy_stream(reinterpret_cast<double*>(d + r * dpitch),
+                        reinterpret_cast<const double*>(slot_[j] + r * k.nc), k.nc / 8);
           else
             std::memcpy(d + r * dpitch, slot_[j] + r * k.nc, k.nc);
         }

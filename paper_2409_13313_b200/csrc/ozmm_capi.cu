@@ -1873,7 +1873,11 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   // element for the range error (host_stage.hpp copy_screen), so no scanner has
   // to re-read them; with C staged too, the old C entries are checked for inf /
   // NaN as the result overwrites them (copy_patch) instead of by a separate scan.
-  const bool screen_ab = no_c && pg_a && pg_b, patch_c = no_c && pg_c;
+  // staged C of a beta = 0 call: the non-finite-C patch rides on the copy-out (C
+  // scanned up front by scanner threads instead: 150-160 vs 146-151 ms at C3,
+  // profiles/r2/cscan_rejected.txt)
+  const bool patch_c = no_c && pg_c;
+  const bool screen_ab = no_c && pg_a && pg_b;
   std::atomic<uint64_t> big_ab{0};
   auto h2d = [&](bool pg, void* dst, size_t dp, const void* src, size_t sp, size_t w, size_t rows,
                  const char* what, bool screen = false) {

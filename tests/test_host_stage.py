@@ -1,5 +1,6 @@
 """The host entry's copy team (csrc/host_stage.hpp WorkerPool), CPU only: many
-back-to-back jobs, every index exactly once on its own job's function."""
+back-to-back jobs, every index exactly once on its own job's function; and the
+staging copy loops (copy_screen / copy_patch / copy_stream) against scalar loops."""
 import os
 import shutil
 import subprocess
@@ -19,4 +20,4 @@ def test_worker_pool_stress(tmp_path):
                          capture_output=True, text=True)
     assert res.returncode == 0, res.stderr
     out = subprocess.run([str(exe), "20000"], capture_output=True, text=True, timeout=300)
-    assert out.returncode == 0 and "POOL-OK" in out.stdout, out.stdout + out.stderr
+    assert out.returncode == 0 and "POOL-OK" in out.stdout and "COPY-OK" in out.stdout, out.stdout + out.stderr
