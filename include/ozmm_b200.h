@@ -207,16 +207,29 @@ int ozmm_dgemm_ex(ozmm_handle_t h, char transa, char transb, int64_t m, int64_t 
                   double beta, double* C, int64_t ldc, int k, const ozmm_options_t* opt,
                   ozmm_counts_t* counts, ozmm_timings_t* timings);
 
-/* Host-pointer variant (what the reference API takes): copies A, B, C to the
- * device, runs ozmm_dgemm_ex, copies C back.  Synchronous.  Range errors are
- * returned directly (sync_check is implied) and leave C untouched.  Host
- * buffers may be pinned or pageable: pageable ones are registered with the
- * driver for the duration of the call (cudaHostRegister) when that succeeds,
- * and copied through the driver's staging otherwise. */
+/* Host-pointer variant (what the reference API takes, scheme.hpp:96-98): A, B
+ * (and C when beta != 0) stream to the device in panels while the GPU splits
+ * and multiplies, finished strips of the result stream back; C is overwritten
+ * in place.  Synchronous.  Range errors are returned directly (sync_check is
+ * implied) and leave C untouched.  Host buffers may be pinned (copied by the
+ * DMA engines) or pageable (staged through pinned slots by a team of host
+ * threads: ozmm_options_t.host_staging / host_threads). */
 int ozmm_dgemm_host(ozmm_handle_t h, char transa, char transb, int64_t m, int64_t n, int64_t p,
                     double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
                     double beta, double* C, int64_t ldc, int k, const ozmm_options_t* opt,
                     ozmm_counts_t* counts, ozmm_timings_t* timings);
+
+/* The same with a separate result D (m x p, row stride ldd): C is only read, as
+ * the reference's ozaki_gemm_ex returns a NEW matrix and leaves C const
+ * (scheme.cpp:281, :289) -- the C++ / Python drop-ins use it instead of copying
+ * C first.  D may equal C (then it is ozmm_dgemm_host) but may not otherwise
+ * overlap it (OZMM_ERR_ARG).  On any error D's contents are unspecified and C
+ * is untouched. */
+int ozmm_dgemm_host_out(ozmm_handle_t h, char transa, char transb, int64_t m, int64_t n,
+                        int64_t p, double alpha, const double* A, int64_t lda, const double* B,
+                        int64_t ldb, double beta, const double* C, int64_t ldc, double* D,
+                        int64_t ldd, int k, const ozmm_options_t* opt, ozmm_counts_t* counts,
+                        ozmm_timings_t* timings);
 
 /* ---- the two halves, for sharded (multi-GPU) callers and parity tests ---- */
 /* Row stride of a slice plane for inner dimension n: round_up(n, 16). */

@@ -142,8 +142,7 @@ OzakiResultT<Mat> ozaki_gemm_ex(double alpha, const Mat& a, const Mat& b, double
     throw std::invalid_argument("ozaki_gemm: C shape mismatch");
   if (cfg.k < 1) throw ConfigError("k must be >= 1");
   const std::int64_t m = a.rows(), n = a.cols(), p = b.cols();
-  Mat out(c.rows(), c.cols());
-  std::copy(c.data(), c.data() + m * p, out.data());
+  Mat out(c.rows(), c.cols());  // the new result matrix: C is only read (scheme.cpp:281, :289)
   ozmm_options_t opt{};
   opt.method = cfg.method;
   opt.overflow_wrap = cfg.overflow_wrap;
@@ -153,8 +152,8 @@ OzakiResultT<Mat> ozaki_gemm_ex(double alpha, const Mat& a, const Mat& b, double
   ozmm_counts_t cnt{};
   ozmm_timings_t tim{};
   ozmm_handle_t h = thread_handle();
-  throw_status(ozmm_dgemm_host(h, 'N', 'N', m, n, p, alpha, a.data(), n, b.data(), p, beta,
-                               out.data(), p, cfg.k, &opt, &cnt, &tim),
+  throw_status(ozmm_dgemm_host_out(h, 'N', 'N', m, n, p, alpha, a.data(), n, b.data(), p, beta,
+                                   c.data(), p, out.data(), p, cfg.k, &opt, &cnt, &tim),
                h);
   OzakiResultT<Mat> res{std::move(out), {}, {}};
   res.counts = {cnt.int8_gemms, cnt.fp64_flushes, cnt.r, cnt.w};

@@ -77,20 +77,21 @@ inline uint64_t copy_screen(double* dst, const double* src, size_t n) {
   return acc;
 }
 
-// C <- result (n doubles), where the device wrote fl(alpha d) for beta = 0 and
-// C was never uploaded: an old C entry that is inf / NaN still enters the
-// reference's fl(fl(alpha d) + fl(beta c)) (scheme.cpp:287), so it is applied
-// here, reading each old entry just before it is overwritten.
-inline void copy_patch(double* c, const double* res, size_t n, double beta) {
+// dst <- result (n doubles), where the device wrote fl(alpha d) for beta = 0 and
+// C was never uploaded: an old C entry (cin, the caller's C -- dst itself for an
+// in-place call) that is inf / NaN still enters the reference's
+// fl(fl(alpha d) + fl(beta c)) (scheme.cpp:287), so it is applied here, each old
+// entry read before its position of dst is written.
+inline void copy_patch(double* dst, const double* res, const double* cin, size_t n, double beta) {
   auto one = [&](size_t i) {
     double v = res[i];
     uint64_t b;
-    std::memcpy(&b, c + i, 8);
+    std::memcpy(&b, cin + i, 8);
     if ((b & kExpMask) == kExpMask) {
-      const double z = beta * c[i];
+      const double z = beta * cin[i];
       v = v + z;
     }
-    c[i] = v;
+    dst[i] = v;
   };
   size_t i = 0;
 #if defined(__SSE2__)
@@ -98,16 +99,16 @@ inline void copy_patch(double* c, const double* res, size_t n, double beta) {
   // movemask); a group with an inf / NaN entry takes the scalar path
   const __m128i ke = _mm_set1_epi32(0x7FF00000);
   for (; i + 4 <= n; i += 4) {
-    const __m128i c0 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(c + i));
-    const __m128i c1 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(c + i + 2));
+    const __m128i c0 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(cin + i));
+    const __m128i c1 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(cin + i + 2));
     const __m128i e0 = _mm_cmpeq_epi32(_mm_and_si128(c0, ke), ke);
     const __m128i e1 = _mm_cmpeq_epi32(_mm_and_si128(c1, ke), ke);
     if ((_mm_movemask_epi8(_mm_or_si128(e0, e1)) & 0xF0F0) != 0) {
       for (size_t j = i; j < i + 4; ++j) one(j);
       continue;
     }
-    _mm_storeu_si128(reinterpret_cast<__m128i*>(c + i), _mm_loadu_si128(reinterpret_cast<const __m128i*>(res + i)));
-    _mm_storeu_si128(reinterpret_cast<__m128i*>(c + i + 2),
+    _mm_storeu_si128(reinterpret_cast<__m128i*>(dst + i), _mm_loadu_si128(reinterpret_cast<const __m128i*>(res + i)));
+    _mm_storeu_si128(reinterpret_cast<__m128i*>(dst + i + 2),
                      _mm_loadu_si128(reinterpret_cast<const __m128i*>(res + i + 2)));
   }
 #endif
@@ -303,9 +304,12 @@ class HostStager {
   // dst (pageable host, dpitch) <- src (device, spitch), after the work already
   // enqueued on s.  Returns when every byte has landed in dst.
   // patch_beta != nullptr (double elements, C of a beta = 0 call that was not
-  // uploaded): copy_patch instead of a plain copy.
+  // uploaded): copy_patch against the caller's C at cin (cpitch; dst itself for an
+  // in-place call) instead of a plain copy.
   cudaError_t d2h(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
-                  cudaStream_t s, const double* patch_beta = nullptr) {
+                  cudaStream_t s, const double* patch_beta = nullptr, const void* cin = nullptr,
+                  size_t cpitch = 0) {
+    if (cin == nullptr) cin = dst, cpitch = dpitch;
     const std::vector<Blk> blks = blocks(width, height);
     const int nt = std::min<int>(pool_->size(), static_cast<int>(blks.size()));
     std::atomic<int> err{0};
@@ -329,10 +333,12 @@ class HostStager {
         if (e != cudaSuccess) break;
         const Blk& k = blks[mine[i]];
         uint8_t* d = static_cast<uint8_t*>(dst) + k.r0 * dpitch + k.c0;
+        const uint8_t* ci = static_cast<const uint8_t*>(cin) + k.r0 * cpitch + k.c0;
         for (size_t r = 0; r < k.nr; ++r) {
           if (patch_beta)
             copy_patch(reinterpret_cast<double*>(d + r * dpitch),
-                       reinterpret_cast<const double*>(slot_[j] + r * k.nc), k.nc / 8, *patch_beta);
+                       reinterpret_cast<const double*>(slot_[j] + r * k.nc),
+                       reinterpret_cast<const double*>(ci + r * cpitch), k.nc / 8, *patch_beta);
           else if (k.nc % 8 == 0)  // streaming stores: 150-157 vs 159-180 ms with plain ones
             copy_stream(reinterpret_cast<double*>(d + r * dpitch),
                         reinterpret_cast<const double*>(slot_[j] + r * k.nc), k.nc / 8);

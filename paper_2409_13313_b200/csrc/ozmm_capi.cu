@@ -1448,6 +1448,11 @@ int gemm_slices_checked(Handle* h, int64_t m, int64_t n, int64_t p, int k, int b
   return launch_gemm(h, m, n, p, k, beta_bits, r, As, lds_a, plane_a, mu, Bs, lds_b, plane_b, nu,
                      alpha, beta, write_only ? nullptr : C, C, ldc, opt, fl);
 }
+// the pipelined host entry behind ozmm_dgemm_host / ozmm_dgemm_host_out
+int dgemm_host_impl(Handle* h, char transa, char transb, int64_t m, int64_t n, int64_t p, double alpha,
+                    const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                    const double* C, int64_t ldc, double* Cout, int64_t ldo, int k,
+                    const ozmm_options_t* opt, ozmm_counts_t* counts, ozmm_timings_t* timings);
 }  // namespace
 
 extern "C" {
@@ -1629,11 +1634,12 @@ int ozmm_dgemm(ozmm_handle_t h, char transa, char transb, int64_t m, int64_t n, 
 // (only ozIMMU_H, the hot path, gets the pipelined host entry below).
 int dgemm_host_simple(Handle* h, char transa, char transb, int64_t m, int64_t n, int64_t p,
                       double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
-                      double beta, double* C, int64_t ldc, int k, const ozmm_options_t* opt,
-                      ozmm_counts_t* counts, ozmm_timings_t* timings) {
+                      double beta, const double* C, int64_t ldc, double* Cout, int64_t ldo, int k,
+                      const ozmm_options_t* opt, ozmm_counts_t* counts, ozmm_timings_t* timings) {
   const bool ta = is_trans(transa), tb = is_trans(transb);
   const int64_t arows = ta ? n : m, brows = tb ? p : n, acols = ta ? m : n, bcols = tb ? n : p;
-  if (lda < acols || ldb < bcols || ldc < p) return set_err(h, OZMM_ERR_ARG, "leading dimension too small");
+  if (lda < acols || ldb < bcols || ldc < p || ldo < p)
+    return set_err(h, OZMM_ERR_ARG, "leading dimension too small");
   CUDA_TRY(h, cudaSetDevice(h->device));
   if (int rc = ensure(h, &h->host_a, &h->host_a_n, static_cast<size_t>(arows) * acols)) return rc;
   if (int rc = ensure(h, &h->host_b, &h->host_b_n, static_cast<size_t>(brows) * bcols)) return rc;
@@ -1651,7 +1657,7 @@ int dgemm_host_simple(Handle* h, char transa, char transb, int64_t m, int64_t n,
                              h->host_a, acols, h->host_b, bcols, beta, h->host_c, p, k, &o,
                              counts, timings))
     return rc;
-  CUDA_TRY(h, cudaMemcpy2DAsync(C, D * ldc, h->host_c, D * p, D * p, m, cudaMemcpyDeviceToHost,
+  CUDA_TRY(h, cudaMemcpy2DAsync(Cout, D * ldo, h->host_c, D * p, D * p, m, cudaMemcpyDeviceToHost,
                                 h->stream));
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   return OZMM_OK;
@@ -1661,6 +1667,42 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
                     int64_t p, double alpha, const double* A, int64_t lda, const double* B,
                     int64_t ldb, double beta, double* C, int64_t ldc, int k,
                     const ozmm_options_t* opt, ozmm_counts_t* counts, ozmm_timings_t* timings) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return set_err(nullptr, OZMM_ERR_ARG, "null handle");
+  return dgemm_host_impl(h, transa, transb, m, n, p, alpha, A, lda, B, ldb, beta, C, ldc, C, ldc, k, opt,
+                         counts, timings);
+}
+
+int ozmm_dgemm_host_out(ozmm_handle_t handle, char transa, char transb, int64_t m, int64_t n,
+                        int64_t p, double alpha, const double* A, int64_t lda, const double* B,
+                        int64_t ldb, double beta, const double* C, int64_t ldc, double* D,
+                        int64_t ldd, int k, const ozmm_options_t* opt, ozmm_counts_t* counts,
+                        ozmm_timings_t* timings) {
+  // The reference's ozaki_gemm_ex leaves C alone and returns a new matrix
+  // (scheme.cpp:281, :289): with a separate destination no copy of C is needed.
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return set_err(nullptr, OZMM_ERR_ARG, "null handle");
+  if (!C || !D) return set_err(h, OZMM_ERR_ARG, "null pointer");
+  if (D != C) {
+    // the destination may not overlap C (or A / B): the result is written while C is still read
+    const char* c0 = reinterpret_cast<const char*>(C);
+    const char* c1 = reinterpret_cast<const char*>(C + (m - 1) * ldc + p);
+    const char* d0 = reinterpret_cast<const char*>(D);
+    const char* d1 = reinterpret_cast<const char*>(D + (m - 1) * ldd + p);
+    if (m >= 1 && p >= 1 && d0 < c1 && c0 < d1) return set_err(h, OZMM_ERR_ARG, "D overlaps C (pass D == C for in place)");
+  }
+  return dgemm_host_impl(h, transa, transb, m, n, p, alpha, A, lda, B, ldb, beta, C, ldc, D, ldd, k, opt,
+                         counts, timings);
+}
+
+}  // extern "C"
+
+namespace {
+int dgemm_host_impl(Handle* h, char transa, char transb, int64_t m, int64_t n, int64_t p, double alpha,
+                    const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                    const double* C, int64_t ldc, double* Cout, int64_t ldo, int k,
+                    const ozmm_options_t* opt, ozmm_counts_t* counts, ozmm_timings_t* timings) {
+
   // Pipelined host entry (the reference's calling convention: host matrices in,
   // C overwritten).  op(A) is cut into row panels A_s and op(B) into column
   // panels B_s (about 16 of each), sent over PCIe in the order A_0 B_0 A_1 B_1
@@ -1685,8 +1727,10 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   // on the device the original is copied back on error; in the no-C mode the
   // D2H copies are not issued until the last split has run and the flags are
   // clear, so C is never written on error.
-  Handle* h = reinterpret_cast<Handle*>(handle);
-  if (!h) return set_err(nullptr, OZMM_ERR_ARG, "null handle");
+  //
+  // Output.  The result goes to Cout (ldo): C itself for ozmm_dgemm_host, a
+  // separate matrix for ozmm_dgemm_host_out, which then never writes C.
+  ozmm_handle_t handle = reinterpret_cast<ozmm_handle_t>(h);
   if (!valid_trans(transa) || !valid_trans(transb))
     return set_err(h, OZMM_ERR_ARG, "trans must be 'N' or 'T'");
   if (k < 1) return set_err(h, OZMM_ERR_CONFIG, "k must be >= 1");
@@ -1697,11 +1741,12 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   // (forced beta / r), take the plain copy-in / ozmm_dgemm_ex / copy-out route
   if ((opt && opt->method != OZMM_METHOD_OZIMMU_H) ||
       (opt && !opt->overflow_wrap && (opt->force_beta || opt->force_r)))
-    return dgemm_host_simple(h, transa, transb, m, n, p, alpha, A, lda, B, ldb, beta, C, ldc, k,
+    return dgemm_host_simple(h, transa, transb, m, n, p, alpha, A, lda, B, ldb, beta, C, ldc, Cout, ldo, k,
                              opt, counts, timings);
   const bool ta = is_trans(transa), tb = is_trans(transb);
   const int64_t acols = ta ? m : n, bcols = tb ? n : p;
-  if (lda < acols || ldb < bcols || ldc < p) return set_err(h, OZMM_ERR_ARG, "leading dimension too small");
+  if (lda < acols || ldb < bcols || ldc < p || ldo < p)
+    return set_err(h, OZMM_ERR_ARG, "leading dimension too small");
   if (opt && (opt->col_split < 0 || opt->col_split > 2)) return set_err(h, OZMM_ERR_ARG, "options: col_split must be 0..2");
   // host entry: the one-pass column split by default -- the panel splits run under the
   // PCIe transfers, so the kernel's extra time is hidden and B crosses HBM once
@@ -1765,8 +1810,9 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   if (hs_mode < 0 || hs_mode > 2 || (opt && opt->host_threads < 0))
     return set_err(h, OZMM_ERR_ARG, "options: host_staging must be 0..2 and host_threads >= 0");
   auto staged = [&](const void* ptr) { return hs_mode == 2 || (hs_mode == 0 && ozb::host_pageable(ptr)); };
-  const bool pg_a = staged(A), pg_b = staged(B), pg_c = staged(C);
-  if (pg_a || pg_b || pg_c) {
+  // pg_c: the result's destination; pg_ci: C when it is uploaded (beta != 0)
+  const bool pg_a = staged(A), pg_b = staged(B), pg_c = staged(Cout), pg_ci = Cout == C ? pg_c : staged(C);
+  if (pg_a || pg_b || pg_c || pg_ci) {
     // default team: every hardware thread, at most 16 (16-core box, C3 call: 8 threads
     // 157-162 ms, 12 155-159 ms, 16 147-150 ms; profiles/r2/stage_sweep3.txt)
     int nt = opt && opt->host_threads
@@ -1783,7 +1829,7 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
     // quarter of a thread's share of the largest staged matrix); grown when a later
     // call is larger.  C3 pageable call, 16 threads: 2 MB x 4 146-148 ms, 4 MB x 2
     // 143-157, 8 MB x 2 153-170, 1 MB x 8 151-152 (profiles/r2/stage_sweep4.txt)
-    const size_t big = D * static_cast<size_t>(std::max({pg_a ? m * n : 0, pg_b ? n * p : 0, pg_c ? m * p : 0}));
+    const size_t big = D * static_cast<size_t>(std::max({pg_a ? m * n : 0, pg_b ? n * p : 0, pg_c || pg_ci ? m * p : 0}));
     size_t slot = size_t(256) << 10;
     while (slot < (size_t(2) << 20) && slot * 4 * nt < big) slot <<= 1;
     int nslots = 4;
@@ -1884,8 +1930,10 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
     return cu(pg ? h->stage_in.h2d(dst, dp, src, sp, w, rows, h->s_in, screen ? &big_ab : nullptr)
                  : cudaMemcpy2DAsync(dst, dp, src, sp, w, rows, cudaMemcpyHostToDevice, h->s_in), what);
   };
-  auto d2h = [&](void* dst, size_t dp, const void* src, size_t sp, size_t w, size_t rows, const char* what) {
-    return cu(pg_c ? h->stage_out.d2h(dst, dp, src, sp, w, rows, h->s_out, patch_c ? &beta : nullptr)
+  // cin / cp: the caller's C at the same block (read by the fused non-finite-C patch)
+  auto d2h = [&](void* dst, size_t dp, const void* src, size_t sp, size_t w, size_t rows, const void* cin,
+                 size_t cp, const char* what) {
+    return cu(pg_c ? h->stage_out.d2h(dst, dp, src, sp, w, rows, h->s_out, patch_c ? &beta : nullptr, cin, cp)
                    : cudaMemcpy2DAsync(dst, dp, src, sp, w, rows, cudaMemcpyDeviceToHost, h->s_out), what);
   };
 
@@ -1944,7 +1992,7 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
           if (any >> 63)
             for (int64_t j = 0; j < p; ++j)
               if ((row[j] & 0x7FF0000000000000ull) == 0x7FF0000000000000ull)
-                bad[t].push_back({i * ldc + j, C[i * ldc + j]});
+                bad[t].push_back({i * ldo + j, C[i * ldc + j]});  // (index into Cout, old c)
         }
         if (!patch_c) --c_scans_left;
         if (screen_ab) return;  // the staging copies screen A and B
@@ -1989,7 +2037,7 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   // else is asynchronous.
   auto copy_c = [&](int q) {
     const Strip& t = strips[q];
-    h2d(pg_c, dC + t.r0 * p + t.c0, D * p, C + t.r0 * ldc + t.c0, D * ldc, D * t.cols, t.rows, "H2D C");
+    h2d(pg_ci, dC + t.r0 * p + t.c0, D * p, C + t.r0 * ldc + t.c0, D * ldc, D * t.cols, t.rows, "H2D C");
     cu(cudaEventRecord(evC[q], h->s_in), "event");
   };
   for (size_t o = 0; o < order.size() && rc == OZMM_OK; ++o) {
@@ -2053,7 +2101,8 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   auto copy_out = [&](int q) {
     const Strip& t = strips[q];
     cu(cudaStreamWaitEvent(h->s_out, evG[q], 0), "wait");
-    d2h(C + t.r0 * ldc + t.c0, D * ldc, dO + t.r0 * p + t.c0, D * p, D * t.cols, t.rows, "D2H C");
+    d2h(Cout + t.r0 * ldo + t.c0, D * ldo, dO + t.r0 * p + t.c0, D * p, D * t.cols, t.rows,
+        C + t.r0 * ldc + t.c0, D * ldc, "D2H C");
     if (trace) cu(cudaEventRecord(evO[q], h->s_out), "event");
   };
   bool range_err = false;
@@ -2118,7 +2167,7 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
         }
         if (area == R * Cc) {
           for (int q = 0; q < qd; ++q) cu(cudaStreamWaitEvent(h->s_out, evG[q], 0), "wait");
-          d2h(C, D * ldc, dO, D * p, D * Cc, R, "D2H C");
+          d2h(Cout, D * ldo, dO, D * p, D * Cc, R, C, D * ldc, "D2H C");
           if (trace)
             for (int q = 0; q < qd; ++q) cu(cudaEventRecord(evO[q], h->s_out), "event");
           q0 = qd;
@@ -2145,9 +2194,9 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   if (rc == OZMM_OK && !no_c) {
     int f[2] = {0, 0};
     cu(cudaMemcpy(f, h->flags, sizeof f, cudaMemcpyDeviceToHost), "flags");
-    if (f[1]) {  // restore the caller's C, then report like the reference's throw
+    if (f[1]) {  // restore the caller's C (in place), then report like the reference's throw
       range_err = true;
-      cu(cudaMemcpy2D(C, D * ldc, dC, D * p, D * p, m, cudaMemcpyDeviceToHost), "restore C");
+      if (Cout == C) cu(cudaMemcpy2D(Cout, D * ldo, dC, D * p, D * p, m, cudaMemcpyDeviceToHost), "restore C");
     }
   }
   if (range_err) {
@@ -2161,7 +2210,7 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
     for (const auto& v : bad)
       for (const auto& [idx, c] : v) {
         const double z = beta * c;
-        C[idx] = C[idx] + z;
+        Cout[idx] = Cout[idx] + z;
       }
   }
   if (trace && rc == OZMM_OK) {
@@ -2192,4 +2241,4 @@ int ozmm_dgemm_host(ozmm_handle_t handle, char transa, char transb, int64_t m, i
   return rc;
 }
 
-}  // extern "C"
+}  // namespace

@@ -98,6 +98,9 @@ _SIG = {
     "ozmm_dgemm_host": ([_vp, C.c_char, C.c_char, _i64, _i64, _i64, C.c_double, _vp, _i64, _vp,
                          _i64, C.c_double, _vp, _i64, C.c_int, C.POINTER(Options),
                          C.POINTER(Counts), C.POINTER(Timings)], C.c_int),
+    "ozmm_dgemm_host_out": ([_vp, C.c_char, C.c_char, _i64, _i64, _i64, C.c_double, _vp, _i64,
+                             _vp, _i64, C.c_double, _vp, _i64, _vp, _i64, C.c_int,
+                             C.POINTER(Options), C.POINTER(Counts), C.POINTER(Timings)], C.c_int),
     "ozmm_slice_ld": ([_i64], _i64),
     "ozmm_split": ([_vp, C.c_char, C.c_char, _i64, _i64, _vp, _i64, C.c_int, C.c_int, _vp, _i64,
                     _vp], C.c_int),
@@ -490,18 +493,22 @@ def ozaki_gemm_ex(alpha: float, a, b, beta: float, c, cfg: SchemeConfig | None =
     if c.shape != (m, p):
         raise ValueError("ozaki_gemm: C shape mismatch")
     h = handle or default_handle(0)
-    # in place only when ``out`` is C itself; otherwise ``out`` is filled after success
+    # in place only when ``out`` is C itself; otherwise the result goes to a new
+    # array (ozmm_dgemm_host_out reads C and writes the result: no copy of C, as
+    # the reference returns a new matrix) and a distinct ``out`` is filled after
+    # success
     inplace = (out is not None and out.flags.c_contiguous and out.shape == c.shape
                and out.ctypes.data == c.ctypes.data)
-    res = out if inplace else c.copy()
+    res = out if inplace else np.empty((m, p), np.float64)
     opt = _options(cfg, timings, None, tile_n, sync_check=True, signed_slices=signed_slices,
                    kpair=kpair, stages=stages, host_panels=host_panels, cta_pair=cta_pair,
                    host_staging=host_staging, col_split=col_split)
     h.set_stream(None)
-    h.check(lib.ozmm_dgemm_host(h.h, b"T" if transa else b"N", b"T" if transb else b"N", m, n,
-                                p, alpha, a.ctypes.data, a.shape[1], b.ctypes.data, b.shape[1],
-                                beta, res.ctypes.data, p, cfg.k, C.byref(opt), C.byref(counts),
-                                C.byref(tim) if timings else None))
+    h.check(lib.ozmm_dgemm_host_out(h.h, b"T" if transa else b"N", b"T" if transb else b"N", m,
+                                    n, p, alpha, a.ctypes.data, a.shape[1], b.ctypes.data,
+                                    b.shape[1], beta, c.ctypes.data, p, res.ctypes.data, p, cfg.k,
+                                    C.byref(opt), C.byref(counts),
+                                    C.byref(tim) if timings else None))
     if out is not None and res is not out:
         np.copyto(out, res)
         res = out

@@ -46,13 +46,22 @@ static int check_copies() {
         const double co = c[off + i];
         want[i] = std::isfinite(co) ? src[i] : src[i] + 0.5 * co;
       }
-      ozb::copy_patch(c.data() + off, src.data(), n, 0.5);
+      // separate destination first (c is the old C), then in place
+      std::fill(dst.begin(), dst.end(), -7.0);
+      ozb::copy_patch(dst.data() + off, src.data(), c.data() + off, n, 0.5);
+      ozb::copy_patch(c.data() + off, src.data(), c.data() + off, n, 0.5);
       for (size_t i = 0; i < n; ++i) {
-        const bool ok = std::isnan(want[i]) ? std::isnan(c[off + i]) : std::memcmp(&want[i], &c[off + i], 8) == 0;
-        if (!ok) {
-          std::printf("FAIL copy_patch off=%zu n=%zu i=%zu\n", off, n, i);
-          return 1;
+        for (const double* got : {dst.data() + off, c.data() + off}) {
+          const bool ok = std::isnan(want[i]) ? std::isnan(got[i]) : std::memcmp(&want[i], &got[i], 8) == 0;
+          if (!ok) {
+            std::printf("FAIL copy_patch off=%zu n=%zu i=%zu\n", off, n, i);
+            return 1;
+          }
         }
+      }
+      if (dst[off + n] != -7.0) {
+        std::printf("FAIL copy_patch wrote past n (off=%zu n=%zu)\n", off, n);
+        return 1;
       }
     }
   }

@@ -347,3 +347,74 @@ def test_split_dump_argument_errors(oz):
         oz.split_dump(a, 33)  # kMaxK = 32 (csrc/ozimmu_gemm.cuh)
     with pytest.raises(OverflowError):
         oz.split_dump(np.full((4, 8), 2.0 ** 950), 4)
+
+
+def _host_out_call(oz, ta, tb, m, n, p, alpha, A, B, beta, C, D, k, **opt_kw):
+    """ozmm_dgemm_host_out: C read-only, the result in D (ldd from D's row stride)."""
+    h = oz.default_handle(0)
+    h.set_stream(None)
+    opt = oz.Options()
+    for key, v in opt_kw.items():
+        setattr(opt, key, v)
+    return oz.lib.ozmm_dgemm_host_out(h.h, b"T" if ta else b"N", b"T" if tb else b"N", m, n, p,
+                                      alpha, A.ctypes.data, A.strides[0] // 8, B.ctypes.data,
+                                      B.strides[0] // 8, beta, C.ctypes.data, C.strides[0] // 8,
+                                      D.ctypes.data, D.strides[0] // 8, k, ctypes.byref(opt),
+                                      None, None)
+
+
+@pytest.mark.parametrize("staging", [0, 1, 2])
+@pytest.mark.parametrize("pinned_out", [False, True])
+@pytest.mark.parametrize("case", [
+    # (transa, transb, m, n, p, alpha, beta, method)
+    (False, False, 700, 1100, 530, 1.0, 0.0, 0),   # beta = 0: C not uploaded, patch from C
+    (True, False, 512, 900, 384, 1.5, 0.5, 0),     # beta != 0: C uploaded
+    (False, True, 333, 640, 257, -2.0, 0.0, 0),    # alpha < 0: C uploaded
+    (False, False, 300, 700, 260, 1.0, 0.25, 1),   # ozIMMU: the copy-in / copy-out route
+])
+def test_host_out_entry_matches_in_place(oz, checker, staging, pinned_out, case):
+    """ozmm_dgemm_host_out (the reference's new-matrix semantics, scheme.cpp:281,
+    :289): the result equals the in-place ozmm_dgemm_host bit for bit, C is not
+    written (not even its padding), and D's padding columns stay untouched."""
+    ta, tb, m, n, p, alpha, beta, method = case
+    k = 8
+    A0, B0, C0 = inputs(oz, m, n, p, 81, phi=1.0)
+    C0[3, 5], C0[m - 1, p - 2], C0[m // 2, 0] = np.inf, np.nan, -np.inf
+    sa = np.ascontiguousarray(A0.T) if ta else A0
+    sb = np.ascontiguousarray(B0.T) if tb else B0
+    cfg_kw = dict(host_staging=staging, host_panels=3, sync_check=1, method=method)
+    Cin = np.full((m, p + 3), -5.0)
+    Cin[:, :p] = C0
+    want = Cin.copy()
+    assert _host_call(oz, ta, tb, m, n, p, alpha, sa, sb, beta, want[:, :p], k, **cfg_kw) == 0
+    keep = []
+    if pinned_out:
+        D, t = _pinned_like(np.full((m, p + 2), 7.0))
+        keep.append(t)
+    else:
+        D = np.full((m, p + 2), 7.0)
+    before = Cin.copy()
+    rc = _host_out_call(oz, ta, tb, m, n, p, alpha, sa, sb, beta, Cin[:, :p], D[:, :p], k, **cfg_kw)
+    assert rc == oz.OZMM_OK, oz.lib.ozmm_last_error(oz.default_handle(0).h)
+    assert_bitwise(D[:, :p], want[:, :p], f"staging={staging} pinned_out={pinned_out}")
+    assert (D[:, p:] == 7.0).all(), "padding columns of D were written"
+    assert before.tobytes() == Cin.tobytes(), "C was written"
+
+
+def test_host_out_entry_errors(oz):
+    """Overlapping D and C is refused; a range error leaves C untouched."""
+    m, n, p, k = 256, 512, 128, 8
+    A, B, C = inputs(oz, m, n, p, 91)
+    big = np.zeros((m, p + 8))
+    rc = _host_out_call(oz, False, False, m, n, p, 1.0, A, B, 0.5, big[:, :p], big[:, 8:], k)
+    assert rc == oz.OZMM_ERR_ARG
+    A2 = A.copy()
+    A2[7, 3] = 2.0 ** 950
+    D = np.zeros((m, p))
+    before = C.copy()
+    rc = _host_out_call(oz, False, False, m, n, p, 1.0, A2, B, 0.0, C, D, k)
+    assert rc == oz.OZMM_ERR_RANGE
+    assert before.tobytes() == C.tobytes()
+    # the same handle is clean afterwards
+    rc = _host_out_call(oz, False, False, m, n, p, 1.0, A, B, 0.0, C, D, k)
+    assert rc == oz.OZMM_OK
