@@ -46,6 +46,11 @@ constexpr int kMaxChunks = 528;    // >= k(k+1)/2 for k <= kMaxK (r = 1)
 constexpr int kMaxProducts = 528;  // k(k+1)/2 for k <= kMaxK
 constexpr int kMaxBatches = 192;
 constexpr int kMaxPasses = 384;
+// CTA-pair epilogue actions (schedule.hpp FlushAct): flush accumulator, park
+// accumulator, flush a parked chunk; at most 2 per chunk, at most kMaxPark slots
+constexpr int kActFlush = 0, kActPark = 1, kActUnpark = 2;
+constexpr int kMaxActs = 2 * kMaxChunks;
+constexpr int kMaxPark = 16;
 constexpr int kMaxAGroups = 528;
 constexpr int kGemmThreads = 320;
 constexpr int kEpiWarps = 8;
@@ -118,6 +123,15 @@ struct GemmParams {
   // the K blocks the previous one loaded last (still in L2); the INT32 sums are
   // order-free, so results are unchanged
   int ksnake;
+  // CTA-pair kernel: per batch its chunk ids (accumulator ci holds b_cid[b * 4 + ci])
+  // and its epilogue actions act[b_act0[b] .. b_act1[b]) (schedule.hpp FlushAct:
+  // chunk id | kind << 10 | accumulator << 12 | park slot << 16); park: per-SM
+  // scratch of park_slots INT32 128 x 128 tiles per CTA, or null when nothing is parked
+  uint16_t b_cid[kMaxBatches * 4];
+  uint16_t b_act0[kMaxBatches], b_act1[kMaxBatches];
+  uint32_t act[kMaxActs];
+  int32_t* park;
+  int park_slots;
 };
 
 template <int kBN>

@@ -476,14 +476,26 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
           asm volatile("prefetch.global.L2 [%0];" ::"l"(P.c_in + static_cast<int64_t>(r) * P.ldc + c));
       }
     }
+    // parked chunks (schedule.hpp FlushAct): this CTA's scratch, one SM per CTA
+    // (the host enables parking only when the shared memory admits one CTA per SM);
+    // layout [slot][column/4][row] of uint4, so a warp's 32 rows are contiguous
+    uint4* park = nullptr;
+    if (P.park != nullptr) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      if (smid >= 256u) __trap();  // the host sizes the scratch for 256 SM ids (kParkSmIds)
+      park = reinterpret_cast<uint4*>(P.park) + static_cast<int64_t>(smid) * P.park_slots * (kBM * kBN / 4);
+    }
+    const int prow = quarter * 32 + lane;  // this thread's row of the CTA's tile
     for (int b = 0; b < P.nbatch; ++b) {
-      const int c0 = P.b_c0[b], nc = P.b_nc[b];
+      const int nc = P.b_nc[b];
+      const uint16_t* cid = P.b_cid + b * Cfg::kNAcc;
       if (P.bias) {
         // per-column part of the batch's offset corrections, while its MMAs run:
         // ccol[ci][j] = sum_{(s,t) in chunk} o_s lsb[t][col] + o_s o_t n
         asm volatile("bar.sync 1, %0;" ::"r"(kPairEpiWarps * 32) : "memory");  // previous batch done
         for (int idx = threadIdx.x - 4 * 32; idx < nc * kBN; idx += kPairEpiWarps * 32) {
-          const int ci = idx / kBN, j = idx % kBN, c = c0 + ci, g = P.c_g[c];
+          const int ci = idx / kBN, j = idx % kBN, c = cid[ci], g = P.c_g[c];
           const int col = col_tile * kBN + j;
           uint32_t acc = 0;
           for (int s = P.c_s[c]; s <= P.c_e[c]; ++s) {
@@ -503,7 +515,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
       for (int ci = 0; ci < Cfg::kNAcc; ++ci) {
         rrow[ci] = 0;
         if (P.bias && row_ok && ci < nc) {
-          const int c = c0 + ci;
+          const int c = cid[ci];
           for (int s = P.c_s[c]; s <= P.c_e[c]; ++s) {
             const int t = P.c_g[c] - s;
             rrow[ci] += (t == 1 ? o1 : os) * static_cast<uint32_t>(P.lsa[(s - 1) * P.lsa_plane + row * P.lsa_lstride]);
@@ -515,14 +527,61 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
       if (trace && warp == 4 && lane == 0 && (b == 0 || b == P.nbatch - 1))
         trace[b == 0 ? 12 : 13] = ptx::globaltimer();
 #pragma unroll 1
-      for (int ci = 0; ci < nc; ++ci) {
-        const int c = c0 + ci;
-        uint32_t rr = rrow[0];
+      for (int a = P.b_act0[b]; a < P.b_act1[b]; ++a) {
+        // action word: chunk id | kind << 10 | accumulator << 12 | park slot << 16
+        const uint32_t act = P.act[a];
+        const int c = static_cast<int>(act & 0x3FFu), kind = static_cast<int>((act >> 10) & 3u);
+        const int ci = static_cast<int>((act >> 12) & 3u), slot = static_cast<int>(act >> 16);
+        const bool from_park = kind == kActUnpark;
+        uint32_t rr = 0;
+        if (!from_park) {
+          rr = rrow[0];
 #pragma unroll
-        for (int x = 1; x < Cfg::kNAcc; ++x)
-          if (ci == x) rr = rrow[x];
-        const uint32_t* cc_s = ccol + ci * kBN + cslice * kCols;
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + ci * kBN + cslice * kCols;
+          for (int x = 1; x < Cfg::kNAcc; ++x)
+            if (ci == x) rr = rrow[x];
+        }
+        const uint32_t* cc_s = ccol + (from_park ? 0 : ci) * kBN + cslice * kCols;
+        const bool corr = P.bias && !from_park;  // parked values are already corrected
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + (from_park ? 0 : ci) * kBN +
+                               cslice * kCols;
+        uint4* pk = park ? park + static_cast<int64_t>(slot) * (kBM * kBN / 4) + (cslice * kCols / 4) * kBM + prow
+                         : nullptr;
+        if (kind == kActPark) {
+          // exact INT32 chunk sums (offset terms removed) to the park slot
+#pragma unroll
+          for (int cc = 0; cc < kCols; cc += 2 * kLd) {
+            uint32_t v0[kLd], v1[kLd];
+            ptx::tmem_ld_32x32b<kLd>(taddr + cc, v0);
+            ptx::tmem_ld_32x32b<kLd>(taddr + cc + kLd, v1);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int q = 0; q < 2 * kLd; q += 4) {
+              uint32_t w[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int j = q + u;
+                w[u] = (j < kLd ? v0[j] : v1[j - kLd]) - (corr ? rr + cc_s[cc + j] : 0u);
+              }
+              pk[((cc + q) / 4) * kBM] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+          continue;
+        }
+        // 32 INT32 sums of this thread's row at columns cc.. (TMEM or park slot)
+        auto load32 = [&](int cc, uint32_t (&v0)[kLd], uint32_t (&v1)[kLd]) {
+          if (from_park) {
+#pragma unroll
+            for (int q = 0; q < 2 * kLd; q += 4) {
+              const uint4 x = pk[((cc + q) / 4) * kBM];
+              uint32_t* dst = q < kLd ? v0 + q : v1 + (q - kLd);
+              dst[0] = x.x, dst[1] = x.y, dst[2] = x.z, dst[3] = x.w;
+            }
+          } else {
+            ptx::tmem_ld_32x32b<kLd>(taddr + cc, v0);
+            ptx::tmem_ld_32x32b<kLd>(taddr + cc + kLd, v1);
+            ptx::tmem_ld_wait();
+          }
+        };
         // Fast flush (group-wise scaling): ru = mu 2^(2 - beta g) and cv = nu_j are
         // powers of two, so t = fl(fl(ru acc) cv) = acc 2^(Er + Ec) exactly whenever
         // both products stay normal -- the reference's two rounded multiplies are
@@ -542,13 +601,11 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
 #pragma unroll
           for (int cc = 0; cc < kCols; cc += 2 * kLd) {
             uint32_t v0[kLd], v1[kLd];
-            ptx::tmem_ld_32x32b<kLd>(taddr + cc, v0);
-            ptx::tmem_ld_32x32b<kLd>(taddr + cc + kLd, v1);
-            ptx::tmem_ld_wait();
+            load32(cc, v0, v1);
 #pragma unroll
             for (int q = 0; q < 2 * kLd; q += 4) {
               const uint4 e4 = ptx::lds_u32x4(ec_addr + 4 * (cc + q));
-              const uint4 c4 = P.bias ? ptx::lds_u32x4(cc_addr + 4 * (cc + q)) : make_uint4(0, 0, 0, 0);
+              const uint4 c4 = corr ? ptx::lds_u32x4(cc_addr + 4 * (cc + q)) : make_uint4(0, 0, 0, 0);
               const uint32_t esh[4] = {e4.x, e4.y, e4.z, e4.w}, cor[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
@@ -564,26 +621,30 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
         } else {
           const double ru = flush_row_scale(P, c, row, mu);
 #pragma unroll
-          for (int cc = 0; cc < kCols; cc += kLd) {
-            uint32_t v[kLd];
-            ptx::tmem_ld_32x32b<kLd>(taddr + cc, v);
-            ptx::tmem_ld_wait();
-            if (P.bias) {
+          for (int cc = 0; cc < kCols; cc += 2 * kLd) {
+            uint32_t v0[kLd], v1[kLd];
+            load32(cc, v0, v1);
 #pragma unroll
-              for (int j = 0; j < kLd; ++j) v[j] -= rr + cc_s[cc + j];
-            }
-            if (P.dump != nullptr && row_ok) {
-              int32_t* dst = P.dump + (static_cast<int64_t>(c) * P.m + row) * P.p;
+            for (int hh = 0; hh < 2; ++hh) {
+              uint32_t* v = hh ? v1 : v0;
+              const int c1 = cc + hh * kLd;
+              if (corr) {
 #pragma unroll
-              for (int j = 0; j < kLd; ++j)
-                if (col0 + cc + j < P.p) dst[col0 + cc + j] = static_cast<int32_t>(v[j]);
-            }
+                for (int j = 0; j < kLd; ++j) v[j] -= rr + cc_s[c1 + j];
+              }
+              if (P.dump != nullptr && row_ok) {
+                int32_t* dst = P.dump + (static_cast<int64_t>(c) * P.m + row) * P.p;
 #pragma unroll
-            for (int j = 0; j < kLd; ++j) {
-              const double cv = flush_col_scale(P, c, col0 + cc + j, nu_s[cslice * kCols + cc + j]);
-              const double t =
-                  __dmul_rn(__dmul_rn(ru, static_cast<double>(static_cast<int32_t>(v[j]))), cv);
-              d[cc + j] = __dadd_rn(d[cc + j], t);
+                for (int j = 0; j < kLd; ++j)
+                  if (col0 + c1 + j < P.p) dst[col0 + c1 + j] = static_cast<int32_t>(v[j]);
+              }
+#pragma unroll
+              for (int j = 0; j < kLd; ++j) {
+                const double cv = flush_col_scale(P, c, col0 + c1 + j, nu_s[cslice * kCols + c1 + j]);
+                const double t =
+                    __dmul_rn(__dmul_rn(ru, static_cast<double>(static_cast<int32_t>(v[j]))), cv);
+                d[c1 + j] = __dadd_rn(d[c1 + j], t);
+              }
             }
           }
         }

@@ -44,6 +44,9 @@
 #define OZMM_ENV(name) (static_cast<const char*>(nullptr))
 #endif
 
+// SM ids the park scratch covers (the kernel traps beyond it); B200 has 148 SMs
+constexpr int kParkSmIds = 256;
+
 namespace {
 
 thread_local std::string g_thread_err;
@@ -121,6 +124,8 @@ struct Handle {
   size_t lsa_n = 0;
   int32_t* lsb = nullptr;
   size_t lsb_n = 0;
+  int32_t* park = nullptr;  // CTA-pair kernel: parked INT32 chunk tiles, per SM id
+  size_t park_n = 0;
   double* tscratch = nullptr;  // transposed operand for per-slice RN column splits
   size_t tscratch_n = 0;
   // device staging for the host-pointer entry (grown lazily, reused)
@@ -539,12 +544,25 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
   P.c_out = Cout;
   P.ldc = ldc;
   P.dump = dump;
+  static_assert(ozb::kFlushTmem == ozb::kActFlush && ozb::kPark == ozb::kActPark &&
+                    ozb::kFlushParked == ozb::kActUnpark,
+                "schedule.hpp FlushKind and the kernel's action codes must agree");
   for (size_t b = 0; b < S.batches.size(); ++b) {
-    P.b_c0[b] = static_cast<uint16_t>(S.batches[b].c0);
-    P.b_nc[b] = static_cast<uint16_t>(S.batches[b].nc);
-    P.b_pass0[b] = static_cast<uint16_t>(S.batches[b].pass0);
-    P.b_pass1[b] = static_cast<uint16_t>(S.batches[b].pass1);
+    const ozb::Batch& B = S.batches[b];
+    P.b_c0[b] = static_cast<uint16_t>(B.c0);
+    P.b_nc[b] = static_cast<uint16_t>(B.nc);
+    P.b_pass0[b] = static_cast<uint16_t>(B.pass0);
+    P.b_pass1[b] = static_cast<uint16_t>(B.pass1);
+    for (int ci = 0; ci < B.nc && ci < 4; ++ci) P.b_cid[b * 4 + ci] = static_cast<uint16_t>(B.cids[ci]);
+    P.b_act0[b] = static_cast<uint16_t>(B.act0);
+    P.b_act1[b] = static_cast<uint16_t>(B.act1);
   }
+  for (size_t a = 0; a < S.acts.size(); ++a) {
+    const ozb::FlushAct& x = S.acts[a];
+    P.act[a] = static_cast<uint32_t>(x.c) | (static_cast<uint32_t>(x.kind) << 10) |
+               (static_cast<uint32_t>(std::max(0, x.ci)) << 12) | (static_cast<uint32_t>(std::max(0, x.slot)) << 16);
+  }
+  P.park_slots = S.park_slots;
   for (size_t q = 0; q < S.passes.size(); ++q) {
     P.p_alo[q] = static_cast<uint8_t>(S.passes[q].alo);
     P.p_ahi[q] = static_cast<uint8_t>(S.passes[q].ahi);
@@ -581,6 +599,13 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
       }
       P.b_c0[0] = P.b_c0[b], P.b_nc[0] = P.b_nc[b];
       P.b_pass0[0] = 0, P.b_pass1[0] = static_cast<uint16_t>(q1 - q0);
+      // its chunks flushed straight from TMEM
+      for (int ci = 0; ci < P.b_nc[b]; ++ci) {
+        P.b_cid[ci] = P.b_cid[b * 4 + ci];
+        P.act[ci] = static_cast<uint32_t>(P.b_cid[ci]) | (ozb::kActFlush << 10) | (static_cast<uint32_t>(ci) << 12);
+      }
+      P.b_act0[0] = 0, P.b_act1[0] = P.b_nc[b];
+      P.park_slots = 0;
       P.nbatch = 1, P.npass = q1 - q0;
     }
   }
@@ -594,6 +619,7 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
 
 bool schedule_fits(const ozb::Schedule& S) {
   return S.batches.size() <= static_cast<size_t>(ozb::kMaxBatches) &&
+         S.acts.size() <= static_cast<size_t>(ozb::kMaxActs) && S.park_slots <= ozb::kMaxPark &&
          S.passes.size() <= static_cast<size_t>(ozb::kMaxPasses) &&
          S.products.size() <= static_cast<size_t>(ozb::kMaxProducts) &&
          S.chunks.size() <= static_cast<size_t>(ozb::kMaxChunks) &&
@@ -673,8 +699,25 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   // ... and no two consecutive products into one accumulator (C3 +1 %)
   cm.avoid_raw = cm.interleave;
   if (const char* e = OZMM_ENV("OZMM_AVOID_RAW")) cm.avoid_raw = std::atoi(e) != 0;
-  const ozb::Schedule S = ozb::make_schedule(k, fl.per_product ? 1 : r, Cfg::kNAcc,
-                                             static_cast<int64_t>(bwin) * Cfg::kBTile, slot_bytes, bwin, cm);
+  const int64_t r_eff = fl.per_product ? 1 : r;
+  ozb::Schedule S = ozb::make_schedule(k, r_eff, Cfg::kNAcc, static_cast<int64_t>(bwin) * Cfg::kBTile,
+                                       slot_bytes, bwin, cm);
+  // Chunks batched by shared A slices instead of in flush order, the ones ahead
+  // of their turn parked by the epilogue (schedule.hpp make_schedule_free): taken
+  // when the model says >= 3 % cheaper -- small r (C4: 26 -> 12 A loads per K
+  // block) and the r = 8 schedules with split groups (C5 k >= 12).  Results are
+  // unchanged: the INT32 sums are exact and the FP64 flushes keep their order.
+  {
+    int free_mode = -1;  // -1 auto, 0 off, 1 on when it fits
+    if (const char* e = OZMM_ENV("OZMM_SCHED_FREE")) free_mode = std::atoi(e);
+    if (free_mode != 0) {
+      ozb::Schedule F = ozb::make_schedule_free(k, r_eff, Cfg::kNAcc, static_cast<int64_t>(bwin) * Cfg::kBTile,
+                                                slot_bytes, bwin, cm);
+      if (F.park_slots > 0 && schedule_fits(F) &&
+          (free_mode == 1 || ozb::schedule_cost(F, cm) < 0.97 * ozb::schedule_cost(S, cm)))
+        S = std::move(F);
+    }
+  }
   if (!schedule_fits(S))
     return set_err(h, OZMM_ERR_UNSUPPORTED, "schedule too large (k=%d, r=%lld)", k,
                    static_cast<long long>(r));
@@ -728,6 +771,12 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   P.n_kb = n_kb;
   P.kpair = kpair;
   P.b_buf_slots = b_slots;
+  if (S.park_slots > 0) {
+    // one slot set per SM id (the kernel indexes by %smid; one CTA per SM, below)
+    const size_t want = static_cast<size_t>(kParkSmIds) * S.park_slots * ozb::kBM * kBN;
+    if (int rc = ensure(h, &h->park, &h->park_n, want)) return rc;
+    P.park = h->park;
+  }
   for (const auto& ps : S.passes)
     for (int i = ps.p0; i < ps.p1; ++i) {
       const auto& pr = S.products[i];
@@ -747,7 +796,9 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
     return rc;
   if (fl.biased() && (fl.per_product || fl.scale_mode != 0))
     return set_err(h, OZMM_ERR_UNSUPPORTED, "offset-binary slices need the CTA-pair ozIMMU_H kernel");
-  const size_t smem = Cfg::smem_bytes(b_slots, stages);
+  size_t smem = Cfg::smem_bytes(b_slots, stages);
+  // parked chunks live in per-SM scratch: never two CTAs on one SM
+  if (S.park_slots > 0) smem = std::max(smem, static_cast<size_t>(h->smem_optin / 2 + 1024));
   if (!h->pair_attr_set[kPairs - 1]) {
     CUDA_TRY(h, cudaFuncSetAttribute(ozb::ozimmu_gemm_pair_kernel<kBN, kPairs>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1050,6 +1101,7 @@ int ozmm_destroy(ozmm_handle_t handle) {
   cudaFree(h->tscratch);
   cudaFree(h->lsa);
   cudaFree(h->lsb);
+  cudaFree(h->park);
   cudaFree(h->host_a);
   cudaFree(h->host_b);
   cudaFree(h->host_c);
@@ -1196,11 +1248,11 @@ int ozmm_debug_schedule(int k, int64_t r, int cta_pair, int tile_n, int* rows, i
     for (int i = ps.p0; i < ps.p1; ++i) {
       const ozb::Product& pr = S.products[i];
       const ozb::Batch& b = S.batches[ps.batch];
-      const ozb::Chunk& c = S.chunks[b.c0 + pr.ci];
+      const ozb::Chunk& c = S.chunks[b.cids[pr.ci]];
       int* row = rows + 8 * i;
       row[0] = ps.batch;
       row[1] = q;
-      row[2] = b.c0 + pr.ci;  // global chunk index (flush order)
+      row[2] = b.cids[pr.ci];  // global chunk index (flush order)
       row[3] = c.g;
       row[4] = pr.s;
       row[5] = pr.t;
@@ -1730,7 +1782,6 @@ int dgemm_host_impl(Handle* h, char transa, char transb, int64_t m, int64_t n, i
   //
   // Output.  The result goes to Cout (ldo): C itself for ozmm_dgemm_host, a
   // separate matrix for ozmm_dgemm_host_out, which then never writes C.
-  ozmm_handle_t handle = reinterpret_cast<ozmm_handle_t>(h);
   if (!valid_trans(transa) || !valid_trans(transb))
     return set_err(h, OZMM_ERR_ARG, "trans must be 'N' or 'T'");
   if (k < 1) return set_err(h, OZMM_ERR_CONFIG, "k must be >= 1");

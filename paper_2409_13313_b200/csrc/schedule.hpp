@@ -47,8 +47,22 @@ struct AGroup {
 };
 
 struct Batch {
-  int c0, nc;        // chunk range
+  int c0, nc;        // chunk range (consecutive batches; c0 = cids[0] otherwise)
   int pass0, pass1;  // pass range [pass0, pass1)
+  std::vector<int> cids;  // the batch's chunks (global ids); accumulator ci holds cids[ci]
+  int act0 = 0, act1 = 0;  // its epilogue actions [act0, act1)
+};
+
+// Epilogue action after a batch's MMAs (CTA-pair kernel).  The FP64 flushes must
+// run in the reference's chunk order (scheme.cpp:91-94); a batch may hold chunks
+// whose turn has not come yet: they are PARKED (exact INT32 tile, corrections
+// applied, into per-CTA scratch) and flushed from there later.
+enum FlushKind { kFlushTmem = 0, kPark = 1, kFlushParked = 2 };
+struct FlushAct {
+  int kind;
+  int c;     // global chunk id
+  int ci;    // accumulator (kFlushTmem, kPark)
+  int slot;  // park slot (kPark, kFlushParked)
 };
 
 struct Schedule {
@@ -57,7 +71,9 @@ struct Schedule {
   std::vector<Pass> passes;
   std::vector<Product> products;
   std::vector<AGroup> agroups;
+  std::vector<FlushAct> acts;
   int a_slots = 0, b_slots = 0;  // max slice tiles per stage over passes
+  int park_slots = 0;            // park slots the schedule needs (0: chunks consecutive)
 };
 
 // ceil(log2 n) via bit width (split.cpp:20-22).
@@ -136,6 +152,16 @@ inline std::vector<Product> batch_products(const std::vector<Chunk>& chunks, int
   return prods;
 }
 
+// Products of a batch given by its chunk ids (accumulator ci = position in ids).
+inline std::vector<Product> batch_products_ids(const std::vector<Chunk>& chunks, const std::vector<int>& ids) {
+  std::vector<Product> prods;
+  for (int ci = 0; ci < static_cast<int>(ids.size()); ++ci) {
+    const Chunk& c = chunks[ids[ci]];
+    for (int s = c.s0; s <= c.s1; ++s) prods.push_back({ci, s, c.g - s, false});
+  }
+  return prods;
+}
+
 inline double pass_cost(const std::vector<Product>& prods, int u, int v, const PassCost& cm) {
   int np = 0, tlo = 1 << 20, thi = -1;
   uint64_t amask[4] = {0, 0, 0, 0};
@@ -177,48 +203,26 @@ inline double best_windows(const std::vector<Product>& prods, int b_windows, con
 
 }  // namespace detail
 
-// stage_slot_bytes(a, b) must be <= max_stage_bytes for every pass (a single
-// product always fits: 1 A tile + 1 B tile).
-//
-// b_windows > 0 (the CTA-pair kernel, whose A slices stream through a ring and
-// only the B slices of a K block are resident): batches are cut by dynamic
-// programming over the chunk sequence (consecutive chunks, at most n_acc per
-// batch, minimising the PassCost model), and each batch's products are split
-// into passes by windows of at most b_windows consecutive B slices (again the
-// cheapest split), so every streamed A tile feeds as many products as possible
-// and no batch degenerates into a fill-bound sweep.  Otherwise batches take
-// n_acc chunks in turn and passes are cut greedily in flush order under
-// stage_slot_bytes (the single-CTA kernels stage every slice of a pass).
+
+namespace detail {
+
+// Batches from chunk-id sets (in execution order): passes, products, A groups,
+// and the epilogue actions (flush in chunk order, park what runs ahead).
 template <class SlotBytes>
-inline Schedule make_schedule(int k, int64_t r, int n_acc, int64_t max_stage_bytes,
-                              SlotBytes stage_slot_bytes, int b_windows = 0,
-                              const PassCost& cm = PassCost{}) {
-  Schedule S;
-  S.chunks = make_chunks(k, r);
+inline void build_batches(Schedule& S, const std::vector<std::vector<int>>& sets, SlotBytes stage_slot_bytes,
+                          int64_t max_stage_bytes, int b_windows, const PassCost& cm) {
   const int w = static_cast<int>(S.chunks.size());
-  // batch boundaries
-  std::vector<int> starts;
-  if (b_windows > 0 && !cm.greedy) {
-    std::vector<double> best(w + 1, 1e300);
-    std::vector<int> from(w + 1, 0);
-    best[0] = 0.0;
-    for (int e = 1; e <= w; ++e)
-      for (int b = std::max(0, e - n_acc); b < e; ++b) {
-        const auto prods = detail::batch_products(S.chunks, b, e - b);
-        const double c = best[b] + cm.batch + detail::best_windows(prods, b_windows, cm, nullptr);
-        if (c < best[e] - 1e-9) best[e] = c, from[e] = b;
-      }
-    for (int e = w; e > 0; e = from[e]) starts.push_back(from[e]);
-    std::reverse(starts.begin(), starts.end());
-  } else {
-    for (int c0 = 0; c0 < w; c0 += n_acc) starts.push_back(c0);
-  }
-  for (size_t bi = 0; bi < starts.size(); ++bi) {
+  std::vector<char> done(w, 0);
+  std::vector<int> park_of(w, -1);
+  std::vector<char> slot_busy;
+  int next = 0;
+  for (const std::vector<int>& ids : sets) {
     Batch b;
-    b.c0 = starts[bi];
-    b.nc = (bi + 1 < starts.size() ? starts[bi + 1] : w) - b.c0;
+    b.cids = ids;
+    b.c0 = ids[0];
+    b.nc = static_cast<int>(ids.size());
     b.pass0 = static_cast<int>(S.passes.size());
-    const std::vector<Product> prods = detail::batch_products(S.chunks, b.c0, b.nc);
+    const std::vector<Product> prods = batch_products_ids(S.chunks, ids);
     std::vector<bool> seen(b.nc, false);
     // the passes, as product subsets
     std::vector<std::vector<Product>> pass_sets;
@@ -321,8 +325,133 @@ inline Schedule make_schedule(int k, int64_t r, int n_acc, int64_t max_stage_byt
       S.passes.push_back(ps);
     }
     b.pass1 = static_cast<int>(S.passes.size());
+    // epilogue actions: flush every chunk whose turn has come (this batch's from
+    // TMEM, earlier ones from their park slot), park the rest of this batch
+    b.act0 = static_cast<int>(S.acts.size());
+    for (int c : ids) done[c] = 1;
+    while (next < w && done[next]) {
+      int ci = -1;
+      for (int x = 0; x < b.nc; ++x)
+        if (ids[x] == next) ci = x;
+      if (ci >= 0) {
+        S.acts.push_back({kFlushTmem, next, ci, -1});
+      } else {
+        S.acts.push_back({kFlushParked, next, -1, park_of[next]});
+        slot_busy[park_of[next]] = 0;
+      }
+      ++next;
+    }
+    for (int x = 0; x < b.nc; ++x) {
+      const int c = ids[x];
+      if (c < next) continue;
+      int sl = 0;
+      while (sl < static_cast<int>(slot_busy.size()) && slot_busy[sl]) ++sl;
+      if (sl == static_cast<int>(slot_busy.size())) slot_busy.push_back(0);
+      slot_busy[sl] = 1;
+      park_of[c] = sl;
+      S.acts.push_back({kPark, c, x, sl});
+    }
+    S.park_slots = std::max(S.park_slots, static_cast<int>(slot_busy.size()));
+    b.act1 = static_cast<int>(S.acts.size());
     S.batches.push_back(b);
   }
+}
+
+}  // namespace detail
+
+// stage_slot_bytes(a, b) must be <= max_stage_bytes for every pass (a single
+// product always fits: 1 A tile + 1 B tile).
+//
+// b_windows > 0 (the CTA-pair kernel, whose A slices stream through a ring and
+// only the B slices of a K block are resident): batches are cut by dynamic
+// programming over the chunk sequence (consecutive chunks, at most n_acc per
+// batch, minimising the PassCost model), and each batch's products are split
+// into passes by windows of at most b_windows consecutive B slices (again the
+// cheapest split), so every streamed A tile feeds as many products as possible
+// and no batch degenerates into a fill-bound sweep.  Otherwise batches take
+// n_acc chunks in turn and passes are cut greedily in flush order under
+// stage_slot_bytes (the single-CTA kernels stage every slice of a pass).
+template <class SlotBytes>
+inline Schedule make_schedule(int k, int64_t r, int n_acc, int64_t max_stage_bytes,
+                              SlotBytes stage_slot_bytes, int b_windows = 0,
+                              const PassCost& cm = PassCost{}) {
+  Schedule S;
+  S.chunks = make_chunks(k, r);
+  const int w = static_cast<int>(S.chunks.size());
+  // batch boundaries
+  std::vector<int> starts;
+  if (b_windows > 0 && !cm.greedy) {
+    std::vector<double> best(w + 1, 1e300);
+    std::vector<int> from(w + 1, 0);
+    best[0] = 0.0;
+    for (int e = 1; e <= w; ++e)
+      for (int b = std::max(0, e - n_acc); b < e; ++b) {
+        const auto prods = detail::batch_products(S.chunks, b, e - b);
+        const double c = best[b] + cm.batch + detail::best_windows(prods, b_windows, cm, nullptr);
+        if (c < best[e] - 1e-9) best[e] = c, from[e] = b;
+      }
+    for (int e = w; e > 0; e = from[e]) starts.push_back(from[e]);
+    std::reverse(starts.begin(), starts.end());
+  } else {
+    for (int c0 = 0; c0 < w; c0 += n_acc) starts.push_back(c0);
+  }
+  std::vector<std::vector<int>> sets;
+  for (size_t bi = 0; bi < starts.size(); ++bi) {
+    const int c0 = starts[bi], c1 = bi + 1 < starts.size() ? starts[bi + 1] : w;
+    std::vector<int> ids;
+    for (int c = c0; c < c1; ++c) ids.push_back(c);
+    sets.push_back(std::move(ids));
+  }
+  detail::build_batches(S, sets, stage_slot_bytes, max_stage_bytes, b_windows, cm);
+  return S;
+}
+
+// Modelled cost of a CTA-pair schedule per K block (PassCost units).
+inline double schedule_cost(const Schedule& S, const PassCost& cm) {
+  double c = 0.0;
+  for (const Batch& b : S.batches) {
+    c += cm.batch;
+    for (int q = b.pass0; q < b.pass1; ++q) {
+      const Pass& p = S.passes[q];
+      c += std::max(cm.prod * (p.p1 - p.p0), cm.a_tile * (p.g1 - p.g0) + cm.b_tile * (p.bhi - p.blo + 1));
+    }
+  }
+  return c;
+}
+
+// CTA-pair schedule over chunks taken in (first A slice, group) order instead of
+// flush order.  With small r (C4: r = 2, 20 chunks of <= 2 products) consecutive
+// chunks in flush order are the pieces of ONE group -- disjoint A and B slices,
+// one product per slice tile -- while chunks at the same position of consecutive
+// groups share their A slices and all but one B slice.  Batches are cut by the
+// same dynamic programming over this order; chunks computed ahead of their turn
+// are parked by the epilogue (Schedule::acts) so the FP64 flushes still run in
+// the reference's order (scheme.cpp:91-94).
+template <class SlotBytes>
+inline Schedule make_schedule_free(int k, int64_t r, int n_acc, int64_t max_stage_bytes,
+                                   SlotBytes stage_slot_bytes, int b_windows, const PassCost& cm) {
+  Schedule S;
+  S.chunks = make_chunks(k, r);
+  const int w = static_cast<int>(S.chunks.size());
+  std::vector<int> order(w);
+  for (int c = 0; c < w; ++c) order[c] = c;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+    return S.chunks[x].s0 != S.chunks[y].s0 ? S.chunks[x].s0 < S.chunks[y].s0 : S.chunks[x].g < S.chunks[y].g;
+  });
+  std::vector<double> best(w + 1, 1e300);
+  std::vector<int> from(w + 1, 0);
+  best[0] = 0.0;
+  for (int e = 1; e <= w; ++e)
+    for (int b = std::max(0, e - n_acc); b < e; ++b) {
+      const std::vector<int> ids(order.begin() + b, order.begin() + e);
+      const auto prods = detail::batch_products_ids(S.chunks, ids);
+      const double c = best[b] + cm.batch + detail::best_windows(prods, b_windows, cm, nullptr);
+      if (c < best[e] - 1e-9) best[e] = c, from[e] = b;
+    }
+  std::vector<std::vector<int>> sets;
+  for (int e = w; e > 0; e = from[e]) sets.emplace_back(order.begin() + from[e], order.begin() + e);
+  std::reverse(sets.begin(), sets.end());
+  detail::build_batches(S, sets, stage_slot_bytes, max_stage_bytes, b_windows, cm);
   return S;
 }
 

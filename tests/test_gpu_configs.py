@@ -242,3 +242,48 @@ def test_large_k_bit_exact(oz, checker, k, phi, r, method):
     got = oz.ozaki_gemm(1.5, dev(A), dev(B), 0.5, dev(C), cfg).cpu().numpy()
     assert_bitwise(got, want, f"device k={k}")
     assert_bitwise(oz.ozaki_gemm(1.5, A, B, 0.5, C, cfg), want, f"host k={k}")
+
+
+@pytest.mark.parametrize("k,r,signed", [(8, 2, False), (9, 2, False), (12, 2, False), (8, 1, False),
+                                        (7, 3, False), (14, 4, False), (12, 8, False), (14, 8, False),
+                                        (10, 8, True), (8, 2, True)])
+def test_parked_schedules_bit_exact(oz, checker, k, r, signed):
+    """Schedules that batch chunks by shared A slices and park the ones ahead of
+    their turn (schedule.hpp make_schedule_free; taken for small r and split
+    groups): INT32 chunk sums (the dump, flushed from TMEM or from the park slot)
+    and the final C equal the reference's, device and host entries, with the
+    FP64 flushes in the reference's order (scheme.cpp:91-94)."""
+    m, n, p = 300, 1500, 260
+    A = oz.gen_phi_matrix(m, n, 1.0, 131)
+    B = oz.gen_phi_matrix(n, p, 1.0, 132)
+    C = oz.gen_phi_matrix(m, p, 1.0, 133)
+    cfg = oz.config_for("ozIMMU_H", k)
+    cfg.force_r = r
+    cfg.overflow = oz.OverflowMode.Wrapping  # forced r: no Checked verification pass needed
+    want = checker.gemm(1.5, A, B, 0.5, C, k=k, force_r=r)
+    from oracle import oracle
+    if os.path.exists(oracle.REF_SO):
+        ch = oracle.RefLib().groupwise_chunks(A, B, k, force_r=r)
+        dump = torch.zeros((ch.acc.shape[0], m, p), dtype=torch.int32, device="cuda")
+        got = oz.ozaki_gemm(1.5, dev(A), dev(B), 0.5, dev(C), cfg, chunk_dump=dump,
+                            signed_slices=signed)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(dump.cpu().numpy(), ch.acc)
+        assert_bitwise(got.cpu().numpy(), want, f"device (dump) k={k} r={r}")
+    got = oz.ozaki_gemm(1.5, dev(A), dev(B), 0.5, dev(C), cfg, signed_slices=signed).cpu().numpy()
+    assert_bitwise(got, want, f"device k={k} r={r}")
+    assert_bitwise(oz.ozaki_gemm(1.5, A, B, 0.5, C, cfg), want, f"host k={k} r={r}")
+
+
+def test_parked_schedule_c4_shape(oz, checker):
+    """n = 65536 (r = 2 without forcing, C4's inner dimension): the parked schedule
+    on a 256 x 65536 x 384 problem, against the reference."""
+    m, n, p, k = 256, 65536, 384, 8
+    A = oz.gen_phi_matrix(m, n, 0.5, 141)
+    B = oz.gen_phi_matrix(n, p, 0.5, 142)
+    C = oz.gen_phi_matrix(m, p, 0.5, 143)
+    want = checker.gemm(1.0, A, B, 0.0, C, k=k)
+    cfg = oz.config_for("ozIMMU_H", k)
+    got = oz.ozaki_gemm(1.0, dev(A), dev(B), 0.0, dev(C), cfg).cpu().numpy()
+    assert_bitwise(got, want, "C4-shaped device")
+    assert oz.ozaki_gemm_ex(1.0, dev(A), dev(B), 0.0, dev(C), cfg).counts.r == 2
