@@ -704,9 +704,10 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
                                        slot_bytes, bwin, cm);
   // Chunks batched by shared A slices instead of in flush order, the ones ahead
   // of their turn parked by the epilogue (schedule.hpp make_schedule_free): taken
-  // when the model says >= 3 % cheaper -- small r (C4: 26 -> 12 A loads per K
-  // block) and the r = 8 schedules with split groups (C5 k >= 12).  Results are
-  // unchanged: the INT32 sums are exact and the FP64 flushes keep their order.
+  // whenever the model says cheaper -- small r (C4: 26 -> 12 A loads per K block,
+  // +58 %) and the r = 8 schedules with split groups (C5 k = 10 / 12 / 14: +4 /
+  // +15 / +12 %; profiles/r2/park_schedules.txt).  Results are unchanged: the
+  // INT32 sums are exact and the FP64 flushes keep their order.
   {
     int free_mode = -1;  // -1 auto, 0 off, 1 on when it fits
     if (const char* e = OZMM_ENV("OZMM_SCHED_FREE")) free_mode = std::atoi(e);
@@ -714,7 +715,7 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
       ozb::Schedule F = ozb::make_schedule_free(k, r_eff, Cfg::kNAcc, static_cast<int64_t>(bwin) * Cfg::kBTile,
                                                 slot_bytes, bwin, cm);
       if (F.park_slots > 0 && schedule_fits(F) &&
-          (free_mode == 1 || ozb::schedule_cost(F, cm) < 0.97 * ozb::schedule_cost(S, cm)))
+          (free_mode == 1 || ozb::schedule_cost(F, cm) < 0.995 * ozb::schedule_cost(S, cm)))
         S = std::move(F);
     }
   }

@@ -87,7 +87,7 @@ int main() {
         std::printf("FAIL standard schedule parks (k=%d r=%ld)\n", k, r);
         return 1;
       }
-      if (F.park_slots > 0 && F.park_slots <= 16 && ozb::schedule_cost(F, cm) < 0.97 * ozb::schedule_cost(S, cm))
+      if (F.park_slots > 0 && F.park_slots <= 16 && ozb::schedule_cost(F, cm) < 0.995 * ozb::schedule_cost(S, cm))
         ++nfree;
     }
   const int cfg[][2] = {{8, 2}, {8, 8}, {9, 8}, {10, 8}, {12, 8}, {14, 8}, {8, 16}, {14, 16}};
