@@ -2,7 +2,8 @@
 combination of the knobs a caller can turn (shape including 1-element edges,
 k in 1..32, phi, alpha/beta including zeros and negatives, transposes, method,
 device vs host entry, pinned-free host buffers, column-split path, signed
-planes) must give the reference's bits."""
+planes, forced small r -- which selects the parked schedules, schedule.hpp
+make_schedule_free) must give the reference's bits."""
 import numpy as np
 import pytest
 
@@ -36,10 +37,11 @@ def _case(seed):
                 beta=float(rng.choice([0.0, 0.5, -1.0, 0.0])),
                 ta=bool(rng.random() < 0.3), tb=bool(rng.random() < 0.3),
                 method=str(rng.choice(METHODS)), host=bool(rng.random() < 0.4),
-                col_split=int(rng.choice([0, 1, 2])), signed=bool(rng.random() < 0.2))
+                col_split=int(rng.choice([0, 1, 2])), signed=bool(rng.random() < 0.2),
+                force_r=int(rng.choice([0, 0, 0, 1, 2, 3, 4])))
 
 
-@pytest.mark.parametrize("seed", range(160))
+@pytest.mark.parametrize("seed", range(200))
 def test_random_configuration(env, seed):
     ozmm, ref = env
     c = _case(seed)
@@ -47,10 +49,13 @@ def test_random_configuration(env, seed):
     A = ozmm.gen_phi_matrix(m, n, c["phi"], 1000 + seed)
     B = ozmm.gen_phi_matrix(n, p, c["phi"], 2000 + seed)
     C = ozmm.gen_phi_matrix(m, p, c["phi"], 3000 + seed)
-    want = ref.gemm(c["alpha"], A, B, c["beta"], C, k=k, method=c["method"])
+    r_nat = ozmm.compute_r(n, ozmm.compute_beta(n))
+    force_r = c["force_r"] if 0 < c["force_r"] <= r_nat else 0  # never past the natural r
+    want = ref.gemm(c["alpha"], A, B, c["beta"], C, k=k, method=c["method"], force_r=force_r)
     As = np.ascontiguousarray(A.T) if c["ta"] else A
     Bs = np.ascontiguousarray(B.T) if c["tb"] else B
     cfg = ozmm.config_for(c["method"], k)
+    cfg.force_r = force_r
     kw = dict(transa=c["ta"], transb=c["tb"], col_split=c["col_split"])
     if c["host"]:
         got = ozmm.ozaki_gemm(c["alpha"], As, Bs, c["beta"], C, cfg, **kw)
