@@ -287,3 +287,18 @@ def test_parked_schedule_c4_shape(oz, checker):
     got = oz.ozaki_gemm(1.0, dev(A), dev(B), 0.0, dev(C), cfg).cpu().numpy()
     assert_bitwise(got, want, "C4-shaped device")
     assert oz.ozaki_gemm_ex(1.0, dev(A), dev(B), 0.0, dev(C), cfg).counts.r == 2
+
+
+@pytest.mark.parametrize("k,r", [(8, 2), (12, 8)])
+def test_parked_schedules_quad_bit_exact(oz, checker, k, r):
+    """The 4-CTA variant (cta_pair=3, A multicast) with parked schedules."""
+    m, n, p = 512, 1200, 384
+    A = oz.gen_phi_matrix(m, n, 2.0, 151)
+    B = oz.gen_phi_matrix(n, p, 2.0, 152)
+    C = oz.gen_phi_matrix(m, p, 2.0, 153)
+    cfg = oz.config_for("ozIMMU_H", k)
+    cfg.force_r = r
+    cfg.overflow = oz.OverflowMode.Wrapping
+    want = checker.gemm(-0.5, A, B, 1.5, C, k=k, force_r=r)
+    got = oz.ozaki_gemm(-0.5, dev(A), dev(B), 1.5, dev(C), cfg, cta_pair=3).cpu().numpy()
+    assert_bitwise(got, want, f"quad k={k} r={r}")
