@@ -484,7 +484,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
       uint32_t smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
       if (smid >= 256u) __trap();  // the host sizes the scratch for 256 SM ids (kParkSmIds)
-      park = reinterpret_cast<uint4*>(P.park) + static_cast<int64_t>(smid) * P.park_slots * (kBM * kBN / 4);
+      park = reinterpret_cast<uint4*>(P.park) + static_cast<int64_t>(smid) * kMaxPark * (kBM * kBN / 4);
     }
     const int prow = quarter * 32 + lane;  // this thread's row of the CTA's tile
     for (int b = 0; b < P.nbatch; ++b) {

@@ -773,8 +773,10 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
   P.kpair = kpair;
   P.b_buf_slots = b_slots;
   if (S.park_slots > 0) {
-    // one slot set per SM id (the kernel indexes by %smid; one CTA per SM, below)
-    const size_t want = static_cast<size_t>(kParkSmIds) * S.park_slots * ozb::kBM * kBN;
+    // kMaxPark slots per SM id (the kernel indexes by %smid; one CTA per SM, below):
+    // a fixed stride, so concurrent launches on the handle's streams that park
+    // different numbers of chunks never share a region
+    const size_t want = static_cast<size_t>(kParkSmIds) * ozb::kMaxPark * ozb::kBM * kBN;
     if (int rc = ensure(h, &h->park, &h->park_n, want)) return rc;
     P.park = h->park;
   }
