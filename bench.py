@@ -215,8 +215,8 @@ def run_reference_arm(args, rank, world):
         return
     k = args.k
     ms = args.cpu_sample
-    # bounded: a few seconds per step on the box's host cores
-    steps, warm = max(1, min(args.steps, 3)), min(args.warmup, 1)
+    # bounded: ~3 s per call on the box's host cores, at most 5 timed + 5 warm-up calls
+    steps, warm = max(1, min(args.steps, 5)), min(args.warmup, 5)
     cb = cpu_reference(ms, args.n, ms, k, args.phi, steps, warm, full_p=args.p)
     line = {
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
