@@ -719,6 +719,34 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
         S = std::move(F);
     }
   }
+  // OZMM_SCHED_SETS (diag): explicit batches as chunk ids in execution order,
+  // "0.1.2/3.4.5/6.7.8.9" -- chunks ahead of their turn are parked as usual
+  if (const char* e = OZMM_ENV("OZMM_SCHED_SETS")) {
+    std::vector<std::vector<int>> sets(1);
+    int v = -1;
+    for (const char* c = e;; ++c) {
+      if (*c >= '0' && *c <= '9') {
+        v = (v < 0 ? 0 : 10 * v) + (*c - '0');
+        continue;
+      }
+      if (v >= 0) sets.back().push_back(v), v = -1;
+      if (*c == '/') sets.emplace_back();
+      if (*c == '\0') break;
+    }
+    ozb::Schedule X;
+    X.chunks = ozb::make_chunks(k, r_eff);
+    std::vector<int> seen(X.chunks.size(), 0);
+    bool ok = true;
+    for (const auto& s : sets) {
+      ok = ok && !s.empty() && static_cast<int>(s.size()) <= Cfg::kNAcc;
+      for (int c : s) ok = ok && c < static_cast<int>(seen.size()) && !seen[c]++;
+    }
+    for (int x : seen) ok = ok && x == 1;
+    if (!ok) return set_err(h, OZMM_ERR_ARG, "OZMM_SCHED_SETS: not a partition of the %d chunks",
+                            static_cast<int>(X.chunks.size()));
+    ozb::detail::build_batches(X, sets, slot_bytes, static_cast<int64_t>(bwin) * Cfg::kBTile, bwin, cm);
+    S = std::move(X);
+  }
   if (!schedule_fits(S))
     return set_err(h, OZMM_ERR_UNSUPPORTED, "schedule too large (k=%d, r=%lld)", k,
                    static_cast<long long>(r));
