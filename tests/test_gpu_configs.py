@@ -302,3 +302,21 @@ def test_parked_schedules_quad_bit_exact(oz, checker, k, r):
     want = checker.gemm(-0.5, A, B, 1.5, C, k=k, force_r=r)
     got = oz.ozaki_gemm(-0.5, dev(A), dev(B), 1.5, dev(C), cfg, cta_pair=3).cpu().numpy()
     assert_bitwise(got, want, f"quad k={k} r={r}")
+
+
+@pytest.mark.parametrize("k,r,panels", [(8, 2, 8), (12, 8, 6), (10, 3, 16)])
+def test_parked_schedules_pipelined_host_strips(oz, checker, k, r, panels):
+    """The host entry's pipelined strips (several strip GEMMs in flight on the
+    handle's streams) with parked schedules: every strip's CTAs park into the
+    per-SM-id scratch at its fixed stride; C equals the reference's for
+    in-place and separate-output calls."""
+    m, n, p = 1536, 2048, 1280
+    A = oz.gen_phi_matrix(m, n, 1.0, 161)
+    B = oz.gen_phi_matrix(n, p, 1.0, 162)
+    C = oz.gen_phi_matrix(m, p, 1.0, 163)
+    cfg = oz.config_for("ozIMMU_H", k)
+    cfg.force_r = r
+    cfg.overflow = oz.OverflowMode.Wrapping
+    want = checker.gemm(1.5, A, B, 0.5, C, k=k, force_r=r)
+    got = oz.ozaki_gemm(1.5, A, B, 0.5, C, cfg, host_panels=panels)
+    assert_bitwise(got, want, f"host strips k={k} r={r} panels={panels}")
