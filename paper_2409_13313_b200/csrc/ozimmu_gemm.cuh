@@ -125,13 +125,9 @@ struct GemmParams {
   int ksnake;
   // CTA-pair kernel: per batch its chunk ids (accumulator ci holds b_cid[b * 4 + ci])
   // and its epilogue actions act[b_act0[b] .. b_act1[b]) (schedule.hpp FlushAct:
-  // chunk id | kind << 10 | accumulator << 12 | park slot << 16 | (add slot + 1) << 20:
-  // the partial sum of a chunk's earlier pieces, added on flush / park); park: per-SM
-  // scratch of park_slots INT32 128 x 128 tiles per CTA, or null when nothing is parked.
-  // b_us / b_ue: the A-slice range of the piece accumulator ci holds (the offset
-  // corrections are those of its products only)
+  // chunk id | kind << 10 | accumulator << 12 | park slot << 16); park: per-SM
+  // scratch of park_slots INT32 128 x 128 tiles per CTA, or null when nothing is parked
   uint16_t b_cid[kMaxBatches * 4];
-  uint8_t b_us[kMaxBatches * 4], b_ue[kMaxBatches * 4];
   uint16_t b_act0[kMaxBatches], b_act1[kMaxBatches];
   uint32_t act[kMaxActs];
   int32_t* park;

@@ -498,7 +498,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
           const int ci = idx / kBN, j = idx % kBN, c = cid[ci], g = P.c_g[c];
           const int col = col_tile * kBN + j;
           uint32_t acc = 0;
-          for (int s = P.b_us[b * Cfg::kNAcc + ci]; s <= P.b_ue[b * Cfg::kNAcc + ci]; ++s) {
+          for (int s = P.c_s[c]; s <= P.c_e[c]; ++s) {
             const int t = g - s;
             const uint32_t oa = s == 1 ? o1 : os, ob = t == 1 ? o1 : os;
             const uint32_t ls = col < P.p ? static_cast<uint32_t>(P.lsb[(t - 1) * P.lsb_plane + col * P.lsb_lstride]) : 0u;
@@ -516,7 +516,7 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
         rrow[ci] = 0;
         if (P.bias && row_ok && ci < nc) {
           const int c = cid[ci];
-          for (int s = P.b_us[b * Cfg::kNAcc + ci]; s <= P.b_ue[b * Cfg::kNAcc + ci]; ++s) {
+          for (int s = P.c_s[c]; s <= P.c_e[c]; ++s) {
             const int t = P.c_g[c] - s;
             rrow[ci] += (t == 1 ? o1 : os) * static_cast<uint32_t>(P.lsa[(s - 1) * P.lsa_plane + row * P.lsa_lstride]);
           }
@@ -528,12 +528,10 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
         trace[b == 0 ? 12 : 13] = ptx::globaltimer();
 #pragma unroll 1
       for (int a = P.b_act0[b]; a < P.b_act1[b]; ++a) {
-        // action word: chunk id | kind << 10 | accumulator << 12 | park slot << 16 |
-        // (slot of the chunk's earlier pieces + 1) << 20
+        // action word: chunk id | kind << 10 | accumulator << 12 | park slot << 16
         const uint32_t act = P.act[a];
         const int c = static_cast<int>(act & 0x3FFu), kind = static_cast<int>((act >> 10) & 3u);
-        const int ci = static_cast<int>((act >> 12) & 3u), slot = static_cast<int>((act >> 16) & 0xFu);
-        const int add = static_cast<int>(act >> 20) - 1;
+        const int ci = static_cast<int>((act >> 12) & 3u), slot = static_cast<int>(act >> 16);
         const bool from_park = kind == kActUnpark;
         uint32_t rr = 0;
         if (!from_park) {
@@ -548,11 +546,6 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
                                cslice * kCols;
         uint4* pk = park ? park + static_cast<int64_t>(slot) * (kBM * kBN / 4) + (cslice * kCols / 4) * kBM + prow
                          : nullptr;
-        // partial sum of the chunk's earlier pieces (already corrected), added to the
-        // TMEM values before their correction: exact in wrapping INT32
-        const uint4* pa = park && add >= 0
-                              ? park + static_cast<int64_t>(add) * (kBM * kBN / 4) + (cslice * kCols / 4) * kBM + prow
-                              : nullptr;
         if (kind == kActPark) {
           // exact INT32 chunk sums (offset terms removed) to the park slot
 #pragma unroll
@@ -564,12 +557,10 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
 #pragma unroll
             for (int q = 0; q < 2 * kLd; q += 4) {
               uint32_t w[4];
-              const uint4 x = pa ? pa[((cc + q) / 4) * kBM] : make_uint4(0, 0, 0, 0);
-              const uint32_t xa[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const int j = q + u;
-                w[u] = (j < kLd ? v0[j] : v1[j - kLd]) - (corr ? rr + cc_s[cc + j] : 0u) + xa[u];
+                w[u] = (j < kLd ? v0[j] : v1[j - kLd]) - (corr ? rr + cc_s[cc + j] : 0u);
               }
               pk[((cc + q) / 4) * kBM] = make_uint4(w[0], w[1], w[2], w[3]);
             }
@@ -589,14 +580,6 @@ __global__ void __cluster_dims__(2 * kPairs, 1, 1) __launch_bounds__(kPairThread
             ptx::tmem_ld_32x32b<kLd>(taddr + cc, v0);
             ptx::tmem_ld_32x32b<kLd>(taddr + cc + kLd, v1);
             ptx::tmem_ld_wait();
-            if (pa) {
-#pragma unroll
-              for (int q = 0; q < 2 * kLd; q += 4) {
-                const uint4 x = pa[((cc + q) / 4) * kBM];
-                uint32_t* dst = q < kLd ? v0 + q : v1 + (q - kLd);
-                dst[0] += x.x, dst[1] += x.y, dst[2] += x.z, dst[3] += x.w;
-              }
-            }
           }
         };
         // Fast flush (group-wise scaling): ru = mu 2^(2 - beta g) and cv = nu_j are

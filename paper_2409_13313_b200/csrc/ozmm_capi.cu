@@ -553,20 +553,14 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
     P.b_nc[b] = static_cast<uint16_t>(B.nc);
     P.b_pass0[b] = static_cast<uint16_t>(B.pass0);
     P.b_pass1[b] = static_cast<uint16_t>(B.pass1);
-    for (int ci = 0; ci < B.nc && ci < 4; ++ci) {
-      P.b_cid[b * 4 + ci] = static_cast<uint16_t>(B.cids[ci]);
-      const bool piece = ci < static_cast<int>(B.units.size());
-      P.b_us[b * 4 + ci] = static_cast<uint8_t>(piece ? B.units[ci].s0 : S.chunks[B.cids[ci]].s0);
-      P.b_ue[b * 4 + ci] = static_cast<uint8_t>(piece ? B.units[ci].s1 : S.chunks[B.cids[ci]].s1);
-    }
+    for (int ci = 0; ci < B.nc && ci < 4; ++ci) P.b_cid[b * 4 + ci] = static_cast<uint16_t>(B.cids[ci]);
     P.b_act0[b] = static_cast<uint16_t>(B.act0);
     P.b_act1[b] = static_cast<uint16_t>(B.act1);
   }
   for (size_t a = 0; a < S.acts.size(); ++a) {
     const ozb::FlushAct& x = S.acts[a];
     P.act[a] = static_cast<uint32_t>(x.c) | (static_cast<uint32_t>(x.kind) << 10) |
-               (static_cast<uint32_t>(std::max(0, x.ci)) << 12) | (static_cast<uint32_t>(std::max(0, x.slot)) << 16) |
-               (static_cast<uint32_t>(x.add + 1) << 20);
+               (static_cast<uint32_t>(std::max(0, x.ci)) << 12) | (static_cast<uint32_t>(std::max(0, x.slot)) << 16);
   }
   P.park_slots = S.park_slots;
   for (size_t q = 0; q < S.passes.size(); ++q) {
@@ -608,7 +602,6 @@ void fill_params(ozb::GemmParams& P, const ozb::Schedule& S, int64_t m, int64_t 
       // its chunks flushed straight from TMEM
       for (int ci = 0; ci < P.b_nc[b]; ++ci) {
         P.b_cid[ci] = P.b_cid[b * 4 + ci];
-        P.b_us[ci] = P.b_us[b * 4 + ci], P.b_ue[ci] = P.b_ue[b * 4 + ci];
         P.act[ci] = static_cast<uint32_t>(P.b_cid[ci]) | (ozb::kActFlush << 10) | (static_cast<uint32_t>(ci) << 12);
       }
       P.b_act0[0] = 0, P.b_act1[0] = P.b_nc[b];
@@ -726,44 +719,32 @@ int launch_gemm_pair(Handle* h, int64_t m, int64_t n, int64_t p, int k, int beta
         S = std::move(F);
     }
   }
-  // OZMM_SCHED_SETS (diag): explicit batches as chunk ids (or pieces c:s0-s1) in
-  // execution order, "0.1.2.8:1-1/3.4.5/6.7.8:2-8.9" -- pieces and chunks ahead
-  // of their turn are parked as usual
+  // OZMM_SCHED_SETS (diag): explicit batches as chunk ids in execution order,
+  // "0.1.2/3.4.5/6.7.8.9" -- chunks ahead of their turn are parked as usual
   if (const char* e = OZMM_ENV("OZMM_SCHED_SETS")) {
+    std::vector<std::vector<int>> sets(1);
+    int v = -1;
+    for (const char* c = e;; ++c) {
+      if (*c >= '0' && *c <= '9') {
+        v = (v < 0 ? 0 : 10 * v) + (*c - '0');
+        continue;
+      }
+      if (v >= 0) sets.back().push_back(v), v = -1;
+      if (*c == '/') sets.emplace_back();
+      if (*c == '\0') break;
+    }
     ozb::Schedule X;
     X.chunks = ozb::make_chunks(k, r_eff);
-    const int w = static_cast<int>(X.chunks.size());
-    std::vector<std::vector<ozb::Unit>> sets(1);
-    std::vector<int> cover(w, 0);
+    std::vector<int> seen(X.chunks.size(), 0);
     bool ok = true;
-    const char* c = e;
-    auto num = [&]() {
-      int v = 0;
-      if (*c < '0' || *c > '9') ok = false;
-      while (*c >= '0' && *c <= '9') v = 10 * v + (*c++ - '0');
-      return v;
-    };
-    while (ok) {
-      ozb::Unit u{num(), 0, 0};
-      if (!ok || u.c >= w) break;
-      u.s0 = X.chunks[u.c].s0, u.s1 = X.chunks[u.c].s1;
-      if (*c == ':') {
-        ++c, u.s0 = num();
-        if (*c++ != '-') ok = false;
-        u.s1 = num();
-      }
-      ok = ok && u.s0 >= X.chunks[u.c].s0 && u.s1 <= X.chunks[u.c].s1 && u.s0 <= u.s1;
-      for (const auto& v : sets.back()) ok = ok && v.c != u.c;
-      cover[u.c] += ok ? u.s1 - u.s0 + 1 : 0;
-      sets.back().push_back(u);
-      ok = ok && static_cast<int>(sets.back().size()) <= Cfg::kNAcc;
-      if (*c == '\0') break;
-      if (*c == '/') sets.emplace_back();
-      ++c;
+    for (const auto& s : sets) {
+      ok = ok && !s.empty() && static_cast<int>(s.size()) <= Cfg::kNAcc;
+      for (int c : s) ok = ok && c < static_cast<int>(seen.size()) && !seen[c]++;
     }
-    for (int x = 0; x < w; ++x) ok = ok && cover[x] == X.chunks[x].s1 - X.chunks[x].s0 + 1;
-    if (!ok) return set_err(h, OZMM_ERR_ARG, "OZMM_SCHED_SETS: not a partition of the %d chunks", w);
-    ozb::detail::build_batches_units(X, sets, slot_bytes, static_cast<int64_t>(bwin) * Cfg::kBTile, bwin, cm);
+    for (int x : seen) ok = ok && x == 1;
+    if (!ok) return set_err(h, OZMM_ERR_ARG, "OZMM_SCHED_SETS: not a partition of the %d chunks",
+                            static_cast<int>(X.chunks.size()));
+    ozb::detail::build_batches(X, sets, slot_bytes, static_cast<int64_t>(bwin) * Cfg::kBTile, bwin, cm);
     S = std::move(X);
   }
   if (!schedule_fits(S))

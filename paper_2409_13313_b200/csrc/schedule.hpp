@@ -46,19 +46,10 @@ struct AGroup {
   int p0, p1;
 };
 
-// A piece of a chunk: its products s = s0..s1 (t = g - s).  A chunk may be
-// computed in pieces spread over several batches; their exact INT32 partial
-// sums are added in the epilogue (integer addition is exact, and the full
-// chunk sum fits INT32 by the r bound), so the flush is unchanged.
-struct Unit {
-  int c, s0, s1;
-};
-
 struct Batch {
   int c0, nc;        // chunk range (consecutive batches; c0 = cids[0] otherwise)
   int pass0, pass1;  // pass range [pass0, pass1)
   std::vector<int> cids;  // the batch's chunks (global ids); accumulator ci holds cids[ci]
-  std::vector<Unit> units;  // accumulator ci holds products units[ci].s0 .. s1 of cids[ci]
   int act0 = 0, act1 = 0;  // its epilogue actions [act0, act1)
 };
 
@@ -72,7 +63,6 @@ struct FlushAct {
   int c;     // global chunk id
   int ci;    // accumulator (kFlushTmem, kPark)
   int slot;  // park slot (kPark, kFlushParked)
-  int add = -1;  // kFlushTmem / kPark: park slot whose partial sum is added (pieces), -1 none
 };
 
 struct Schedule {
@@ -84,7 +74,6 @@ struct Schedule {
   std::vector<FlushAct> acts;
   int a_slots = 0, b_slots = 0;  // max slice tiles per stage over passes
   int park_slots = 0;            // park slots the schedule needs (0: chunks consecutive)
-  int pieces = 0;                // chunks computed in more than one piece
 };
 
 // ceil(log2 n) via bit width (split.cpp:20-22).
@@ -173,14 +162,6 @@ inline std::vector<Product> batch_products_ids(const std::vector<Chunk>& chunks,
   return prods;
 }
 
-// Products of a batch of chunk pieces (accumulator ci = position in units).
-inline std::vector<Product> batch_products_units(const std::vector<Chunk>& chunks, const std::vector<Unit>& us) {
-  std::vector<Product> prods;
-  for (int ci = 0; ci < static_cast<int>(us.size()); ++ci)
-    for (int s = us[ci].s0; s <= us[ci].s1; ++s) prods.push_back({ci, s, chunks[us[ci].c].g - s, false});
-  return prods;
-}
-
 inline double pass_cost(const std::vector<Product>& prods, int u, int v, const PassCost& cm) {
   int np = 0, tlo = 1 << 20, thi = -1;
   uint64_t amask[4] = {0, 0, 0, 0};
@@ -225,36 +206,23 @@ inline double best_windows(const std::vector<Product>& prods, int b_windows, con
 
 namespace detail {
 
-// Batches from sets of chunk pieces (in execution order): passes, products, A
-// groups, and the epilogue actions.  The FP64 flushes run in chunk order: a
-// chunk is flushed when all its pieces are done and its turn has come -- from
-// TMEM (plus the parked partial sum of its earlier pieces) or from its park
-// slot; a piece whose chunk is not complete, or whose turn has not come, is
-// PARKED (added to the slot of its earlier pieces).
+// Batches from chunk-id sets (in execution order): passes, products, A groups,
+// and the epilogue actions (flush in chunk order, park what runs ahead).
 template <class SlotBytes>
-inline void build_batches_units(Schedule& S, const std::vector<std::vector<Unit>>& sets,
-                                SlotBytes stage_slot_bytes, int64_t max_stage_bytes, int b_windows,
-                                const PassCost& cm) {
+inline void build_batches(Schedule& S, const std::vector<std::vector<int>>& sets, SlotBytes stage_slot_bytes,
+                          int64_t max_stage_bytes, int b_windows, const PassCost& cm) {
   const int w = static_cast<int>(S.chunks.size());
-  std::vector<int> left(w), park_of(w, -1), npieces(w, 0);
-  for (int c = 0; c < w; ++c) left[c] = S.chunks[c].s1 - S.chunks[c].s0 + 1;
+  std::vector<char> done(w, 0);
+  std::vector<int> park_of(w, -1);
   std::vector<char> slot_busy;
-  auto take_slot = [&]() {
-    int sl = 0;
-    while (sl < static_cast<int>(slot_busy.size()) && slot_busy[sl]) ++sl;
-    if (sl == static_cast<int>(slot_busy.size())) slot_busy.push_back(0);
-    slot_busy[sl] = 1;
-    return sl;
-  };
   int next = 0;
-  for (const std::vector<Unit>& us : sets) {
+  for (const std::vector<int>& ids : sets) {
     Batch b;
-    for (const Unit& u : us) b.cids.push_back(u.c);
-    b.units = us;
-    b.c0 = us[0].c;
-    b.nc = static_cast<int>(us.size());
+    b.cids = ids;
+    b.c0 = ids[0];
+    b.nc = static_cast<int>(ids.size());
     b.pass0 = static_cast<int>(S.passes.size());
-    const std::vector<Product> prods = batch_products_units(S.chunks, us);
+    const std::vector<Product> prods = batch_products_ids(S.chunks, ids);
     std::vector<bool> seen(b.nc, false);
     // the passes, as product subsets
     std::vector<std::vector<Product>> pass_sets;
@@ -358,46 +326,35 @@ inline void build_batches_units(Schedule& S, const std::vector<std::vector<Unit>
     }
     b.pass1 = static_cast<int>(S.passes.size());
     // epilogue actions: flush every chunk whose turn has come (this batch's from
-    // TMEM plus its parked partial, earlier ones from their park slot), park the
-    // rest of this batch (partial pieces added to their chunk's slot)
+    // TMEM, earlier ones from their park slot), park the rest of this batch
     b.act0 = static_cast<int>(S.acts.size());
-    for (const Unit& u : us) left[u.c] -= u.s1 - u.s0 + 1, ++npieces[u.c];
-    while (next < w && left[next] == 0) {
+    for (int c : ids) done[c] = 1;
+    while (next < w && done[next]) {
       int ci = -1;
       for (int x = 0; x < b.nc; ++x)
-        if (us[x].c == next) ci = x;
+        if (ids[x] == next) ci = x;
       if (ci >= 0) {
-        S.acts.push_back({kFlushTmem, next, ci, -1, park_of[next]});
+        S.acts.push_back({kFlushTmem, next, ci, -1});
       } else {
-        S.acts.push_back({kFlushParked, next, -1, park_of[next], -1});
+        S.acts.push_back({kFlushParked, next, -1, park_of[next]});
+        slot_busy[park_of[next]] = 0;
       }
-      if (park_of[next] >= 0) slot_busy[park_of[next]] = 0;
       ++next;
     }
     for (int x = 0; x < b.nc; ++x) {
-      const int c = us[x].c;
+      const int c = ids[x];
       if (c < next) continue;
-      const int add = park_of[c];
-      if (park_of[c] < 0) park_of[c] = take_slot();
-      S.acts.push_back({kPark, c, x, park_of[c], add});
+      int sl = 0;
+      while (sl < static_cast<int>(slot_busy.size()) && slot_busy[sl]) ++sl;
+      if (sl == static_cast<int>(slot_busy.size())) slot_busy.push_back(0);
+      slot_busy[sl] = 1;
+      park_of[c] = sl;
+      S.acts.push_back({kPark, c, x, sl});
     }
     S.park_slots = std::max(S.park_slots, static_cast<int>(slot_busy.size()));
     b.act1 = static_cast<int>(S.acts.size());
     S.batches.push_back(b);
   }
-  for (int c = 0; c < w; ++c) S.pieces += npieces[c] > 1 ? 1 : 0;
-}
-
-// Batches from chunk-id sets (whole chunks).
-template <class SlotBytes>
-inline void build_batches(Schedule& S, const std::vector<std::vector<int>>& sets, SlotBytes stage_slot_bytes,
-                          int64_t max_stage_bytes, int b_windows, const PassCost& cm) {
-  std::vector<std::vector<Unit>> us;
-  for (const auto& ids : sets) {
-    us.emplace_back();
-    for (int c : ids) us.back().push_back({c, S.chunks[c].s0, S.chunks[c].s1});
-  }
-  build_batches_units(S, us, stage_slot_bytes, max_stage_bytes, b_windows, cm);
 }
 
 }  // namespace detail
