@@ -1949,38 +1949,25 @@ int dgemm_host_impl(Handle* h, char transa, char transb, int64_t m, int64_t n, i
     bool trig_a;
     int trig;
   };
-  // The last arrival's strip is the call's tail: its GEMM, then its D2H.  It is
-  // cut into `tail_pieces` column pieces, each launched and copied back on its
-  // own, so the D2H of the first pieces runs under the GEMM of the later ones
-  // (only the last piece's copy is exposed).
-  int tail_pieces = 1;
-  if (const char* e = OZMM_ENV("OZMM_TAIL_PIECES")) tail_pieces = std::max(1, std::min(8, std::atoi(e)));
   std::vector<Strip> strips;
-  std::vector<int> strip_of(order.size(), -1), strip_end(order.size(), -1);
+  std::vector<int> strip_of(order.size(), -1);
   {
     int64_t na_arr = 0, nb_arr = 0;
     for (size_t o = 0; o < order.size(); ++o) {
       const int i = order[o].idx;
-      const int q0 = static_cast<int>(strips.size());
       if (order[o].is_a) {
         if (nb_arr > 0) {
-          const int64_t r0 = i * pa, rows = std::min(pa, m - i * pa), cols = std::min<int64_t>(p, nb_arr * pb);
-          // pieces of whole 256-column blocks (two 128-column tiles)
-          const int np = o + 1 == order.size() ? static_cast<int>(std::max<int64_t>(
-                                                     1, std::min<int64_t>(tail_pieces, cols / 256)))
-                                               : 1;
-          for (int x = 0; x < np; ++x) {
-            const int64_t c0 = (cols / 256) * x / np * 256, c1 = x + 1 == np ? cols : (cols / 256) * (x + 1) / np * 256;
-            strips.push_back({r0, rows, c0, c1 - c0, true, i});
-          }
+          strip_of[o] = static_cast<int>(strips.size());
+          strips.push_back({i * pa, std::min(pa, m - i * pa), 0, std::min<int64_t>(p, nb_arr * pb), true, i});
         }
         ++na_arr;
       } else {
-        if (na_arr > 0)
+        if (na_arr > 0) {
+          strip_of[o] = static_cast<int>(strips.size());
           strips.push_back({0, std::min<int64_t>(m, na_arr * pa), i * pb, std::min(pb, p - i * pb), false, i});
+        }
         ++nb_arr;
       }
-      if (static_cast<int>(strips.size()) > q0) strip_of[o] = q0, strip_end[o] = static_cast<int>(strips.size());
     }
   }
   const int ns = static_cast<int>(strips.size());
@@ -2153,8 +2140,7 @@ int dgemm_host_impl(Handle* h, char transa, char transb, int64_t m, int64_t n, i
       cu(cudaEventRecord(evB[s0], h->s_in), "event");
     }
     const int q = strip_of[o];
-    if (!no_c && q >= 0)
-      for (int x = q; x < strip_end[o]; ++x) copy_c(x);
+    if (!no_c && q >= 0) copy_c(q);
     // split (high-priority stream), as soon as the panel lands
     h->stream = h->s_split;
     if (order[o].is_a) {
@@ -2175,23 +2161,22 @@ int dgemm_host_impl(Handle* h, char transa, char transb, int64_t m, int64_t n, i
       cu(cudaEventRecord(evSB[s0], h->s_split), "event");
     }
     if (q < 0 || rc != OZMM_OK) continue;
-    // the strip (or tail pieces) of C this arrival completes
-    for (int x = q; x < strip_end[o] && rc == OZMM_OK; ++x) {
-      const Strip& t = strips[x];
-      cudaStream_t sg = h->s_gemm[x & 1];
-      cu(cudaStreamWaitEvent(sg, t.trig_a ? evSA[t.trig] : evSB[t.trig], 0), "wait");
-      if (!no_c) cu(cudaStreamWaitEvent(sg, evC[x], 0), "wait");
-      h->stream = sg;
-      if (trace) cu(cudaEventRecord(evGs[x], sg), "event");
-      if (offset) {
-        fl.lsa = h->lsa + t.r0;
-        fl.lsb = h->lsb + t.c0;
-      }
+    // the strip of C this arrival completes
+    const Strip& t = strips[q];
+    cudaStream_t sg = h->s_gemm[q & 1];
+    cu(cudaStreamWaitEvent(sg, t.trig_a ? evSA[t.trig] : evSB[t.trig], 0), "wait");
+    if (!no_c) cu(cudaStreamWaitEvent(sg, evC[q], 0), "wait");
+    h->stream = sg;
+    if (trace) cu(cudaEventRecord(evGs[q], sg), "event");
+    if (offset) {
+      fl.lsa = h->lsa + t.r0;
+      fl.lsb = h->lsb + t.c0;
+    }
+    if (rc == OZMM_OK)
       rc = launch_gemm(h, t.rows, n, t.cols, k, beta_bits, r, h->slices_a + t.r0 * lds, lds, m * lds,
                        h->mu + t.r0, h->slices_b + t.c0 * lds, lds, p * lds, h->nu + t.c0, alpha, beta,
                        no_c ? nullptr : dC + t.r0 * p + t.c0, dO + t.r0 * p + t.c0, p, opt, fl);
-      cu(cudaEventRecord(evG[x], sg), "event");
-    }
+    cu(cudaEventRecord(evG[q], sg), "event");
   }
   cu(cudaEventRecord(evSplit, h->s_split), "event");
   h->stream = user;
