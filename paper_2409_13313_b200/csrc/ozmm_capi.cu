@@ -138,9 +138,6 @@ struct Handle {
   double* host_o = nullptr;  // GEMM output for the host entry (the input C stays intact)
   size_t host_o_n = 0;
   cudaStream_t s_in = nullptr, s_out = nullptr;  // copy streams of the host entry
-  cudaStream_t s_mir = nullptr;                   // host entry: strip results -> pinned mirror
-  double* mirror = nullptr;  // pinned mirror of a pageable result (host entry), grown lazily
-  size_t mirror_n = 0;       // bytes
   cudaStream_t s_split = nullptr;                 // host entry: panel splits (high priority)
   cudaStream_t s_gemm[2] = {nullptr, nullptr};    // host entry: strip GEMMs
   cudaStream_t s_aux = nullptr;                   // device entry: B's column maxima
@@ -1142,8 +1139,6 @@ int ozmm_destroy(ozmm_handle_t handle) {
   cudaFree(h->host_o);
   if (h->s_in) cudaStreamDestroy(h->s_in);
   if (h->s_out) cudaStreamDestroy(h->s_out);
-  if (h->s_mir) cudaStreamDestroy(h->s_mir);
-  if (h->mirror) cudaFreeHost(h->mirror);
   if (h->s_split) cudaStreamDestroy(h->s_split);
   for (auto sg : h->s_gemm)
     if (sg) cudaStreamDestroy(sg);
@@ -1880,7 +1875,6 @@ int dgemm_host_impl(Handle* h, char transa, char transb, int64_t m, int64_t n, i
   if (int rc = ensure(h, &h->colmax, &h->colmax_n, static_cast<size_t>(std::max(pa, pb)))) return rc;
   if (!h->s_in) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
   if (!h->s_out) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
-  if (!h->s_mir) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->s_mir, cudaStreamNonBlocking));
   if (!h->s_split) {
     int lo = 0, hi = 0;
     CUDA_TRY(h, cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -1927,29 +1921,6 @@ int dgemm_host_impl(Handle* h, char transa, char transb, int64_t m, int64_t n, i
       if (st->ready() && st->slot_bytes() < slot) st->release();
       CUDA_TRY(h, st->init(slot, nslots, h->pool.get()));
     }
-  }
-  // Pageable result: each strip's result is copied by DMA into a pinned mirror of
-  // C as soon as its GEMM ends -- before the range gate, beside the incoming H2D
-  // (PCIe is full duplex) -- and the copy team moves mirror -> C once the gate is
-  // open.  Through the slot rings the whole 2 GB D2H at C3 waited for the gate
-  // (opened only when the last staged panel was screened) and ran at ~34 GB/s
-  // (profiles/r2/e2e_trace_r2.txt).  The mirror is one pinned buffer of m x p
-  // doubles kept on the handle (at most 8 GiB; otherwise, or if pinning fails,
-  // the slot rings as before).
-  double* mirror = nullptr;
-  {
-    bool want_mirror = pg_c && D * static_cast<size_t>(m) * p <= (size_t(8) << 30);
-    if (const char* e = OZMM_ENV("OZMM_MIRROR")) want_mirror = want_mirror && std::atoi(e) != 0;
-    const size_t bytes = D * static_cast<size_t>(m) * p;
-    if (want_mirror && h->mirror_n < bytes) {
-      if (h->mirror) cudaFreeHost(h->mirror);
-      h->mirror = nullptr, h->mirror_n = 0;
-      if (cudaHostAlloc(reinterpret_cast<void**>(&h->mirror), bytes, cudaHostAllocDefault) == cudaSuccess)
-        h->mirror_n = bytes;
-      else
-        h->mirror = nullptr, cudaGetLastError();  // no pinned memory to spare: slot rings
-    }
-    if (want_mirror) mirror = h->mirror;
   }
 
   // Panel arrival order over PCIe: A_s then B_s per step, except that the last
@@ -2006,8 +1977,7 @@ int dgemm_host_impl(Handle* h, char transa, char transb, int64_t m, int64_t n, i
   const bool trace = OZMM_ENV("OZMM_TRACE") != nullptr;
   const auto t_entry = std::chrono::steady_clock::now();
   for (auto& e : ev) CUDA_TRY(h, cudaEventCreateWithFlags(&e, trace ? 0 : cudaEventDisableTiming));
-  std::vector<cudaEvent_t> evGs(trace ? ns : 0), evO(trace ? ns : 0), evM(mirror ? ns : 0);
-  for (auto& e : evM) CUDA_TRY(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  std::vector<cudaEvent_t> evGs(trace ? ns : 0), evO(trace ? ns : 0);
   for (auto& e : evGs) CUDA_TRY(h, cudaEventCreate(&e));
   for (auto& e : evO) CUDA_TRY(h, cudaEventCreate(&e));
   cudaEvent_t* evA = ev.data();
@@ -2138,7 +2108,7 @@ int dgemm_host_impl(Handle* h, char transa, char transb, int64_t m, int64_t n, i
   fold_flags_kernel<<<1, 1, 0, user>>>(h->flags);
   cu(cudaGetLastError(), "fold flags");
   cu(cudaEventRecord(evStart, user), "event");
-  for (cudaStream_t s : {h->s_in, h->s_out, h->s_mir, h->s_split, h->s_gemm[0], h->s_gemm[1]})
+  for (cudaStream_t s : {h->s_in, h->s_out, h->s_split, h->s_gemm[0], h->s_gemm[1]})
     cu(cudaStreamWaitEvent(s, evStart, 0), "wait");
 
   // One issue loop over the panel arrivals: the panel's H2D copy (each followed by
@@ -2207,38 +2177,10 @@ int dgemm_host_impl(Handle* h, char transa, char transb, int64_t m, int64_t n, i
                        h->mu + t.r0, h->slices_b + t.c0 * lds, lds, p * lds, h->nu + t.c0, alpha, beta,
                        no_c ? nullptr : dC + t.r0 * p + t.c0, dO + t.r0 * p + t.c0, p, opt, fl);
     cu(cudaEventRecord(evG[q], sg), "event");
-    if (mirror) {  // the strip's result to the pinned mirror as soon as it is done
-      cu(cudaStreamWaitEvent(h->s_mir, evG[q], 0), "wait");
-      cu(cudaMemcpy2DAsync(mirror + t.r0 * p + t.c0, D * p, dO + t.r0 * p + t.c0, D * p, D * t.cols, t.rows,
-                           cudaMemcpyDeviceToHost, h->s_mir),
-         "D2H mirror");
-      cu(cudaEventRecord(evM[q], h->s_mir), "event");
-      if (trace) cu(cudaEventRecord(evO[q], h->s_mir), "event");
-    }
   }
   cu(cudaEventRecord(evSplit, h->s_split), "event");
   h->stream = user;
-  // mirror -> the caller's C, one strip at a time as its DMA completes, rows split
-  // over the copy team (streaming stores; the non-finite-C patch as in the rings)
-  auto mirror_out = [&](int q) {
-    const Strip& t = strips[q];
-    cu(cudaEventSynchronize(evM[q]), "sync");
-    if (rc != OZMM_OK) return;
-    const double* src = mirror + t.r0 * p + t.c0;
-    double* dst = Cout + t.r0 * ldo + t.c0;
-    const double* cin = C + t.r0 * ldc + t.c0;
-    const int nt = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(h->pool->size(), t.rows)));
-    h->pool->run(nt, [&](int th) {
-      for (int64_t r = t.rows * th / nt; r < t.rows * (th + 1) / nt; ++r) {
-        if (patch_c)
-          ozb::copy_patch(dst + r * ldo, src + r * p, cin + r * ldc, static_cast<size_t>(t.cols), beta);
-        else
-          ozb::copy_stream(dst + r * ldo, src + r * p, static_cast<size_t>(t.cols));
-      }
-    });
-  };
   auto copy_out = [&](int q) {
-    if (mirror) return mirror_out(q);
     const Strip& t = strips[q];
     cu(cudaStreamWaitEvent(h->s_out, evG[q], 0), "wait");
     d2h(Cout + t.r0 * ldo + t.c0, D * ldo, dO + t.r0 * p + t.c0, D * p, D * t.cols, t.rows,
@@ -2295,7 +2237,7 @@ int dgemm_host_impl(Handle* h, char transa, char transb, int64_t m, int64_t n, i
     // writes in narrow 8 KB row pieces drop to ~31 GB/s while the GEMM runs,
     // full rows keep ~52-57 GB/s (tools/d2h_2d.py).  The rest goes per strip.
     int q0 = 0;
-    if (rc == OZMM_OK && !range_err && !mirror) {
+    if (rc == OZMM_OK && !range_err) {
       int qd = 0;
       while (qd < ns && cudaEventQuery(evG[qd]) == cudaSuccess) ++qd;
       for (; qd > 1; --qd) {
@@ -2319,7 +2261,7 @@ int dgemm_host_impl(Handle* h, char transa, char transb, int64_t m, int64_t n, i
   }
   for (auto& th : scanners)
     if (th.joinable()) th.join();
-  for (cudaStream_t s : {h->s_in, h->s_split, h->s_gemm[0], h->s_gemm[1], h->s_out, h->s_mir})
+  for (cudaStream_t s : {h->s_in, h->s_split, h->s_gemm[0], h->s_gemm[1], h->s_out})
     cu(cudaStreamSynchronize(s), "sync");
   if (rc == OZMM_OK && no_c && !range_err) {
     // early gate: the host scan proved the later panels clean; confirm on the device
@@ -2370,7 +2312,6 @@ int dgemm_host_impl(Handle* h, char transa, char transb, int64_t m, int64_t n, i
   }
   for (auto& e : evGs) cudaEventDestroy(e);
   for (auto& e : evO) cudaEventDestroy(e);
-  for (auto& e : evM) cudaEventDestroy(e);
   for (auto& e : ev) cudaEventDestroy(e);
   if (rc == OZMM_OK && counts) {
     counts->int8_gemms = static_cast<int64_t>(k) * (k + 1) / 2;
